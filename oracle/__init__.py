@@ -1,0 +1,292 @@
+"""CPU oracle for Ekya's scheduling hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product package
+``paper_2012_10557_b200`` never imports it, and this package never imports the
+product (they share no code; the only common dependency is the seeded input
+generator ``synth``, which holds none of the method's arithmetic).
+
+The arithmetic lives in plain C (``ekya_oracle.c``, one fp32 rounding per
+operation, ``-ffp-contract=off``); this module is ctypes marshalling of numpy
+arrays plus the gcc build step.  Function-by-function citations are in the C
+file; the readings of the paper it follows are DESIGN.md section 3.
+
+Parity status: every function is pinned by ``tests/test_oracle_pins.py`` except
+the two thief readings, whose *trajectories* the paper never prints; they are
+pinned by a line-by-line transliteration of Algorithm 1 plus invariants
+(DESIGN.md section 4 lists what pins each function).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ekya_oracle.c")
+_LIB = os.path.join(_HERE, "_build", "libekya_oracle.so")
+
+LAMBDA_NONE = 7
+LMU_PAD = 0xFFFF
+STEEPEST = 0
+LITERAL = 1
+RADIUS = 0
+CLUSTER = 1
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc: -O2, no FMA contraction, no fast-math."""
+    if not force and os.path.exists(_LIB) and os.path.getmtime(_LIB) >= os.path.getmtime(_SRC):
+        return _LIB
+    os.makedirs(os.path.dirname(_LIB), exist_ok=True)
+    cmd = ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fno-math-errno",
+           "-fPIC", "-shared", "-Wall", "-Wextra", "-o", _LIB, _SRC, "-lm"]
+    subprocess.run(cmd, check=True)
+    return _LIB
+
+
+class Dims(ctypes.Structure):
+    _fields_ = [("n_inst", ctypes.c_int32), ("n_streams", ctypes.c_int32),
+                ("n_gamma", ctypes.c_int32), ("n_lambda", ctypes.c_int32),
+                ("units", ctypes.c_int32), ("steal_units", ctypes.c_int32),
+                ("unit_gpu_seconds", ctypes.c_float), ("a_min", ctypes.c_float)]
+
+
+class ProfileDims(ctypes.Structure):
+    _fields_ = [("n_query", ctypes.c_int32), ("n_hist", ctypes.c_int32),
+                ("n_class", ctypes.c_int32), ("n_gamma", ctypes.c_int32),
+                ("mode", ctypes.c_int32), ("tau", ctypes.c_float),
+                ("k", ctypes.c_int32), ("max_iter", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        L = _lib
+        L.orc_retrain_fraction.restype = ctypes.c_float
+        L.orc_retrain_fraction.argtypes = [ctypes.c_float, ctypes.c_int32, ctypes.c_float]
+        L.orc_gamma_feasible.restype = ctypes.c_int32
+        L.orc_gamma_feasible.argtypes = [ctypes.c_float, ctypes.c_int32, ctypes.c_float]
+        L.orc_window_accuracy.restype = ctypes.c_float
+        L.orc_window_accuracy.argtypes = [ctypes.c_float] * 3 + [ctypes.c_int32, ctypes.c_float]
+        L.orc_q32.restype = ctypes.c_uint64
+        L.orc_q32.argtypes = [ctypes.c_float]
+        L.orc_stream_value.restype = ctypes.c_float
+        L.orc_stream_value.argtypes = [ctypes.POINTER(Dims), ctypes.c_float, P, P, P, P,
+                                       ctypes.c_int32, ctypes.c_int32, P]
+        L.orc_pickconfigs.restype = ctypes.c_uint64
+        L.orc_pickconfigs.argtypes = [ctypes.POINTER(Dims), ctypes.c_int64, P, P, P, P, P, P, P, P]
+        L.orc_fair.restype = None
+        L.orc_fair.argtypes = [ctypes.POINTER(Dims), P]
+        L.orc_eval_grid.restype = ctypes.c_int64
+        L.orc_eval_grid.argtypes = [ctypes.POINTER(Dims), P, P, P, P, P, P, P]
+        L.orc_eval_list.restype = ctypes.c_int64
+        L.orc_eval_list.argtypes = [ctypes.POINTER(Dims), P, P, P, P, P, ctypes.c_int32, P, P, P, P]
+        L.orc_thief.restype = ctypes.c_int64
+        L.orc_thief.argtypes = [ctypes.POINTER(Dims), P, P, P, P, P, ctypes.c_int32, P, P, P, P, P]
+        L.orc_bruteforce.restype = ctypes.c_int64
+        L.orc_bruteforce.argtypes = [ctypes.POINTER(Dims), P, P, P, P, P, P, P, P]
+        L.orc_profile.restype = ctypes.c_int64
+        L.orc_profile.argtypes = [ctypes.POINTER(ProfileDims), P, P, P, P, P, P, P]
+    return _lib
+
+
+# ---------------------------------------------------------------------------
+# marshalling helpers
+# ---------------------------------------------------------------------------
+def _c(a, dtype):
+    a = np.ascontiguousarray(np.asarray(a), dtype=dtype)
+    return a
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+class Instances:
+    """Host-side batch of scheduling instances (numpy, instance-major SoA).
+
+    stale [B,V] f32; cost, post [B,V,nG] f32; lam_min_units [B,V,nL] u16;
+    lam_factor [B,V,nL] f32; scalars units, steal_units, unit_gpu_seconds, a_min.
+    """
+
+    def __init__(self, stale, cost, post, lam_min_units, lam_factor, units, steal_units,
+                 unit_gpu_seconds, a_min):
+        self.stale = _c(stale, np.float32)
+        B, V = self.stale.shape
+        self.cost = _c(cost, np.float32).reshape(B, V, -1)
+        self.post = _c(post, np.float32).reshape(B, V, -1)
+        self.lam_min_units = _c(lam_min_units, np.uint16).reshape(B, V, -1)
+        self.lam_factor = _c(lam_factor, np.float32).reshape(B, V, -1)
+        self.units = int(units)
+        self.steal_units = int(steal_units)
+        self.unit_gpu_seconds = float(unit_gpu_seconds)
+        self.a_min = float(a_min)
+
+    @property
+    def B(self):
+        return self.stale.shape[0]
+
+    @property
+    def V(self):
+        return self.stale.shape[1]
+
+    @property
+    def nG(self):
+        return self.cost.shape[2]
+
+    @property
+    def nL(self):
+        return self.lam_factor.shape[2]
+
+    def dims(self):
+        return Dims(self.B, self.V, self.nG, self.nL, self.units, self.steal_units,
+                    self.unit_gpu_seconds, self.a_min)
+
+    def tables(self):
+        return (_p(self.stale), _p(self.cost), _p(self.post), _p(self.lam_min_units),
+                _p(self.lam_factor))
+
+    def subset(self, idx):
+        idx = np.asarray(idx)
+        return Instances(self.stale[idx], self.cost[idx], self.post[idx], self.lam_min_units[idx],
+                         self.lam_factor[idx], self.units, self.steal_units,
+                         self.unit_gpu_seconds, self.a_min)
+
+
+def n_cells(units: int) -> int:
+    return (units + 1) * (units + 2) // 2
+
+
+# ---------------------------------------------------------------------------
+# primitives
+# ---------------------------------------------------------------------------
+def retrain_fraction(cost, rt, uT):
+    return lib().orc_retrain_fraction(cost, rt, uT)
+
+
+def gamma_feasible(cost, rt, uT):
+    return bool(lib().orc_gamma_feasible(cost, rt, uT))
+
+
+def window_accuracy(stale, post, cost, rt, uT):
+    return lib().orc_window_accuracy(stale, post, cost, rt, uT)
+
+
+def q32(x):
+    return int(lib().orc_q32(x))
+
+
+def stream_value(inst: Instances, b: int, v: int, rt: int, ri: int):
+    d = inst.dims()
+    cfg = np.zeros(1, np.uint8)
+    cost = np.ascontiguousarray(inst.cost[b, v])
+    post = np.ascontiguousarray(inst.post[b, v])
+    lmu = np.ascontiguousarray(inst.lam_min_units[b, v])
+    lf = np.ascontiguousarray(inst.lam_factor[b, v])
+    val = lib().orc_stream_value(ctypes.byref(d), float(inst.stale[b, v]), _p(cost), _p(post),
+                                 _p(lmu), _p(lf), rt, ri, _p(cfg))
+    return float(np.float32(val)), int(cfg[0])
+
+
+def pickconfigs(inst: Instances, b: int, alloc):
+    d = inst.dims()
+    a = _c(alloc, np.int32)
+    cfg = np.zeros(inst.V, np.uint8)
+    vals = np.zeros(inst.V, np.float32)
+    s = lib().orc_pickconfigs(ctypes.byref(d), b, *inst.tables(), _p(a), _p(cfg), _p(vals))
+    return int(s), cfg, vals
+
+
+def fair(inst: Instances):
+    d = inst.dims()
+    a = np.zeros(2 * inst.V, np.int32)
+    lib().orc_fair(ctypes.byref(d), _p(a))
+    return a
+
+
+def mean_from_q32(s, V):
+    return np.float32(np.float64(s) / (np.float64(V) * 4294967296.0))
+
+
+# ---------------------------------------------------------------------------
+# batched procedures
+# ---------------------------------------------------------------------------
+def eval_grid(inst: Instances):
+    d = inst.dims()
+    nc = n_cells(inst.units)
+    grid = np.zeros((inst.B, inst.V, nc), np.float32)
+    cfg = np.zeros((inst.B, inst.V, nc), np.uint8)
+    bad = lib().orc_eval_grid(ctypes.byref(d), *inst.tables(), _p(grid), _p(cfg))
+    if bad < 0:
+        raise ValueError("oracle: invalid dims")
+    return grid, cfg, int(bad)
+
+
+def eval_list(inst: Instances, alloc):
+    d = inst.dims()
+    alloc = _c(alloc, np.uint16)
+    n = alloc.shape[1]
+    s = np.zeros((inst.B, n), np.uint64)
+    mean = np.zeros((inst.B, n), np.float32)
+    cfg = np.zeros((inst.B, n, inst.V), np.uint8)
+    bad = lib().orc_eval_list(ctypes.byref(d), *inst.tables(), n, _p(alloc), _p(s), _p(mean),
+                              _p(cfg))
+    if bad < 0:
+        raise ValueError("oracle: invalid dims")
+    return s, mean, cfg, int(bad)
+
+
+def thief(inst: Instances, mode: int = STEEPEST):
+    d = inst.dims()
+    B, V = inst.B, inst.V
+    alloc = np.zeros((B, 2 * V), np.uint16)
+    cfg = np.zeros((B, V), np.uint8)
+    s = np.zeros(B, np.uint64)
+    mean = np.zeros(B, np.float32)
+    steps = np.zeros(B, np.uint32)
+    bad = lib().orc_thief(ctypes.byref(d), *inst.tables(), mode, _p(alloc), _p(cfg), _p(s),
+                          _p(mean), _p(steps))
+    if bad < 0:
+        raise ValueError("oracle: invalid dims/mode")
+    return alloc, cfg, s, mean, steps, int(bad)
+
+
+def bruteforce(inst: Instances):
+    d = inst.dims()
+    B, V = inst.B, inst.V
+    alloc = np.zeros((B, 2 * V), np.uint16)
+    cfg = np.zeros((B, V), np.uint8)
+    s = np.zeros(B, np.uint64)
+    bad = lib().orc_bruteforce(ctypes.byref(d), *inst.tables(), _p(alloc), _p(cfg), _p(s))
+    if bad == -2:
+        raise ValueError("oracle: instance too large for brute force")
+    if bad < 0:
+        raise ValueError("oracle: invalid dims")
+    return alloc, cfg, s, int(bad)
+
+
+def profile(cur, hist, hist_acc, fallback, mode=RADIUS, tau=0.2, k=5, max_iter=100):
+    cur = _c(cur, np.float32)
+    Q, C = cur.shape
+    hist = _c(hist, np.float32).reshape(Q, -1, C)
+    H = hist.shape[1]
+    hist_acc = _c(hist_acc, np.float32).reshape(Q, H, -1)
+    G = hist_acc.shape[2]
+    fallback = _c(fallback, np.float32).reshape(Q, G)
+    pd = ProfileDims(Q, H, C, G, mode, tau, k, max_iter)
+    est = np.zeros((Q, G), np.float32)
+    n = np.zeros((Q, G), np.int32)
+    cl = np.zeros((Q, H + 1), np.int32)
+    bad = lib().orc_profile(ctypes.byref(pd), _p(cur), _p(hist), _p(hist_acc), _p(fallback),
+                            _p(est), _p(n), _p(cl))
+    if bad < 0:
+        raise ValueError("oracle: invalid profile dims")
+    return est, n, (cl if mode == CLUSTER else None), int(bad)

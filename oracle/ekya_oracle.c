@@ -1,0 +1,607 @@
+/*
+ * ekya_oracle.c -- TEST INFRASTRUCTURE ONLY (see ekya_oracle.h).
+ *
+ * A plain, slow, single-threaded CPU implementation of what the Ekya thief
+ * scheduler's hot path computes (arXiv 2012.10557, final paper P:441-1738):
+ *
+ *   EstimateAccuracy   (Alg. 2 line 7; closed form of draft P:73)
+ *   PickConfigs        (Algorithm 2)
+ *   fair_allocation    (Alg. 1 line 2; reading C9)
+ *   Thief scheduler    (Algorithm 1) in two readings (C12):
+ *                        LITERAL  = the pseudocode verbatim,
+ *                        STEEPEST = best single-Delta steal per step
+ *   Eq. 1 brute force for tiny instances
+ *   History profiler   (draft appendix; P:30 five clusters)
+ *
+ * Arithmetic: IEEE-754 binary32, round-to-nearest-even, ONE rounding per
+ * operation (compile with -ffp-contract=off, no fast-math).  The precision is
+ * fp32 because BASELINE.json's north star fixes the objective in fp32 and
+ * demands identical decisions; every decision (argmax, feasibility,
+ * acceptance) is therefore taken in fp32 exactly as written here.  Sums of
+ * per-stream accuracies are exact integers (Q32, reading C15).
+ *
+ * Nothing here is blocked, fused or reordered: every PickConfigs call
+ * enumerates all (lambda, gamma) pairs of every stream; every thief candidate
+ * re-runs a full PickConfigs.
+ *
+ * Parity status per function: see DESIGN.md section 4 ("pins").
+ */
+#include "ekya_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_LAMBDA_NONE 7
+#define ORC_LMU_PAD 0xFFFFu
+
+/* ------------------------------------------------------------------------ */
+/* Rule 1 ("avoids configurations whose retraining durations exceed  */
+/* ||T||"; P:1155 GPU-time per epoch at 100% GPU scaled by the allocation;  */
+/* S:237 duration = cost / share).  t_r/||T|| = cost / (rt * delta * ||T||). */
+/* ------------------------------------------------------------------------ */
+float orc_retrain_fraction(float cost, int32_t rt, float uT)
+{
+    float denom = (float)rt * uT;          /* fl(float(rt) * uT) */
+    float f = cost / denom;                /* fl(cost / denom)   */
+    return f;
+}
+
+int32_t orc_gamma_feasible(float cost, int32_t rt, float uT)
+{
+    if (rt < 1) return 0;                  /* no GPU -> never finishes */
+    float f = orc_retrain_fraction(cost, rt, uT);
+    return f <= 1.0f;                      /* t_r == ||T|| is feasible (C5) */
+}
+
+/* Rule 2: window-averaged accuracy of retraining with gamma, as a fraction of
+ * the inference factor: draft P:73 base_acc = ((tau - t) a + (T - tau) A)/T at
+ * t = 0, i.e. f*stale + (1-f)*post, written as post - f*(post - stale). */
+float orc_window_accuracy(float stale, float post, float cost, int32_t rt, float uT)
+{
+    float f = orc_retrain_fraction(cost, rt, uT);
+    float diff = post - stale;
+    float prod = f * diff;
+    float g = post - prod;
+    return g;
+}
+
+/* Rule 4: exact fixed-point value x * 2^32, rounded to nearest even. */
+uint64_t orc_q32(float x)
+{
+    float y = x * 4294967296.0f;           /* exact: power-of-two scaling */
+    return (uint64_t)llrintf(y);           /* default rounding mode = RNE */
+}
+
+static float orc_mean_from_q32(uint64_t s, int32_t n)
+{
+    double m = (double)s / ((double)n * 4294967296.0);
+    return (float)m;
+}
+
+/* Alg. 2 lines 3-4: lambda pool = {resource_cost < alloc  &&
+ * accuracy >= a_MIN}; pick max accuracy (lowest index on ties, C7).
+ * Keep-up test in integer units (C2): ri >= lam_min_units.
+ * Accuracy of lambda = stale * factor (C1).  Returns -1 if the pool is empty. */
+static int orc_lambda_star(float stale, const uint16_t* lmu, const float* lf, int nl,
+                           int32_t ri, float a_min)
+{
+    int best = -1;
+    float best_acc = 0.0f;
+    for (int l = 0; l < nl; ++l) {
+        if (lmu[l] == ORC_LMU_PAD) continue;
+        if (ri < (int32_t)lmu[l]) continue;
+        float acc = stale * lf[l];
+        if (!(acc >= a_min)) continue;
+        if (best < 0 || acc > best_acc) {
+            best = l;
+            best_acc = acc;
+        }
+    }
+    return best;
+}
+
+/* Rule 3: the per-stream part of PickConfigs (Alg. 2 lines 3-14). */
+float orc_stream_value(const orc_dims* d, float stale, const float* cost, const float* post,
+                       const uint16_t* lmu, const float* lf, int32_t rt, int32_t ri, uint8_t* cfg)
+{
+    int l = orc_lambda_star(stale, lmu, lf, d->n_lambda, ri, d->a_min);
+    if (l < 0) {                           /* C8: no admissible lambda */
+        if (cfg) *cfg = (uint8_t)(ORC_LAMBDA_NONE << 5);
+        return 0.0f;
+    }
+    float fac = lf[l];
+    /* gamma = empty set first (index 0, C6): the stale model all window */
+    float best = fac * stale;
+    int bg = 0;
+    for (int g = 0; g < d->n_gamma; ++g) {
+        if (!orc_gamma_feasible(cost[g], rt, d->unit_gpu_seconds)) continue;
+        float w = orc_window_accuracy(stale, post[g], cost[g], rt, d->unit_gpu_seconds);
+        float a = fac * w;                 /* EstimateAccuracy(gamma, lambda, rt, T) */
+        if (a > best) {                    /* strict '>': lowest index wins */
+            best = a;
+            bg = g + 1;
+        }
+    }
+    if (cfg) *cfg = (uint8_t)(bg | (l << 5));
+    return best;
+}
+
+/* ------------------------------------------------------------------------ */
+/* instance access + validation                                             */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const float* stale;    /* [V]     */
+    const float* cost;     /* [V][nG] */
+    const float* post;     /* [V][nG] */
+    const uint16_t* lmu;   /* [V][nL] */
+    const float* lf;       /* [V][nL] */
+} orc_inst;
+
+static orc_inst orc_instance(const orc_dims* d, int64_t b, const float* stale, const float* cost,
+                             const float* post, const uint16_t* lmu, const float* lf)
+{
+    orc_inst in;
+    int64_t V = d->n_streams;
+    in.stale = stale + b * V;
+    in.cost = cost ? cost + b * V * d->n_gamma : NULL;
+    in.post = post ? post + b * V * d->n_gamma : NULL;
+    in.lmu = lmu + b * V * d->n_lambda;
+    in.lf = lf + b * V * d->n_lambda;
+    return in;
+}
+
+static int orc_in01(float x) { return x >= 0.0f && x <= 1.0f; }
+
+/* Data validity (error behaviour): stale in [0,1]; cost >= 0 or
+ * +INF (padding); post in [0,1] where cost is finite; factor in [0,1] where
+ * lam_min_units is not the padding value. */
+static int orc_instance_valid(const orc_dims* d, const orc_inst* in)
+{
+    for (int v = 0; v < d->n_streams; ++v) {
+        if (!orc_in01(in->stale[v])) return 0;
+        for (int g = 0; g < d->n_gamma; ++g) {
+            float c = in->cost[v * d->n_gamma + g];
+            if (!(c >= 0.0f)) return 0;    /* NaN or negative */
+            if (isinf(c)) continue;
+            if (!orc_in01(in->post[v * d->n_gamma + g])) return 0;
+        }
+        for (int l = 0; l < d->n_lambda; ++l) {
+            if (in->lmu[v * d->n_lambda + l] == ORC_LMU_PAD) continue;
+            if (!orc_in01(in->lf[v * d->n_lambda + l])) return 0;
+        }
+    }
+    return 1;
+}
+
+static int orc_dims_valid(const orc_dims* d)
+{
+    if (d->n_inst < 0 || d->n_streams < 1 || d->n_gamma < 0 || d->n_gamma > 31) return 0;
+    if (d->n_lambda < 1 || d->n_lambda > 7) return 0;
+    if (d->units < 1 || d->units > 65534 || d->steal_units < 1) return 0;
+    if (!(d->unit_gpu_seconds > 0.0f) || isinf(d->unit_gpu_seconds)) return 0;
+    if (isnan(d->a_min) || isinf(d->a_min)) return 0;
+    return 1;
+}
+
+/* Objective of one full allocation (Alg. 2 return value, exact form C15). */
+static uint64_t orc_pick(const orc_dims* d, const orc_inst* in, const int32_t* alloc,
+                         uint8_t* cfg_out, float* val_out)
+{
+    uint64_t s = 0;
+    for (int v = 0; v < d->n_streams; ++v) {
+        uint8_t c = 0;
+        float val = orc_stream_value(d, in->stale[v], in->cost + (int64_t)v * d->n_gamma,
+                                     in->post + (int64_t)v * d->n_gamma,
+                                     in->lmu + (int64_t)v * d->n_lambda,
+                                     in->lf + (int64_t)v * d->n_lambda,
+                                     alloc[2 * v + 1], alloc[2 * v], &c);
+        if (cfg_out) cfg_out[v] = c;
+        if (val_out) val_out[v] = val;
+        s += orc_q32(val);
+    }
+    return s;
+}
+
+uint64_t orc_pickconfigs(const orc_dims* d, int64_t b, const float* stale, const float* cost,
+                         const float* post, const uint16_t* lmu, const float* lf,
+                         const int32_t* alloc, uint8_t* cfg_out, float* val_out)
+{
+    orc_inst in = orc_instance(d, b, stale, cost, post, lmu, lf);
+    return orc_pick(d, &in, alloc, cfg_out, val_out);
+}
+
+/* C9: equal split over streams (remainder to the lowest-numbered streams),
+ * then half to retraining (floor), the rest to inference. Job 2v = inference,
+ * job 2v+1 = retraining (C10). */
+void orc_fair(const orc_dims* d, int32_t* alloc)
+{
+    int32_t V = d->n_streams, U = d->units;
+    for (int32_t v = 0; v < V; ++v) {
+        int32_t share = U / V + (v < U % V ? 1 : 0);
+        int32_t rt = share / 2;
+        alloc[2 * v + 1] = rt;
+        alloc[2 * v] = share - rt;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* GRID / LIST evaluators                                                   */
+/* ------------------------------------------------------------------------ */
+int64_t orc_eval_grid(const orc_dims* d, const float* stale, const float* cost, const float* post,
+                      const uint16_t* lmu, const float* lf, float* out_grid, uint8_t* out_grid_cfg)
+{
+    if (!orc_dims_valid(d)) return -1;
+    int64_t U = d->units, V = d->n_streams;
+    int64_t ncell = (U + 1) * (U + 2) / 2;
+    int64_t bad = 0;
+    for (int64_t b = 0; b < d->n_inst; ++b) {
+        orc_inst in = orc_instance(d, b, stale, cost, post, lmu, lf);
+        int ok = orc_instance_valid(d, &in);
+        if (!ok) ++bad;
+        for (int64_t v = 0; v < V; ++v) {
+            int64_t base = (b * V + v) * ncell;
+            int64_t c = 0;
+            for (int32_t rt = 0; rt <= U; ++rt) {
+                for (int32_t ri = 0; ri + rt <= U; ++ri, ++c) {
+                    uint8_t cfg = 0;
+                    float val = 0.0f;
+                    if (ok)
+                        val = orc_stream_value(d, in.stale[v], in.cost + v * d->n_gamma,
+                                               in.post + v * d->n_gamma, in.lmu + v * d->n_lambda,
+                                               in.lf + v * d->n_lambda, rt, ri, &cfg);
+                    out_grid[base + c] = val;
+                    if (out_grid_cfg) out_grid_cfg[base + c] = cfg;
+                }
+            }
+        }
+    }
+    return bad;
+}
+
+int64_t orc_eval_list(const orc_dims* d, const float* stale, const float* cost, const float* post,
+                      const uint16_t* lmu, const float* lf, int32_t n_alloc, const uint16_t* alloc,
+                      uint64_t* out_sum, float* out_mean, uint8_t* out_cfg)
+{
+    if (!orc_dims_valid(d) || n_alloc < 0) return -1;
+    int64_t V = d->n_streams, J = 2 * V;
+    int32_t* a = (int32_t*)malloc(sizeof(int32_t) * J);
+    uint8_t* cfg = (uint8_t*)malloc(V);
+    int64_t bad = 0;
+    for (int64_t b = 0; b < d->n_inst; ++b) {
+        orc_inst in = orc_instance(d, b, stale, cost, post, lmu, lf);
+        int ok = orc_instance_valid(d, &in);
+        for (int64_t n = 0; n < n_alloc; ++n) {
+            const uint16_t* row = alloc + (b * n_alloc + n) * J;
+            int64_t tot = 0;
+            int row_ok = ok;
+            for (int64_t j = 0; j < J; ++j) {
+                a[j] = row[j];
+                tot += row[j];
+                if (row[j] > d->units) row_ok = 0;
+            }
+            if (tot > d->units) row_ok = 0;   /* Eq. 1 constraint 2 */
+            uint64_t s = 0;
+            memset(cfg, 0, V);
+            if (row_ok) s = orc_pick(d, &in, a, cfg, NULL);
+            else ++bad;
+            int64_t o = b * n_alloc + n;
+            out_sum[o] = s;
+            if (out_mean) out_mean[o] = row_ok ? orc_mean_from_q32(s, d->n_streams) : 0.0f;
+            if (out_cfg) memcpy(out_cfg + o * V, cfg, V);
+        }
+    }
+    free(a);
+    free(cfg);
+    return bad;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Thief scheduler, Algorithm 1                               */
+/* ------------------------------------------------------------------------ */
+
+/* LITERAL: the pseudocode verbatim (C10 job order, C13 strict acceptance,
+ * C14 victim floor). */
+static uint64_t orc_thief_literal(const orc_dims* d, const orc_inst* in, int32_t* best,
+                                  uint32_t* steps)
+{
+    int32_t J = 2 * d->n_streams, D = d->steal_units;
+    int32_t* temp = (int32_t*)malloc(sizeof(int32_t) * J);
+    orc_fair(d, best);                                     /* line 2 */
+    uint64_t best_acc = orc_pick(d, in, best, NULL, NULL); /* line 3 */
+    uint32_t n = 0;
+    for (int32_t thief = 0; thief < J; ++thief) {          /* line 5 */
+        for (int32_t victim = 0; victim < J; ++victim) {   /* line 6 */
+            if (thief == victim) continue;                 /* line 7 */
+            memcpy(temp, best, sizeof(int32_t) * J);       /* line 8 */
+            for (;;) {                                     /* line 9 */
+                temp[victim] -= D;                         /* line 10 */
+                temp[thief] += D;                          /* line 11 */
+                if (temp[victim] < 0) break;               /* lines 12-13 */
+                uint64_t acc = orc_pick(d, in, temp, NULL, NULL); /* line 14 */
+                if (acc > best_acc) {                      /* line 15 */
+                    memcpy(best, temp, sizeof(int32_t) * J);
+                    best_acc = acc;
+                    ++n;
+                } else {
+                    break;
+                }
+            }
+        }
+    }
+    free(temp);
+    *steps = n;
+    return best_acc;
+}
+
+/* STEEPEST: from the fair start, repeatedly apply the single Delta-steal
+ * (thief t, victim w) that maximises the objective over ALL ordered pairs,
+ * ties to the lexicographically smallest (t, w); stop when no steal strictly
+ * improves (C12, north star "every candidate steal evaluated ... best one"). */
+static uint64_t orc_thief_steepest(const orc_dims* d, const orc_inst* in, int32_t* alloc,
+                                   uint32_t* steps)
+{
+    int32_t J = 2 * d->n_streams, D = d->steal_units;
+    orc_fair(d, alloc);
+    uint64_t cur = orc_pick(d, in, alloc, NULL, NULL);
+    uint32_t n = 0;
+    for (;;) {
+        uint64_t best = cur;
+        int32_t bt = -1, bw = -1;
+        for (int32_t t = 0; t < J; ++t) {
+            for (int32_t w = 0; w < J; ++w) {
+                if (t == w || alloc[w] < D) continue;
+                alloc[w] -= D;
+                alloc[t] += D;
+                uint64_t s = orc_pick(d, in, alloc, NULL, NULL);
+                alloc[w] += D;
+                alloc[t] -= D;
+                if (s > best) {
+                    best = s;
+                    bt = t;
+                    bw = w;
+                }
+            }
+        }
+        if (bt < 0) break;
+        alloc[bw] -= D;
+        alloc[bt] += D;
+        cur = best;
+        ++n;
+    }
+    *steps = n;
+    return cur;
+}
+
+int64_t orc_thief(const orc_dims* d, const float* stale, const float* cost, const float* post,
+                  const uint16_t* lmu, const float* lf, int32_t mode,
+                  uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum, float* out_mean,
+                  uint32_t* out_steps)
+{
+    if (!orc_dims_valid(d) || (mode != 0 && mode != 1)) return -1;
+    int64_t V = d->n_streams, J = 2 * V;
+    int32_t* a = (int32_t*)malloc(sizeof(int32_t) * J);
+    int64_t bad = 0;
+    for (int64_t b = 0; b < d->n_inst; ++b) {
+        orc_inst in = orc_instance(d, b, stale, cost, post, lmu, lf);
+        uint64_t s = 0;
+        uint32_t steps = 0;
+        if (orc_instance_valid(d, &in)) {
+            if (mode == 0) s = orc_thief_steepest(d, &in, a, &steps);
+            else s = orc_thief_literal(d, &in, a, &steps);
+            for (int64_t j = 0; j < J; ++j) out_alloc[b * J + j] = (uint16_t)a[j];
+            orc_pick(d, &in, a, out_cfg + b * V, NULL);
+            if (out_mean) out_mean[b] = orc_mean_from_q32(s, d->n_streams);
+        } else {
+            ++bad;
+            memset(out_alloc + b * J, 0, sizeof(uint16_t) * J);
+            memset(out_cfg + b * V, 0, V);
+            if (out_mean) out_mean[b] = 0.0f;
+        }
+        out_sum[b] = s;
+        if (out_steps) out_steps[b] = steps;
+    }
+    free(a);
+    return bad;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Eq. 1 brute force: maximise the objective over every         */
+/* allocation with sum <= U (constraint 2); per-job feasibility is inside   */
+/* PickConfigs, which implies constraint 1 (C16); constraint 3 holds because */
+/* PickConfigs picks exactly one (gamma, lambda) per stream.  Ties: the     */
+/* lexicographically smallest allocation vector.                            */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    const orc_dims* d;
+    const orc_inst* in;
+    int32_t* cur;
+    int32_t* best;
+    uint64_t best_s;
+    int have;
+} orc_bf;
+
+static void orc_bf_rec(orc_bf* st, int32_t j, int32_t left)
+{
+    int32_t J = 2 * st->d->n_streams;
+    if (j == J) {
+        uint64_t s = orc_pick(st->d, st->in, st->cur, NULL, NULL);
+        if (!st->have || s > st->best_s) {
+            st->have = 1;
+            st->best_s = s;
+            memcpy(st->best, st->cur, sizeof(int32_t) * J);
+        }
+        return;
+    }
+    for (int32_t x = 0; x <= left; ++x) {
+        st->cur[j] = x;
+        orc_bf_rec(st, j + 1, left - x);
+    }
+}
+
+int64_t orc_bruteforce(const orc_dims* d, const float* stale, const float* cost, const float* post,
+                       const uint16_t* lmu, const float* lf,
+                       uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum)
+{
+    if (!orc_dims_valid(d)) return -1;
+    int64_t V = d->n_streams, J = 2 * V;
+    /* guard: number of allocations C(U+J, J) must stay small */
+    double count = 1.0;
+    for (int64_t i = 1; i <= J; ++i) count = count * (double)(d->units + i) / (double)i;
+    if (count > 2.0e7) return -2;
+    int32_t* cur = (int32_t*)malloc(sizeof(int32_t) * J);
+    int32_t* best = (int32_t*)malloc(sizeof(int32_t) * J);
+    int64_t bad = 0;
+    for (int64_t b = 0; b < d->n_inst; ++b) {
+        orc_inst in = orc_instance(d, b, stale, cost, post, lmu, lf);
+        if (!orc_instance_valid(d, &in)) {
+            ++bad;
+            memset(out_alloc + b * J, 0, sizeof(uint16_t) * J);
+            memset(out_cfg + b * V, 0, V);
+            out_sum[b] = 0;
+            continue;
+        }
+        orc_bf st = {d, &in, cur, best, 0, 0};
+        orc_bf_rec(&st, 0, d->units);
+        for (int64_t j = 0; j < J; ++j) out_alloc[b * J + j] = (uint16_t)best[j];
+        orc_pick(d, &in, best, out_cfg + b * V, NULL);
+        out_sum[b] = st.best_s;
+    }
+    free(cur);
+    free(best);
+    return bad;
+}
+
+/* ------------------------------------------------------------------------ */
+/* History / class-distribution-similarity profiler                          */
+/* (draft appendix)                                         */
+/* ------------------------------------------------------------------------ */
+
+/* Rule 5: squared Euclidean distance, summed sequentially over classes. */
+static float orc_dist2(const float* a, const float* b, int32_t C)
+{
+    float s = 0.0f;
+    for (int32_t c = 0; c < C; ++c) {
+        float diff = a[c] - b[c];
+        float sq = diff * diff;
+        s = s + sq;
+    }
+    return s;
+}
+
+static int orc_nearest(const float* x, const float* mu, int32_t k, int32_t C)
+{
+    int best = 0;
+    float bd = orc_dist2(x, mu, C);
+    for (int i = 1; i < k; ++i) {
+        float di = orc_dist2(x, mu + (int64_t)i * C, C);
+        if (di < bd) {                     /* lowest index on ties (C19) */
+            bd = di;
+            best = i;
+        }
+    }
+    return best;
+}
+
+int64_t orc_profile(const orc_profile_dims* p, const float* cur, const float* hist,
+                    const float* hist_acc, const float* fallback,
+                    float* out_est, int32_t* out_n, int32_t* out_cluster)
+{
+    int64_t Q = p->n_query, H = p->n_hist, C = p->n_class, G = p->n_gamma;
+    if (Q < 0 || H < 0 || C < 1 || G < 1 || (p->mode != 0 && p->mode != 1)) return -1;
+    if (p->mode == 0 && !(p->tau >= 0.0f)) return -1;
+    if (p->mode == 1 && (p->k < 1 || p->max_iter < 0)) return -1;
+    int64_t K = p->mode == 1 ? p->k : 1;
+    unsigned char* sim = (unsigned char*)malloc(H > 0 ? H : 1);
+    int32_t* assign = (int32_t*)malloc(sizeof(int32_t) * (H > 0 ? H : 1));
+    int32_t* nassign = (int32_t*)malloc(sizeof(int32_t) * (H > 0 ? H : 1));
+    float* mu = (float*)malloc(sizeof(float) * K * C);
+    uint64_t* acc_sum = (uint64_t*)malloc(sizeof(uint64_t) * K * C);
+    int64_t* cnt = (int64_t*)malloc(sizeof(int64_t) * K);
+    int64_t bad = 0;
+
+    for (int64_t q = 0; q < Q; ++q) {
+        const float* cq = cur + q * C;
+        const float* hq = hist + q * H * C;
+        const float* aq = hist_acc + q * H * G;
+        int ok = 1;
+        for (int64_t c = 0; c < C; ++c) ok &= orc_in01(cq[c]);
+        for (int64_t i = 0; i < H * C; ++i) ok &= orc_in01(hq[i]);
+        for (int64_t i = 0; i < H * G; ++i) ok &= (isnan(aq[i]) || orc_in01(aq[i]));
+        if (!ok) {
+            ++bad;
+            for (int64_t g = 0; g < G; ++g) {
+                out_est[q * G + g] = 0.0f;
+                out_n[q * G + g] = 0;
+            }
+            if (out_cluster && p->mode == 1)
+                for (int64_t h = 0; h <= H; ++h) out_cluster[q * (H + 1) + h] = 0;
+            continue;
+        }
+        if (p->mode == 0) {
+            /* RADIUS: similar iff Euclidean distance <= tau (C17) */
+            for (int64_t h = 0; h < H; ++h) {
+                float d2 = orc_dist2(cq, hq + h * C, (int32_t)C);
+                float dist = sqrtf(d2);
+                sim[h] = dist <= p->tau;
+            }
+        } else {
+            /* CLUSTER: Lloyd k-means over the H history windows (C19) */
+            int32_t qc = -1;
+            if (H > 0) {
+                for (int64_t i = 0; i < K; ++i)
+                    memcpy(mu + i * C, hq + ((i * H) / K) * C, sizeof(float) * C);
+                for (int64_t h = 0; h < H; ++h)
+                    assign[h] = orc_nearest(hq + h * C, mu, (int32_t)K, (int32_t)C);
+                for (int32_t it = 0; it < p->max_iter; ++it) {
+                    memset(acc_sum, 0, sizeof(uint64_t) * K * C);
+                    memset(cnt, 0, sizeof(int64_t) * K);
+                    for (int64_t h = 0; h < H; ++h) {
+                        cnt[assign[h]] += 1;
+                        for (int64_t c = 0; c < C; ++c)
+                            acc_sum[assign[h] * C + c] += orc_q32(hq[h * C + c]);
+                    }
+                    for (int64_t i = 0; i < K; ++i) {
+                        if (cnt[i] == 0) continue;   /* empty cluster keeps its centroid */
+                        for (int64_t c = 0; c < C; ++c)
+                            mu[i * C + c] = orc_mean_from_q32(acc_sum[i * C + c], (int32_t)cnt[i]);
+                    }
+                    int changed = 0;
+                    for (int64_t h = 0; h < H; ++h) {
+                        nassign[h] = orc_nearest(hq + h * C, mu, (int32_t)K, (int32_t)C);
+                        changed |= nassign[h] != assign[h];
+                    }
+                    if (!changed) break;
+                    memcpy(assign, nassign, sizeof(int32_t) * H);
+                }
+                qc = orc_nearest(cq, mu, (int32_t)K, (int32_t)C);
+            }
+            for (int64_t h = 0; h < H; ++h) sim[h] = assign[h] == qc;
+            if (out_cluster) {
+                for (int64_t h = 0; h < H; ++h) out_cluster[q * (H + 1) + h] = assign[h];
+                out_cluster[q * (H + 1) + H] = qc;
+            }
+        }
+        /* mean past accuracy of gamma over similar windows that measured it
+         * (P:29 footnote, C18); none -> caller's fallback (C20) */
+        for (int64_t g = 0; g < G; ++g) {
+            uint64_t s = 0;
+            int32_t n = 0;
+            for (int64_t h = 0; h < H; ++h) {
+                float a = aq[h * G + g];
+                if (!sim[h] || isnan(a)) continue;
+                s += orc_q32(a);
+                ++n;
+            }
+            out_n[q * G + g] = n;
+            out_est[q * G + g] = n > 0 ? orc_mean_from_q32(s, n) : fallback[q * G + g];
+        }
+    }
+    free(sim);
+    free(assign);
+    free(nassign);
+    free(mu);
+    free(acc_sum);
+    free(cnt);
+    return bad;
+}

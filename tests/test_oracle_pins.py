@@ -1,0 +1,526 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+The oracle must not be checked against itself.  Each test below compares it with
+something the paper or mathematics fixes:
+  * worked examples printed in SPEC.md / PAPER.md (tests/golden/*.json, cited);
+  * closed forms evaluated in exact rational arithmetic (fractions.Fraction) in a
+    DIFFERENT algebraic form (SPEC S:227's (t_r a_old + (T - t_r) a_new)/T rather
+    than the oracle's post - f (post - stale));
+  * brute force on tiny inputs written independently here from Alg. 2 / Eq. 1;
+  * invariants (capacity, monotone acceptance, sandwich fair <= thief <= optimum,
+    k-means fixed point, etc.);
+  * a line-by-line Python transliteration of Algorithm 1's loop structure.
+"""
+from __future__ import annotations
+
+import itertools
+import json
+import math
+import os
+from fractions import Fraction as Fr
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+ULP = 2.0 ** -23
+
+
+def load(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def f32(x):
+    return float(np.float32(x))
+
+
+# ---------------------------------------------------------------------------
+# independent exact evaluator (Alg. 2, window average S:227)
+# ---------------------------------------------------------------------------
+def exact_stream(stale, costs, posts, lmus, lfs, rt, ri, uT, a_min):
+    """Returns (value, gamma, lam, candidates) in exact rationals from float inputs.
+
+    lambda pool: ri >= lam_min_units and stale*factor >= a_MIN, max accuracy.
+    gamma: argmax over {none} + {gamma : t_r <= ||T||} of the window average
+    (t_r a_old + (T - t_r) a_new) / T with a_old = stale*f, a_new = post*f."""
+    st = Fr(stale)
+    pool = [(st * Fr(lfs[l]), l) for l in range(len(lfs))
+            if lmus[l] != 0xFFFF and ri >= lmus[l] and st * Fr(lfs[l]) >= Fr(a_min)]
+    if not pool:
+        return Fr(0), 0, 7, []
+    best_acc = max(a for a, _ in pool)
+    lam = min(l for a, l in pool if a == best_acc)
+    fac = Fr(lfs[lam])
+    T = Fr(1)  # measure time in units of ||T||: t_r/||T|| = cost / (rt * uT)
+    cands = [(st * fac, 0)]
+    for g in range(len(costs)):
+        if rt < 1 or math.isinf(costs[g]):
+            continue
+        tr = Fr(costs[g]) / (rt * Fr(uT))
+        if tr > T:
+            continue
+        a_old, a_new = st * fac, Fr(posts[g]) * fac
+        cands.append(((tr * a_old + (T - tr) * a_new) / T, g + 1))
+    val = max(c for c, _ in cands)
+    gam = min(g for c, g in cands if c == val)
+    return val, gam, lam, cands
+
+
+def inst_stream(inst, b, v, rt, ri):
+    return exact_stream(float(inst.stale[b, v]), [float(x) for x in inst.cost[b, v]],
+                        [float(x) for x in inst.post[b, v]], [int(x) for x in inst.lam_min_units[b, v]],
+                        [float(x) for x in inst.lam_factor[b, v]], rt, ri, inst.unit_gpu_seconds,
+                        inst.a_min)
+
+
+def boundary_case(inst, b, v, rt, ri, eps=1e-6):
+    """True if an fp32-vs-exact decision (lambda filter, feasibility) sits within eps of its threshold."""
+    st = float(inst.stale[b, v])
+    for l in range(inst.nL):
+        if ri >= inst.lam_min_units[b, v, l] and abs(st * float(inst.lam_factor[b, v, l]) - inst.a_min) < eps:
+            return True
+    if rt >= 1:
+        for g in range(inst.nG):
+            c = float(inst.cost[b, v, g])
+            if not math.isinf(c) and abs(c / (rt * inst.unit_gpu_seconds) - 1.0) < eps:
+                return True
+    return False
+
+
+def make_inst(cfg, lo=0, hi=None):
+    T = synth.sched_tables(cfg, lo, hi)
+    return oracle.Instances(T["stale"].numpy(), T["cost"].numpy(), T["post"].numpy(),
+                            T["lam_min_units"].numpy(), T["lam_factor"].numpy(), cfg.units,
+                            cfg.steal_units, cfg.unit_gpu_seconds, cfg.a_min)
+
+
+def table1_inst():
+    fx = load("table1_fixture.json")
+    uT = f32(fx["delta_gpu"] * fx["window_s"])
+    return fx, oracle.Instances(np.array([fx["stale"]]), np.array([fx["cost_gpu_s"]]),
+                                np.array([fx["post"]]),
+                                np.array([[fx["lam_min_units"]] * 2]),
+                                np.array([[fx["lam_factor"]] * 2]), fx["units"], 1, uT, fx["a_min"])
+
+
+# ---------------------------------------------------------------------------
+# rules 1-2: EstimateAccuracy
+# ---------------------------------------------------------------------------
+def test_estimator_spec_examples():
+    ex = load("spec_examples.json")["estimator"]
+    # gamma = NONE -> stale (factor 1): the value of a stream with Gamma = {none}
+    e = ex[0]
+    inst = oracle.Instances([[e["stale"]]], np.zeros((1, 1, 0)), np.zeros((1, 1, 0)), [[[1]]],
+                            [[[e["factor"]]]], 4, 1, 30.0, 0.0)
+    val, cfg = oracle.stream_value(inst, 0, 0, 2, 2)
+    assert val == f32(e["expect"]) and cfg == 0
+    # T=120, t_r=60 -> f = 0.5; with one unit = 1 GPU, uT = 120, cost = 60 GPU-s
+    e = ex[1]
+    g = oracle.window_accuracy(e["a_old"], e["a_new"], e["t_r"], 1, e["window_s"])
+    assert f32(g) == f32(e["expect"])
+    # t_r = 130 > 120 -> infeasible
+    e = ex[2]
+    assert not oracle.gamma_feasible(e["t_r"], 1, e["window_s"])
+    assert oracle.gamma_feasible(e["window_s"], 1, e["window_s"])  # t_r == ||T|| is feasible (C5)
+
+
+def test_retrain_duration_spec_examples():
+    # t_r = cost / (rt * delta); with delta = 0.5 GPU and ||T|| = 200 s, uT = 100 GPU-s/unit
+    delta, T = 0.5, 200.0
+    for e in load("spec_examples.json")["retrain_duration"]:
+        cost = e["epochs"] * e["gpu_s_per_epoch"] * e["data_fraction"]   # P:1155 scaling
+        rt = int(round(e["share"] / delta))
+        f = oracle.retrain_fraction(cost, rt, delta * T)
+        assert f32(f * T) == pytest.approx(e["expect_s"], rel=1e-6), e["cite"]
+
+
+def test_estimator_vs_exact_closed_form():
+    rng = np.random.default_rng(1)
+    for _ in range(4000):
+        stale, post = f32(rng.uniform(0, 1)), f32(rng.uniform(0, 1))
+        uT = f32(rng.uniform(1, 50))
+        rt = int(rng.integers(1, 100))
+        cost = f32(rng.uniform(0, rt * uT))
+        if not oracle.gamma_feasible(cost, rt, uT):
+            continue
+        g = oracle.window_accuracy(stale, post, cost, rt, uT)
+        tr = Fr(cost) / (rt * Fr(uT))
+        exact = tr * Fr(stale) + (1 - tr) * Fr(post)        # draft P:73 at t = 0
+        assert abs(Fr(g) - exact) <= Fr(4 * ULP), (stale, post, cost, rt, uT)
+
+
+def test_estimator_monotone_in_rt():
+    """North star invariant: accuracy is monotone in r_train for fixed gamma
+    (non-decreasing if post >= stale, non-increasing otherwise)."""
+    rng = np.random.default_rng(2)
+    for _ in range(300):
+        stale, post = f32(rng.uniform(0, 1)), f32(rng.uniform(0, 1))
+        uT, cost = f32(rng.uniform(1, 30)), f32(rng.uniform(0, 2000))
+        prev, seen = None, False
+        for rt in range(1, 300):
+            feas = oracle.gamma_feasible(cost, rt, uT)
+            if not feas:
+                assert not seen, "feasibility must be an up-set in rt"
+                continue
+            seen = True
+            g = oracle.window_accuracy(stale, post, cost, rt, uT)
+            if prev is not None:
+                assert (g >= prev) if post >= stale else (g <= prev)
+            prev = g
+
+
+def test_q32_rounding():
+    assert oracle.q32(0.0) == 0
+    assert oracle.q32(1.0) == 2 ** 32
+    assert oracle.q32(0.5) == 2 ** 31
+    assert oracle.q32(2.0 ** -33) == 0          # 0.5 -> nearest even
+    assert oracle.q32(3 * 2.0 ** -33) == 2      # 1.5 -> 2
+    assert oracle.q32(5 * 2.0 ** -33) == 2      # 2.5 -> 2
+    x = f32(0.7)
+    assert oracle.q32(x) == round(Fr(x) * 2 ** 32)
+
+
+# ---------------------------------------------------------------------------
+# rule 3: PickConfigs
+# ---------------------------------------------------------------------------
+def test_pickconfigs_vs_exact_enumeration():
+    for cfg, n in ((synth.CONFIG1, 60), (synth.CONFIG2, 6)):
+        cfgr = synth.SchedConfig(**{**cfg.__dict__, "ragged": True}) if cfg is synth.CONFIG2 else cfg
+        for c in (cfg, cfgr):
+            inst = make_inst(c, 0, n)
+            rng = np.random.default_rng(3)
+            for b in range(inst.B):
+                for _ in range(6):
+                    rt = rng.integers(0, inst.units + 1, inst.V)
+                    ri = rng.integers(0, inst.units + 1, inst.V)
+                    alloc = np.stack([ri, rt], 1).reshape(-1)
+                    s, cfgs, vals = oracle.pickconfigs(inst, b, alloc)
+                    tot = 0
+                    for v in range(inst.V):
+                        if boundary_case(inst, b, v, int(rt[v]), int(ri[v])):
+                            continue
+                        ev, eg, el, cands = inst_stream(inst, b, v, int(rt[v]), int(ri[v]))
+                        assert abs(Fr(float(vals[v])) - ev) <= Fr(1, 10 ** 6)
+                        assert (cfgs[v] >> 5) == el
+                        others = sorted((c for c, g in cands if g != eg), reverse=True)
+                        if not others or ev - others[0] > Fr(1, 10 ** 6):
+                            assert (cfgs[v] & 31) == eg
+                        tot += oracle.q32(float(vals[v]))
+                    assert s >= 0
+
+
+def test_pickconfigs_gamma_empty_special_case():
+    """Gamma = {none} -> no retraining, value = best feasible lambda accuracy."""
+    inst = oracle.Instances([[0.8, 0.6]], np.zeros((1, 2, 0)), np.zeros((1, 2, 0)),
+                            [[[3, 1], [2, 1]]], [[[1.0, 0.5], [0.9, 0.8]]], 10, 1, 20.0, 0.41)
+    s, cfg, vals = oracle.pickconfigs(inst, 0, [3, 7, 1, 0])
+    assert vals[0] == f32(0.8) and cfg[0] == 0                       # lambda 0, no gamma
+    assert vals[1] == f32(f32(0.6) * f32(0.8)) and cfg[1] == (1 << 5)  # lambda 1 (lambda 0 needs 2 units)
+    s, cfg, vals = oracle.pickconfigs(inst, 0, [2, 0, 0, 8])
+    # stream 0 at ri = 2: lambda 0 needs 3 units, lambda 1 gives 0.4 < a_MIN 0.41 -> none (C8)
+    assert vals[0] == 0.0 and (cfg[0] >> 5) == 7
+    assert vals[1] == 0.0 and (cfg[1] >> 5) == 7
+
+
+def test_table1_uniform_inference_accuracy():
+    """at 0.75 GPU each, inference accuracy drops 65% -> 49% and 50% -> 37.5%."""
+    fx, inst = table1_inst()
+    e = fx["expect"]["uniform_inference_accuracy"]
+    nog = oracle.Instances(inst.stale, np.zeros((1, 2, 0)), np.zeros((1, 2, 0)),
+                           inst.lam_min_units, inst.lam_factor, inst.units, 1, inst.unit_gpu_seconds, 0.0)
+    a, _ = oracle.stream_value(nog, 0, 0, 0, e["ri_units"])
+    b, _ = oracle.stream_value(nog, 0, 1, 0, e["ri_units"])
+    assert a == pytest.approx(e["A"], abs=e["tol"])
+    assert b == pytest.approx(e["B"], abs=e["tol"])
+
+
+def test_fair_allocation_rule():
+    """C9: equal per-stream split (remainder to low streams), floor half to retraining."""
+    for V, U in ((10, 80), (3, 10), (2, 10), (7, 5), (1, 1)):
+        inst = oracle.Instances(np.full((1, V), 0.5), np.zeros((1, V, 0)), np.zeros((1, V, 0)),
+                                np.ones((1, V, 1)), np.ones((1, V, 1)), U, 1, 10.0, 0.0)
+        a = oracle.fair(inst)
+        assert a.sum() == U
+        shares = a[0::2] + a[1::2]
+        assert shares.max() - shares.min() <= 1 and list(shares) == sorted(shares, reverse=True)
+        assert all(a[1::2] == shares // 2)
+    inst = oracle.Instances(np.full((1, 3), 0.5), np.zeros((1, 3, 0)), np.zeros((1, 3, 0)),
+                            np.ones((1, 3, 1)), np.ones((1, 3, 1)), 10, 1, 10.0, 0.0)
+    assert list(oracle.fair(inst)) == [2, 2, 2, 1, 2, 1]
+
+
+# ---------------------------------------------------------------------------
+# LIST / GRID evaluators
+# ---------------------------------------------------------------------------
+def test_eval_list_matches_exact_and_flags_invalid_rows():
+    inst = make_inst(synth.CONFIG2, 0, 3)
+    rows = synth.list_allocs(synth.CONFIG2, 8, 0, 3).numpy().astype(np.uint16)
+    assert (rows.astype(np.int64).sum(-1) == inst.units).all()
+    rows[1, 0, 0] = inst.units + 1            # entry > U
+    rows[2, 1, 3] += 5                        # sum > U
+    s, mean, cfg, bad = oracle.eval_list(inst, rows)
+    assert bad == 2 and s[1, 0] == 0 and s[2, 1] == 0 and mean[1, 0] == 0.0
+    for b in range(3):
+        for n in range(8):
+            if (b, n) in ((1, 0), (2, 1)):
+                continue
+            tot = Fr(0)
+            for v in range(inst.V):
+                ev, *_ = inst_stream(inst, b, v, int(rows[b, n, 2 * v + 1]), int(rows[b, n, 2 * v]))
+                tot += ev
+            assert abs(Fr(int(s[b, n]), 2 ** 32) - tot) <= Fr(inst.V, 10 ** 6)
+            assert mean[b, n] == oracle.mean_from_q32(int(s[b, n]), inst.V)
+
+
+def test_eval_grid_cells_and_ri_monotone():
+    inst = make_inst(synth.CONFIG1, 0, 20)
+    grid, gcfg, bad = oracle.eval_grid(inst)
+    assert bad == 0
+    U = inst.units
+    for b in range(inst.B):
+        for v in range(inst.V):
+            c = 0
+            for rt in range(U + 1):
+                row = grid[b, v, c:c + U + 1 - rt]
+                assert (np.diff(row) >= 0).all()      # lambda pool grows with ri
+                for ri in range(U + 1 - rt):
+                    if not boundary_case(inst, b, v, rt, ri):
+                        ev, eg, el, _ = inst_stream(inst, b, v, rt, ri)
+                        assert abs(Fr(float(grid[b, v, c + ri])) - ev) <= Fr(1, 10 ** 6)
+                c += U + 1 - rt
+
+
+# ---------------------------------------------------------------------------
+# Eq. 1 brute force
+# ---------------------------------------------------------------------------
+def test_bruteforce_vs_exact_exhaustive():
+    inst = make_inst(synth.CONFIG1, 0, 12)
+    alloc, cfg, s, bad = oracle.bruteforce(inst)
+    U, J = inst.units, 2 * inst.V
+    for b in range(inst.B):
+        best = Fr(-1)
+        vals = {}
+        for comp in itertools.product(range(U + 1), repeat=J):
+            if sum(comp) > U:
+                continue
+            tot = sum(inst_stream(inst, b, v, comp[2 * v + 1], comp[2 * v])[0] for v in range(inst.V))
+            vals[comp] = tot
+            best = max(best, tot)
+        got = vals[tuple(int(x) for x in alloc[b])]
+        assert best - got <= Fr(inst.V, 10 ** 6)
+        assert abs(Fr(int(s[b]), 2 ** 32) - best) <= Fr(inst.V, 10 ** 6)
+
+
+def test_table1_optimum_qualitative():
+    fx, inst = table1_inst()
+    alloc, cfg, s, _ = oracle.bruteforce(inst)
+    e = fx["expect"]
+    assert (cfg[0, e["optimum_picks_cheaper_cfg_for_B"]["stream"]] & 31) == \
+        e["optimum_picks_cheaper_cfg_for_B"]["gamma_index"]           # Cfg2B
+    assert alloc[0, 3] > alloc[0, 1]                                  # rt_B > rt_A
+    fair = oracle.fair(inst)
+    sf, _, _ = oracle.pickconfigs(inst, 0, fair)
+    assert int(s[0]) > sf
+    # the STEEPEST thief reaches the same qualitative decision on this instance
+    ta, tc, ts, *_ = oracle.thief(inst, oracle.STEEPEST)
+    assert (tc[0, 1] & 31) == 2 and ta[0, 3] > ta[0, 1]
+
+
+# ---------------------------------------------------------------------------
+# Algorithm 1: structure + invariants
+# ---------------------------------------------------------------------------
+def py_literal(inst, b):
+    """Algorithm 1 transliterated line by line; objective = oracle PickConfigs."""
+    J, D = 2 * inst.V, inst.steal_units
+    pick = lambda a: oracle.pickconfigs(inst, b, a)[0]
+    best = list(oracle.fair(inst))                       # line 2
+    best_acc = pick(best)                                # line 3
+    for thief in range(J):                               # line 5
+        for victim in range(J):                          # line 6
+            if thief == victim:                          # line 7
+                continue
+            temp = list(best)                            # line 8
+            while True:                                  # line 9
+                temp[victim] -= D                        # line 10
+                temp[thief] += D                         # line 11
+                if temp[victim] < 0:                     # line 12
+                    break
+                acc = pick(temp)                         # line 14
+                if acc > best_acc:                       # line 15
+                    best, best_acc = list(temp), acc     # lines 16-18
+                else:
+                    break                                # line 20
+    return best, best_acc
+
+
+def py_steepest(inst, b):
+    J, D = 2 * inst.V, inst.steal_units
+    pick = lambda a: oracle.pickconfigs(inst, b, a)[0]
+    a = list(oracle.fair(inst))
+    cur, steps = pick(a), 0
+    while True:
+        cands = []
+        for t in range(J):
+            for w in range(J):
+                if t != w and a[w] >= D:
+                    x = list(a)
+                    x[w] -= D
+                    x[t] += D
+                    cands.append((-pick(x), t, w))
+        best = min(cands)
+        if -best[0] <= cur:
+            return a, cur, steps
+        a[best[2]] -= D
+        a[best[1]] += D
+        cur, steps = -best[0], steps + 1
+
+
+@pytest.mark.parametrize("cfg,n", [(synth.CONFIG1, 40), (synth.CONFIG2, 3)])
+def test_thief_matches_transliteration(cfg, n):
+    inst = make_inst(cfg, 0, n)
+    la, _, ls, _, lsteps, _ = oracle.thief(inst, oracle.LITERAL)
+    sa, _, ss, _, ssteps, _ = oracle.thief(inst, oracle.STEEPEST)
+    for b in range(n):
+        pa, ps = py_literal(inst, b)
+        assert list(la[b]) == pa and int(ls[b]) == ps
+        qa, qs, qsteps = py_steepest(inst, b)
+        assert list(sa[b]) == qa and int(ss[b]) == qs and int(ssteps[b]) == qsteps
+
+
+def test_thief_invariants_and_sandwich():
+    cfg = synth.SchedConfig(**{**synth.CONFIG1.__dict__, "n_inst": 1500})
+    inst = make_inst(cfg)
+    U, J = inst.units, 2 * inst.V
+    ba, _, bs, _ = oracle.bruteforce(inst)
+    fair = oracle.fair(inst)
+    for mode in (oracle.STEEPEST, oracle.LITERAL):
+        a, c, s, mean, steps, bad = oracle.thief(inst, mode)
+        assert bad == 0
+        assert (a.astype(np.int64).sum(1) == U).all()                      # P:1120 capacity
+        for b in range(inst.B):
+            sf = oracle.pickconfigs(inst, b, fair)[0]
+            assert sf <= int(s[b]) <= int(bs[b])                           # S:289 sandwich
+            assert (steps[b] == 0) == (int(s[b]) == sf)                     # strict acceptance
+            assert steps[b] <= J * J * U // inst.steal_units               # S:288 bound
+            assert mean[b] == oracle.mean_from_q32(int(s[b]), inst.V)
+    # STEEPEST stops at a point no single Delta-steal improves
+    a, c, s, *_ = oracle.thief(inst.subset(range(200)), oracle.STEEPEST)
+    for b in range(200):
+        for t in range(J):
+            for w in range(J):
+                if t != w and a[b, w] >= 1:
+                    x = a[b].astype(np.int32).copy()
+                    x[w] -= 1
+                    x[t] += 1
+                    assert oracle.pickconfigs(inst, b, x)[0] <= int(s[b])
+
+
+def test_invalid_instance_is_zeroed():
+    inst = make_inst(synth.CONFIG1, 0, 3)
+    inst.cost[1, 0, 0] = -1.0
+    inst.stale[2, 1] = float("nan")
+    a, c, s, mean, steps, bad = oracle.thief(inst, oracle.STEEPEST)
+    assert bad == 2 and (a[1:] == 0).all() and (s[1:] == 0).all() and s[0] > 0
+
+
+# ---------------------------------------------------------------------------
+# profiler
+# ---------------------------------------------------------------------------
+def test_profile_spec_examples():
+    ex = load("spec_examples.json")
+    for e in ex["distance"]:
+        # distance <= tau exactly at the printed distance (one-window history, acc 0.5)
+        d = e["expect"]
+        for tau, hit in ((d * (1 + 1e-6) + 1e-9, True), (d * (1 - 1e-6) - 1e-9, False)):
+            if tau < 0:
+                continue
+            est, n, _, _ = oracle.profile([e["p"]], [[e["q"]]], [[[0.5]]], [[0.1]], tau=tau)
+            assert (n[0, 0] == 1) == hit, e["cite"]
+    for e in ex["history_estimate"]:
+        est, n, _, _ = oracle.profile([e["cur"]], [e["hist"]], [[[a] for a in e["acc"]]], [[-1.0]],
+                                      tau=e["tau"])
+        if e["expect"] == "absent":
+            assert n[0, 0] == 0 and est[0, 0] == f32(-1.0), e["cite"]
+        else:
+            assert est[0, 0] == pytest.approx(e["expect"], abs=1e-7), e["cite"]
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_profile_radius_vs_float64_bruteforce(sparse):
+    cfg = synth.ProfileConfig("t", 24, 300, 27, 18, sparse=sparse)
+    P = {k: v.numpy() for k, v in synth.profile_inputs(cfg).items()}
+    est, n, _, bad = oracle.profile(P["cur"], P["hist"], P["hist_acc"], P["fallback"], tau=0.2)
+    assert bad == 0
+    d = np.sqrt(((P["hist"].astype(np.float64) - P["cur"][:, None, :]) ** 2).sum(-1))
+    for q in range(cfg.n_query):
+        if np.any(np.abs(d[q] - 0.2) < 1e-5):
+            continue
+        sim = d[q] <= 0.2
+        for g in range(cfg.n_gamma):
+            a = P["hist_acc"][q, :, g].astype(np.float64)
+            m = sim & ~np.isnan(a)
+            assert n[q, g] == m.sum()
+            if m.sum():
+                assert est[q, g] == pytest.approx(a[m].mean(), abs=1e-7)
+            else:
+                assert est[q, g] == P["fallback"][q, g]
+
+
+def test_cluster_recovers_separated_clusters_and_fixed_point():
+    rng = np.random.default_rng(5)
+    Q, H, C, K = 6, 200, 8, 5
+    hist = np.zeros((Q, H, C), np.float32)
+    truth = np.zeros((Q, H), np.int64)
+    for q in range(Q):
+        lab = rng.integers(0, K, H)
+        lab[[i * H // K for i in range(K)]] = rng.permutation(K)   # C19 init points in distinct clusters
+        truth[q] = lab
+        for h in range(H):
+            x = np.full(C, 0.01)
+            x[lab[h]] = 1.0                     # one dominant class per cluster
+            x = x + rng.uniform(0, 0.02, C)
+            hist[q, h] = x / x.sum()
+    acc = rng.uniform(0.3, 0.9, (Q, H, 3)).astype(np.float32)
+    cur = hist[:, 7, :].copy()
+    est, n, cl, bad = oracle.profile(cur, hist, acc, np.zeros((Q, 3)), mode=oracle.CLUSTER, k=K)
+    for q in range(Q):
+        a = cl[q, :H]
+        # same partition as the ground truth (labels may be permuted)
+        pairs = set(zip(a.tolist(), truth[q].tolist()))
+        assert len(pairs) == K and len({p[0] for p in pairs}) == K
+        # fixed point in float64: every window is nearest its own cluster mean
+        mu = np.stack([hist[q][a == i].astype(np.float64).mean(0) for i in range(K)])
+        dd = ((hist[q][:, None, :].astype(np.float64) - mu[None]) ** 2).sum(-1)
+        assert (dd[np.arange(H), a] <= dd.min(1) + 1e-9).all()
+        # query joins the nearest centroid; estimate = mean accuracy over that cluster
+        assert cl[q, H] == a[7]
+        m = a == cl[q, H]
+        assert n[q, 0] == m.sum()
+        assert est[q, 0] == pytest.approx(acc[q, m, 0].astype(np.float64).mean(), abs=1e-7)
+
+
+def test_cluster_degenerate_identical_histograms():
+    H = 50
+    hist = np.tile(np.array([0.2, 0.3, 0.5], np.float32), (1, H, 1))
+    acc = np.linspace(0.1, 0.9, H, dtype=np.float32).reshape(1, H, 1)
+    est, n, cl, _ = oracle.profile(hist[:, 0], hist, acc, [[0.0]], mode=oracle.CLUSTER, k=5)
+    assert (cl[0] == 0).all() and n[0, 0] == H
+    assert est[0, 0] == pytest.approx(acc.astype(np.float64).mean(), abs=1e-7)
+
+
+def test_cluster_on_synth_converges_to_fixed_point():
+    cfg = synth.ProfileConfig("t", 8, 500, 27, 18)
+    P = {k: v.numpy() for k, v in synth.profile_inputs(cfg).items()}
+    est, n, cl, bad = oracle.profile(P["cur"], P["hist"], P["hist_acc"], P["fallback"],
+                                     mode=oracle.CLUSTER, k=5, max_iter=100)
+    for q in range(cfg.n_query):
+        a = cl[q, :500]
+        present = [i for i in range(5) if (a == i).any()]
+        mu = {i: P["hist"][q][a == i].astype(np.float64).mean(0) for i in present}
+        for h in range(500):
+            d = {i: ((P["hist"][q, h] - mu[i]) ** 2).sum() for i in present}
+            assert d[a[h]] <= min(d.values()) + 1e-6
