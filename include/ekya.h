@@ -1,0 +1,188 @@
+/*
+ * ekya.h -- C ABI of the B200 (sm_100a) hot path of Ekya's thief scheduler.
+ *
+ * Paper: "Ekya: Continuous Learning of Video Analytics Models on Edge Compute
+ * Servers" (arXiv 2012.10557).  P:<n> = line of PAPER.md (final paper
+ * P:441-1738), S:<n> = line of SPEC.md.  The arithmetic contract (one IEEE
+ * binary32 rounding per operation, exact Q32 objective sums) and the readings
+ * C1..C23 are in DESIGN.md sections 2-3.
+ *
+ * Conventions for every call
+ *  - All array pointers are DEVICE pointers owned by the caller (e.g. torch
+ *    tensors).  Layout: instance-major, row-major, no padding.  The library
+ *    never allocates on these paths and never keeps a pointer after returning.
+ *  - Every compute call is asynchronous on `stream` (0 = legacy default).
+ *  - Return value: EKYA_OK (0) or a negative EKYA_ERR_* code.  Host-side
+ *    argument checks fail synchronously before anything is launched.
+ *  - Data errors found on the device (R-ERR in DESIGN.md: NaN/negative cost,
+ *    accuracies or factors outside [0,1], LIST rows with an entry > U or a sum
+ *    > U) do not abort: the affected instance / row gets all-zero outputs and
+ *    a device error word is set; ekya_last_error() synchronises and returns
+ *    EKYA_ERR_DATA once (then clears it).
+ *  - Infeasibility is data, not an error: a stream with no admissible lambda
+ *    contributes 0 and reports lambda = 7 (C8); an infeasible gamma is never
+ *    chosen.
+ *
+ * Job numbering (C10): job 2v is stream v's inference job (r_infer units),
+ * job 2v+1 its retraining job (r_train units).
+ *
+ * Config byte (cfg): bits 0..4 = gamma (0 = no retraining, 1..|Gamma| = the
+ * retraining config gamma-1), bits 5..7 = lambda (0..6, 7 = none).
+ */
+#ifndef EKYA_H
+#define EKYA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EKYA_OK               0
+#define EKYA_ERR_ARG         -1   /* null pointer / bad enum / bad handle          */
+#define EKYA_ERR_LIMIT       -2   /* |Gamma| > 31, |Lambda| > 7, U > 65534, ...     */
+#define EKYA_ERR_SHAPE       -3   /* sizes inconsistent or too large for a mode      */
+#define EKYA_ERR_CUDA        -4   /* a CUDA runtime call failed                      */
+#define EKYA_ERR_NCCL        -5   /* an NCCL call failed / comm not initialised      */
+#define EKYA_ERR_DATA        -6   /* (ekya_last_error only) device found bad data   */
+
+#define EKYA_LAMBDA_NONE      7
+#define EKYA_LMU_PAD     0xFFFFu  /* lam_min_units padding sentinel (unused lambda) */
+/* gamma padding sentinel: cost = +INF (never feasible)                             */
+
+/* cudaStream_t without including the CUDA headers */
+typedef struct CUstream_st* ekya_stream_t;
+
+typedef struct ekya_handle ekya_handle;
+
+/* Create a handle bound to CUDA device `device`.  `workspace_bytes` is ignored
+ * (reserved; the handle owns only its 64-byte device error word and counters). */
+int  ekya_create(ekya_handle** h, int device, size_t workspace_bytes);
+void ekya_destroy(ekya_handle* h);
+/* Synchronises the device, returns EKYA_ERR_DATA if any kernel since the last
+ * call found bad data (then clears the flag), EKYA_ERR_CUDA on a sticky CUDA
+ * error, else EKYA_OK. */
+int  ekya_last_error(ekya_handle* h);
+/* Number of kernels this handle has launched so far (for launch accounting). */
+uint64_t ekya_launch_count(const ekya_handle* h);
+const char* ekya_version(void);
+
+/* Problem statement of a batch of scheduling instances (Eq. 1, P:876-973;
+ * notation Table 2).  [ClusterSpec S:43-46, RetrainWindow S:27-30] */
+typedef struct {
+    int32_t n_inst;            /* B >= 0 independent instances                     */
+    int32_t n_streams;         /* V = |V| >= 1 video streams per instance          */
+    int32_t n_gamma;           /* max |Gamma_v|, 0..31 (excluding gamma = none)    */
+    int32_t n_lambda;          /* max |Lambda_v|, 1..7                             */
+    int32_t units;             /* U = G/delta total allocation units, 1..65534     */
+    int32_t steal_units;       /* Delta/delta >= 1 (C11)                           */
+    float   unit_gpu_seconds;  /* uT = delta * ||T|| GPU-seconds per unit, > 0     */
+    float   a_min;             /* a_MIN, finite                           */
+} ekya_dims;
+
+/* Resource-accuracy profiles (D3/D4).  [ConfigProfile S:58-61,
+ * InferenceConfig S:38-41, WindowTrace.stale_accuracy S:64] */
+typedef struct {
+    const float*    stale;          /* [B][V]     current-model accuracy in [0,1]                */
+    const float*    cost;           /* [B][V][nG] GPU-seconds to retrain at 100% GPU;
+                                       +INF = padding; may be NULL iff nG == 0                  */
+    const float*    post;           /* [B][V][nG] estimated post-retraining accuracy in [0,1]
+                                       (e.g. ekya_profile_estimate's out_est)                   */
+    const uint16_t* lam_min_units;  /* [B][V][nL] smallest r_infer that keeps up under the
+                                       strict "<" of P:1088 (C2); 0xFFFF = padding              */
+    const float*    lam_factor;     /* [B][V][nL] accuracy multiplier in [0,1] (C1)             */
+} ekya_tables;
+
+/* ---------------------------------------------------------------------------
+ * ekya_eval_allocations -- PickConfigs (Algorithm 2) over many
+ * allocations.  [pick_configs S:244-252]
+ *
+ * mode EKYA_EVAL_LIST: for each instance b and each of its n_alloc full
+ *   allocation vectors alloc[b][n][0..2V) (u16 units, job order C10), the
+ *   exact objective out_sum_q32[b][n] = sum_v Q32(value_v) (u64), optionally
+ *   out_mean[b][n] = (float)(S / (V 2^32)) and out_cfg[b][n][v].  Requires the
+ *   per-instance tables (V*(U+1)*(5*nL+1) bytes) to fit in 200 KB of shared
+ *   memory, else EKYA_ERR_SHAPE.
+ * mode EKYA_EVAL_GRID: for each (b, v) and every split with r_train + r_infer
+ *   <= U, out_grid[b][v][c] = value of stream v alone (f32) and
+ *   out_grid_cfg[b][v][c] = its argmax config byte, cell c = rowstart(rt) + ri,
+ *   rowstart(rt) = rt*(U+1) - rt*(rt-1)/2, i.e. (U+1)(U+2)/2 cells per stream
+ *   (north star "for every v, gamma, lambda and (r_train, r_infer) ... per-stream
+ *   argmax").  U <= 4094 in GRID mode.
+ * Outputs not used by the mode may be NULL; out_mean/out_cfg/out_grid_cfg are
+ * optional.
+ * ------------------------------------------------------------------------- */
+enum { EKYA_EVAL_LIST = 0, EKYA_EVAL_GRID = 1 };
+int ekya_eval_allocations(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int mode,
+                          int32_t n_alloc, const uint16_t* alloc,
+                          uint64_t* out_sum_q32, float* out_mean, uint8_t* out_cfg,
+                          float* out_grid, uint8_t* out_grid_cfg, ekya_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * ekya_thief_schedule -- Algorithm 1 for each instance, from
+ * the fair start (C9).  [thief_schedule S:254-262]
+ *   EKYA_THIEF_STEEPEST: per step apply the single Delta-steal (thief t,
+ *     victim w) with the largest objective gain over all ordered pairs,
+ *     lexicographically smallest (t, w) on ties; stop when no steal strictly
+ *     improves (C12, north star).
+ *   EKYA_THIEF_LITERAL: the pseudocode verbatim (thief, then victim loops,
+ *     steal repeatedly while strictly improving).
+ * Outputs: out_alloc[b][2V] (u16 units, sum = U), out_cfg[b][V],
+ * out_sum_q32[b] (exact objective), optional out_mean[b], out_steps[b]
+ * (accepted steals).  Any V, U within the limits.
+ * ------------------------------------------------------------------------- */
+enum { EKYA_THIEF_STEEPEST = 0, EKYA_THIEF_LITERAL = 1 };
+int ekya_thief_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int mode,
+                        uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum_q32,
+                        float* out_mean, uint32_t* out_steps, ekya_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * ekya_profile_estimate -- history / class-distribution-similarity estimator
+ * (draft appendix).  [history_estimate S:165-173,
+ * distribution_distance S:175-183]
+ * For each query q (one stream's current window) with current class
+ * histogram cur[q][C], history histograms hist[q][H][C] and the accuracy
+ * hist_acc[q][H][G] each history window reached with retraining config g (NaN
+ * = not measured), out_est[q][g] = mean accuracy over the SIMILAR windows that
+ * measured g (exact Q32 mean), out_n[q][g] = their count; no such window ->
+ * out_est = fallback[q][g] (the online micro-profiler's estimate), n = 0.
+ *   mode 0 RADIUS : similar iff Euclidean distance <= tau (C17).
+ *   mode 1 CLUSTER: Lloyd k-means (k clusters, "5 clusters", C19) over the
+ *                   H windows; similar iff same cluster as the query's nearest
+ *                   centroid.  out_cluster[q][0..H) = window clusters,
+ *                   out_cluster[q][H] = the query's cluster (may be NULL).
+ * Limits: 1 <= C <= 1024, 1 <= G <= 256, H >= 0, 1 <= k <= 32, max_iter >= 0.
+ * With q = b*V + v, out_est is exactly ekya_tables.post for a batch.
+ * ------------------------------------------------------------------------- */
+enum { EKYA_PROFILE_RADIUS = 0, EKYA_PROFILE_CLUSTER = 1 };
+typedef struct {
+    int32_t n_query, n_hist, n_class, n_gamma;
+    int32_t mode;
+    float   tau;
+    int32_t k, max_iter;
+} ekya_profile_dims;
+int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p,
+                          const float* cur, const float* hist, const float* hist_acc,
+                          const float* fallback, float* out_est, int32_t* out_n,
+                          int32_t* out_cluster, ekya_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU (one process per GPU).  Instances are independent, so ranks own
+ * contiguous instance blocks and the only collective is a gather of the fixed-
+ * size decision records to a root rank (north star "only a final NCCL gather").
+ * ekya_comm_unique_id: fills 128 bytes (ncclUniqueId) on the root; broadcast
+ *   them out of band (e.g. torch.distributed), then every rank calls
+ *   ekya_comm_init with the same bytes.
+ * ekya_gather_decisions: root_buf[r*bytes_per_rank ...] <- rank r's `local`
+ *   (device pointers; root_buf used on the root only), enqueued on `stream`.
+ * ------------------------------------------------------------------------- */
+int ekya_comm_unique_id(void* out_id_128_bytes);
+int ekya_comm_init(ekya_handle* h, const void* id_128_bytes, int nranks, int rank);
+int ekya_gather_decisions(ekya_handle* h, const void* local, size_t bytes_per_rank,
+                          void* root_buf, int root, ekya_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EKYA_H */

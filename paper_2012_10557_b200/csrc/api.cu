@@ -1,0 +1,148 @@
+// api.cu -- the extern "C" boundary of libekya (include/ekya.h): handle
+// management, synchronous argument checks, and dispatch to the launchers.
+#include <cmath>
+#include <cstdlib>
+#include <new>
+
+#include "launch.h"
+
+using namespace ekya;
+
+namespace {
+
+bool dims_ok(const ekya_dims* d, int* why) {
+    if (!d) { *why = EKYA_ERR_ARG; return false; }
+    if (d->n_inst < 0 || d->n_streams < 1) { *why = EKYA_ERR_SHAPE; return false; }
+    if (d->n_gamma < 0 || d->n_gamma > kMaxGamma || d->n_lambda < 1 || d->n_lambda > kMaxLambda ||
+        d->units < 1 || d->units > 65534 || d->steal_units < 1) {
+        *why = EKYA_ERR_LIMIT;
+        return false;
+    }
+    if (!(d->unit_gpu_seconds > 0.0f) || std::isinf(d->unit_gpu_seconds) || std::isnan(d->a_min) ||
+        std::isinf(d->a_min)) {
+        *why = EKYA_ERR_ARG;
+        return false;
+    }
+    return true;
+}
+
+bool tables_ok(const ekya_dims* d, const ekya_tables* t) {
+    if (!t) return false;
+    if (d->n_inst == 0) return true;
+    if (!t->stale || !t->lam_min_units || !t->lam_factor) return false;
+    if (d->n_gamma > 0 && (!t->cost || !t->post)) return false;
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ekya_version(void) { return "ekya-b200 0.1 (sm_100a)"; }
+
+int ekya_create(ekya_handle** out, int device, size_t /*workspace_bytes*/) {
+    if (!out) return EKYA_ERR_ARG;
+    *out = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess) return EKYA_ERR_CUDA;
+    ekya_handle* h = new (std::nothrow) ekya_handle();
+    if (!h) return EKYA_ERR_ARG;
+    h->device = device;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    h->sm_count = v;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    h->smem_optin = (size_t)v;
+    if (cudaMalloc(&h->dstate, sizeof(DevState)) != cudaSuccess ||
+        cudaMemset(h->dstate, 0, sizeof(DevState)) != cudaSuccess) {
+        delete h;
+        return EKYA_ERR_CUDA;
+    }
+    h->launches = 0;
+    h->nccl_comm = nullptr;
+    h->nranks = 1;
+    h->rank = 0;
+    *out = h;
+    return EKYA_OK;
+}
+
+void ekya_comm_destroy_internal(ekya_handle* h);
+
+void ekya_destroy(ekya_handle* h) {
+    if (!h) return;
+    ekya_comm_destroy_internal(h);
+    cudaFree(h->dstate);
+    delete h;
+}
+
+int ekya_last_error(ekya_handle* h) {
+    if (!h) return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    if (cudaDeviceSynchronize() != cudaSuccess) return EKYA_ERR_CUDA;
+    DevState st;
+    if (cudaMemcpy(&st, h->dstate, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) return EKYA_ERR_CUDA;
+    if (st.err) {
+        cudaMemset(h->dstate, 0, sizeof(DevState));
+        return EKYA_ERR_DATA;
+    }
+    return EKYA_OK;
+}
+
+uint64_t ekya_launch_count(const ekya_handle* h) { return h ? h->launches : 0; }
+
+int ekya_eval_allocations(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int mode,
+                          int32_t n_alloc, const uint16_t* alloc, uint64_t* out_sum_q32,
+                          float* out_mean, uint8_t* out_cfg, float* out_grid, uint8_t* out_grid_cfg,
+                          ekya_stream_t stream) {
+    if (!h) return EKYA_ERR_ARG;
+    int why = EKYA_OK;
+    if (!dims_ok(d, &why)) return why;
+    if (!tables_ok(d, t)) return EKYA_ERR_ARG;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    if (mode == EKYA_EVAL_LIST) {
+        if (n_alloc < 0) return EKYA_ERR_SHAPE;
+        if (d->n_inst > 0 && n_alloc > 0 && (!alloc || !out_sum_q32)) return EKYA_ERR_ARG;
+        return launch_eval_list(h, *d, *t, n_alloc, alloc, out_sum_q32, out_mean, out_cfg, s);
+    }
+    if (mode == EKYA_EVAL_GRID) {
+        if (d->n_inst > 0 && !out_grid) return EKYA_ERR_ARG;
+        return launch_eval_grid(h, *d, *t, out_grid, out_grid_cfg, s);
+    }
+    return EKYA_ERR_ARG;
+}
+
+int ekya_thief_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int mode,
+                        uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum_q32,
+                        float* out_mean, uint32_t* out_steps, ekya_stream_t stream) {
+    if (!h) return EKYA_ERR_ARG;
+    int why = EKYA_OK;
+    if (!dims_ok(d, &why)) return why;
+    if (!tables_ok(d, t)) return EKYA_ERR_ARG;
+    if (mode != EKYA_THIEF_STEEPEST && mode != EKYA_THIEF_LITERAL) return EKYA_ERR_ARG;
+    if (d->n_inst > 0 && (!out_alloc || !out_cfg || !out_sum_q32)) return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    return launch_thief(h, *d, *t, mode, out_alloc, out_cfg, out_sum_q32, out_mean, out_steps,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p, const float* cur,
+                          const float* hist, const float* hist_acc, const float* fallback,
+                          float* out_est, int32_t* out_n, int32_t* out_cluster, ekya_stream_t stream) {
+    if (!h || !p) return EKYA_ERR_ARG;
+    if (p->n_query < 0 || p->n_hist < 0) return EKYA_ERR_SHAPE;
+    if (p->n_class < 1 || p->n_class > 1024 || p->n_gamma < 1 || p->n_gamma > 256) return EKYA_ERR_LIMIT;
+    if (p->mode == EKYA_PROFILE_RADIUS) {
+        if (!(p->tau >= 0.0f)) return EKYA_ERR_ARG;
+    } else if (p->mode == EKYA_PROFILE_CLUSTER) {
+        if (p->k < 1 || p->k > 32 || p->max_iter < 0) return EKYA_ERR_LIMIT;
+    } else {
+        return EKYA_ERR_ARG;
+    }
+    if (p->n_query > 0 && (!cur || !fallback || !out_est || !out_n)) return EKYA_ERR_ARG;
+    if (p->n_query > 0 && p->n_hist > 0 && (!hist || !hist_acc)) return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    return launch_profile(h, *p, cur, hist, hist_acc, fallback, out_est, out_n, out_cluster,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

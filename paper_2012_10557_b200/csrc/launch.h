@@ -1,0 +1,38 @@
+// launch.h -- host-side launchers behind the C ABI (internal to libekya).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/ekya.h"
+#include "ekya_common.cuh"
+
+struct ekya_handle {
+    int device;
+    int sm_count;
+    size_t smem_optin;                 // max dynamic shared memory per block
+    ekya::DevState* dstate;            // device error word
+    unsigned long long launches;       // kernels launched through this handle
+    void* nccl_comm;                   // ncclComm_t when initialised
+    int nranks, rank;
+};
+
+namespace ekya {
+
+int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, float* out_grid,
+                     uint8_t* out_grid_cfg, cudaStream_t s);
+int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int n_alloc,
+                     const uint16_t* alloc, uint64_t* out_sum, float* out_mean, uint8_t* out_cfg,
+                     cudaStream_t s);
+int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int mode,
+                 uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum, float* out_mean,
+                 uint32_t* out_steps, cudaStream_t s);
+int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur, const float* hist,
+                   const float* hist_acc, const float* fallback, float* out_est, int32_t* out_n,
+                   int32_t* out_cluster, cudaStream_t s);
+
+inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? EKYA_OK : EKYA_ERR_CUDA; }
+
+}  // namespace ekya

@@ -1,0 +1,387 @@
+// thief.cu -- ekya_thief_schedule: Algorithm 1, one warp per
+// scheduling instance.
+//
+// A Delta-steal (thief t, victim w) changes at most the two streams s(t), s(w),
+// so the objective change is an exact integer
+//     dS(t, w) = up[t] + down[w]        if s(t) != s(w)
+//     dS(t, w) = move[t]                if s(t) == s(w)  (w = t ^ 1)
+// where, per stream, up/down/move are Q32 differences of the stream value at
+// the seven splits {(rt,ri), (rt,ri+D), (rt+D,ri), (rt,ri-D), (rt-D,ri),
+// (rt+D,ri-D), (rt-D,ri+D)}.  These arrays live in shared memory and only the
+// touched streams are re-evaluated after a step, so a step costs O(J) instead of
+// the oracle's O(J^2) full PickConfigs recomputations, with bit-identical
+// decisions (integer arithmetic, identical tie rules).
+//
+// Stream evaluation is warp-parallel over gamma (lane 0 = no retraining,
+// lane g = config g-1): each lane computes rule 2 at rt-D, rt, rt+D, a warp
+// max (REDUX) gives G*(rt'), and value(rt', ri') = fl(f_{lambda*(ri')} G*(rt'))
+// (exact because x -> fl(c x) is monotone).
+//
+// STEEPEST (C12): per step, per stream best down (value desc, index asc) ->
+// warp top-2 by stream -> per thief its best victim -> warp argmax over thieves
+// with lexicographic (t, w) ties; accept iff dS > 0.
+// LITERAL: thieves in order; victims scanned 32 at a time with a warp ballot of
+// "first steal improves" -- victims before the first set bit leave the state
+// unchanged, exactly as in the sequential loop -- then the steal chain on that
+// victim, then the scan resumes after it.
+#include <algorithm>
+
+#include "launch.h"
+
+namespace ekya {
+
+namespace {
+
+constexpr int kThiefThreads = 128;      // 4 warps = 4 instances per CTA
+constexpr long long kInvalid = (long long)0x8000000000000000ULL;
+constexpr long long kKeyOff = 1LL << 40;
+
+struct ThiefParams {
+    ekya_dims d;
+    ekya_tables t;
+    DevState* st;
+    int mode;
+    uint16_t* out_alloc;
+    uint8_t* out_cfg;
+    unsigned long long* out_sum;
+    float* out_mean;
+    uint32_t* out_steps;
+    int warps;           // warps per CTA
+    size_t warp_bytes;   // shared bytes per warp
+};
+
+struct WarpState {
+    int* alloc;                  // [J]
+    unsigned long long* cur;     // [V]  Q32 value of each stream now
+    long long* up;               // [J]
+    long long* dn;               // [J]  kInvalid if alloc < D
+    long long* mv;               // [J]  same-stream move with thief j; kInvalid if victim < D
+};
+
+__host__ __device__ inline size_t thief_warp_bytes(int V) {
+    int J = 2 * V;
+    size_t b = sizeof(unsigned long long) * (size_t)V + sizeof(long long) * 3 * (size_t)J +
+               sizeof(int) * (size_t)J;
+    return (b + 15) & ~size_t(15);
+}
+
+__device__ inline WarpState carve(unsigned char* base, int V) {
+    int J = 2 * V;
+    WarpState w;
+    w.cur = reinterpret_cast<unsigned long long*>(base);
+    w.up = reinterpret_cast<long long*>(w.cur + V);
+    w.dn = w.up + J;
+    w.mv = w.dn + J;
+    w.alloc = reinterpret_cast<int*>(w.mv + J);
+    return w;
+}
+
+__device__ __forceinline__ unsigned long long shfl_max_u64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
+        x = y > x ? y : x;
+    }
+    return x;
+}
+
+__device__ __forceinline__ unsigned long long shfl_sum_u64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// key for (delta, job): larger delta first, then smaller job index; 0 = none
+__device__ __forceinline__ unsigned long long dkey(long long delta, int j) {
+    return ((unsigned long long)(delta + kKeyOff) << 16) | (unsigned long long)(0xFFFF - j);
+}
+__device__ __forceinline__ long long key_delta(unsigned long long k) { return (long long)(k >> 16) - kKeyOff; }
+__device__ __forceinline__ int key_job(unsigned long long k) { return 0xFFFF - (int)(k & 0xFFFF); }
+
+struct InstView {
+    const float* stale;     // [V]
+    const float* cost;      // [V][nG]
+    const float* post;
+    const uint16_t* lmu;    // [V][nL]
+    const float* lf;
+};
+
+// Warp-collective: G*(rt') for rt' = rt + D*(k-1), k = 0,1,2 (or -1 if rt' < 0).
+__device__ __forceinline__ void gstar3(const InstView& in, int v, int nG, int rt, int D, float uT,
+                                       float* G) {
+    const int lane = threadIdx.x & 31;
+    const float stale = __ldg(in.stale + v);
+    float cost = 0.0f, post = 0.0f;
+    if (lane >= 1 && lane <= nG) {
+        cost = __ldg(in.cost + (size_t)v * nG + lane - 1);
+        post = __ldg(in.post + (size_t)v * nG + lane - 1);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        int r = rt + D * (k - 1);
+        float g = -1.0f;
+        if (lane == 0) g = stale;
+        else if (lane <= nG) {
+            float w;
+            if (window_acc(stale, post, cost, r, uT, &w)) g = w;
+        }
+        // values are >= 0 or -1: signed-int order of the bit patterns = float order
+        int m = __reduce_max_sync(0xffffffffu, __float_as_int(g));
+        G[k] = r < 0 ? -1.0f : __int_as_float(m);
+    }
+}
+
+// Warp-collective update of stream v's entries in the state arrays.
+__device__ void update_stream(const InstView& in, const WarpState& S, int v, const ekya_dims& d) {
+    const int D = d.steal_units, nG = d.n_gamma, nL = d.n_lambda;
+    const int ri = S.alloc[2 * v], rt = S.alloc[2 * v + 1];
+    float G[3];
+    gstar3(in, v, nG, rt, D, d.unit_gpu_seconds, G);
+    const float stale = __ldg(in.stale + v);
+    const uint16_t* lmu = in.lmu + (size_t)v * nL;
+    const float* lf = in.lf + (size_t)v * nL;
+    float fac[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        int r = ri + D * (k - 1);
+        int l = r < 0 ? -1 : lambda_star(stale, lmu, lf, nL, r, d.a_min);
+        fac[k] = l < 0 ? -1.0f : __ldg(lf + l);
+    }
+    auto val = [&](int a, int b) -> unsigned long long {   // a: rt index, b: ri index
+        if (fac[b] < 0.0f) return 0ULL;
+        return q32(fmul(fac[b], G[a]));
+    };
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long c = val(1, 1);
+        long long cc = (long long)c;
+        S.cur[v] = c;
+        S.up[2 * v] = (long long)val(1, 2) - cc;
+        S.up[2 * v + 1] = (long long)val(2, 1) - cc;
+        S.dn[2 * v] = ri >= D ? (long long)val(1, 0) - cc : kInvalid;
+        S.dn[2 * v + 1] = rt >= D ? (long long)val(0, 1) - cc : kInvalid;
+        // thief = inference (2v), victim = training: (rt - D, ri + D)
+        S.mv[2 * v] = rt >= D ? (long long)val(0, 2) - cc : kInvalid;
+        // thief = training (2v+1), victim = inference: (rt + D, ri - D)
+        S.mv[2 * v + 1] = ri >= D ? (long long)val(2, 0) - cc : kInvalid;
+    }
+    __syncwarp();
+}
+
+// Warp-collective: exact argmax config byte of stream v at its current split.
+__device__ uint8_t stream_cfg(const InstView& in, int v, int ri, int rt, const ekya_dims& d) {
+    const int lane = threadIdx.x & 31, nG = d.n_gamma, nL = d.n_lambda;
+    const float stale = __ldg(in.stale + v);
+    int l = lambda_star(stale, in.lmu + (size_t)v * nL, in.lf + (size_t)v * nL, nL, ri, d.a_min);
+    if (l < 0) return (uint8_t)(kLambdaNone << 5);
+    float fac = __ldg(in.lf + (size_t)v * nL + l);
+    float a = -1.0f;
+    if (lane == 0) a = fmul(fac, stale);
+    else if (lane <= nG) {
+        float w;
+        if (window_acc(stale, __ldg(in.post + (size_t)v * nG + lane - 1),
+                       __ldg(in.cost + (size_t)v * nG + lane - 1), rt, d.unit_gpu_seconds, &w))
+            a = fmul(fac, w);
+    }
+    int m = __reduce_max_sync(0xffffffffu, __float_as_int(a));
+    unsigned hits = __ballot_sync(0xffffffffu, __float_as_int(a) == m);
+    return (uint8_t)((__ffs(hits) - 1) | (l << 5));
+}
+
+__device__ __forceinline__ bool lit_cond(const WarpState& S, int t, int w, int J) {
+    if (w >= J || w == t) return false;
+    if ((w >> 1) == (t >> 1)) return S.mv[t] != kInvalid && S.mv[t] > 0;
+    long long dn = S.dn[w];
+    return dn != kInvalid && S.up[t] + dn > 0;
+}
+
+__global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const ekya_dims& d = p.d;
+    const int V = d.n_streams, J = 2 * V, D = d.steal_units, U = d.units, nG = d.n_gamma,
+              nL = d.n_lambda;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpState S = carve(smem + warp * p.warp_bytes, V);
+    const long long b = (long long)blockIdx.x * p.warps + warp;
+    if (b >= d.n_inst) return;
+
+    InstView in{p.t.stale + b * V, p.t.cost + b * V * nG, p.t.post + b * V * nG,
+                p.t.lam_min_units + b * V * nL, p.t.lam_factor + b * V * nL};
+
+    // ---- validity (R-ERR) ----
+    bool ok = true;
+    for (int i = lane; i < V; i += 32) ok &= in01(__ldg(in.stale + i));
+    for (int i = lane; i < V * nG; i += 32) {
+        float c = __ldg(in.cost + i);
+        if (!(c >= 0.0f)) ok = false;
+        else if (!isinf(c)) ok &= in01(__ldg(in.post + i));
+    }
+    for (int i = lane; i < V * nL; i += 32)
+        if (__ldg(in.lmu + i) != kLmuPad) ok &= in01(__ldg(in.lf + i));
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok) {
+        for (int j = lane; j < J; j += 32) p.out_alloc[b * J + j] = 0;
+        for (int v = lane; v < V; v += 32) p.out_cfg[b * V + v] = 0;
+        if (lane == 0) {
+            p.out_sum[b] = 0;
+            if (p.out_mean) p.out_mean[b] = 0.0f;
+            if (p.out_steps) p.out_steps[b] = 0;
+            flag_data_error(p.st);
+        }
+        return;
+    }
+
+    // ---- fair start (C9) + initial per-stream entries ----
+    for (int v = lane; v < V; v += 32) {
+        int share = U / V + (v < U % V ? 1 : 0);
+        int rt = share / 2;
+        S.alloc[2 * v + 1] = rt;
+        S.alloc[2 * v] = share - rt;
+    }
+    __syncwarp();
+    for (int v = 0; v < V; ++v) update_stream(in, S, v, d);
+
+    unsigned steps = 0;
+    if (p.mode == EKYA_THIEF_STEEPEST) {
+        const unsigned max_steps = 1u << 26;
+        for (;;) {
+            // per-stream best down, top-2 by stream
+            unsigned long long k1 = 0;
+            for (int v = lane; v < V; v += 32) {
+                unsigned long long k = 0;
+                long long d0 = S.dn[2 * v], d1 = S.dn[2 * v + 1];
+                if (d0 != kInvalid) k = dkey(d0, 2 * v);
+                if (d1 != kInvalid) { unsigned long long kk = dkey(d1, 2 * v + 1); k = kk > k ? kk : k; }
+                k1 = k > k1 ? k : k1;
+            }
+            k1 = shfl_max_u64(k1);
+            const int s1 = k1 ? (key_job(k1) >> 1) : -1;
+            unsigned long long k2 = 0;
+            for (int v = lane; v < V; v += 32) {
+                if (v == s1) continue;
+                unsigned long long k = 0;
+                long long d0 = S.dn[2 * v], d1 = S.dn[2 * v + 1];
+                if (d0 != kInvalid) k = dkey(d0, 2 * v);
+                if (d1 != kInvalid) { unsigned long long kk = dkey(d1, 2 * v + 1); k = kk > k ? kk : k; }
+                k2 = k > k2 ? k : k2;
+            }
+            k2 = shfl_max_u64(k2);
+            // per thief: best victim, then argmax over thieves
+            unsigned long long bestkey = 0;
+            int bestw = -1;
+            for (int t = lane; t < J; t += 32) {
+                unsigned long long ck = ((t >> 1) != s1) ? k1 : k2;
+                bool have = false;
+                long long tot = 0;
+                int w = -1;
+                if (ck) {
+                    tot = S.up[t] + key_delta(ck);
+                    w = key_job(ck);
+                    have = true;
+                }
+                long long m = S.mv[t];
+                if (m != kInvalid) {
+                    int ws = t ^ 1;
+                    if (!have || m > tot || (m == tot && ws < w)) {
+                        tot = m;
+                        w = ws;
+                        have = true;
+                    }
+                }
+                if (have) {
+                    unsigned long long tk = dkey(tot, t);
+                    if (tk > bestkey) {
+                        bestkey = tk;
+                        bestw = w;
+                    }
+                }
+            }
+            unsigned long long gk = shfl_max_u64(bestkey);
+            if (gk == 0 || key_delta(gk) <= 0) break;
+            const int t = key_job(gk);
+            unsigned owner = __ballot_sync(0xffffffffu, bestkey == gk);
+            const int w = __shfl_sync(0xffffffffu, bestw, __ffs(owner) - 1);
+            if (lane == 0) {
+                S.alloc[w] -= D;
+                S.alloc[t] += D;
+            }
+            __syncwarp();
+            update_stream(in, S, t >> 1, d);
+            if ((w >> 1) != (t >> 1)) update_stream(in, S, w >> 1, d);
+            if (++steps >= max_steps) {
+                if (lane == 0) flag_data_error(p.st);
+                break;
+            }
+        }
+    } else {
+        for (int t = 0; t < J; ++t) {
+            int pos = 0;
+            while (pos < J) {
+                unsigned m = __ballot_sync(0xffffffffu, lit_cond(S, t, pos + lane, J));
+                if (!m) {
+                    pos += 32;
+                    continue;
+                }
+                const int w = pos + __ffs(m) - 1;
+                do {
+                    if (lane == 0) {
+                        S.alloc[w] -= D;
+                        S.alloc[t] += D;
+                    }
+                    __syncwarp();
+                    update_stream(in, S, t >> 1, d);
+                    if ((w >> 1) != (t >> 1)) update_stream(in, S, w >> 1, d);
+                    ++steps;
+                } while (lit_cond(S, t, w, J));
+                pos = w + 1;
+            }
+        }
+    }
+
+    // ---- decision output (A6) ----
+    unsigned long long part = 0;
+    for (int v = lane; v < V; v += 32) part += S.cur[v];
+    const unsigned long long sum = shfl_sum_u64(part);
+    for (int j = lane; j < J; j += 32) p.out_alloc[b * J + j] = (uint16_t)S.alloc[j];
+    for (int v = 0; v < V; ++v) {
+        uint8_t c = stream_cfg(in, v, S.alloc[2 * v], S.alloc[2 * v + 1], d);
+        if (lane == 0) p.out_cfg[b * V + v] = c;
+    }
+    if (lane == 0) {
+        p.out_sum[b] = sum;
+        if (p.out_mean) p.out_mean[b] = mean_q32(sum, V);
+        if (p.out_steps) p.out_steps[b] = steps;
+    }
+}
+
+}  // namespace
+
+int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int mode,
+                 uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum, float* out_mean,
+                 uint32_t* out_steps, cudaStream_t s) {
+    if (d.n_streams > 1024) return EKYA_ERR_SHAPE;
+    ThiefParams p{};
+    p.d = d;
+    p.t = t;
+    p.st = h->dstate;
+    p.mode = mode;
+    p.out_alloc = out_alloc;
+    p.out_cfg = out_cfg;
+    p.out_sum = reinterpret_cast<unsigned long long*>(out_sum);
+    p.out_mean = out_mean;
+    p.out_steps = out_steps;
+    p.warps = kThiefThreads / 32;
+    p.warp_bytes = thief_warp_bytes(d.n_streams);
+    size_t smem = p.warp_bytes * p.warps;
+    if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
+    if (d.n_inst == 0) return EKYA_OK;
+    cudaError_t e = cudaFuncSetAttribute(thief_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return EKYA_ERR_CUDA;
+    long long grid = (d.n_inst + p.warps - 1) / p.warps;
+    if (grid > 0x7fffffffLL) return EKYA_ERR_SHAPE;
+    thief_kernel<<<(unsigned)grid, kThiefThreads, smem, s>>>(p);
+    h->launches++;
+    return cuda_status(cudaGetLastError());
+}
+
+}  // namespace ekya

@@ -1,0 +1,292 @@
+"""Thin Python binding of libekya (include/ekya.h): argument marshalling only.
+
+Every function forwards torch tensors' device pointers and the current CUDA
+stream to the C ABI of the same name; every step of the hot path runs in the
+sm_100a kernels of ``libekya.so``.  There is no CPU fallback: if the library is
+missing or a tensor is not a contiguous CUDA tensor of the documented dtype,
+this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libekya.so")
+
+EKYA_OK = 0
+ERRORS = {-1: "EKYA_ERR_ARG", -2: "EKYA_ERR_LIMIT", -3: "EKYA_ERR_SHAPE", -4: "EKYA_ERR_CUDA",
+          -5: "EKYA_ERR_NCCL", -6: "EKYA_ERR_DATA"}
+EVAL_LIST, EVAL_GRID = 0, 1
+THIEF_STEEPEST, THIEF_LITERAL = 0, 1
+PROFILE_RADIUS, PROFILE_CLUSTER = 0, 1
+LAMBDA_NONE = 7
+SYMBOLS = ["ekya_create", "ekya_destroy", "ekya_last_error", "ekya_launch_count", "ekya_version",
+           "ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate",
+           "ekya_comm_unique_id", "ekya_comm_init", "ekya_gather_decisions"]
+
+
+class EkyaError(RuntimeError):
+    def __init__(self, code, what):
+        super().__init__(f"{what} failed: {ERRORS.get(code, code)}")
+        self.code = code
+
+
+class Dims(ctypes.Structure):
+    """ekya_dims (include/ekya.h)."""
+    _fields_ = [("n_inst", ctypes.c_int32), ("n_streams", ctypes.c_int32),
+                ("n_gamma", ctypes.c_int32), ("n_lambda", ctypes.c_int32),
+                ("units", ctypes.c_int32), ("steal_units", ctypes.c_int32),
+                ("unit_gpu_seconds", ctypes.c_float), ("a_min", ctypes.c_float)]
+
+
+class Tables(ctypes.Structure):
+    """ekya_tables: device pointers."""
+    _fields_ = [("stale", ctypes.c_void_p), ("cost", ctypes.c_void_p), ("post", ctypes.c_void_p),
+                ("lam_min_units", ctypes.c_void_p), ("lam_factor", ctypes.c_void_p)]
+
+
+class ProfileDims(ctypes.Structure):
+    _fields_ = [("n_query", ctypes.c_int32), ("n_hist", ctypes.c_int32),
+                ("n_class", ctypes.c_int32), ("n_gamma", ctypes.c_int32),
+                ("mode", ctypes.c_int32), ("tau", ctypes.c_float),
+                ("k", ctypes.c_int32), ("max_iter", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libekya.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libekya.so not built at {path}; run __graft_entry__.build()")
+    L = ctypes.CDLL(path)
+    P, I32, U64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64
+    L.ekya_create.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_size_t]
+    L.ekya_create.restype = ctypes.c_int
+    L.ekya_destroy.argtypes = [P]
+    L.ekya_destroy.restype = None
+    L.ekya_last_error.argtypes = [P]
+    L.ekya_last_error.restype = ctypes.c_int
+    L.ekya_launch_count.argtypes = [P]
+    L.ekya_launch_count.restype = U64
+    L.ekya_version.argtypes = []
+    L.ekya_version.restype = ctypes.c_char_p
+    L.ekya_eval_allocations.argtypes = [P, ctypes.POINTER(Dims), ctypes.POINTER(Tables), ctypes.c_int,
+                                        I32, P, P, P, P, P, P, P]
+    L.ekya_eval_allocations.restype = ctypes.c_int
+    L.ekya_thief_schedule.argtypes = [P, ctypes.POINTER(Dims), ctypes.POINTER(Tables), ctypes.c_int,
+                                      P, P, P, P, P, P]
+    L.ekya_thief_schedule.restype = ctypes.c_int
+    L.ekya_profile_estimate.argtypes = [P, ctypes.POINTER(ProfileDims), P, P, P, P, P, P, P, P]
+    L.ekya_profile_estimate.restype = ctypes.c_int
+    L.ekya_comm_unique_id.argtypes = [P]
+    L.ekya_comm_unique_id.restype = ctypes.c_int
+    L.ekya_comm_init.argtypes = [P, P, ctypes.c_int, ctypes.c_int]
+    L.ekya_comm_init.restype = ctypes.c_int
+    L.ekya_gather_decisions.argtypes = [P, P, ctypes.c_size_t, P, ctypes.c_int, P]
+    L.ekya_gather_decisions.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(code, what):
+    if code != EKYA_OK:
+        raise EkyaError(code, what)
+
+
+def _ptr(t, dtype, name, optional=False):
+    if t is None:
+        if optional:
+            return None
+        raise ValueError(f"{name} is required")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr()) if t.numel() else None
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Handle:
+    """Owns an ekya_handle (device error word + launch counter + optional NCCL comm)."""
+
+    def __init__(self, device: int | None = None):
+        L = load_library()
+        dev = torch.cuda.current_device() if device is None else int(device)
+        self.device = dev
+        h = ctypes.c_void_p()
+        _check(L.ekya_create(ctypes.byref(h), dev, 0), "ekya_create")
+        self._h = h
+
+    @property
+    def ptr(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            load_library().ekya_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def last_error(self) -> int:
+        return load_library().ekya_last_error(self._h)
+
+    def launch_count(self) -> int:
+        return int(load_library().ekya_launch_count(self._h))
+
+
+def make_dims(n_inst, n_streams, n_gamma, n_lambda, units, steal_units, unit_gpu_seconds, a_min):
+    return Dims(n_inst, n_streams, n_gamma, n_lambda, units, steal_units, unit_gpu_seconds, a_min)
+
+
+def make_tables(stale, cost, post, lam_min_units, lam_factor):
+    """Device tables; keep the tensors alive while the returned struct is in use."""
+    return Tables(_ptr(stale, torch.float32, "stale"), _ptr(cost, torch.float32, "cost", True),
+                  _ptr(post, torch.float32, "post", True),
+                  _ptr(lam_min_units, torch.uint16, "lam_min_units"),
+                  _ptr(lam_factor, torch.float32, "lam_factor"))
+
+
+def dims_from(tables: dict, units, steal_units, unit_gpu_seconds, a_min):
+    B, V = tables["stale"].shape
+    return make_dims(B, V, tables["cost"].shape[2], tables["lam_factor"].shape[2], units, steal_units,
+                     unit_gpu_seconds, a_min)
+
+
+# ---------------------------------------------------------------------------
+# C-ABI entry points (same names)
+# ---------------------------------------------------------------------------
+def ekya_eval_allocations(h: Handle, dims: Dims, tables: Tables, mode: int, n_alloc=0, alloc=None,
+                          out_sum_q32=None, out_mean=None, out_cfg=None, out_grid=None,
+                          out_grid_cfg=None, stream=None):
+    L = load_library()
+    code = L.ekya_eval_allocations(
+        h.ptr, ctypes.byref(dims), ctypes.byref(tables), mode, n_alloc,
+        _ptr(alloc, torch.uint16, "alloc", True), _ptr(out_sum_q32, torch.uint64, "out_sum_q32", True),
+        _ptr(out_mean, torch.float32, "out_mean", True), _ptr(out_cfg, torch.uint8, "out_cfg", True),
+        _ptr(out_grid, torch.float32, "out_grid", True),
+        _ptr(out_grid_cfg, torch.uint8, "out_grid_cfg", True), _stream(stream))
+    _check(code, "ekya_eval_allocations")
+
+
+def ekya_thief_schedule(h: Handle, dims: Dims, tables: Tables, mode: int, out_alloc, out_cfg,
+                        out_sum_q32, out_mean=None, out_steps=None, stream=None):
+    L = load_library()
+    code = L.ekya_thief_schedule(h.ptr, ctypes.byref(dims), ctypes.byref(tables), mode,
+                                 _ptr(out_alloc, torch.uint16, "out_alloc"),
+                                 _ptr(out_cfg, torch.uint8, "out_cfg"),
+                                 _ptr(out_sum_q32, torch.uint64, "out_sum_q32"),
+                                 _ptr(out_mean, torch.float32, "out_mean", True),
+                                 _ptr(out_steps, torch.uint32, "out_steps", True), _stream(stream))
+    _check(code, "ekya_thief_schedule")
+
+
+def ekya_profile_estimate(h: Handle, pdims: ProfileDims, cur, hist, hist_acc, fallback, out_est,
+                          out_n, out_cluster=None, stream=None):
+    L = load_library()
+    code = L.ekya_profile_estimate(h.ptr, ctypes.byref(pdims), _ptr(cur, torch.float32, "cur"),
+                                   _ptr(hist, torch.float32, "hist", True),
+                                   _ptr(hist_acc, torch.float32, "hist_acc", True),
+                                   _ptr(fallback, torch.float32, "fallback"),
+                                   _ptr(out_est, torch.float32, "out_est"),
+                                   _ptr(out_n, torch.int32, "out_n"),
+                                   _ptr(out_cluster, torch.int32, "out_cluster", True), _stream(stream))
+    _check(code, "ekya_profile_estimate")
+
+
+def ekya_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().ekya_comm_unique_id(buf), "ekya_comm_unique_id")
+    return buf.raw
+
+
+def ekya_comm_init(h: Handle, uid: bytes, nranks: int, rank: int):
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(load_library().ekya_comm_init(h.ptr, buf, nranks, rank), "ekya_comm_init")
+
+
+def ekya_gather_decisions(h: Handle, local, root_buf, root=0, stream=None):
+    if not local.is_cuda or not local.is_contiguous():
+        raise ValueError("local must be a contiguous CUDA tensor")
+    rb = None
+    if root_buf is not None:
+        if not root_buf.is_cuda or not root_buf.is_contiguous():
+            raise ValueError("root_buf must be a contiguous CUDA tensor")
+        rb = ctypes.c_void_p(root_buf.data_ptr())
+    nbytes = local.numel() * local.element_size()
+    _check(load_library().ekya_gather_decisions(h.ptr, ctypes.c_void_p(local.data_ptr()), nbytes, rb,
+                                                root, _stream(stream)), "ekya_gather_decisions")
+
+
+# ---------------------------------------------------------------------------
+# convenience wrappers that allocate outputs (still marshalling only)
+# ---------------------------------------------------------------------------
+def n_cells(units: int) -> int:
+    return (units + 1) * (units + 2) // 2
+
+
+def eval_grid(h, tables: dict, units, steal_units, unit_gpu_seconds, a_min, with_cfg=True, stream=None):
+    dims = dims_from(tables, units, steal_units, unit_gpu_seconds, a_min)
+    B, V = dims.n_inst, dims.n_streams
+    dev = tables["stale"].device
+    grid = torch.empty((B, V, n_cells(units)), dtype=torch.float32, device=dev)
+    gcfg = torch.empty((B, V, n_cells(units)), dtype=torch.uint8, device=dev) if with_cfg else None
+    ekya_eval_allocations(h, dims, make_tables(**tables), EVAL_GRID, out_grid=grid, out_grid_cfg=gcfg,
+                          stream=stream)
+    return grid, gcfg
+
+
+def eval_list(h, tables: dict, alloc, units, steal_units, unit_gpu_seconds, a_min, stream=None):
+    dims = dims_from(tables, units, steal_units, unit_gpu_seconds, a_min)
+    B, N, V = alloc.shape[0], alloc.shape[1], dims.n_streams
+    dev = alloc.device
+    s = torch.empty((B, N), dtype=torch.uint64, device=dev)
+    mean = torch.empty((B, N), dtype=torch.float32, device=dev)
+    cfg = torch.empty((B, N, V), dtype=torch.uint8, device=dev)
+    ekya_eval_allocations(h, dims, make_tables(**tables), EVAL_LIST, N, alloc, s, mean, cfg,
+                          stream=stream)
+    return s, mean, cfg
+
+
+def thief_schedule(h, tables: dict, units, steal_units, unit_gpu_seconds, a_min, mode=THIEF_STEEPEST,
+                   stream=None):
+    dims = dims_from(tables, units, steal_units, unit_gpu_seconds, a_min)
+    B, V = dims.n_inst, dims.n_streams
+    dev = tables["stale"].device
+    alloc = torch.empty((B, 2 * V), dtype=torch.uint16, device=dev)
+    cfg = torch.empty((B, V), dtype=torch.uint8, device=dev)
+    s = torch.empty(B, dtype=torch.uint64, device=dev)
+    mean = torch.empty(B, dtype=torch.float32, device=dev)
+    steps = torch.empty(B, dtype=torch.uint32, device=dev)
+    ekya_thief_schedule(h, dims, make_tables(**tables), mode, alloc, cfg, s, mean, steps, stream=stream)
+    return alloc, cfg, s, mean, steps
+
+
+def profile_estimate(h, cur, hist, hist_acc, fallback, mode=PROFILE_RADIUS, tau=0.2, k=5, max_iter=100,
+                     with_cluster=False, stream=None):
+    Q, C = cur.shape
+    H = hist.shape[1]
+    G = fallback.shape[1]
+    pd = ProfileDims(Q, H, C, G, mode, tau, k, max_iter)
+    est = torch.empty((Q, G), dtype=torch.float32, device=cur.device)
+    n = torch.empty((Q, G), dtype=torch.int32, device=cur.device)
+    cl = torch.empty((Q, H + 1), dtype=torch.int32, device=cur.device) if with_cluster else None
+    ekya_profile_estimate(h, pd, cur, hist, hist_acc, fallback, est, n, cl, stream=stream)
+    return est, n, cl

@@ -1,0 +1,91 @@
+"""CPU-side checks of the C ABI boundary (-m "not gpu"): the library builds, loads,
+exports every symbol include/ekya.h declares, and rejects bad arguments
+synchronously without touching a device."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ekya.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2012_10557_b200 import build
+    build.build()
+    from paper_2012_10557_b200 import ekya
+    return ekya.load_library()
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ekya_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("ekya_profile_estimate", "ekya_eval_allocations", "ekya_thief_schedule",
+              "ekya_comm_init", "ekya_gather_decisions"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2012_10557_b200 import ekya
+    out = subprocess.run(["nm", "-D", "--defined-only", ekya.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(ekya_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    assert set(ekya.SYMBOLS) <= exported
+    for s in declared_symbols():
+        assert hasattr(lib, s)
+
+
+def test_library_is_sm100a(lib):
+    from paper_2012_10557_b200 import ekya
+    out = subprocess.run(["cuobjdump", "--list-elf", ekya.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_null_handle_rejected(lib):
+    from paper_2012_10557_b200 import ekya
+    assert b"sm_100a" in lib.ekya_version()
+    d = ekya.make_dims(1, 1, 0, 1, 4, 1, 10.0, 0.0)
+    t = ekya.Tables()
+    assert lib.ekya_eval_allocations(None, ctypes.byref(d), ctypes.byref(t), 0, 0, None, None, None,
+                                     None, None, None, None) == -1
+    assert lib.ekya_thief_schedule(None, ctypes.byref(d), ctypes.byref(t), 0, None, None, None, None,
+                                   None, None) == -1
+    assert lib.ekya_profile_estimate(None, None, None, None, None, None, None, None, None, None) == -1
+    assert lib.ekya_launch_count(None) == 0
+    assert lib.ekya_gather_decisions(None, None, 0, None, 0, None) == -1
+
+
+def test_binding_refuses_cpu_tensors():
+    import torch
+    from paper_2012_10557_b200 import ekya
+    with pytest.raises(ValueError):
+        ekya._ptr(torch.zeros(3), torch.float32, "x")
+
+
+def test_product_does_not_import_oracle():
+    import ast
+    pkg = os.path.join(ROOT, "paper_2012_10557_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                tree = ast.parse(open(os.path.join(dirpath, f)).read())
+                for node in ast.walk(tree):
+                    if isinstance(node, ast.Import):
+                        assert not any(a.name.split(".")[0] == "oracle" for a in node.names), f
+                    if isinstance(node, ast.ImportFrom) and node.module:
+                        assert node.module.split(".")[0] != "oracle", f
+            if f.endswith((".cu", ".cuh", ".h")):
+                for line in open(os.path.join(dirpath, f)):
+                    assert not (line.lstrip().startswith("#include") and "oracle" in line), f

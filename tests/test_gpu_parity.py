@@ -1,0 +1,319 @@
+"""GPU parity tests (-m gpu): the CUDA path through the C ABI vs the CPU oracle on
+the same seeded inputs.
+
+Bar (BASELINE.json north star): integer units, configs and exact Q32 objective
+sums bit-exact; fp32 outputs (values, means, estimates) bit-exact as well,
+because both sides follow the same one-rounding-per-operation contract
+ -- strictly tighter than the north star's 1e-5 relative.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def h():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2012_10557_b200 import build
+    build.build()
+    from paper_2012_10557_b200 import ekya
+    return ekya.Handle(0)
+
+
+def ek():
+    from paper_2012_10557_b200 import ekya
+    return ekya
+
+
+def tables(cfg, lo=0, hi=None):
+    T = synth.sched_tables(cfg, lo, hi)
+    inst = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            cfg.units, cfg.steal_units, cfg.unit_gpu_seconds, cfg.a_min)
+    return {k: v.cuda() for k, v in T.items()}, inst
+
+
+def args(cfg):
+    return (cfg.units, cfg.steal_units, cfg.unit_gpu_seconds, cfg.a_min)
+
+
+def variant(cfg, **kw):
+    return synth.SchedConfig(**{**cfg.__dict__, **kw})
+
+
+SCHED_CASES = [
+    ("c1", variant(synth.CONFIG1, n_inst=300)),
+    ("c2", variant(synth.CONFIG2, n_inst=48)),
+    ("c2-ragged", variant(synth.CONFIG2, n_inst=48, ragged=True)),
+    ("c2-steal3", variant(synth.CONFIG2, n_inst=16, steal_units=3)),
+    ("v1", variant(synth.CONFIG2, n_inst=16, n_streams=1, units=8)),
+    ("nogamma", variant(synth.CONFIG2, n_inst=16, n_gamma=0)),
+    ("u1", variant(synth.CONFIG1, n_inst=32, units=1)),
+    ("odd", variant(synth.CONFIG2, n_inst=37, n_streams=7, n_gamma=31, n_lambda=5, units=53, a_min=0.0)),
+]
+
+
+_SIGNED = {torch.uint16: torch.int16, torch.uint32: torch.int32, torch.uint64: torch.int64}
+
+
+def pick(t, idx):
+    """t[idx] for any dtype (unsigned types are indexed through a signed view)."""
+    if t.dtype in _SIGNED:
+        return t.view(_SIGNED[t.dtype])[idx].view(t.dtype)
+    return t[idx]
+
+
+def assert_eq(a, b, what):
+    a = a.cpu().numpy() if torch.is_tensor(a) else a
+    assert a.shape == b.shape, (what, a.shape, b.shape)
+    if not np.array_equal(a, b):
+        bad = np.argwhere(a != b)
+        raise AssertionError(f"{what}: {len(bad)} mismatches, first at {bad[:5].tolist()}: "
+                             f"{a[tuple(bad[0])]} vs {b[tuple(bad[0])]}")
+
+
+@pytest.mark.parametrize("name,cfg", SCHED_CASES, ids=[c[0] for c in SCHED_CASES])
+def test_grid_bitexact(h, name, cfg):
+    Td, inst = tables(cfg)
+    grid, gcfg = ek().eval_grid(h, Td, *args(cfg))
+    og, ocfg, bad = oracle.eval_grid(inst)
+    assert bad == 0 and h.last_error() == 0
+    assert_eq(grid, og, "grid values")
+    assert_eq(gcfg, ocfg, "grid configs")
+
+
+@pytest.mark.parametrize("name,cfg", SCHED_CASES, ids=[c[0] for c in SCHED_CASES])
+def test_list_bitexact(h, name, cfg):
+    Td, inst = tables(cfg)
+    rows = synth.list_allocs(cfg, 300)
+    s, mean, cfg_ = ek().eval_list(h, Td, rows.cuda(), *args(cfg))
+    os_, om, ocf, bad = oracle.eval_list(inst, rows.numpy())
+    assert bad == 0 and h.last_error() == 0
+    assert_eq(s, os_, "sum_q32")
+    assert_eq(mean, om, "mean")
+    assert_eq(cfg_, ocf, "cfg")
+
+
+def test_list_over_all_allocations_equals_bruteforce(h):
+    """Eq. 1 on config 1: LIST over every allocation with sum <= U, argmax on the host,
+    equals the oracle's brute force (value and lexicographically smallest allocation)."""
+    import itertools
+    cfg = variant(synth.CONFIG1, n_inst=64)
+    Td, inst = tables(cfg)
+    J, U = 4, cfg.units
+    comps = np.array([c for c in itertools.product(range(U + 1), repeat=J) if sum(c) <= U], np.uint16)
+    rows = torch.from_numpy(np.broadcast_to(comps, (cfg.n_inst,) + comps.shape).copy())
+    s, mean, _ = ek().eval_list(h, Td, rows.cuda(), *args(cfg))
+    s = s.cpu().numpy()
+    ba, bc, bs, _ = oracle.bruteforce(inst)
+    for b in range(cfg.n_inst):
+        best = s[b].max()
+        assert best == bs[b]
+        first = np.flatnonzero(s[b] == best)[0]      # comps are in lexicographic order
+        assert list(comps[first]) == list(ba[b])
+
+
+def test_list_invalid_rows_and_data_errors(h):
+    cfg = variant(synth.CONFIG2, n_inst=4)
+    T = synth.sched_tables(cfg)
+    T["cost"][3, 2, 5] = float("nan")                 # instance 3 invalid
+    inst = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            *args(cfg))
+    Td = {k: v.cuda() for k, v in T.items()}
+    rows = synth.list_allocs(cfg, 40)
+    rows[0, 3, 4] = cfg.units + 1                      # entry > U
+    rows[1, 7, 0] += 3                                 # sum > U
+    s, mean, c = ek().eval_list(h, Td, rows.cuda(), *args(cfg))
+    assert h.last_error() == -6
+    os_, om, ocf, bad = oracle.eval_list(inst, rows.numpy())
+    assert bad == 2 + 40
+    assert_eq(s, os_, "sum_q32")
+    assert_eq(mean, om, "mean")
+    assert_eq(c, ocf, "cfg")
+    s, mean, c = ek().eval_list(h, Td, rows.cuda(), *args(cfg))
+    assert h.last_error() == -6                        # EKYA_ERR_DATA, then cleared
+    assert h.last_error() == 0
+
+
+@pytest.mark.parametrize("mode", [0, 1], ids=["steepest", "literal"])
+@pytest.mark.parametrize("name,cfg", SCHED_CASES, ids=[c[0] for c in SCHED_CASES])
+def test_thief_bitexact(h, name, cfg, mode):
+    Td, inst = tables(cfg)
+    a, c, s, m, st = ek().thief_schedule(h, Td, *args(cfg), mode=mode)
+    oa, oc, osum, omean, osteps, bad = oracle.thief(inst, mode)
+    assert bad == 0 and h.last_error() == 0
+    assert_eq(a, oa, "alloc")
+    assert_eq(s, osum, "sum_q32")
+    assert_eq(m, omean, "mean")
+    assert_eq(c, oc, "cfg")
+    assert_eq(st, osteps, "steps")
+    assert (a.cpu().numpy().astype(np.int64).sum(1) == cfg.units).all()
+
+
+def test_thief_invalid_instance_zeroed(h):
+    cfg = variant(synth.CONFIG2, n_inst=6)
+    T = synth.sched_tables(cfg)
+    T["stale"][2, 1] = 1.5
+    T["lam_factor"][4, 0, 0] = -0.1
+    inst = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            *args(cfg))
+    Td = {k: v.cuda() for k, v in T.items()}
+    a, c, s, m, st = ek().thief_schedule(h, Td, *args(cfg))
+    oa, oc, osum, omean, osteps, bad = oracle.thief(inst, 0)
+    assert bad == 2 and h.last_error() == -6
+    assert_eq(a, oa, "alloc")
+    assert_eq(s, osum, "sum")
+
+
+def test_thief_scaleout_shape(h):
+    """Config 5 shape (V=100, U=800): LITERAL on 3 instances, STEEPEST on 1."""
+    cfg = variant(synth.CONFIG5, n_inst=3)
+    Td, inst = tables(cfg)
+    a, c, s, m, st = ek().thief_schedule(h, Td, *args(cfg), mode=1)
+    oa, oc, osum, omean, osteps, _ = oracle.thief(inst, 1)
+    assert_eq(a, oa, "literal alloc")
+    assert_eq(s, osum, "literal sum")
+    assert_eq(c, oc, "literal cfg")
+    Td1 = {k: v[:1].contiguous() for k, v in Td.items()}
+    a, c, s, m, st = ek().thief_schedule(h, Td1, *args(cfg), mode=0)
+    oa, oc, osum, omean, osteps, _ = oracle.thief(inst.subset([0]), 0)
+    assert_eq(a, oa, "steepest alloc")
+    assert_eq(s, osum, "steepest sum")
+    assert_eq(st, osteps, "steepest steps")
+
+
+def test_empty_batch(h):
+    cfg = variant(synth.CONFIG2, n_inst=0)
+    Td, inst = tables(cfg)
+    a, c, s, m, st = ek().thief_schedule(h, Td, *args(cfg))
+    assert a.shape == (0, 20)
+    grid, _ = ek().eval_grid(h, Td, *args(cfg))
+    assert grid.numel() == 0
+
+
+def test_limits_rejected_synchronously(h):
+    cfg = variant(synth.CONFIG2, n_inst=2)
+    Td, _ = tables(cfg)
+    e = ek()
+    with pytest.raises(e.EkyaError) as ex:
+        e.thief_schedule(h, Td, 65535, 1, 20.0, 0.4)
+    assert ex.value.code == -2
+    with pytest.raises(e.EkyaError):
+        e.thief_schedule(h, Td, 80, 0, 20.0, 0.4)
+
+
+# ---------------------------------------------------------------------------
+# profiler
+# ---------------------------------------------------------------------------
+PROF_CASES = [
+    ("dense", synth.ProfileConfig("p", 96, 500, 27, 18)),
+    ("sparse", synth.ProfileConfig("p", 96, 500, 27, 18, sparse=True)),
+    ("ragged", synth.ProfileConfig("p", 33, 137, 5, 3)),
+    ("nohist", synth.ProfileConfig("p", 8, 0, 27, 18)),
+    ("big-h", synth.ProfileConfig("p", 6, 1500, 27, 18)),
+]
+
+
+@pytest.mark.parametrize("mode", [0, 1], ids=["radius", "cluster"])
+@pytest.mark.parametrize("name,pc", PROF_CASES, ids=[c[0] for c in PROF_CASES])
+def test_profile_bitexact(h, name, pc, mode):
+    P = synth.profile_inputs(pc)
+    Pd = {k: v.cuda() for k, v in P.items()}
+    est, n, cl = ek().profile_estimate(h, Pd["cur"], Pd["hist"], Pd["hist_acc"], Pd["fallback"], mode=mode,
+                                       with_cluster=True)
+    oe, on, ocl, bad = oracle.profile(P["cur"].numpy(), P["hist"].numpy(), P["hist_acc"].numpy(),
+                                      P["fallback"].numpy(), mode=mode)
+    assert bad == 0 and h.last_error() == 0
+    assert_eq(n, on, "n_similar")
+    assert_eq(est, oe, "estimate")
+    if mode == 1:
+        assert_eq(cl, ocl, "clusters")
+
+
+def test_profile_invalid_query(h):
+    pc = synth.ProfileConfig("p", 5, 50, 27, 18)
+    P = synth.profile_inputs(pc)
+    P["hist"][2, 7, 3] = -0.5
+    P["hist_acc"][4, 1, 1] = 2.0
+    Pd = {k: v.cuda() for k, v in P.items()}
+    for mode in (0, 1):
+        est, n, _ = ek().profile_estimate(h, Pd["cur"], Pd["hist"], Pd["hist_acc"], Pd["fallback"], mode=mode)
+        oe, on, _, bad = oracle.profile(*(P[k].numpy() for k in ("cur", "hist", "hist_acc", "fallback")),
+                                        mode=mode)
+        assert bad == 2 and h.last_error() == -6
+        assert_eq(est, oe, "estimate")
+        assert_eq(n, on, "n")
+
+
+def test_profile_output_feeds_thief_tables(h):
+    """With q = b*V + v, out_est is the post table of a batch (ABI contract)."""
+    cfg = variant(synth.CONFIG2, n_inst=8)
+    Td, inst = tables(cfg)
+    pc = synth.ProfileConfig("p", cfg.n_inst * cfg.n_streams, 200, 27, cfg.n_gamma)
+    P = {k: v.cuda() for k, v in synth.profile_inputs(pc).items()}
+    est, n, _ = ek().profile_estimate(h, P["cur"], P["hist"], P["hist_acc"], P["fallback"])
+    Td["post"] = est.view(cfg.n_inst, cfg.n_streams, cfg.n_gamma).contiguous()
+    a, c, s, m, st = ek().thief_schedule(h, Td, *args(cfg))
+    inst2 = oracle.Instances(inst.stale, inst.cost, Td["post"].cpu().numpy(), inst.lam_min_units,
+                             inst.lam_factor, *args(cfg))
+    oa, oc, osum, *_ = oracle.thief(inst2, 0)
+    assert_eq(a, oa, "alloc")
+    assert_eq(s, osum, "sum")
+
+
+# ---------------------------------------------------------------------------
+# full BASELINE sizes, in the launch configuration bench.py times, sampled
+# ---------------------------------------------------------------------------
+def test_config4_full_batch_sampled(h):
+    cfg = synth.CONFIG4
+    Td = synth.sched_tables(cfg, device="cuda")
+    e = ek()
+    a, c, s, m, st = e.thief_schedule(h, Td, *args(cfg), mode=0)
+    grid, gcfg = e.eval_grid(h, Td, *args(cfg))
+    rows = synth.list_allocs(cfg, 256, 0, cfg.n_inst, device="cuda")
+    ls, lm, lc = e.eval_list(h, Td, rows, *args(cfg))
+    assert h.last_error() == 0
+    assert (a.cpu().numpy().astype(np.int64).sum(1) == cfg.units).all()
+    sample = [0, 1, 4095, 31337, 65535] + list(np.random.default_rng(7).integers(0, cfg.n_inst, 11))
+    Tc = synth.sched_tables(cfg)              # CPU generation of the same instances
+    for k in Tc:
+        assert torch.equal(pick(Tc[k], sample), pick(Td[k], sample).cpu()), f"device/host generator mismatch: {k}"
+    inst = oracle.Instances(*(pick(Tc[k], sample).numpy() for k in ("stale", "cost", "post", "lam_min_units",
+                                                              "lam_factor")), *args(cfg))
+    oa, oc, osum, omean, osteps, _ = oracle.thief(inst, 0)
+    assert_eq(pick(a, sample), oa, "alloc")
+    assert_eq(pick(s, sample), osum, "sum")
+    assert_eq(pick(c, sample), oc, "cfg")
+    og, ocfg, _ = oracle.eval_grid(inst)
+    assert_eq(pick(grid, sample), og, "grid")
+    assert_eq(pick(gcfg, sample), ocfg, "grid cfg")
+    os_, om, ocf, _ = oracle.eval_list(inst, pick(rows, sample).cpu().numpy())
+    assert_eq(pick(ls, sample), os_, "list sum")
+    assert_eq(pick(lc, sample), ocf, "list cfg")
+
+
+def test_config3_full_batch_sampled(h):
+    pc = synth.CONFIG3
+    e = ek()
+    for mode in (0, 1):
+        P = synth.profile_inputs(pc, device="cuda")
+        est, n, cl = e.profile_estimate(h, P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=mode,
+                                        with_cluster=(mode == 1))
+        assert h.last_error() == 0
+        sample = [0, 1, 65535] + list(np.random.default_rng(8).integers(0, pc.n_query, 9))
+        del P
+        for q in sample:
+            Pc = synth.profile_inputs(pc, q, q + 1)
+            oe, on, ocl, _ = oracle.profile(*(Pc[k].numpy() for k in ("cur", "hist", "hist_acc", "fallback")),
+                                            mode=mode)
+            assert_eq(est[q:q + 1], oe, f"est q={q}")
+            assert_eq(n[q:q + 1], on, f"n q={q}")
+            if mode == 1:
+                assert_eq(cl[q:q + 1], ocl, f"cluster q={q}")
