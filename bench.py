@@ -1,0 +1,506 @@
+#!/usr/bin/env python
+"""bench.py -- Ekya thief-scheduler hot path on B200 (driver contract: one JSON line).
+
+A step = one pass of the whole hot path over one batch:
+  A1  ekya_profile_estimate on config 3 (65,536 Waymo-shaped queries, C=27,
+      H=500, |Gamma|=18) in CLUSTER mode (BASELINE config 3: "5-cluster
+      similarity estimate") and RADIUS mode (north star: distance threshold);
+  A3  ekya_eval_allocations GRID and LIST (4,096 allocations per instance) on
+      config 4 (65,536 Cityscapes-shaped 10-stream instances, |Gamma|=18,
+      |Lambda|=5, U=80);
+  A4-A6 ekya_thief_schedule STEEPEST and LITERAL on config 4.
+Metric (BASELINE.json): scheduler allocations evaluated per second, where one
+allocation = one (instance, stream, r_train, r_infer) split reduced over
+Gamma x Lambda: GRID cells + LIST rows x V.  Thief schedules/s,
+profile queries/s and per-kernel roofline fractions are reported under "rows".
+
+--impl reference times the CPU oracle (tier rules: there is no reference
+implementation) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "scheduler allocations evaluated/sec and thief schedules/sec; % HBM roofline"
+UNIT = "allocations/s"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured", d
+    return 6650.0, "fallback", {}
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+class Workload:
+    def __init__(self, n_inst, n_alloc, n_query, inst_offset=0, query_offset=0):
+        self.cfg = synth.SchedConfig(**{**synth.CONFIG4.__dict__, "n_inst": inst_offset + n_inst,
+                                        "n_alloc": n_alloc})
+        self.pcfg = synth.ProfileConfig(**{**synth.CONFIG3.__dict__, "n_query": query_offset + n_query})
+        self.B, self.N, self.Q = n_inst, n_alloc, n_query
+        self.i0, self.q0 = inst_offset, query_offset
+        c = self.cfg
+        self.V, self.J, self.U = c.n_streams, 2 * c.n_streams, c.units
+        self.nc = (c.units + 1) * (c.units + 2) // 2
+        self.args = (c.units, c.steal_units, c.unit_gpu_seconds, c.a_min)
+
+    # units of the metric in one step
+    def allocations(self):
+        return self.B * self.V * self.nc + self.B * self.N * self.V
+
+    # algorithmic bytes per launch
+    def table_bytes(self):
+        c = self.cfg
+        return self.B * self.V * (4 + 8 * c.n_gamma + 6 * c.n_lambda)
+
+    def grid_bytes(self):
+        return self.table_bytes() + self.B * self.V * self.nc * 5
+
+    def list_bytes(self):
+        return self.table_bytes() + self.B * self.N * (2 * self.J + 8 + 4 + self.V)
+
+    def profile_bytes(self):
+        p = self.pcfg
+        return self.Q * (4 * (p.n_hist * (p.n_class + p.n_gamma) + p.n_class + p.n_gamma) + 8 * p.n_gamma)
+
+    def thief_bytes(self):
+        return self.table_bytes() + self.B * (2 * self.J + self.V + 16)
+
+
+def gen_device(w: Workload, dev):
+    """Generate the batch on the device in chunks (bit-identical to CPU generation)."""
+    T = synth.sched_tables(w.cfg, w.i0, w.i0 + w.B, device=dev)
+    rows = torch.empty((w.B, w.N, w.J), dtype=torch.uint16, device=dev)
+    ch = 1024
+    for b0 in range(0, w.B, ch):
+        b1 = min(w.B, b0 + ch)
+        rows[b0:b1] = synth.list_allocs(w.cfg, w.N, w.i0 + b0, w.i0 + b1, device=dev)
+    p = w.pcfg
+    P = {"cur": torch.empty((w.Q, p.n_class), device=dev),
+         "hist": torch.empty((w.Q, p.n_hist, p.n_class), device=dev),
+         "hist_acc": torch.empty((w.Q, p.n_hist, p.n_gamma), device=dev),
+         "fallback": torch.empty((w.Q, p.n_gamma), device=dev)}
+    ch = 2048
+    for q0 in range(0, w.Q, ch):
+        q1 = min(w.Q, q0 + ch)
+        part = synth.profile_inputs(p, w.q0 + q0, w.q0 + q1, device=dev)
+        for k in P:
+            P[k][q0:q1] = part[k]
+        del part
+    torch.cuda.synchronize()
+    return T, rows, P
+
+
+class Outputs:
+    def __init__(self, w: Workload, dev):
+        B, V, J, N, Q, G = w.B, w.V, w.J, w.N, w.Q, w.pcfg.n_gamma
+        self.grid = torch.empty((B, V, w.nc), dtype=torch.float32, device=dev)
+        self.grid_cfg = torch.empty((B, V, w.nc), dtype=torch.uint8, device=dev)
+        self.lsum = torch.empty((B, N), dtype=torch.uint64, device=dev)
+        self.lmean = torch.empty((B, N), dtype=torch.float32, device=dev)
+        self.lcfg = torch.empty((B, N, V), dtype=torch.uint8, device=dev)
+        # decision records (one contiguous buffer per mode: gathered to the root for N > 1)
+        from paper_2012_10557_b200 import shard
+        self.rec_bytes = shard.record_bytes(B, V)
+        self.dec = []
+        for _ in range(2):
+            buf = torch.empty(self.rec_bytes, dtype=torch.uint8, device=dev)
+            self.dec.append(dict(buf=buf, **shard.record_views(buf, B, V)))
+        self.est = [torch.empty((Q, G), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.n = [torch.empty((Q, G), dtype=torch.int32, device=dev) for _ in range(2)]
+
+
+def run_step(ek, h, w, T, rows, P, O, timer=None):
+    """One pass of the whole hot path.  Returns nothing; all work on the current stream."""
+    dims = ek.dims_from(T, *w.args)
+    tabs = ek.make_tables(**T)
+    p = w.pcfg
+    steps = [
+        ("profile_cluster", lambda: ek.ekya_profile_estimate(
+            h, ek.ProfileDims(w.Q, p.n_hist, p.n_class, p.n_gamma, ek.PROFILE_CLUSTER, p.tau, p.k, p.max_iter),
+            P["cur"], P["hist"], P["hist_acc"], P["fallback"], O.est[1], O.n[1])),
+        ("profile_radius", lambda: ek.ekya_profile_estimate(
+            h, ek.ProfileDims(w.Q, p.n_hist, p.n_class, p.n_gamma, ek.PROFILE_RADIUS, p.tau, p.k, p.max_iter),
+            P["cur"], P["hist"], P["hist_acc"], P["fallback"], O.est[0], O.n[0])),
+        ("eval_grid", lambda: ek.ekya_eval_allocations(h, dims, tabs, ek.EVAL_GRID, out_grid=O.grid,
+                                                       out_grid_cfg=O.grid_cfg)),
+        ("eval_list", lambda: ek.ekya_eval_allocations(h, dims, tabs, ek.EVAL_LIST, w.N, rows, O.lsum,
+                                                       O.lmean, O.lcfg)),
+        ("thief_steepest", lambda: ek.ekya_thief_schedule(h, dims, tabs, ek.THIEF_STEEPEST, O.dec[0]["alloc"],
+                                                          O.dec[0]["cfg"], O.dec[0]["sum"], O.dec[0]["mean"],
+                                                          O.dec[0]["steps"])),
+        ("thief_literal", lambda: ek.ekya_thief_schedule(h, dims, tabs, ek.THIEF_LITERAL, O.dec[1]["alloc"],
+                                                         O.dec[1]["cfg"], O.dec[1]["sum"], O.dec[1]["mean"],
+                                                         O.dec[1]["steps"])),
+    ]
+    for name, fn in steps:
+        if timer is not None:
+            timer.start(name)
+        fn()
+        if timer is not None:
+            timer.stop(name)
+
+
+class KernelTimer:
+    """CUDA events on the launching (current) stream around each launch."""
+
+    def __init__(self):
+        self.ev = {}
+
+    def start(self, name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.ev.setdefault(name, []).append([e, None])
+
+    def stop(self, name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.ev[name][-1][1] = e
+
+    def totals_ms(self):
+        return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.ev.items()}
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_sample(n_inst=48, n_query=32):
+    """One bounded sample of the same workload, run through the oracle.  Returns
+    (seconds, allocations evaluated, description)."""
+    import oracle
+    w = Workload(n_inst, synth.CONFIG4.n_alloc, n_query)
+    T = synth.sched_tables(w.cfg, 0, n_inst)
+    inst = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            *w.args)
+    rows = synth.list_allocs(w.cfg, w.N, 0, n_inst).numpy()
+    P = {k: v.numpy() for k, v in synth.profile_inputs(w.pcfg, 0, n_query).items()}
+    t0 = time.perf_counter()
+    oracle.profile(P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=oracle.CLUSTER)
+    oracle.profile(P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=oracle.RADIUS)
+    oracle.eval_grid(inst)
+    oracle.eval_list(inst, rows)
+    oracle.thief(inst, oracle.STEEPEST)
+    oracle.thief(inst, oracle.LITERAL)
+    dt = time.perf_counter() - t0
+    desc = (f"{n_inst} of 65536 config-4 instances (GRID, LIST x4096, thief STEEPEST+LITERAL) + "
+            f"{n_query} of 65536 config-3 queries (CLUSTER+RADIUS); single thread")
+    return dt, w.allocations(), desc
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    for _ in range(args.warmup):
+        oracle_sample(args.ref_inst, args.ref_query)
+    ts, units = [], 0
+    desc = ""
+    for _ in range(args.steps):
+        dt, units, desc = oracle_sample(args.ref_inst, args.ref_query)
+        ts.append(dt)
+    tot = float(sum(ts))
+    value = units * args.steps / tot
+    w = Workload(synth.CONFIG4.n_inst, synth.CONFIG4.n_alloc, synth.CONFIG3.n_query)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config_block(w, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(w, args):
+    return {"workload": "config4 (65,536 x 10-stream Cityscapes-shaped instances, |Gamma|=18, |Lambda|=5, "
+                        "U=80, Delta=0.1 GPU, GRID + LIST(4096/inst) + thief STEEPEST+LITERAL) + config3 "
+                        "(65,536 Waymo-shaped profiler queries, C=27, H=500, |Gamma|=18, CLUSTER k=5 + RADIUS "
+                        "tau=0.2)",
+            "instances_per_gpu": w.B, "streams": w.V, "units": w.U, "list_rows_per_instance": w.N,
+            "profile_queries_per_gpu": w.Q,
+            "l2": "not flushed: every step streams > 126 MB (GRID writes 11 GB, profile reads 5.9 GB)",
+            "parallelism": f"instance sharding x{args.gpus} + NCCL gather of decisions" if args.gpus > 1
+            else "single GPU"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    from paper_2012_10557_b200 import ekya as ek
+    ek.load_library()          # fails loudly if the CUDA library is missing
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    h = ek.Handle(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        uid = [ek.ekya_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ek.ekya_comm_init(h, uid[0], world, rank)
+    w = Workload(args.n_inst, args.n_alloc, args.n_query, inst_offset=rank * args.n_inst,
+                 query_offset=rank * args.n_query)
+    T, rows, P = gen_device(w, dev)
+    O = Outputs(w, dev)
+    root_buf = [torch.empty(world * O.rec_bytes, dtype=torch.uint8, device=dev) if rank == 0 else None
+                for _ in range(2)]
+
+    def step(timer=None):
+        run_step(ek, h, w, T, rows, P, O, timer)
+        if world > 1:
+            if timer is not None:
+                timer.start("gather")
+            for m in range(2):
+                ek.ekya_gather_decisions(h, O.dec[m]["buf"], root_buf[m], root=0)
+            if timer is not None:
+                timer.stop("gather")
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert h.last_error() == 0, "device reported a data error"
+
+    # ---- device-resident timed region ----
+    timer = KernelTimer()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = h.launch_count()
+    with ClockSampler(local_rank) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            step(timer)
+        t1.record()
+        torch.cuda.synchronize()
+    barrier()
+    launches = h.launch_count() - l0
+    ms = t0.elapsed_time(t1)
+    per = timer.totals_ms()
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+
+    # ---- end-to-end through the public API with host buffers ----
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e = run_e2e(ek, h, w, T, rows, P, O, args, world)
+
+    if rank != 0:
+        return
+    peak, peak_kind, _ = measured_peaks()
+    total_units = w.allocations() * world * args.steps
+    value = total_units / (ms / 1000.0)
+    rows_out = {}
+    bytes_of = {"eval_grid": w.grid_bytes(), "eval_list": w.list_bytes(), "profile_radius": w.profile_bytes(),
+                "profile_cluster": w.profile_bytes(), "thief_steepest": w.thief_bytes(),
+                "thief_literal": w.thief_bytes()}
+    for k, t in per.items():
+        avg = t / args.steps
+        r = {"ms_per_launch": avg, "share": t / ms}
+        if k in bytes_of:
+            gbs = bytes_of[k] / (avg / 1000.0) / 1e9
+            r["algorithmic_gb_per_s"] = gbs
+            r["hbm_frac"] = gbs / peak
+        if k.startswith("thief"):
+            r["schedules_per_s"] = w.B * world / (avg / 1000.0)
+        if k.startswith("profile"):
+            r["queries_per_s"] = w.Q * world / (avg / 1000.0)
+        if k == "eval_grid":
+            r["cells_per_s"] = w.B * w.V * w.nc * world / (avg / 1000.0)
+        if k == "eval_list":
+            r["allocation_vectors_per_s"] = w.B * w.N * world / (avg / 1000.0)
+        rows_out[k] = r
+    dom = max((k for k in per if k in bytes_of and not k.startswith("thief")), key=lambda k: per[k])
+    dom_avg = per[dom] / args.steps
+    achieved = bytes_of[dom] / (dom_avg / 1000.0) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(dom)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-based generator, paper shapes)",
+        "config": config_block(w, args),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": bytes_of[dom]},
+        "rows": rows_out,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if args.cpu_baseline and world == 1 or (args.cpu_baseline and rank == 0):
+        import oracle
+        oracle.build()
+        dt, units, desc = oracle_sample(args.ref_inst, args.ref_query)
+        line["cpu_baseline"] = {"value": units / dt, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                                "seconds": dt}
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(ek, h, w, T, rows, P, O, args, world):
+    """Same step through the public API, inputs copied from pinned host memory
+    and the decisions/estimates/objectives read back, every step."""
+    host_in = {("T", k): v.cpu().pin_memory() for k, v in T.items()}
+    host_in[("rows", "")] = rows.cpu().pin_memory()
+    for k, v in P.items():
+        host_in[("P", k)] = v.cpu().pin_memory()
+    outs = [O.dec[0]["buf"], O.dec[1]["buf"], O.est[0], O.n[0], O.est[1], O.n[1], O.lsum, O.lmean]
+    host_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
+    h2d = sum(v.numel() * v.element_size() for v in host_in.values())
+    d2h = sum(o.numel() * o.element_size() for o in outs)
+
+    def e2e_step():
+        for (grp, k), v in host_in.items():
+            dst = T[k] if grp == "T" else rows if grp == "rows" else P[k]
+            dst.copy_(v, non_blocking=True)
+        run_step(ek, h, w, T, rows, P, O)
+        for o, ho in zip(outs, host_out):
+            ho.copy_(o, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=rows.device)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    return {"value": w.allocations() * world * args.e2e_steps / (ms / 1000.0), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": ms / args.e2e_steps, "steps": args.e2e_steps,
+            "read_back": "thief decisions (both modes), profile estimates+counts (both modes), LIST objectives "
+                         "(sum_q32, mean); GRID/LIST config tables stay device-resident"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-inst", type=int, default=synth.CONFIG4.n_inst)
+    ap.add_argument("--n-alloc", type=int, default=synth.CONFIG4.n_alloc)
+    ap.add_argument("--n-query", type=int, default=synth.CONFIG3.n_query)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--ref-inst", type=int, default=48)
+    ap.add_argument("--ref-query", type=int, default=32)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -173,17 +173,37 @@ __device__ __forceinline__ int nearest(const float* x, const float* mu, int k, i
     return best;
 }
 
+struct ClusterLayout {
+    size_t hist, acc, cur, mu, assign, sim, ps, pn, total;
+};
+
+__host__ __device__ inline ClusterLayout cluster_layout(int H, int C, int G, int K) {
+    ClusterLayout L;
+    size_t o = 0;
+    L.hist = o;   o += al16((size_t)H * C * 4 + 16);
+    L.acc = o;    o += al16((size_t)H * G * 4 + 16);
+    L.cur = o;    o += al16((size_t)C * 4);
+    L.mu = o;     o += al16((size_t)K * C * 4);
+    L.assign = o; o += al16((size_t)(H + 1) * 4);
+    L.sim = o;    o += al16((size_t)H + 1);
+    L.ps = o;     o += al16((size_t)kProfThreads * 8);
+    L.pn = o;     o += al16((size_t)kProfThreads * 4);
+    L.total = o;
+    return L;
+}
+
 __global__ void __launch_bounds__(kProfThreads) cluster_kernel(ProfParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int H = P.p.n_hist, C = P.p.n_class, G = P.p.n_gamma, K = P.p.k;
-    unsigned char* hbuf = smem;
-    unsigned char* abuf = hbuf + al16((size_t)H * C * 4 + 16);
-    float* cur_s = reinterpret_cast<float*>(abuf + al16((size_t)H * G * 4 + 16));
-    float* mu = cur_s + ((C + 3) & ~3);
-    int* assign = reinterpret_cast<int*>(mu + ((K * C + 3) & ~3));
-    unsigned char* sim = reinterpret_cast<unsigned char*>(assign + H + 1);
-    unsigned long long* ps = reinterpret_cast<unsigned long long*>(sim + al16(H + 1));
-    int* pn = reinterpret_cast<int*>(ps + kProfThreads);
+    ClusterLayout Lc = cluster_layout(H, C, G, K);
+    unsigned char* hbuf = smem + Lc.hist;
+    unsigned char* abuf = smem + Lc.acc;
+    float* cur_s = reinterpret_cast<float*>(smem + Lc.cur);
+    float* mu = reinterpret_cast<float*>(smem + Lc.mu);
+    int* assign = reinterpret_cast<int*>(smem + Lc.assign);
+    unsigned char* sim = smem + Lc.sim;
+    unsigned long long* ps = reinterpret_cast<unsigned long long*>(smem + Lc.ps);
+    int* pn = reinterpret_cast<int*>(smem + Lc.pn);
     __shared__ int s_qc;
 
     for (long long q = blockIdx.x; q < P.p.n_query; q += gridDim.x) {
@@ -295,9 +315,7 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
         int grid = resident(h, (const void*)radius_kernel, smem, p.n_query);
         radius_kernel<<<grid, kProfThreads, smem, s>>>(P);
     } else {
-        size_t smem = al16((size_t)H * C * 4 + 16) + al16((size_t)H * G * 4 + 16) +
-                      (size_t)(((C + 3) & ~3) + ((K * C + 3) & ~3)) * 4 + (size_t)(H + 1) * 4 +
-                      al16(H + 1) + fixed;
+        size_t smem = cluster_layout(H, C, G, K).total;
         if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
         cudaError_t e = cudaFuncSetAttribute(cluster_kernel,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -129,7 +129,7 @@ def test_list_invalid_rows_and_data_errors(h):
     Td = {k: v.cuda() for k, v in T.items()}
     rows = synth.list_allocs(cfg, 40)
     rows[0, 3, 4] = cfg.units + 1                      # entry > U
-    rows[1, 7, 0] += 3                                 # sum > U
+    rows[1, 7, 0] = int(rows[1, 7, 0]) + 3             # sum > U
     s, mean, c = ek().eval_list(h, Td, rows.cuda(), *args(cfg))
     assert h.last_error() == -6
     os_, om, ocf, bad = oracle.eval_list(inst, rows.numpy())
@@ -191,7 +191,7 @@ def test_thief_scaleout_shape(h):
 
 def test_empty_batch(h):
     cfg = variant(synth.CONFIG2, n_inst=0)
-    Td, inst = tables(cfg)
+    Td = {k: v.cuda() for k, v in synth.sched_tables(cfg).items()}
     a, c, s, m, st = ek().thief_schedule(h, Td, *args(cfg))
     assert a.shape == (0, 20)
     grid, _ = ek().eval_grid(h, Td, *args(cfg))
