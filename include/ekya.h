@@ -12,6 +12,11 @@
  *    tensors).  Layout: instance-major, row-major, no padding.  The library
  *    never allocates on these paths and never keeps a pointer after returning.
  *  - Every compute call is asynchronous on `stream` (0 = legacy default).
+ *  - Input arrays are read by the TMA bulk-copy engine in whole 16-byte
+ *    granules: the library may read (never write) bytes of the 16-byte-aligned
+ *    granules that contain an input array's first and last element, i.e. at
+ *    most 15 bytes before/after it.  Such reads never cross a page, so any
+ *    cudaMalloc / torch allocation is safe.
  *  - Return value: EKYA_OK (0) or a negative EKYA_ERR_* code.  Host-side
  *    argument checks fail synchronously before anything is launched.
  *  - Data errors found on the device (R-ERR in DESIGN.md: NaN/negative cost,

@@ -121,10 +121,14 @@ class Instances:
                  unit_gpu_seconds, a_min):
         self.stale = _c(stale, np.float32)
         B, V = self.stale.shape
-        self.cost = _c(cost, np.float32).reshape(B, V, -1)
-        self.post = _c(post, np.float32).reshape(B, V, -1)
-        self.lam_min_units = _c(lam_min_units, np.uint16).reshape(B, V, -1)
-        self.lam_factor = _c(lam_factor, np.float32).reshape(B, V, -1)
+
+        def shaped(a, dt):
+            a = _c(a, dt)
+            return a if a.ndim == 3 else a.reshape(B, V, -1)
+        self.cost = shaped(cost, np.float32)
+        self.post = shaped(post, np.float32)
+        self.lam_min_units = shaped(lam_min_units, np.uint16)
+        self.lam_factor = shaped(lam_factor, np.float32)
         self.units = int(units)
         self.steal_units = int(steal_units)
         self.unit_gpu_seconds = float(unit_gpu_seconds)
@@ -276,11 +280,13 @@ def bruteforce(inst: Instances):
 def profile(cur, hist, hist_acc, fallback, mode=RADIUS, tau=0.2, k=5, max_iter=100):
     cur = _c(cur, np.float32)
     Q, C = cur.shape
-    hist = _c(hist, np.float32).reshape(Q, -1, C)
-    H = hist.shape[1]
-    hist_acc = _c(hist_acc, np.float32).reshape(Q, H, -1)
-    G = hist_acc.shape[2]
-    fallback = _c(fallback, np.float32).reshape(Q, G)
+    fallback = _c(fallback, np.float32)
+    G = fallback.shape[-1]
+    fallback = fallback.reshape(Q, G)
+    hist = _c(hist, np.float32)
+    H = hist.shape[1] if hist.ndim == 3 else hist.size // max(1, Q * C)
+    hist = hist.reshape(Q, H, C)
+    hist_acc = _c(hist_acc, np.float32).reshape(Q, H, G)
     pd = ProfileDims(Q, H, C, G, mode, tau, k, max_iter)
     est = np.zeros((Q, G), np.float32)
     n = np.zeros((Q, G), np.int32)

@@ -118,3 +118,94 @@ __device__ __forceinline__ void store_from_smem(void* dst, const unsigned char* 
 }
 
 }  // namespace ekya
+
+// ---------------------------------------------------------------------------
+// sm_90+/sm_100a asynchronous bulk copies (TMA bulk engine) and mbarriers
+// ---------------------------------------------------------------------------
+namespace ekya {
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+// make mbarrier initialisation visible to the async proxy
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// order generic-proxy shared-memory writes before subsequent async-proxy reads
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// global -> shared bulk copy; completion counted on `bar` (bytes % 16 == 0, 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// shared -> global bulk copy (bulk-group completion)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Granule staging: the 16-byte granules covering [src, src + bytes) are copied
+// to `dst` (16-B aligned) so that src lands at dst + (src & 15).  Returns the
+// number of bytes the copy moves; *out receives the shared pointer of src.
+struct Granules {
+    const unsigned char* g0;
+    unsigned bytes;
+    unsigned off;
+};
+__device__ __forceinline__ Granules granules(const void* src, size_t bytes) {
+    uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    uintptr_t a0 = a & ~uintptr_t(15);
+    uintptr_t a1 = (a + bytes + 15) & ~uintptr_t(15);
+    Granules g;
+    g.g0 = reinterpret_cast<const unsigned char*>(a0);
+    g.bytes = bytes ? (unsigned)(a1 - a0) : 0u;
+    g.off = (unsigned)(a - a0);
+    return g;
+}
+
+}  // namespace ekya

@@ -1,20 +1,26 @@
 // profile.cu -- ekya_profile_estimate: the class-distribution-similarity
 // accuracy estimator (draft appendix).
 //
-// RADIUS (HBM-bound): one CTA per query (grid-stride, 2 CTAs/SM).  The query's
-// history histograms and history accuracies are staged into shared memory with
-// 16-byte vector loads (chunks of Hc windows when a query does not fit), one
-// thread per window computes the sequential squared distance (rule 5; row
-// stride C words, conflict-free for odd C) and the <= tau test, then a fixed
-// thread -> gamma mapping accumulates exact Q32 sums and counts over similar,
-// measured windows; partials are combined in shared memory and divided once in
-// double precision (rule 5), exactly as the oracle.
+// Both modes run one persistent CTA (512 threads) per SM that walks its
+// queries through a two-stage shared-memory pipeline fed by the TMA bulk-copy
+// engine (cp.async.bulk + mbarrier): while the CTA computes query j, the
+// history histograms / accuracies of query j+1 are in flight, so HBM streams
+// continuously and no thread stalls on a global load.
 //
-// CLUSTER (ALU-bound): one CTA per query holds the whole history in shared
-// memory and runs Lloyd's algorithm (C19): thread-per-window assignment,
-// thread-per-(cluster, class) exact Q32 centroid sums, convergence by block
-// vote; the query joins its nearest centroid and the same per-gamma reduction
-// follows.
+// RADIUS (HBM-bound): one thread per history window computes rule 5's
+// sequential squared distance from shared memory (row stride C words: bank-
+// conflict free for odd C) and the <= tau test; a fixed thread -> gamma mapping
+// then accumulates exact Q32 sums and counts over similar, measured windows;
+// the partials are combined once per query and divided in double (rule 5).
+// Queries whose history does not fit a stage are processed in window chunks.
+//
+// CLUSTER (ALU-bound): Lloyd's algorithm (C19) per query on the staged
+// history.  Each thread keeps its window's histogram in registers across
+// iterations and reads centroids as float4 broadcasts; cluster sums are exact
+// Q32 integers maintained INCREMENTALLY (only windows whose assignment changed
+// are moved between clusters, with 64-bit shared atomics), which is
+// bit-identical to the oracle's full recomputation because integer addition is
+// associative.
 #include <algorithm>
 #include <cfloat>
 
@@ -24,7 +30,8 @@ namespace ekya {
 
 namespace {
 
-constexpr int kProfThreads = 256;
+constexpr int kProfThreads = 512;
+constexpr int kStages = 2;
 
 struct ProfParams {
     ekya_profile_dims p;
@@ -36,35 +43,85 @@ struct ProfParams {
     int* out_n;
     int* out_cluster;
     DevState* st;
-    int Hc;          // windows per staged chunk (RADIUS)
+    int Hc;             // windows per staged chunk
+    int stages;         // 1 or 2
+    int acc_staged;     // CLUSTER: accuracy tile staged in shared memory
+    size_t stage_bytes; // bytes per stage
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// per-gamma partial sums: thread t owns gamma t % G and window residue t / G
+// per-stage layout: [cur][fallback][hist chunk][acc chunk], each padded by 16 B for granule staging
+struct StageLayout {
+    size_t cur, fb, hist, acc, total;
+};
+__host__ __device__ inline StageLayout stage_layout(int C, int G, int Hc, bool with_acc) {
+    StageLayout L;
+    size_t o = 0;
+    L.cur = o;  o += al16((size_t)C * 4) + 16;
+    L.fb = o;   o += al16((size_t)G * 4) + 16;
+    L.hist = o; o += al16((size_t)Hc * C * 4) + 16;
+    L.acc = o;  o += with_acc ? al16((size_t)Hc * G * 4) + 16 : 0;
+    L.total = al16(o);
+    return L;
+}
+
+struct StagePtrs {
+    const float* cur;
+    const float* fb;
+    const float* hist;
+    const float* acc;
+};
+
+// Leader thread: arm the stage barrier and issue the bulk copies of one work item.
+__device__ __forceinline__ void issue_item(const ProfParams& P, unsigned char* stage, unsigned long long* bar,
+                                           long long q, int h0, int hn, bool with_acc, const StageLayout& L) {
+    const int H = P.p.n_hist, C = P.p.n_class, G = P.p.n_gamma;
+    Granules gc = granules(P.cur + q * C, (size_t)C * 4);
+    Granules gf = granules(P.fallback + q * G, (size_t)G * 4);
+    Granules gh = granules(P.hist + ((size_t)q * H + h0) * C, (size_t)hn * C * 4);
+    Granules ga = with_acc ? granules(P.acc + ((size_t)q * H + h0) * G, (size_t)hn * G * 4) : Granules{nullptr, 0, 0};
+    mbar_arrive_expect_tx(bar, gc.bytes + gf.bytes + gh.bytes + ga.bytes);
+    bulk_g2s(stage + L.cur, gc.g0, gc.bytes, bar);
+    bulk_g2s(stage + L.fb, gf.g0, gf.bytes, bar);
+    if (gh.bytes) bulk_g2s(stage + L.hist, gh.g0, gh.bytes, bar);
+    if (ga.bytes) bulk_g2s(stage + L.acc, ga.g0, ga.bytes, bar);
+}
+
+__device__ __forceinline__ StagePtrs stage_ptrs(const ProfParams& P, unsigned char* stage, long long q, int h0,
+                                                bool with_acc, const StageLayout& L) {
+    const int H = P.p.n_hist, C = P.p.n_class, G = P.p.n_gamma;
+    StagePtrs s;
+    s.cur = reinterpret_cast<const float*>(stage + L.cur + granules(P.cur + q * C, 4).off);
+    s.fb = reinterpret_cast<const float*>(stage + L.fb + granules(P.fallback + q * G, 4).off);
+    s.hist = reinterpret_cast<const float*>(stage + L.hist + granules(P.hist + ((size_t)q * H + h0) * C, 4).off);
+    s.acc = with_acc ? reinterpret_cast<const float*>(stage + L.acc +
+                                                      granules(P.acc + ((size_t)q * H + h0) * G, 4).off)
+                     : nullptr;
+    return s;
+}
+
+// ---- per-gamma exact accumulation: thread t owns gamma t % G and windows h = t / G (mod ngrp)
 struct GammaAcc {
     int g, grp, ngrp;
     unsigned long long s;
     int n;
 };
 
-__device__ __forceinline__ GammaAcc gamma_acc_init(int G) {
-    GammaAcc a;
+__device__ __forceinline__ void gacc_reset(GammaAcc& a, int G) {
     a.ngrp = kProfThreads / G;
     a.g = threadIdx.x % G;
     a.grp = threadIdx.x / G;
     a.s = 0;
     a.n = 0;
-    return a;
 }
 
-// accumulate windows [0, hn) of a staged accuracy tile; returns false on bad data
-__device__ __forceinline__ bool gamma_acc_add(GammaAcc& a, const float* acc_s, const unsigned char* sim,
-                                              int hn, int G) {
+// windows [0, hn) of an accuracy tile (shared or global), similarity flags in sim[]
+__device__ __forceinline__ bool gacc_add(GammaAcc& a, const float* acc, const unsigned char* sim, int hn, int G) {
     bool ok = true;
     if (a.grp >= a.ngrp) return ok;
     for (int h = a.grp; h < hn; h += a.ngrp) {
-        float x = acc_s[(size_t)h * G + a.g];
+        float x = acc[(size_t)h * G + a.g];
         bool nan = isnan(x);
         ok &= nan || in01(x);
         if (sim[h] && !nan) {
@@ -75,9 +132,8 @@ __device__ __forceinline__ bool gamma_acc_add(GammaAcc& a, const float* acc_s, c
     return ok;
 }
 
-// combine partials and write est / n for query q
-__device__ __forceinline__ void gamma_acc_finish(const GammaAcc& a, unsigned long long* ps, int* pn,
-                                                 const ProfParams& P, long long q, bool ok) {
+__device__ __forceinline__ void gacc_finish(const GammaAcc& a, unsigned long long* ps, int* pn, const float* fb,
+                                            const ProfParams& P, long long q, bool ok) {
     const int G = P.p.n_gamma;
     if (a.grp < a.ngrp) {
         ps[threadIdx.x] = a.s;
@@ -91,176 +147,286 @@ __device__ __forceinline__ void gamma_acc_finish(const GammaAcc& a, unsigned lon
             s += ps[r * G + threadIdx.x];
             n += pn[r * G + threadIdx.x];
         }
-        float est;
-        if (!ok) {
-            est = 0.0f;
-            n = 0;
-        } else {
-            est = n > 0 ? mean_q32(s, n) : __ldg(P.fallback + q * G + threadIdx.x);
-        }
+        float est = 0.0f;
+        if (!ok) n = 0;
+        else est = n > 0 ? mean_q32(s, n) : fb[threadIdx.x];
         P.out_est[q * G + threadIdx.x] = est;
         P.out_n[q * G + threadIdx.x] = n;
     }
 }
 
-__global__ void __launch_bounds__(kProfThreads) radius_kernel(ProfParams P) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int H = P.p.n_hist, C = P.p.n_class, G = P.p.n_gamma, Hc = P.Hc;
-    const float tau = P.p.tau;
-    unsigned char* hbuf = smem;
-    unsigned char* abuf = hbuf + al16((size_t)Hc * C * 4 + 16);
-    float* cur_s = reinterpret_cast<float*>(abuf + al16((size_t)Hc * G * 4 + 16));
-    unsigned char* sim = reinterpret_cast<unsigned char*>(cur_s + ((C + 3) & ~3));
-    unsigned long long* ps = reinterpret_cast<unsigned long long*>(sim + al16(Hc));
-    int* pn = reinterpret_cast<int*>(ps + kProfThreads);
+struct ScratchLayout {
+    size_t bars, sim, ps, pn, mu, sums, cnt, assign, chg, misc, total;
+};
+__host__ __device__ inline ScratchLayout scratch_layout(int H, int Hc, int C, int K, bool cluster) {
+    ScratchLayout L;
+    const int CP = (C + 3) & ~3;
+    size_t o = 0;
+    L.bars = o;   o += 64;
+    L.sim = o;    o += al16((size_t)(cluster ? H : Hc) + 1);
+    L.ps = o;     o += al16((size_t)kProfThreads * 8);
+    L.pn = o;     o += al16((size_t)kProfThreads * 4);
+    L.mu = o;     o += cluster ? al16((size_t)K * CP * 4) : 0;
+    L.sums = o;   o += cluster ? al16((size_t)K * C * 8) : 0;
+    L.cnt = o;    o += cluster ? al16((size_t)K * 4) : 0;
+    L.assign = o; o += cluster ? al16((size_t)H * 4) : 0;
+    L.chg = o;    o += cluster ? al16((size_t)H * 4) : 0;
+    L.misc = o;   o += 64;
+    L.total = o;
+    return L;
+}
 
-    for (long long q = blockIdx.x; q < P.p.n_query; q += gridDim.x) {
-        bool ok = true;
-        for (int c = threadIdx.x; c < C; c += blockDim.x) {
-            float x = __ldg(P.cur + q * C + c);
-            ok &= in01(x);
-            cur_s[c] = x;
+// ------------------------------------------------------------------------
+// RADIUS
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(kProfThreads, 1) radius_kernel(ProfParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int H = P.p.n_hist, C = P.p.n_class, G = P.p.n_gamma, Hc = P.Hc, NS = P.stages;
+    const float tau = P.p.tau;
+    const StageLayout L = stage_layout(C, G, Hc, true);
+    const ScratchLayout S = scratch_layout(H, Hc, C, 0, false);
+    unsigned char* scratch = smem + NS * P.stage_bytes;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(scratch + S.bars);
+    unsigned char* sim = scratch + S.sim;
+    unsigned long long* ps = reinterpret_cast<unsigned long long*>(scratch + S.ps);
+    int* pn = reinterpret_cast<int*>(scratch + S.pn);
+
+    const long long Q = P.p.n_query;
+    const int nch = (H + Hc - 1) / Hc;
+    const long long nq_local = Q > blockIdx.x ? (Q - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long long items = nq_local * nch;
+    auto item_q = [&](long long i) { return (long long)blockIdx.x + (i / nch) * gridDim.x; };
+    auto item_h0 = [&](long long i) { return (int)(i % nch) * Hc; };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (long long i = 0; i < NS && i < items; ++i) {
+            int h0 = item_h0(i);
+            issue_item(P, smem + (i % NS) * P.stage_bytes, &bar[i % NS], item_q(i), h0, min(Hc, H - h0), true, L);
         }
-        GammaAcc a = gamma_acc_init(G);
-        for (int h0 = 0; h0 < H; h0 += Hc) {
-            const int hn = min(Hc, H - h0);
-            const float* hs = reinterpret_cast<const float*>(
-                stage_to_smem(hbuf, P.hist + ((size_t)q * H + h0) * C, (size_t)hn * C * 4));
-            const float* as = reinterpret_cast<const float*>(
-                stage_to_smem(abuf, P.acc + ((size_t)q * H + h0) * G, (size_t)hn * G * 4));
-            __syncthreads();
-            for (int h = threadIdx.x; h < hn; h += blockDim.x) {
-                const float* row = hs + (size_t)h * C;
-                float d2 = 0.0f;
-                for (int c = 0; c < C; ++c) {
-                    float x = row[c];
-                    ok &= in01(x);
-                    float diff = fsub(cur_s[c], x);
-                    d2 = fadd(d2, fmul(diff, diff));
-                }
-                sim[h] = __fsqrt_rn(d2) <= tau;
+    }
+    GammaAcc a;
+    bool ok = true;
+    for (long long i = 0; i < items; ++i) {
+        const int s = (int)(i % NS);
+        const long long q = item_q(i);
+        const int h0 = item_h0(i), hn = min(Hc, H - h0);
+        mbar_wait(&bar[s], (unsigned)((i / NS) & 1));
+        const StagePtrs sp = stage_ptrs(P, smem + s * P.stage_bytes, q, h0, true, L);
+        if (h0 == 0) {
+            gacc_reset(a, G);
+            ok = true;
+            for (int c = threadIdx.x; c < C; c += blockDim.x) ok &= in01(sp.cur[c]);
+        }
+        for (int h = threadIdx.x; h < hn; h += blockDim.x) {
+            const float* row = sp.hist + (size_t)h * C;
+            float d2 = 0.0f;
+            for (int c = 0; c < C; ++c) {
+                float x = row[c];
+                ok &= in01(x);
+                float diff = fsub(sp.cur[c], x);
+                d2 = fadd(d2, fmul(diff, diff));
             }
-            __syncthreads();
-            ok &= gamma_acc_add(a, as, sim, hn, G);
-            __syncthreads();
+            sim[h] = __fsqrt_rn(d2) <= tau;
         }
-        ok = __syncthreads_and(ok) != 0;
-        if (!ok && threadIdx.x == 0) flag_data_error(P.st);
-        gamma_acc_finish(a, ps, pn, P, q, ok);
         __syncthreads();
+        ok &= gacc_add(a, sp.acc, sim, hn, G);
+        const bool last = h0 + hn >= H;
+        if (last) {
+            ok = __syncthreads_and(ok) != 0;
+            if (!ok && threadIdx.x == 0) flag_data_error(P.st);
+            gacc_finish(a, ps, pn, sp.fb, P, q, ok);
+        }
+        __syncthreads();   // stage s and sim[] are free again
+        if (threadIdx.x == 0 && i + NS < items) {
+            int h1 = item_h0(i + NS);
+            issue_item(P, smem + s * P.stage_bytes, &bar[s], item_q(i + NS), h1, min(Hc, H - h1), true, L);
+        }
     }
 }
 
-__device__ __forceinline__ float dist2(const float* x, const float* m, int C) {
+// ------------------------------------------------------------------------
+// CLUSTER
+// ------------------------------------------------------------------------
+// squared distance of x (registers, C <= 32) to centroid row m (shared, 16-B aligned)
+__device__ __forceinline__ float dist2_reg(const float (&x)[32], const float* m, int C) {
+    const float4* m4 = reinterpret_cast<const float4*>(m);
     float s = 0.0f;
-    for (int c = 0; c < C; ++c) {
-        float diff = fsub(x[c], m[c]);
-        s = fadd(s, fmul(diff, diff));
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+        if (c4 * 4 < C) {
+            float4 v = m4[c4];
+            float mv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (c4 * 4 + j < C) {
+                    float d = fsub(x[c4 * 4 + j], mv[j]);
+                    s = fadd(s, fmul(d, d));
+                }
+            }
+        }
     }
     return s;
 }
 
-__device__ __forceinline__ int nearest(const float* x, const float* mu, int k, int C) {
+__device__ __forceinline__ float dist2_mem(const float* x, const float* m, int C) {
+    float s = 0.0f;
+    for (int c = 0; c < C; ++c) {
+        float d = fsub(x[c], m[c]);
+        s = fadd(s, fmul(d, d));
+    }
+    return s;
+}
+
+template <bool REG>
+__device__ __forceinline__ int nearest_c(const float (&xr)[32], const float* xm, const float* mu, int K, int C,
+                                         int CP) {
     int best = 0;
-    float bd = dist2(x, mu, C);
-    for (int i = 1; i < k; ++i) {
-        float di = dist2(x, mu + (size_t)i * C, C);
-        if (di < bd) {
-            bd = di;
+    float bd = 0.0f;
+    for (int i = 0; i < K; ++i) {
+        float d = REG ? dist2_reg(xr, mu + i * CP, C) : dist2_mem(xm, mu + i * CP, C);
+        if (i == 0 || d < bd) {   // lowest index on ties (C19)
+            bd = d;
             best = i;
         }
     }
     return best;
 }
 
-struct ClusterLayout {
-    size_t hist, acc, cur, mu, assign, sim, ps, pn, total;
-};
+template <bool REG>
+__global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int H = P.p.n_hist, C = P.p.n_class, G = P.p.n_gamma, K = P.p.k, NS = P.stages;
+    const int CP = (C + 3) & ~3;
+    const bool accs = P.acc_staged != 0;
+    const StageLayout L = stage_layout(C, G, H, accs);
+    const ScratchLayout S = scratch_layout(H, H, C, K, true);
+    unsigned char* scratch = smem + NS * P.stage_bytes;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(scratch + S.bars);
+    unsigned char* sim = scratch + S.sim;
+    unsigned long long* ps = reinterpret_cast<unsigned long long*>(scratch + S.ps);
+    int* pn = reinterpret_cast<int*>(scratch + S.pn);
+    float* mu = reinterpret_cast<float*>(scratch + S.mu);
+    unsigned long long* sums = reinterpret_cast<unsigned long long*>(scratch + S.sums);
+    int* cnt = reinterpret_cast<int*>(scratch + S.cnt);
+    int* assign = reinterpret_cast<int*>(scratch + S.assign);
+    int* chg = reinterpret_cast<int*>(scratch + S.chg);
+    int* misc = reinterpret_cast<int*>(scratch + S.misc);   // [0..1] change counters, [2] query cluster, [3] ok
 
-__host__ __device__ inline ClusterLayout cluster_layout(int H, int C, int G, int K) {
-    ClusterLayout L;
-    size_t o = 0;
-    L.hist = o;   o += al16((size_t)H * C * 4 + 16);
-    L.acc = o;    o += al16((size_t)H * G * 4 + 16);
-    L.cur = o;    o += al16((size_t)C * 4);
-    L.mu = o;     o += al16((size_t)K * C * 4);
-    L.assign = o; o += al16((size_t)(H + 1) * 4);
-    L.sim = o;    o += al16((size_t)H + 1);
-    L.ps = o;     o += al16((size_t)kProfThreads * 8);
-    L.pn = o;     o += al16((size_t)kProfThreads * 4);
-    L.total = o;
-    return L;
-}
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const long long Q = P.p.n_query;
+    const long long items = Q > blockIdx.x ? (Q - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-__global__ void __launch_bounds__(kProfThreads) cluster_kernel(ProfParams P) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int H = P.p.n_hist, C = P.p.n_class, G = P.p.n_gamma, K = P.p.k;
-    ClusterLayout Lc = cluster_layout(H, C, G, K);
-    unsigned char* hbuf = smem + Lc.hist;
-    unsigned char* abuf = smem + Lc.acc;
-    float* cur_s = reinterpret_cast<float*>(smem + Lc.cur);
-    float* mu = reinterpret_cast<float*>(smem + Lc.mu);
-    int* assign = reinterpret_cast<int*>(smem + Lc.assign);
-    unsigned char* sim = smem + Lc.sim;
-    unsigned long long* ps = reinterpret_cast<unsigned long long*>(smem + Lc.ps);
-    int* pn = reinterpret_cast<int*>(smem + Lc.pn);
-    __shared__ int s_qc;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
+        fence_barrier_init();
+        misc[0] = misc[1] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (long long i = 0; i < NS && i < items; ++i)
+            issue_item(P, smem + (i % NS) * P.stage_bytes, &bar[i % NS], blockIdx.x + i * gridDim.x, 0, H, accs, L);
 
-    for (long long q = blockIdx.x; q < P.p.n_query; q += gridDim.x) {
+    for (long long i = 0; i < items; ++i) {
+        const int s = (int)(i % NS);
+        const long long q = blockIdx.x + i * gridDim.x;
+        mbar_wait(&bar[s], (unsigned)((i / NS) & 1));
+        const StagePtrs sp = stage_ptrs(P, smem + s * P.stage_bytes, q, 0, accs, L);
+        const float* hs = sp.hist;
         bool ok = true;
-        for (int c = threadIdx.x; c < C; c += blockDim.x) {
-            float x = __ldg(P.cur + q * C + c);
-            ok &= in01(x);
-            cur_s[c] = x;
-        }
-        const float* hs = reinterpret_cast<const float*>(
-            stage_to_smem(hbuf, P.hist + (size_t)q * H * C, (size_t)H * C * 4));
-        const float* as = reinterpret_cast<const float*>(
-            stage_to_smem(abuf, P.acc + (size_t)q * H * G, (size_t)H * G * 4));
-        __syncthreads();
-        for (int i = threadIdx.x; i < H * C; i += blockDim.x) ok &= in01(hs[i]);
+        for (int c = threadIdx.x; c < C; c += blockDim.x) ok &= in01(sp.cur[c]);
+        int qc = -1;
         if (H > 0) {
-            for (int i = threadIdx.x; i < K * C; i += blockDim.x) {
-                int ci = i / C, c = i - ci * C;
-                mu[i] = hs[(size_t)((long long)ci * H / K) * C + c];
+            // own window's histogram in registers (REG: H <= threads, C <= 32)
+            float xr[32];
+            const int hme = threadIdx.x;
+            if (REG) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) xr[c] = (hme < H && c < C) ? hs[(size_t)hme * C + c] : 0.0f;
             }
+            for (int t = threadIdx.x; t < H * C; t += blockDim.x) ok &= in01(hs[t]);
+            for (int t = threadIdx.x; t < K * CP; t += blockDim.x) {
+                int ci = t / CP, c = t - ci * CP;
+                mu[t] = c < C ? hs[(size_t)(((long long)ci * H) / K) * C + c] : 0.0f;
+            }
+            for (int t = threadIdx.x; t < K * C; t += blockDim.x) sums[t] = 0ULL;
+            for (int t = threadIdx.x; t < K; t += blockDim.x) cnt[t] = 0;
             __syncthreads();
-            for (int h = threadIdx.x; h < H; h += blockDim.x) assign[h] = nearest(hs + (size_t)h * C, mu, K, C);
+            // initial assignment
+            for (int h = threadIdx.x; h < H; h += blockDim.x)
+                assign[h] = nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
+            __syncthreads();
+            // full exact cluster sums (warp per window, lanes over classes)
+            for (int h = warp; h < H; h += nwarps) {
+                const int ah = assign[h];
+                for (int c = lane; c < C; c += 32) atomicAdd(&sums[ah * C + c], q32(hs[(size_t)h * C + c]));
+                if (lane == 0) atomicAdd(&cnt[ah], 1);
+            }
             __syncthreads();
             for (int it = 0; it < P.p.max_iter; ++it) {
-                for (int i = threadIdx.x; i < K * C; i += blockDim.x) {
-                    int ci = i / C, c = i - ci * C;
-                    unsigned long long s = 0;
-                    int n = 0;
-                    for (int h = 0; h < H; ++h) {
-                        if (assign[h] == ci) {
-                            s += q32(hs[(size_t)h * C + c]);
-                            ++n;
-                        }
-                    }
-                    if (n > 0) mu[i] = mean_q32(s, n);   // empty cluster keeps its centroid
+                const int cidx = it & 1;
+                for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
+                    int ci = t / C, c = t - ci * C;
+                    if (cnt[ci] > 0) mu[ci * CP + c] = mean_q32(sums[t], cnt[ci]);   // empty keeps centroid
                 }
                 __syncthreads();
-                // reassign; writing in place is equivalent to the oracle's
-                // "if unchanged stop, else assign = new" (both leave assign = new)
-                int changed = 0;
                 for (int h = threadIdx.x; h < H; h += blockDim.x) {
-                    int x = nearest(hs + (size_t)h * C, mu, K, C);
-                    changed |= x != assign[h];
-                    assign[h] = x;
+                    int na = nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
+                    int oa = assign[h];
+                    if (na != oa) {
+                        int slot = atomicAdd(&misc[cidx], 1);
+                        chg[slot] = h | (oa << 16) | (na << 24);
+                        assign[h] = na;
+                    }
                 }
-                if (!__syncthreads_or(changed)) break;
+                __syncthreads();
+                const int nchg = misc[cidx];
+                if (threadIdx.x == 0) misc[cidx ^ 1] = 0;
+                if (nchg == 0) break;
+                for (int e = warp; e < nchg; e += nwarps) {
+                    const int rec = chg[e];
+                    const int h = rec & 0xFFFF, oa = (rec >> 16) & 0xFF, na = (rec >> 24) & 0xFF;
+                    for (int c = lane; c < C; c += 32) {
+                        unsigned long long v = q32(hs[(size_t)h * C + c]);
+                        atomicAdd(&sums[oa * C + c], 0ULL - v);
+                        atomicAdd(&sums[na * C + c], v);
+                    }
+                    if (lane == 0) {
+                        atomicSub(&cnt[oa], 1);
+                        atomicAdd(&cnt[na], 1);
+                    }
+                }
+                __syncthreads();
             }
-            if (threadIdx.x == 0) s_qc = nearest(cur_s, mu, K, C);
-        } else if (threadIdx.x == 0) {
-            s_qc = -1;
+            __syncthreads();
+            if (threadIdx.x == 0) misc[0] = misc[1] = 0;
+            // the query joins its nearest centroid: lane i computes distance to centroid i
+            if (warp == 0) {
+                unsigned long long key = ~0ULL;
+                for (int ci = lane; ci < K; ci += 32) {
+                    float d = dist2_mem(sp.cur, mu + ci * CP, C);
+                    unsigned long long k = ((unsigned long long)__float_as_uint(d) << 8) | (unsigned)ci;
+                    key = k < key ? k : key;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+                    key = y < key ? y : key;
+                }
+                if (lane == 0) misc[2] = (int)(key & 0xFF);
+            }
+            __syncthreads();
+            qc = misc[2];
         }
-        __syncthreads();
-        const int qc = s_qc;
         for (int h = threadIdx.x; h < H; h += blockDim.x) sim[h] = assign[h] == qc;
         __syncthreads();
-        GammaAcc a = gamma_acc_init(G);
-        ok &= gamma_acc_add(a, as, sim, H, G);
+        GammaAcc a;
+        gacc_reset(a, G);
+        ok &= gacc_add(a, accs ? sp.acc : P.acc + (size_t)q * H * G, sim, H, G);
         ok = __syncthreads_and(ok) != 0;
         if (!ok && threadIdx.x == 0) flag_data_error(P.st);
         if (P.out_cluster) {
@@ -268,17 +434,26 @@ __global__ void __launch_bounds__(kProfThreads) cluster_kernel(ProfParams P) {
             for (int h = threadIdx.x; h < H; h += blockDim.x) oc[h] = ok ? assign[h] : 0;
             if (threadIdx.x == 0) oc[H] = ok ? qc : 0;
         }
-        gamma_acc_finish(a, ps, pn, P, q, ok);
-        __syncthreads();
+        gacc_finish(a, ps, pn, sp.fb, P, q, ok);
+        __syncthreads();   // stage s free
+        if (threadIdx.x == 0 && i + NS < items)
+            issue_item(P, smem + s * P.stage_bytes, &bar[s], blockIdx.x + (i + NS) * gridDim.x, 0, H, accs, L);
     }
 }
 
-int resident(ekya_handle* h, const void* fn, size_t smem, long long work) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kProfThreads, smem);
-    per_sm = std::max(per_sm, 1);
-    long long g = (long long)h->sm_count * per_sm;
-    return (int)std::max(1LL, std::min(g, work));
+// queries with an empty history: every estimate is the caller's fallback
+__global__ void no_history_kernel(ProfParams P) {
+    const long long QG = (long long)P.p.n_query * P.p.n_gamma;
+    const int C = P.p.n_class, G = P.p.n_gamma;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < QG; e += (long long)gridDim.x * blockDim.x) {
+        long long q = e / G;
+        bool ok = true;
+        for (int c = 0; c < C; ++c) ok &= in01(__ldg(P.cur + q * C + c));
+        if (!ok) flag_data_error(P.st);
+        P.out_est[e] = ok ? __ldg(P.fallback + e) : 0.0f;
+        P.out_n[e] = 0;
+        if (P.out_cluster && e % G == 0) P.out_cluster[q] = ok && P.p.mode == EKYA_PROFILE_CLUSTER ? -1 : 0;
+    }
 }
 
 }  // namespace
@@ -297,31 +472,57 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
     P.out_cluster = out_cluster;
     P.st = h->dstate;
     const int C = p.n_class, G = p.n_gamma, H = p.n_hist, K = p.k;
-    const size_t fixed = al16((size_t)C * 4 + 16) + al16((size_t)kProfThreads * 8) +
-                         al16((size_t)kProfThreads * 4) + 256;
     if (p.n_query == 0) return EKYA_OK;
+    const size_t budget = h->smem_optin;
+    if (G > kProfThreads) return EKYA_ERR_LIMIT;
+    if (H == 0) {
+        no_history_kernel<<<h->sm_count * 4, 256, 0, s>>>(P);
+        h->launches++;
+        return cuda_status(cudaGetLastError());
+    }
+    long long grid = std::min<long long>(p.n_query, h->sm_count);
+    cudaError_t e;
     if (p.mode == EKYA_PROFILE_RADIUS) {
-        // two CTAs per SM: budget ~110 KB each
+        const size_t scratch_fixed = scratch_layout(0, 0, C, 0, false).total;
         const size_t per_window = (size_t)(C + G) * 4 + 1;
-        size_t budget = std::min<size_t>(110 * 1024, h->smem_optin);
-        long long hc = (long long)((budget - fixed - 64) / per_window);
+        // two stages of Hc windows each
+        long long hc = (long long)((budget - scratch_fixed - 2 * (stage_layout(C, G, 0, true).total + 64)) /
+                                   (2 * per_window));
         if (hc < 1) return EKYA_ERR_SHAPE;
-        P.Hc = (int)std::max(1LL, std::min<long long>(hc, std::max(H, 1)));
-        size_t smem = al16((size_t)P.Hc * C * 4 + 16) + al16((size_t)P.Hc * G * 4 + 16) +
-                      al16((size_t)((C + 3) & ~3) * 4) + al16(P.Hc) + fixed;
-        cudaError_t e = cudaFuncSetAttribute(radius_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        P.Hc = (int)std::min<long long>(hc, H);
+        P.stages = kStages;
+        P.stage_bytes = stage_layout(C, G, P.Hc, true).total;
+        size_t smem = P.stages * P.stage_bytes + scratch_layout(H, P.Hc, C, 0, false).total;
+        if (smem > budget) return EKYA_ERR_SHAPE;
+        e = cudaFuncSetAttribute(radius_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return EKYA_ERR_CUDA;
-        int grid = resident(h, (const void*)radius_kernel, smem, p.n_query);
-        radius_kernel<<<grid, kProfThreads, smem, s>>>(P);
+        radius_kernel<<<(unsigned)grid, kProfThreads, smem, s>>>(P);
     } else {
-        size_t smem = cluster_layout(H, C, G, K).total;
-        if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
-        cudaError_t e = cudaFuncSetAttribute(cluster_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (H >= 65536 || K > 32) return EKYA_ERR_LIMIT;
+        const size_t scratch = scratch_layout(H, H, C, K, true).total;
+        P.Hc = H;
+        // prefer two stages with the accuracy tile staged, then fewer
+        int cfgs[4][2] = {{2, 1}, {2, 0}, {1, 1}, {1, 0}};
+        size_t smem = 0;
+        bool found = false;
+        for (auto& cf : cfgs) {
+            size_t sb = stage_layout(C, G, H, cf[1] != 0).total;
+            size_t tot = cf[0] * sb + scratch;
+            if (tot <= budget) {
+                P.stages = cf[0];
+                P.acc_staged = cf[1];
+                P.stage_bytes = sb;
+                smem = tot;
+                found = true;
+                break;
+            }
+        }
+        if (!found) return EKYA_ERR_SHAPE;
+        const bool reg = (H <= kProfThreads) && (C <= 32);
+        auto kern = reg ? cluster_kernel<true> : cluster_kernel<false>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return EKYA_ERR_CUDA;
-        int grid = resident(h, (const void*)cluster_kernel, smem, p.n_query);
-        cluster_kernel<<<grid, kProfThreads, smem, s>>>(P);
+        kern<<<(unsigned)grid, kProfThreads, smem, s>>>(P);
     }
     h->launches++;
     return cuda_status(cudaGetLastError());

@@ -7,24 +7,28 @@
 //     dS(t, w) = move[t]                if s(t) == s(w)  (w = t ^ 1)
 // where, per stream, up/down/move are Q32 differences of the stream value at
 // the seven splits {(rt,ri), (rt,ri+D), (rt+D,ri), (rt,ri-D), (rt-D,ri),
-// (rt+D,ri-D), (rt-D,ri+D)}.  These arrays live in shared memory and only the
-// touched streams are re-evaluated after a step, so a step costs O(J) instead of
-// the oracle's O(J^2) full PickConfigs recomputations, with bit-identical
-// decisions (integer arithmetic, identical tie rules).
+// (rt+D,ri-D), (rt-D,ri+D)}.  The arrays live in shared memory and only the
+// touched streams are re-evaluated after a step: O(J) per step instead of the
+// oracle's O(J^2) full PickConfigs recomputations, with bit-identical
+// decisions (exact integers, identical tie rules).
 //
-// Stream evaluation is warp-parallel over gamma (lane 0 = no retraining,
-// lane g = config g-1): each lane computes rule 2 at rt-D, rt, rt+D, a warp
-// max (REDUX) gives G*(rt'), and value(rt', ri') = fl(f_{lambda*(ri')} G*(rt'))
-// (exact because x -> fl(c x) is monotone).
+// Stream evaluation is warp-parallel: lane g evaluates rule 2 for retraining
+// config g (lane 0 = no retraining) at rt-D, rt, rt+D and a REDUX max gives
+// G*(rt'); lambda*(ri') comes from a per-stream breakpoint table (lambda*
+// changes only at the keep-up thresholds) via one REDUX + one shuffle; then
+// value(rt', ri') = fl(f_lambda*(ri') G*(rt')) -- exact because x -> fl(c x) is
+// monotone, and equal to the oracle's max over gamma of fl(f g_gamma).
 //
 // STEEPEST (C12): per step, per stream best down (value desc, index asc) ->
-// warp top-2 by stream -> per thief its best victim -> warp argmax over thieves
-// with lexicographic (t, w) ties; accept iff dS > 0.
+// top-2 by stream -> per thief its best victim -> argmax over thieves with
+// lexicographic (t, w) ties; 64-bit keys reduced with two 32-bit REDUX
+// passes.  Accept iff dS > 0.
 // LITERAL: thieves in order; victims scanned 32 at a time with a warp ballot of
 // "first steal improves" -- victims before the first set bit leave the state
-// unchanged, exactly as in the sequential loop -- then the steal chain on that
+// unchanged, exactly as the sequential loop -- then the steal chain on that
 // victim, then the scan resumes after it.
 #include <algorithm>
+#include <climits>
 
 #include "launch.h"
 
@@ -35,6 +39,7 @@ namespace {
 constexpr int kThiefThreads = 128;      // 4 warps = 4 instances per CTA
 constexpr long long kInvalid = (long long)0x8000000000000000ULL;
 constexpr long long kKeyOff = 1LL << 40;
+constexpr unsigned FULL = 0xffffffffu;
 
 struct ThiefParams {
     ekya_dims d;
@@ -51,43 +56,44 @@ struct ThiefParams {
 };
 
 struct WarpState {
-    int* alloc;                  // [J]
     unsigned long long* cur;     // [V]  Q32 value of each stream now
     long long* up;               // [J]
     long long* dn;               // [J]  kInvalid if alloc < D
     long long* mv;               // [J]  same-stream move with thief j; kInvalid if victim < D
+    int* alloc;                  // [J]
+    int* lthr;                   // [V][8] lambda* breakpoints (INT_MAX = unused)
+    float* lfac;                 // [V][8] factor of lambda* at the breakpoint (-1 = none)
 };
 
 __host__ __device__ inline size_t thief_warp_bytes(int V) {
-    int J = 2 * V;
-    size_t b = sizeof(unsigned long long) * (size_t)V + sizeof(long long) * 3 * (size_t)J +
-               sizeof(int) * (size_t)J;
+    const size_t J = 2 * (size_t)V;
+    size_t b = 8 * (size_t)V + 8 * 3 * J + 4 * J + 2 * 4 * 8 * (size_t)V;
     return (b + 15) & ~size_t(15);
 }
 
 __device__ inline WarpState carve(unsigned char* base, int V) {
-    int J = 2 * V;
+    const int J = 2 * V;
     WarpState w;
     w.cur = reinterpret_cast<unsigned long long*>(base);
     w.up = reinterpret_cast<long long*>(w.cur + V);
     w.dn = w.up + J;
     w.mv = w.dn + J;
     w.alloc = reinterpret_cast<int*>(w.mv + J);
+    w.lthr = w.alloc + J;
+    w.lfac = reinterpret_cast<float*>(w.lthr + 8 * V);
     return w;
 }
 
-__device__ __forceinline__ unsigned long long shfl_max_u64(unsigned long long x) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
-        x = y > x ? y : x;
-    }
-    return x;
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k) {
+    const unsigned hi = (unsigned)(k >> 32);
+    const unsigned mh = __reduce_max_sync(FULL, hi);
+    const unsigned ml = __reduce_max_sync(FULL, hi == mh ? (unsigned)k : 0u);
+    return ((unsigned long long)mh << 32) | ml;
 }
 
 __device__ __forceinline__ unsigned long long shfl_sum_u64(unsigned long long x) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
     return x;
 }
 
@@ -106,74 +112,90 @@ struct InstView {
     const float* lf;
 };
 
-// Warp-collective: G*(rt') for rt' = rt + D*(k-1), k = 0,1,2 (or -1 if rt' < 0).
-__device__ __forceinline__ void gstar3(const InstView& in, int v, int nG, int rt, int D, float uT,
-                                       float* G) {
+// Warp-collective, once per stream: lambda* breakpoints.  lambda*(ri) depends
+// only on {admissible l : lmu_l <= ri}, which equals the set at
+// t* = max{lmu_l admissible, lmu_l <= ri}; so lane k stores t_k = lmu_k (if
+// admissible) and the factor of lambda*(t_k).
+__device__ void init_ladder(const InstView& in, const WarpState& S, int v, const ekya_dims& d) {
+    const int lane = threadIdx.x & 31, nL = d.n_lambda;
+    if (lane < 8) {
+        int t = INT_MAX;
+        float f = -1.0f;
+        if (lane < nL) {
+            const float stale = __ldg(in.stale + v);
+            const uint16_t m = __ldg(in.lmu + (size_t)v * nL + lane);
+            const float acc = fmul(stale, __ldg(in.lf + (size_t)v * nL + lane));
+            if (m != kLmuPad && acc >= d.a_min) {
+                t = m;
+                const int l = lambda_star(stale, in.lmu + (size_t)v * nL, in.lf + (size_t)v * nL, nL, m, d.a_min);
+                f = __ldg(in.lf + (size_t)v * nL + l);
+            }
+        }
+        S.lthr[v * 8 + lane] = t;
+        S.lfac[v * 8 + lane] = f;
+    }
+}
+
+// Warp-collective update of stream v's entries in the state arrays.
+__device__ __forceinline__ void update_stream(const InstView& in, const WarpState& S, int v, const ekya_dims& d) {
     const int lane = threadIdx.x & 31;
+    const int D = d.steal_units, nG = d.n_gamma;
+    const int ri = S.alloc[2 * v], rt = S.alloc[2 * v + 1];
     const float stale = __ldg(in.stale + v);
     float cost = 0.0f, post = 0.0f;
     if (lane >= 1 && lane <= nG) {
         cost = __ldg(in.cost + (size_t)v * nG + lane - 1);
         post = __ldg(in.post + (size_t)v * nG + lane - 1);
     }
+    const int tk = lane < 8 ? S.lthr[v * 8 + lane] : INT_MAX;
+    const float fk = lane < 8 ? S.lfac[v * 8 + lane] : -1.0f;
+    float G[3], fac[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        int r = rt + D * (k - 1);
+        const int r = rt + D * (k - 1);
         float g = -1.0f;
         if (lane == 0) g = stale;
         else if (lane <= nG) {
             float w;
-            if (window_acc(stale, post, cost, r, uT, &w)) g = w;
+            if (window_acc(stale, post, cost, r, d.unit_gpu_seconds, &w)) g = w;
         }
-        // values are >= 0 or -1: signed-int order of the bit patterns = float order
-        int m = __reduce_max_sync(0xffffffffu, __float_as_int(g));
+        // g is >= 0 or the -1 sentinel: signed-int order of the bits = float order
+        const int m = __reduce_max_sync(FULL, __float_as_int(g));
         G[k] = r < 0 ? -1.0f : __int_as_float(m);
+        const int ri2 = ri + D * (k - 1);
+        const unsigned key = (ri2 >= 0 && tk <= ri2) ? ((unsigned)(tk + 1) << 3) | (unsigned)lane : 0u;
+        const unsigned km = __reduce_max_sync(FULL, key);
+        const float f = __shfl_sync(FULL, fk, km & 7u);
+        fac[k] = km ? f : -1.0f;
     }
-}
-
-// Warp-collective update of stream v's entries in the state arrays.
-__device__ void update_stream(const InstView& in, const WarpState& S, int v, const ekya_dims& d) {
-    const int D = d.steal_units, nG = d.n_gamma, nL = d.n_lambda;
-    const int ri = S.alloc[2 * v], rt = S.alloc[2 * v + 1];
-    float G[3];
-    gstar3(in, v, nG, rt, D, d.unit_gpu_seconds, G);
-    const float stale = __ldg(in.stale + v);
-    const uint16_t* lmu = in.lmu + (size_t)v * nL;
-    const float* lf = in.lf + (size_t)v * nL;
-    float fac[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        int r = ri + D * (k - 1);
-        int l = r < 0 ? -1 : lambda_star(stale, lmu, lf, nL, r, d.a_min);
-        fac[k] = l < 0 ? -1.0f : __ldg(lf + l);
-    }
-    auto val = [&](int a, int b) -> unsigned long long {   // a: rt index, b: ri index
-        if (fac[b] < 0.0f) return 0ULL;
-        return q32(fmul(fac[b], G[a]));
-    };
-    if ((threadIdx.x & 31) == 0) {
-        unsigned long long c = val(1, 1);
-        long long cc = (long long)c;
-        S.cur[v] = c;
-        S.up[2 * v] = (long long)val(1, 2) - cc;
-        S.up[2 * v + 1] = (long long)val(2, 1) - cc;
-        S.dn[2 * v] = ri >= D ? (long long)val(1, 0) - cc : kInvalid;
-        S.dn[2 * v + 1] = rt >= D ? (long long)val(0, 1) - cc : kInvalid;
-        // thief = inference (2v), victim = training: (rt - D, ri + D)
-        S.mv[2 * v] = rt >= D ? (long long)val(0, 2) - cc : kInvalid;
-        // thief = training (2v+1), victim = inference: (rt + D, ri - D)
-        S.mv[2 * v + 1] = ri >= D ? (long long)val(2, 0) - cc : kInvalid;
+    // lanes 0..6 each produce one of the seven entries:
+    // lane: 0 cur (rt,ri) 1 (rt,ri+D) 2 (rt+D,ri) 3 (rt,ri-D) 4 (rt-D,ri) 5 (rt+D,ri-D) 6 (rt-D,ri+D)
+    if (lane < 7) {
+        const float Ga = (lane == 2 || lane == 5) ? G[2] : (lane == 4 || lane == 6) ? G[0] : G[1];
+        const float fb = (lane == 1 || lane == 6) ? fac[2] : (lane == 3 || lane == 5) ? fac[0] : fac[1];
+        const unsigned long long val = fb < 0.0f ? 0ULL : q32(fmul(fb, Ga));
+        const unsigned long long c = fac[1] < 0.0f ? 0ULL : q32(fmul(fac[1], G[1]));
+        const long long dv = (long long)val - (long long)c;
+        switch (lane) {
+            case 0: S.cur[v] = c; break;
+            case 1: S.up[2 * v] = dv; break;                                   // inference +D
+            case 2: S.up[2 * v + 1] = dv; break;                               // training  +D
+            case 3: S.dn[2 * v] = ri >= D ? dv : kInvalid; break;              // inference -D
+            case 4: S.dn[2 * v + 1] = rt >= D ? dv : kInvalid; break;          // training  -D
+            case 5: S.mv[2 * v + 1] = ri >= D ? dv : kInvalid; break;          // thief = training
+            case 6: S.mv[2 * v] = rt >= D ? dv : kInvalid; break;              // thief = inference
+        }
     }
     __syncwarp();
 }
 
-// Warp-collective: exact argmax config byte of stream v at its current split.
+// Warp-collective: exact argmax config byte of stream v at its final split.
 __device__ uint8_t stream_cfg(const InstView& in, int v, int ri, int rt, const ekya_dims& d) {
     const int lane = threadIdx.x & 31, nG = d.n_gamma, nL = d.n_lambda;
     const float stale = __ldg(in.stale + v);
-    int l = lambda_star(stale, in.lmu + (size_t)v * nL, in.lf + (size_t)v * nL, nL, ri, d.a_min);
+    const int l = lambda_star(stale, in.lmu + (size_t)v * nL, in.lf + (size_t)v * nL, nL, ri, d.a_min);
     if (l < 0) return (uint8_t)(kLambdaNone << 5);
-    float fac = __ldg(in.lf + (size_t)v * nL + l);
+    const float fac = __ldg(in.lf + (size_t)v * nL + l);
     float a = -1.0f;
     if (lane == 0) a = fmul(fac, stale);
     else if (lane <= nG) {
@@ -182,42 +204,52 @@ __device__ uint8_t stream_cfg(const InstView& in, int v, int ri, int rt, const e
                        __ldg(in.cost + (size_t)v * nG + lane - 1), rt, d.unit_gpu_seconds, &w))
             a = fmul(fac, w);
     }
-    int m = __reduce_max_sync(0xffffffffu, __float_as_int(a));
-    unsigned hits = __ballot_sync(0xffffffffu, __float_as_int(a) == m);
+    const int m = __reduce_max_sync(FULL, __float_as_int(a));
+    const unsigned hits = __ballot_sync(FULL, __float_as_int(a) == m);
     return (uint8_t)((__ffs(hits) - 1) | (l << 5));
 }
 
 __device__ __forceinline__ bool lit_cond(const WarpState& S, int t, int w, int J) {
     if (w >= J || w == t) return false;
     if ((w >> 1) == (t >> 1)) return S.mv[t] != kInvalid && S.mv[t] > 0;
-    long long dn = S.dn[w];
+    const long long dn = S.dn[w];
     return dn != kInvalid && S.up[t] + dn > 0;
+}
+
+__device__ __forceinline__ unsigned long long stream_down_key(const WarpState& S, int v) {
+    unsigned long long k = 0;
+    const long long d0 = S.dn[2 * v], d1 = S.dn[2 * v + 1];
+    if (d0 != kInvalid) k = dkey(d0, 2 * v);
+    if (d1 != kInvalid) {
+        const unsigned long long kk = dkey(d1, 2 * v + 1);
+        k = kk > k ? kk : k;
+    }
+    return k;
 }
 
 __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const ekya_dims& d = p.d;
-    const int V = d.n_streams, J = 2 * V, D = d.steal_units, U = d.units, nG = d.n_gamma,
-              nL = d.n_lambda;
+    const int V = d.n_streams, J = 2 * V, D = d.steal_units, U = d.units, nG = d.n_gamma, nL = d.n_lambda;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    WarpState S = carve(smem + warp * p.warp_bytes, V);
+    const WarpState S = carve(smem + warp * p.warp_bytes, V);
     const long long b = (long long)blockIdx.x * p.warps + warp;
     if (b >= d.n_inst) return;
 
-    InstView in{p.t.stale + b * V, p.t.cost + b * V * nG, p.t.post + b * V * nG,
-                p.t.lam_min_units + b * V * nL, p.t.lam_factor + b * V * nL};
+    const InstView in{p.t.stale + b * V, p.t.cost + b * V * nG, p.t.post + b * V * nG,
+                      p.t.lam_min_units + b * V * nL, p.t.lam_factor + b * V * nL};
 
     // ---- validity (R-ERR) ----
     bool ok = true;
     for (int i = lane; i < V; i += 32) ok &= in01(__ldg(in.stale + i));
     for (int i = lane; i < V * nG; i += 32) {
-        float c = __ldg(in.cost + i);
+        const float c = __ldg(in.cost + i);
         if (!(c >= 0.0f)) ok = false;
         else if (!isinf(c)) ok &= in01(__ldg(in.post + i));
     }
     for (int i = lane; i < V * nL; i += 32)
         if (__ldg(in.lmu + i) != kLmuPad) ok &= in01(__ldg(in.lf + i));
-    ok = __all_sync(0xffffffffu, ok);
+    ok = __all_sync(FULL, ok);
     if (!ok) {
         for (int j = lane; j < J; j += 32) p.out_alloc[b * J + j] = 0;
         for (int v = lane; v < V; v += 32) p.out_cfg[b * V + v] = 0;
@@ -230,13 +262,14 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
         return;
     }
 
-    // ---- fair start (C9) + initial per-stream entries ----
+    // ---- fair start (C9) + per-stream breakpoints and entries ----
     for (int v = lane; v < V; v += 32) {
-        int share = U / V + (v < U % V ? 1 : 0);
-        int rt = share / 2;
+        const int share = U / V + (v < U % V ? 1 : 0);
+        const int rt = share / 2;
         S.alloc[2 * v + 1] = rt;
         S.alloc[2 * v] = share - rt;
     }
+    for (int v = 0; v < V; ++v) init_ladder(in, S, v, d);
     __syncwarp();
     for (int v = 0; v < V; ++v) update_stream(in, S, v, d);
 
@@ -247,29 +280,23 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
             // per-stream best down, top-2 by stream
             unsigned long long k1 = 0;
             for (int v = lane; v < V; v += 32) {
-                unsigned long long k = 0;
-                long long d0 = S.dn[2 * v], d1 = S.dn[2 * v + 1];
-                if (d0 != kInvalid) k = dkey(d0, 2 * v);
-                if (d1 != kInvalid) { unsigned long long kk = dkey(d1, 2 * v + 1); k = kk > k ? kk : k; }
+                const unsigned long long k = stream_down_key(S, v);
                 k1 = k > k1 ? k : k1;
             }
-            k1 = shfl_max_u64(k1);
+            k1 = warp_max_u64(k1);
             const int s1 = k1 ? (key_job(k1) >> 1) : -1;
             unsigned long long k2 = 0;
             for (int v = lane; v < V; v += 32) {
                 if (v == s1) continue;
-                unsigned long long k = 0;
-                long long d0 = S.dn[2 * v], d1 = S.dn[2 * v + 1];
-                if (d0 != kInvalid) k = dkey(d0, 2 * v);
-                if (d1 != kInvalid) { unsigned long long kk = dkey(d1, 2 * v + 1); k = kk > k ? kk : k; }
+                const unsigned long long k = stream_down_key(S, v);
                 k2 = k > k2 ? k : k2;
             }
-            k2 = shfl_max_u64(k2);
+            k2 = warp_max_u64(k2);
             // per thief: best victim, then argmax over thieves
             unsigned long long bestkey = 0;
             int bestw = -1;
             for (int t = lane; t < J; t += 32) {
-                unsigned long long ck = ((t >> 1) != s1) ? k1 : k2;
+                const unsigned long long ck = ((t >> 1) != s1) ? k1 : k2;
                 bool have = false;
                 long long tot = 0;
                 int w = -1;
@@ -278,9 +305,9 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
                     w = key_job(ck);
                     have = true;
                 }
-                long long m = S.mv[t];
+                const long long m = S.mv[t];
                 if (m != kInvalid) {
-                    int ws = t ^ 1;
+                    const int ws = t ^ 1;
                     if (!have || m > tot || (m == tot && ws < w)) {
                         tot = m;
                         w = ws;
@@ -288,18 +315,18 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
                     }
                 }
                 if (have) {
-                    unsigned long long tk = dkey(tot, t);
+                    const unsigned long long tk = dkey(tot, t);
                     if (tk > bestkey) {
                         bestkey = tk;
                         bestw = w;
                     }
                 }
             }
-            unsigned long long gk = shfl_max_u64(bestkey);
+            const unsigned long long gk = warp_max_u64(bestkey);
             if (gk == 0 || key_delta(gk) <= 0) break;
             const int t = key_job(gk);
-            unsigned owner = __ballot_sync(0xffffffffu, bestkey == gk);
-            const int w = __shfl_sync(0xffffffffu, bestw, __ffs(owner) - 1);
+            const unsigned owner = __ballot_sync(FULL, bestkey == gk);
+            const int w = __shfl_sync(FULL, bestw, __ffs(owner) - 1);
             if (lane == 0) {
                 S.alloc[w] -= D;
                 S.alloc[t] += D;
@@ -316,7 +343,7 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
         for (int t = 0; t < J; ++t) {
             int pos = 0;
             while (pos < J) {
-                unsigned m = __ballot_sync(0xffffffffu, lit_cond(S, t, pos + lane, J));
+                const unsigned m = __ballot_sync(FULL, lit_cond(S, t, pos + lane, J));
                 if (!m) {
                     pos += 32;
                     continue;
@@ -343,7 +370,7 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
     const unsigned long long sum = shfl_sum_u64(part);
     for (int j = lane; j < J; j += 32) p.out_alloc[b * J + j] = (uint16_t)S.alloc[j];
     for (int v = 0; v < V; ++v) {
-        uint8_t c = stream_cfg(in, v, S.alloc[2 * v], S.alloc[2 * v + 1], d);
+        const uint8_t c = stream_cfg(in, v, S.alloc[2 * v], S.alloc[2 * v + 1], d);
         if (lane == 0) p.out_cfg[b * V + v] = c;
     }
     if (lane == 0) {
@@ -374,8 +401,7 @@ int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int m
     size_t smem = p.warp_bytes * p.warps;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0) return EKYA_OK;
-    cudaError_t e = cudaFuncSetAttribute(thief_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(thief_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
     long long grid = (d.n_inst + p.warps - 1) / p.warps;
     if (grid > 0x7fffffffLL) return EKYA_ERR_SHAPE;

@@ -71,6 +71,14 @@ def uniform(seed: int, fid: int, *idx, device="cpu"):
     return (h >> 8).to(torch.float32) * (1.0 / 16777216.0)
 
 
+def _div(a, b):
+    """IEEE a / b with b broadcast to a tensor: torch computes tensor / python-scalar
+    as a reciprocal multiply on CUDA, which would break CPU/GPU bit-identity."""
+    if not torch.is_tensor(b):
+        b = torch.full_like(a, float(b))
+    return a / b
+
+
 def _ar(n, device):
     return torch.arange(n, dtype=torch.int64, device=device)
 
@@ -150,13 +158,13 @@ def sched_tables(cfg: SchedConfig, lo: int = 0, hi: int | None = None, device="c
         # cost: log-uniform over a 200x spread: uT * 0.25 * 200^u
         e = u(F_COST, b, v, g) * 7.643856
         cost = (uT * 0.25) * _exp2_approx(e)
-        x = cost / (uT * 10.0)
-        gain = gmax * (x / (1.0 + x))
+        x = _div(cost, uT * 10.0)
+        gain = gmax * _div(x, 1.0 + x)
         noise = (u(F_NOISE1, b, v, g) + u(F_NOISE2, b, v, g) + u(F_NOISE3, b, v, g) - 1.5) * 0.04
         post = torch.clamp((stale + gain) + noise, 0.0, 1.0)
         rho = torch.tensor(list(cfg.rho)[:L], dtype=torch.float32, device=device).view(1, 1, L)
         lf = rho + (1.0 - rho) * beta
-        lmu = torch.floor((rho * demand) / cfg.delta_gpu) + 1.0
+        lmu = torch.floor(_div(rho * demand, cfg.delta_gpu)) + 1.0
     stale = stale.view(B, V)
     cost = cost.expand(B, V, G).contiguous()
     post = post.expand(B, V, G).contiguous()
@@ -235,7 +243,7 @@ def profile_inputs(cfg: ProfileConfig, lo: int = 0, hi: int | None = None, devic
     r = u(F_CENTRE, qc, ci, cc)
     r = r * r
     r = r * r
-    centres = r / _rowsum(r).unsqueeze(-1)                       # [Q,K,C]
+    centres = _div(r, _rowsum(r).unsqueeze(-1).expand_as(r))                       # [Q,K,C]
 
     def windows(hidx):                                           # hidx [1,W] -> [Q,W,C], cluster id
         W = hidx.shape[1]
@@ -248,7 +256,7 @@ def profile_inputs(cfg: ProfileConfig, lo: int = 0, hi: int | None = None, devic
         bg = u(F_BG, q3, h3, c3)
         raw_b = bg * bg * bg
         raw = torch.where(clustered.unsqueeze(-1), raw_c, raw_b)
-        hist = raw / _rowsum(raw).unsqueeze(-1)
+        hist = _div(raw, _rowsum(raw).unsqueeze(-1).expand_as(raw))
         label = torch.where(clustered, cl, K + hidx.expand(Q, W))
         return hist, label
 
