@@ -36,6 +36,21 @@ __host__ __device__ inline size_t tab_bytes(int U) {
     return a16((size_t)(U + 1)) + a16((size_t)(U + 1) * kSlots * 4) + a16((size_t)(U + 1) * kSlots);
 }
 
+// first cell of row rt of a stream's triangle
+__device__ __forceinline__ int rowstart(int rt, int U) { return rt * (U + 1) - rt * (rt - 1) / 2; }
+
+// row of local cell c: the largest rt in [0, U] with rowstart(rt) <= c
+// (float estimate from the quadratic, then exact integer correction)
+__device__ __forceinline__ int row_of(int c, int U) {
+    const float A = 2.0f * (float)U + 3.0f;
+    const float disc = fmaxf(A * A - 8.0f * (float)c, 0.0f);
+    int r = (int)((A - sqrtf(disc)) * 0.5f);
+    r = max(0, min(r, U));
+    while (r < U && rowstart(r + 1, U) <= c) ++r;
+    while (r > 0 && rowstart(r, U) > c) --r;
+    return r;
+}
+
 struct Tabs {
     uint8_t* lad;
     float* tv;
@@ -66,16 +81,48 @@ struct EvalParams {
 // ------------------------------------------------------------------------
 // GRID
 // ------------------------------------------------------------------------
+// Cell-position tables, shared by every stream (the triangle depends only on U):
+// for each of the 4 alignments phi of a stream's first cell within a 16-byte
+// quad, quad k of the stream covers local cells 4k-phi .. 4k-phi+3 and
+// ci[phi][k][j] = (8*rt << 16) | ri of cell 4k-phi+j (0 outside the stream).
+__host__ __device__ inline size_t cellinfo_quads(int U) {
+    const long long NC = (long long)(U + 1) * (U + 2) / 2;
+    return (size_t)((NC + 3) / 4 + 1);
+}
+constexpr int kCellInfoMaxU = 109;   // 4 phases x quads x 16 B <= ~96 KB
+
+template <int GM>
 __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const ekya_dims& d = p.d;
     const int U = d.units, nG = d.n_gamma, nL = d.n_lambda, V = d.n_streams;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned char* mine = smem + (size_t)warp * p.warp_bytes;
+    const bool use_ci = U <= kCellInfoMaxU;
+    const size_t nq_tab = cellinfo_quads(U);
+    uint4* ci = reinterpret_cast<uint4*>(smem);
+    unsigned char* mine = smem + (use_ci ? 4 * nq_tab * sizeof(uint4) : 0) + (size_t)warp * p.warp_bytes;
     StreamIn* sin = reinterpret_cast<StreamIn*>(mine);
     Tabs T = carve_tabs(mine + a16(sizeof(StreamIn)), U);
+    const int NC = (U + 1) * (U + 2) / 2;
 
-    const long long NC = (long long)(U + 1) * (U + 2) / 2;
+    if (use_ci) {
+        for (int t = threadIdx.x; t < (int)(4 * nq_tab); t += blockDim.x) {
+            const int phi = t / (int)nq_tab, k = t - phi * (int)nq_tab;
+            unsigned e[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = 4 * k - phi + j;
+                e[j] = 0;
+                if (c >= 0 && c < NC) {
+                    const int rt = row_of(c, U);
+                    e[j] = ((unsigned)(rt * kSlots) << 16) | (unsigned)(c - rowstart(rt, U));
+                }
+            }
+            ci[t] = make_uint4(e[0], e[1], e[2], e[3]);
+        }
+        __syncthreads();
+    }
+
     const long long nwarps = (long long)gridDim.x * kGridWarps;
     // one warp per instance (validated once), its V streams in turn
     for (long long b = (long long)blockIdx.x * kGridWarps + warp; b < d.n_inst; b += nwarps) {
@@ -85,31 +132,66 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
             const long long item = b * V + v;
             if (ok) {
                 warp_load_stream(sin, p.t, item, nG, nL);
-                warp_build_tables(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tv, T.tc);
+                warp_build_tables<GM>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tv, T.tc);
             }
-            float* og = p.out_grid + item * NC;
-            uint8_t* oc = p.out_grid_cfg ? p.out_grid_cfg + item * NC : nullptr;
-            long long rs = 0;
-            for (int rt = 0; rt <= U; ++rt) {
-                const int len = U + 1 - rt;
-                float tvl = 0.0f;
-                unsigned tcl = 0;
-                if (ok) {
-                    tvl = T.tv[rt * kSlots + (lane & 7)];
-                    tcl = T.tc[rt * kSlots + (lane & 7)];
-                }
-                for (int k = 0; k < len; k += 32) {
-                    const int ri = k + lane;
-                    const bool act = ri < len;
-                    const int l = (act && ok) ? T.lad[ri] : kLambdaNone;
-                    const float val = __shfl_sync(0xffffffffu, tvl, l);
-                    const unsigned c = __shfl_sync(0xffffffffu, tcl, l);
-                    if (act) {
-                        og[rs + ri] = val;
-                        if (oc) oc[rs + ri] = (uint8_t)c;
+            // Flat write of the stream's cells [f0, f0 + NC) in aligned quads of 4
+            // cells: one 16-B value store + one 4-B config store per quad (the
+            // value and config arrays share the quad partition).  The quads at the
+            // two ends may be shared with the neighbouring streams; only this
+            // stream's cells of those are written, with scalar stores.
+            const long long f0 = item * NC, f1 = f0 + NC;
+            const int phi = (int)(f0 & 3);
+            const long long q0 = f0 >> 2;
+            const int nq = (int)(((f1 + 3) >> 2) - q0);
+            const uint4* cit = ci + (size_t)phi * nq_tab;
+            for (int k = lane; k < nq; k += 32) {
+                const long long fq = (q0 + k) << 2;
+                const int c0 = 4 * k - phi;
+                unsigned e[4];
+                if (use_ci) {
+                    const uint4 u = cit[k];
+                    e[0] = u.x; e[1] = u.y; e[2] = u.z; e[3] = u.w;
+                } else {
+                    const int cs = max(c0, 0);
+                    int rt = row_of(cs, U), ri = cs - rowstart(rt, U);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int c = c0 + j;
+                        e[j] = 0;
+                        if (c >= cs && c < NC) {
+                            e[j] = ((unsigned)(rt * kSlots) << 16) | (unsigned)ri;
+                            if (++ri > U - rt) { ++rt; ri = 0; }
+                        }
                     }
                 }
-                rs += len;
+                float v4[4];
+                unsigned cfg4 = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float val = 0.0f;
+                    unsigned cc = 0;
+                    if (ok) {
+                        const int ri = (int)(e[j] & 0xFFFFu);
+                        const int ix = (int)(e[j] >> 16) + T.lad[ri];
+                        val = T.tv[ix];
+                        cc = T.tc[ix];
+                    }
+                    v4[j] = val;
+                    cfg4 |= cc << (8 * j);
+                }
+                if (c0 >= 0 && c0 + 4 <= NC) {
+                    *reinterpret_cast<float4*>(p.out_grid + fq) = make_float4(v4[0], v4[1], v4[2], v4[3]);
+                    if (p.out_grid_cfg) *reinterpret_cast<unsigned*>(p.out_grid_cfg + fq) = cfg4;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int c = c0 + j;
+                        if (c >= 0 && c < NC) {
+                            p.out_grid[fq + j] = v4[j];
+                            if (p.out_grid_cfg) p.out_grid_cfg[fq + j] = (uint8_t)(cfg4 >> (8 * j));
+                        }
+                    }
+                }
             }
             __syncwarp();
         }
@@ -137,6 +219,7 @@ __host__ __device__ inline ListLayout list_layout(int U, int V) {
     return L;
 }
 
+template <int GM>
 __global__ void __launch_bounds__(kListThreads) list_kernel(EvalParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const ekya_dims& d = p.d;
@@ -184,7 +267,7 @@ __global__ void __launch_bounds__(kListThreads) list_kernel(EvalParams p) {
                 for (int v = warp; v < V; v += nw) {
                     warp_load_stream(sin, p.t, b * V + v, nG, nL);
                     Tabs T = carve_tabs(tabs + v * tb, U);
-                    warp_build_tables(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tv, T.tc);
+                    warp_build_tables<GM>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tv, T.tc);
                 }
             }
             ok = wok;
@@ -197,31 +280,34 @@ __global__ void __launch_bounds__(kListThreads) list_kernel(EvalParams p) {
                                                                 granules(src, 2).off);
         uint8_t* cdst = p.out_cfg ? p.out_cfg + (b * N + n0) * V : nullptr;
         uint8_t* cst = smem + L.cfgbuf + (cdst ? granules(cdst, 1).off : 0);
+        const size_t off_tv = a16((size_t)(U + 1));
+        const size_t off_tc = off_tv + a16((size_t)(U + 1) * kSlots * 4);
         for (int r = threadIdx.x; r < rows; r += kListThreads) {
-            const uint16_t* row = rs + (size_t)r * J;
+            // (ri, rt) of stream v is one 32-bit word (alloc is 4-byte aligned, J even)
+            const unsigned* row = reinterpret_cast<const unsigned*>(rs + (size_t)r * J);
             bool rok = ok;
             int tot = 0;
-            for (int j = 0; j < J; ++j) {
-                const int x = row[j];
-                tot += x;
-                rok &= x <= U;
+            unsigned long long S = 0;
+            const unsigned char* tp = tabs;
+            uint8_t* cr = cst + (size_t)r * V;
+            for (int v = 0; v < V; ++v, tp += tb) {
+                const unsigned pr = row[v];
+                int ri = (int)(pr & 0xFFFFu), rt = (int)(pr >> 16);
+                tot += ri + rt;
+                rok &= (ri <= U) & (rt <= U);
+                ri = min(ri, U);
+                rt = min(rt, U);
+                const int e = rt * kSlots + tp[ri];
+                S += q32(reinterpret_cast<const float*>(tp + off_tv)[e]);
+                if (cdst) cr[v] = tp[off_tc + e];
             }
             rok &= tot <= U;                     // Eq. 1 constraint 2
-            unsigned long long S = 0;
-            for (int v = 0; v < V; ++v) {
-                uint8_t c = 0;
-                if (rok) {
-                    const int ri = row[2 * v], rt = row[2 * v + 1];
-                    const unsigned char* tp = tabs + v * tb;
-                    const int l = tp[ri];
-                    const int e = rt * kSlots + l;
-                    const float val = reinterpret_cast<const float*>(tp + a16((size_t)(U + 1)))[e];
-                    c = (tp + a16((size_t)(U + 1)) + a16((size_t)(U + 1) * kSlots * 4))[e];
-                    S += q32(val);
-                }
-                if (cdst) cst[(size_t)r * V + v] = c;
+            if (!rok) {                          // R-ERR: zero the row
+                S = 0;
+                if (cdst)
+                    for (int v = 0; v < V; ++v) cr[v] = 0;
+                if (ok) flag_data_error(p.st);
             }
-            if (!rok && ok) flag_data_error(p.st);
             const long long o = b * N + n0 + r;
             p.out_sum[o] = S;
             if (p.out_mean) p.out_mean[o] = rok ? mean_q32(S, V) : 0.0f;
@@ -247,9 +333,17 @@ int resident_grid(ekya_handle* h, const void* fn, int threads, size_t smem, long
 
 }  // namespace
 
+template <typename F>
+F* pick_gm(int nG, F* k8, F* k16, F* k24, F* k32) {
+    const int g1 = nG + 1;
+    return g1 <= 8 ? k8 : g1 <= 16 ? k16 : g1 <= 24 ? k24 : k32;
+}
+
 int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, float* out_grid,
                      uint8_t* out_grid_cfg, cudaStream_t s) {
     if (d.units > 4094) return EKYA_ERR_SHAPE;
+    if ((reinterpret_cast<uintptr_t>(out_grid) & 15) || (reinterpret_cast<uintptr_t>(out_grid_cfg) & 3))
+        return EKYA_ERR_ARG;
     EvalParams p{};
     p.d = d;
     p.t = t;
@@ -257,14 +351,15 @@ int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, f
     p.out_grid = out_grid;
     p.out_grid_cfg = out_grid_cfg;
     p.warp_bytes = a16(sizeof(StreamIn)) + tab_bytes(d.units);
-    int warps = kGridWarps;
-    size_t smem = p.warp_bytes * warps;
+    const int warps = kGridWarps;
+    size_t smem = p.warp_bytes * warps + (d.units <= kCellInfoMaxU ? 4 * cellinfo_quads(d.units) * 16 : 0);
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0) return EKYA_OK;
-    cudaError_t e = cudaFuncSetAttribute(grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = pick_gm(d.n_gamma, grid_kernel<8>, grid_kernel<16>, grid_kernel<24>, grid_kernel<32>);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
-    int grid = resident_grid(h, (const void*)grid_kernel, kGridWarps * 32, smem, (d.n_inst + warps - 1) / warps);
-    grid_kernel<<<grid, kGridWarps * 32, smem, s>>>(p);
+    int grid = resident_grid(h, (const void*)kern, kGridWarps * 32, smem, (d.n_inst + warps - 1) / warps);
+    kern<<<grid, kGridWarps * 32, smem, s>>>(p);
     h->launches++;
     return cuda_status(cudaGetLastError());
 }
@@ -281,13 +376,15 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     p.out_sum = reinterpret_cast<unsigned long long*>(out_sum);
     p.out_mean = out_mean;
     p.out_cfg = out_cfg;
+    if (reinterpret_cast<uintptr_t>(alloc) & 3) return EKYA_ERR_ARG;
     size_t smem = list_layout(d.units, d.n_streams).total;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0 || n_alloc == 0) return EKYA_OK;
-    cudaError_t e = cudaFuncSetAttribute(list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = pick_gm(d.n_gamma, list_kernel<8>, list_kernel<16>, list_kernel<24>, list_kernel<32>);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
-    int grid = resident_grid(h, (const void*)list_kernel, kListThreads, smem, d.n_inst);
-    list_kernel<<<grid, kListThreads, smem, s>>>(p);
+    int grid = resident_grid(h, (const void*)kern, kListThreads, smem, d.n_inst);
+    kern<<<grid, kListThreads, smem, s>>>(p);
     h->launches++;
     return cuda_status(cudaGetLastError());
 }

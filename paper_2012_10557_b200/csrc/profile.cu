@@ -167,10 +167,10 @@ __host__ __device__ inline ScratchLayout scratch_layout(int H, int Hc, int C, in
     L.ps = o;     o += al16((size_t)kProfThreads * 8);
     L.pn = o;     o += al16((size_t)kProfThreads * 4);
     L.mu = o;     o += cluster ? al16((size_t)K * CP * 4) : 0;
-    L.sums = o;   o += cluster ? al16((size_t)K * C * 8) : 0;
-    L.cnt = o;    o += cluster ? al16((size_t)K * 4) : 0;
+    L.sums = o;   o += cluster ? al16((size_t)(kProfThreads / 32) * K * C * 8) : 0;
+    L.cnt = o;    o += cluster ? al16((size_t)(kProfThreads / 32) * K * 4) : 0;
     L.assign = o; o += cluster ? al16((size_t)H * 4) : 0;
-    L.chg = o;    o += cluster ? al16((size_t)H * 4) : 0;
+    L.chg = o;
     L.misc = o;   o += 64;
     L.total = o;
     return L;
@@ -252,25 +252,44 @@ __global__ void __launch_bounds__(kProfThreads, 1) radius_kernel(ProfParams P) {
 // ------------------------------------------------------------------------
 // CLUSTER
 // ------------------------------------------------------------------------
-// squared distance of x (registers, C <= 32) to centroid row m (shared, 16-B aligned)
-__device__ __forceinline__ float dist2_reg(const float (&x)[32], const float* m, int C) {
-    const float4* m4 = reinterpret_cast<const float4*>(m);
-    float s = 0.0f;
+// Nearest centroid of x (registers, zero-padded to 32 classes) among K
+// centroid rows of CP floats (zero-padded, 16-B aligned): four centroids are
+// processed together for ILP; the padded terms are fl(0 - 0)^2 = +0 and
+// s + 0 = s exactly, so each distance equals rule 5's sequential sum over the C
+// real classes.  Lowest index wins ties (C19).
+__device__ __forceinline__ int nearest_reg(const float (&x)[32], const float* mu, int K, int CP) {
+    int best = 0;
+    float bd = 0.0f;
+    for (int i0 = 0; i0 < K; i0 += 4) {
+        float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int c4 = 0; c4 < 8; ++c4) {
-        if (c4 * 4 < C) {
-            float4 v = m4[c4];
-            float mv[4] = {v.x, v.y, v.z, v.w};
+        for (int c4 = 0; c4 < 8; ++c4) {
+            if (c4 * 4 < CP) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (c4 * 4 + j < C) {
-                    float d = fsub(x[c4 * 4 + j], mv[j]);
-                    s = fadd(s, fmul(d, d));
+                for (int k = 0; k < 4; ++k) {
+                    if (i0 + k < K) {
+                        const float4 m = *reinterpret_cast<const float4*>(mu + (i0 + k) * CP + c4 * 4);
+                        float d0 = fsub(x[c4 * 4 + 0], m.x);
+                        s[k] = fadd(s[k], fmul(d0, d0));
+                        float d1 = fsub(x[c4 * 4 + 1], m.y);
+                        s[k] = fadd(s[k], fmul(d1, d1));
+                        float d2 = fsub(x[c4 * 4 + 2], m.z);
+                        s[k] = fadd(s[k], fmul(d2, d2));
+                        float d3 = fsub(x[c4 * 4 + 3], m.w);
+                        s[k] = fadd(s[k], fmul(d3, d3));
+                    }
                 }
             }
         }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (i0 + k < K && (i0 + k == 0 || s[k] < bd)) {
+                bd = s[k];
+                best = i0 + k;
+            }
+        }
     }
-    return s;
+    return best;
 }
 
 __device__ __forceinline__ float dist2_mem(const float* x, const float* m, int C) {
@@ -285,10 +304,11 @@ __device__ __forceinline__ float dist2_mem(const float* x, const float* m, int C
 template <bool REG>
 __device__ __forceinline__ int nearest_c(const float (&xr)[32], const float* xm, const float* mu, int K, int C,
                                          int CP) {
+    if (REG) return nearest_reg(xr, mu, K, CP);
     int best = 0;
     float bd = 0.0f;
     for (int i = 0; i < K; ++i) {
-        float d = REG ? dist2_reg(xr, mu + i * CP, C) : dist2_mem(xm, mu + i * CP, C);
+        float d = dist2_mem(xm, mu + i * CP, C);
         if (i == 0 || d < bd) {   // lowest index on ties (C19)
             bd = d;
             best = i;
@@ -311,25 +331,40 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
     unsigned long long* ps = reinterpret_cast<unsigned long long*>(scratch + S.ps);
     int* pn = reinterpret_cast<int*>(scratch + S.pn);
     float* mu = reinterpret_cast<float*>(scratch + S.mu);
-    unsigned long long* sums = reinterpret_cast<unsigned long long*>(scratch + S.sums);
-    int* cnt = reinterpret_cast<int*>(scratch + S.cnt);
+    // per-warp exact partial cluster sums: part[w][i][c] = sum of Q32(h_c) over the
+    // windows owned by warp w that sit in cluster i (lane c owns column c, so no atomics)
+    unsigned long long* part = reinterpret_cast<unsigned long long*>(scratch + S.sums);
+    int* pcnt = reinterpret_cast<int*>(scratch + S.cnt);
     int* assign = reinterpret_cast<int*>(scratch + S.assign);
-    int* chg = reinterpret_cast<int*>(scratch + S.chg);
-    int* misc = reinterpret_cast<int*>(scratch + S.misc);   // [0..1] change counters, [2] query cluster, [3] ok
+    int* misc = reinterpret_cast<int*>(scratch + S.misc);   // [2] = query cluster
 
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kProfThreads / 32;
     const long long Q = P.p.n_query;
     const long long items = Q > blockIdx.x ? (Q - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    unsigned long long* mypart = part + (size_t)warp * K * C;
+    int* mycnt = pcnt + warp * K;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&bar[s], 1);
         fence_barrier_init();
-        misc[0] = misc[1] = 0;
     }
     __syncthreads();
     if (threadIdx.x == 0)
         for (long long i = 0; i < NS && i < items; ++i)
             issue_item(P, smem + (i % NS) * P.stage_bytes, &bar[i % NS], blockIdx.x + i * gridDim.x, 0, H, accs, L);
+
+    // move window h (owned by this warp) from cluster oa to na in the warp's partials
+    auto move = [&](int h, int oa, int na, const float* hs) {
+        for (int c = lane; c < C; c += 32) {
+            const unsigned long long v = q32(hs[(size_t)h * C + c]);
+            if (oa >= 0) mypart[oa * C + c] -= v;
+            mypart[na * C + c] += v;
+        }
+        if (lane == 0) {
+            if (oa >= 0) mycnt[oa] -= 1;
+            mycnt[na] += 1;
+        }
+    };
 
     for (long long i = 0; i < items; ++i) {
         const int s = (int)(i % NS);
@@ -341,80 +376,85 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
         for (int c = threadIdx.x; c < C; c += blockDim.x) ok &= in01(sp.cur[c]);
         int qc = -1;
         if (H > 0) {
-            // own window's histogram in registers (REG: H <= threads, C <= 32)
+            // own window's histogram in registers (REG: H <= threads, C <= 32), zero padded
             float xr[32];
-            const int hme = threadIdx.x;
             if (REG) {
+                const int h = threadIdx.x;
 #pragma unroll
-                for (int c = 0; c < 32; ++c) xr[c] = (hme < H && c < C) ? hs[(size_t)hme * C + c] : 0.0f;
+                for (int c = 0; c < 32; ++c) {
+                    float x = 0.0f;
+                    if (h < H && c < C) {
+                        x = hs[(size_t)h * C + c];
+                        ok &= in01(x);
+                    }
+                    xr[c] = x;
+                }
+            } else {
+                for (int t = threadIdx.x; t < H * C; t += blockDim.x) ok &= in01(hs[t]);
             }
-            for (int t = threadIdx.x; t < H * C; t += blockDim.x) ok &= in01(hs[t]);
             for (int t = threadIdx.x; t < K * CP; t += blockDim.x) {
-                int ci = t / CP, c = t - ci * CP;
+                const int ci = t / CP, c = t - ci * CP;
                 mu[t] = c < C ? hs[(size_t)(((long long)ci * H) / K) * C + c] : 0.0f;
             }
-            for (int t = threadIdx.x; t < K * C; t += blockDim.x) sums[t] = 0ULL;
-            for (int t = threadIdx.x; t < K; t += blockDim.x) cnt[t] = 0;
+            for (int t = lane; t < K * C; t += 32) mypart[t] = 0ULL;
+            for (int t = lane; t < K; t += 32) mycnt[t] = 0;
             __syncthreads();
-            // initial assignment
-            for (int h = threadIdx.x; h < H; h += blockDim.x)
-                assign[h] = nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
-            __syncthreads();
-            // full exact cluster sums (warp per window, lanes over classes)
-            for (int h = warp; h < H; h += nwarps) {
-                const int ah = assign[h];
-                for (int c = lane; c < C; c += 32) atomicAdd(&sums[ah * C + c], q32(hs[(size_t)h * C + c]));
-                if (lane == 0) atomicAdd(&cnt[ah], 1);
+            // initial assignment; each warp accumulates its own windows
+            for (int h0 = warp * 32; h0 < H; h0 += kProfThreads) {
+                const int h = h0 + lane;
+                int a = 0;
+                if (h < H) {
+                    a = nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
+                    assign[h] = a;
+                }
+                const int nh = min(32, H - h0);
+                for (int j = 0; j < nh; ++j) move(h0 + j, -1, __shfl_sync(0xffffffffu, a, j), hs);
             }
             __syncthreads();
             for (int it = 0; it < P.p.max_iter; ++it) {
-                const int cidx = it & 1;
+                // centroid update from the exact sums (empty cluster keeps its centroid)
                 for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
-                    int ci = t / C, c = t - ci * C;
-                    if (cnt[ci] > 0) mu[ci * CP + c] = mean_q32(sums[t], cnt[ci]);   // empty keeps centroid
+                    const int ci = t / C, c = t - ci * C;
+                    unsigned long long sum = 0;
+                    int n = 0;
+                    for (int w = 0; w < nwarps; ++w) {
+                        sum += part[((size_t)w * K + ci) * C + c];
+                        n += pcnt[w * K + ci];
+                    }
+                    if (n > 0) mu[ci * CP + c] = mean_q32(sum, n);
                 }
                 __syncthreads();
-                for (int h = threadIdx.x; h < H; h += blockDim.x) {
-                    int na = nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
-                    int oa = assign[h];
-                    if (na != oa) {
-                        int slot = atomicAdd(&misc[cidx], 1);
-                        chg[slot] = h | (oa << 16) | (na << 24);
+                // reassign; each warp moves its own changed windows between clusters
+                int changed = 0;
+                for (int h0 = warp * 32; h0 < H; h0 += kProfThreads) {
+                    const int h = h0 + lane;
+                    int oa = 0, na = 0;
+                    if (h < H) {
+                        na = nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
+                        oa = assign[h];
                         assign[h] = na;
                     }
-                }
-                __syncthreads();
-                const int nchg = misc[cidx];
-                if (threadIdx.x == 0) misc[cidx ^ 1] = 0;
-                if (nchg == 0) break;
-                for (int e = warp; e < nchg; e += nwarps) {
-                    const int rec = chg[e];
-                    const int h = rec & 0xFFFF, oa = (rec >> 16) & 0xFF, na = (rec >> 24) & 0xFF;
-                    for (int c = lane; c < C; c += 32) {
-                        unsigned long long v = q32(hs[(size_t)h * C + c]);
-                        atomicAdd(&sums[oa * C + c], 0ULL - v);
-                        atomicAdd(&sums[na * C + c], v);
-                    }
-                    if (lane == 0) {
-                        atomicSub(&cnt[oa], 1);
-                        atomicAdd(&cnt[na], 1);
+                    unsigned m = __ballot_sync(0xffffffffu, na != oa);
+                    changed |= m != 0;
+                    while (m) {
+                        const int j = __ffs(m) - 1;
+                        m &= m - 1;
+                        move(h0 + j, __shfl_sync(0xffffffffu, oa, j), __shfl_sync(0xffffffffu, na, j), hs);
                     }
                 }
-                __syncthreads();
+                if (!__syncthreads_or(changed)) break;
             }
-            __syncthreads();
-            if (threadIdx.x == 0) misc[0] = misc[1] = 0;
             // the query joins its nearest centroid: lane i computes distance to centroid i
             if (warp == 0) {
                 unsigned long long key = ~0ULL;
                 for (int ci = lane; ci < K; ci += 32) {
-                    float d = dist2_mem(sp.cur, mu + ci * CP, C);
-                    unsigned long long k = ((unsigned long long)__float_as_uint(d) << 8) | (unsigned)ci;
+                    const float d = dist2_mem(sp.cur, mu + ci * CP, C);
+                    const unsigned long long k = ((unsigned long long)__float_as_uint(d) << 8) | (unsigned)ci;
                     key = k < key ? k : key;
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
-                    unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+                    const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
                     key = y < key ? y : key;
                 }
                 if (lane == 0) misc[2] = (int)(key & 0xFF);
