@@ -31,9 +31,9 @@ constexpr int kListStages = 2;
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// per-stream table footprint
+// per-stream table footprint: lad[U+1] + tvc[U+1][8] (uint2)
 __host__ __device__ inline size_t tab_bytes(int U) {
-    return a16((size_t)(U + 1)) + a16((size_t)(U + 1) * kSlots * 4) + a16((size_t)(U + 1) * kSlots);
+    return a16((size_t)(U + 1)) + a16((size_t)(U + 1) * kSlots * 8);
 }
 
 // first cell of row rt of a stream's triangle
@@ -53,14 +53,12 @@ __device__ __forceinline__ int row_of(int c, int U) {
 
 struct Tabs {
     uint8_t* lad;
-    float* tv;
-    uint8_t* tc;
+    uint2* tvc;
 };
 __device__ __forceinline__ Tabs carve_tabs(unsigned char* p, int U) {
     Tabs t;
     t.lad = p;
-    t.tv = reinterpret_cast<float*>(p + a16((size_t)(U + 1)));
-    t.tc = p + a16((size_t)(U + 1)) + a16((size_t)(U + 1) * kSlots * 4);
+    t.tvc = reinterpret_cast<uint2*>(p + a16((size_t)(U + 1)));
     return t;
 }
 
@@ -132,7 +130,7 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
             const long long item = b * V + v;
             if (ok) {
                 warp_load_stream(sin, p.t, item, nG, nL);
-                warp_build_tables<GM>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tv, T.tc);
+                warp_build_tables<GM>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc);
             }
             // Flat write of the stream's cells [f0, f0 + NC) in aligned quads of 4
             // cells: one 16-B value store + one 4-B config store per quad (the
@@ -166,18 +164,16 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
                 }
                 float v4[4];
                 unsigned cfg4 = 0;
+                if (ok) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    float val = 0.0f;
-                    unsigned cc = 0;
-                    if (ok) {
-                        const int ri = (int)(e[j] & 0xFFFFu);
-                        const int ix = (int)(e[j] >> 16) + T.lad[ri];
-                        val = T.tv[ix];
-                        cc = T.tc[ix];
+                    for (int j = 0; j < 4; ++j) {
+                        const uint2 vc = T.tvc[(e[j] >> 16) + T.lad[e[j] & 0xFFFFu]];
+                        v4[j] = __uint_as_float(vc.x);
+                        cfg4 |= vc.y << (8 * j);
                     }
-                    v4[j] = val;
-                    cfg4 |= cc << (8 * j);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v4[j] = 0.0f;
                 }
                 if (c0 >= 0 && c0 + 4 <= NC) {
                     *reinterpret_cast<float4*>(p.out_grid + fq) = make_float4(v4[0], v4[1], v4[2], v4[3]);
@@ -220,7 +216,7 @@ __host__ __device__ inline ListLayout list_layout(int U, int V) {
 }
 
 template <int GM>
-__global__ void __launch_bounds__(kListThreads) list_kernel(EvalParams p) {
+__global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const ekya_dims& d = p.d;
     const int U = d.units, nG = d.n_gamma, nL = d.n_lambda, V = d.n_streams, J = 2 * V;
@@ -267,7 +263,7 @@ __global__ void __launch_bounds__(kListThreads) list_kernel(EvalParams p) {
                 for (int v = warp; v < V; v += nw) {
                     warp_load_stream(sin, p.t, b * V + v, nG, nL);
                     Tabs T = carve_tabs(tabs + v * tb, U);
-                    warp_build_tables<GM>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tv, T.tc);
+                    warp_build_tables<GM>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc);
                 }
             }
             ok = wok;
@@ -280,8 +276,7 @@ __global__ void __launch_bounds__(kListThreads) list_kernel(EvalParams p) {
                                                                 granules(src, 2).off);
         uint8_t* cdst = p.out_cfg ? p.out_cfg + (b * N + n0) * V : nullptr;
         uint8_t* cst = smem + L.cfgbuf + (cdst ? granules(cdst, 1).off : 0);
-        const size_t off_tv = a16((size_t)(U + 1));
-        const size_t off_tc = off_tv + a16((size_t)(U + 1) * kSlots * 4);
+        const size_t off_tvc = a16((size_t)(U + 1));
         for (int r = threadIdx.x; r < rows; r += kListThreads) {
             // (ri, rt) of stream v is one 32-bit word (alloc is 4-byte aligned, J even)
             const unsigned* row = reinterpret_cast<const unsigned*>(rs + (size_t)r * J);
@@ -297,9 +292,9 @@ __global__ void __launch_bounds__(kListThreads) list_kernel(EvalParams p) {
                 rok &= (ri <= U) & (rt <= U);
                 ri = min(ri, U);
                 rt = min(rt, U);
-                const int e = rt * kSlots + tp[ri];
-                S += q32(reinterpret_cast<const float*>(tp + off_tv)[e]);
-                if (cdst) cr[v] = tp[off_tc + e];
+                const uint2 vc = reinterpret_cast<const uint2*>(tp + off_tvc)[rt * kSlots + tp[ri]];
+                S += q32(__uint_as_float(vc.x));
+                if (cdst) cr[v] = (uint8_t)vc.y;
             }
             rok &= tot <= U;                     // Eq. 1 constraint 2
             if (!rok) {                          // R-ERR: zero the row

@@ -292,6 +292,81 @@ __device__ __forceinline__ int nearest_reg(const float (&x)[32], const float* mu
     return best;
 }
 
+// Squared distances of x (registers, zero padded) to N centroid rows, all N
+// chains interleaved for ILP; padded classes contribute fl(0-0)^2 = +0 (exact).
+template <int N>
+__device__ __forceinline__ void dist_n(const float (&x)[32], const float* r0, const float* r1, const float* r2,
+                                       const float* r3, int CP, float (&s)[4]) {
+    const float* rows[4] = {r0, r1, r2, r3};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s[k] = 0.0f;
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+        if (c4 * 4 < CP) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                const float4 m = *reinterpret_cast<const float4*>(rows[k] + c4 * 4);
+                const float d0 = fsub(x[c4 * 4 + 0], m.x);
+                s[k] = fadd(s[k], fmul(d0, d0));
+                const float d1 = fsub(x[c4 * 4 + 1], m.y);
+                s[k] = fadd(s[k], fmul(d1, d1));
+                const float d2 = fsub(x[c4 * 4 + 2], m.z);
+                s[k] = fadd(s[k], fmul(d2, d2));
+                const float d3 = fsub(x[c4 * 4 + 3], m.w);
+                s[k] = fadd(s[k], fmul(d3, d3));
+            }
+        }
+    }
+}
+
+// Nearest of K <= 8 centroids with a per-thread distance cache: only the
+// centroids in `chg` (those whose coordinates changed bitwise since the cache
+// was filled) are recomputed -- an unchanged centroid has bit-identical
+// distances.  Lowest index wins ties (C19).
+__device__ __forceinline__ int nearest_cached(const float (&x)[32], const float* mu, int K, int CP, unsigned chg,
+                                              float (&dc)[8]) {
+    unsigned m = chg;
+    while (m) {   // chg is block-uniform: no divergence
+        int id[4] = {-1, -1, -1, -1};
+        int n = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (m) {
+                id[k] = __ffs(m) - 1;
+                m &= m - 1;
+                ++n;
+            }
+        }
+        float s[4];
+        const float* r0 = mu + max(id[0], 0) * CP;
+        const float* r1 = mu + max(id[1], 0) * CP;
+        const float* r2 = mu + max(id[2], 0) * CP;
+        const float* r3 = mu + max(id[3], 0) * CP;
+        switch (n) {
+            case 1: dist_n<1>(x, r0, r1, r2, r3, CP, s); break;
+            case 2: dist_n<2>(x, r0, r1, r2, r3, CP, s); break;
+            case 3: dist_n<3>(x, r0, r1, r2, r3, CP, s); break;
+            default: dist_n<4>(x, r0, r1, r2, r3, CP, s); break;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (id[k] == j) dc[j] = s[k];
+        }
+    }
+    int best = 0;
+    float bd = dc[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+        if (j < K && dc[j] < bd) {
+            bd = dc[j];
+            best = j;
+        }
+    }
+    return best;
+}
+
 __device__ __forceinline__ float dist2_mem(const float* x, const float* m, int C) {
     float s = 0.0f;
     for (int c = 0; c < C; ++c) {
@@ -319,6 +394,7 @@ __device__ __forceinline__ int nearest_c(const float (&xr)[32], const float* xm,
 
 template <bool REG>
 __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) {
+    // REG && k <= 8: per-thread distance cache, recompute only changed centroids
     extern __shared__ __align__(128) unsigned char smem[];
     const int H = P.p.n_hist, C = P.p.n_class, G = P.p.n_gamma, K = P.p.k, NS = P.stages;
     const int CP = (C + 3) & ~3;
@@ -336,7 +412,8 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
     unsigned long long* part = reinterpret_cast<unsigned long long*>(scratch + S.sums);
     int* pcnt = reinterpret_cast<int*>(scratch + S.cnt);
     int* assign = reinterpret_cast<int*>(scratch + S.assign);
-    int* misc = reinterpret_cast<int*>(scratch + S.misc);   // [2] = query cluster
+    int* misc = reinterpret_cast<int*>(scratch + S.misc);   // [2] query cluster, [3..4] changed-centroid masks
+    const bool cache = REG && K <= 8;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kProfThreads / 32;
     const long long Q = P.p.n_query;
@@ -378,6 +455,9 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
         if (H > 0) {
             // own window's histogram in registers (REG: H <= threads, C <= 32), zero padded
             float xr[32];
+            float dc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dc[j] = 0.0f;
             if (REG) {
                 const int h = threadIdx.x;
 #pragma unroll
@@ -398,13 +478,16 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
             }
             for (int t = lane; t < K * C; t += 32) mypart[t] = 0ULL;
             for (int t = lane; t < K; t += 32) mycnt[t] = 0;
+            if (threadIdx.x == 0) misc[3] = misc[4] = 0;
             __syncthreads();
+            const unsigned all_k = K >= 32 ? 0xffffffffu : ((1u << K) - 1u);
             // initial assignment; each warp accumulates its own windows
             for (int h0 = warp * 32; h0 < H; h0 += kProfThreads) {
                 const int h = h0 + lane;
                 int a = 0;
                 if (h < H) {
-                    a = nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
+                    a = cache ? nearest_cached(xr, mu, K, CP, all_k, dc)
+                              : nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
                     assign[h] = a;
                 }
                 const int nh = min(32, H - h0);
@@ -421,16 +504,25 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
                         sum += part[((size_t)w * K + ci) * C + c];
                         n += pcnt[w * K + ci];
                     }
-                    if (n > 0) mu[ci * CP + c] = mean_q32(sum, n);
+                    if (n > 0) {
+                        const float nm = mean_q32(sum, n);
+                        if (__float_as_uint(nm) != __float_as_uint(mu[ci * CP + c])) {
+                            mu[ci * CP + c] = nm;
+                            atomicOr(reinterpret_cast<unsigned*>(&misc[3 + (it & 1)]), 1u << ci);
+                        }
+                    }
                 }
                 __syncthreads();
+                const unsigned chg = (unsigned)misc[3 + (it & 1)];
+                if (threadIdx.x == 0) misc[3 + ((it + 1) & 1)] = 0;
                 // reassign; each warp moves its own changed windows between clusters
                 int changed = 0;
                 for (int h0 = warp * 32; h0 < H; h0 += kProfThreads) {
                     const int h = h0 + lane;
                     int oa = 0, na = 0;
                     if (h < H) {
-                        na = nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
+                        na = cache ? nearest_cached(xr, mu, K, CP, chg, dc)
+                                   : nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
                         oa = assign[h];
                         assign[h] = na;
                     }
