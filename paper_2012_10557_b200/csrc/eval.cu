@@ -25,9 +25,9 @@ namespace ekya {
 namespace {
 
 constexpr int kGridWarps = 16;
-constexpr int kListThreads = 256;
+constexpr int kListThreads = 512;
 constexpr int kListRows = 512;      // rows per pipeline stage
-constexpr int kListStages = 2;
+constexpr int kListStages = 4;
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -197,20 +197,38 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
 // ------------------------------------------------------------------------
 // LIST
 // ------------------------------------------------------------------------
-struct ListLayout {
-    size_t sin, tabs, stage, cfgbuf, bars, misc, total, stage_bytes;
+// Instance inputs (stale, cost, post, lam_min_units, lam_factor of one
+// instance) staged by the TMA alongside the instance's first row chunk.
+struct InstLayout {
+    size_t stale, cost, post, lmu, lf, total;
 };
-__host__ __device__ inline ListLayout list_layout(int U, int V) {
+__host__ __device__ inline InstLayout inst_layout(int V, int nG, int nL) {
+    InstLayout L;
+    size_t o = 0;
+    L.stale = o; o += a16((size_t)V * 4) + 16;
+    L.cost = o;  o += a16((size_t)V * nG * 4) + 16;
+    L.post = o;  o += a16((size_t)V * nG * 4) + 16;
+    L.lmu = o;   o += a16((size_t)V * nL * 2) + 16;
+    L.lf = o;    o += a16((size_t)V * nL * 4) + 16;
+    L.total = o;
+    return L;
+}
+
+struct ListLayout {
+    size_t sin, tabs, stage, cfgbuf, bars, total, rows_bytes, stage_bytes, cfg_bytes;
+};
+__host__ __device__ inline ListLayout list_layout(int U, int V, int nG, int nL) {
     ListLayout L;
     const int J = 2 * V;
     size_t o = 0;
     L.sin = o;    o += a16(sizeof(StreamIn)) * (kListThreads / 32);
     L.tabs = o;   o += tab_bytes(U) * V;
-    L.stage_bytes = a16((size_t)kListRows * J * 2) + 16;
+    L.rows_bytes = a16((size_t)kListRows * J * 2) + 16;
+    L.stage_bytes = L.rows_bytes + inst_layout(V, nG, nL).total;
     L.stage = o;  o += L.stage_bytes * kListStages;
-    L.cfgbuf = o; o += a16((size_t)kListRows * V) + 16;
-    L.bars = o;   o += 64;
-    L.misc = o;   o += 16;
+    L.cfg_bytes = a16((size_t)kListRows * V) + 16;
+    L.cfgbuf = o; o += L.cfg_bytes * 2;
+    L.bars = o;   o += 8 * kListStages;
     L.total = o;
     return L;
 }
@@ -221,12 +239,12 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     const ekya_dims& d = p.d;
     const int U = d.units, nG = d.n_gamma, nL = d.n_lambda, V = d.n_streams, J = 2 * V;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kListThreads / 32;
-    const ListLayout L = list_layout(U, V);
+    const ListLayout L = list_layout(U, V, nG, nL);
+    const InstLayout IL = inst_layout(V, nG, nL);
     StreamIn* sin = reinterpret_cast<StreamIn*>(smem + L.sin + warp * a16(sizeof(StreamIn)));
     unsigned char* tabs = smem + L.tabs;
     const size_t tb = tab_bytes(U);
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bars);
-    int* misc = reinterpret_cast<int*>(smem + L.misc);
 
     const long long N = p.n_alloc;
     const long long nch = (N + kListRows - 1) / kListRows;
@@ -234,13 +252,30 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     const long long items = nb_local * nch;
     auto item_b = [&](long long i) { return (long long)blockIdx.x + (i / nch) * gridDim.x; };
     auto item_n0 = [&](long long i) { return (i % nch) * kListRows; };
-    auto issue = [&](long long i) {   // leader thread only
+    // leader thread: one row chunk (+ the instance inputs with its first chunk)
+    auto issue = [&](long long i) {
         const long long b = item_b(i), n0 = item_n0(i);
         const long long rows = min((long long)kListRows, N - n0);
-        Granules g = granules(p.alloc + (b * N + n0) * J, (size_t)rows * J * 2);
-        unsigned char* dst = smem + L.stage + (i % kListStages) * L.stage_bytes;
-        mbar_arrive_expect_tx(&bar[i % kListStages], g.bytes);
-        bulk_g2s(dst, g.g0, g.bytes, &bar[i % kListStages]);
+        unsigned char* st = smem + L.stage + (i % kListStages) * L.stage_bytes;
+        unsigned long long* br = &bar[i % kListStages];
+        const Granules g = granules(p.alloc + (b * N + n0) * J, (size_t)rows * J * 2);
+        unsigned tot = g.bytes;
+        Granules gi[5];
+        if (n0 == 0) {
+            gi[0] = granules(p.t.stale + b * V, (size_t)V * 4);
+            gi[1] = granules(p.t.cost + b * V * nG, (size_t)V * nG * 4);
+            gi[2] = granules(p.t.post + b * V * nG, (size_t)V * nG * 4);
+            gi[3] = granules(p.t.lam_min_units + b * V * nL, (size_t)V * nL * 2);
+            gi[4] = granules(p.t.lam_factor + b * V * nL, (size_t)V * nL * 4);
+            for (int k = 0; k < 5; ++k) tot += gi[k].bytes;
+        }
+        mbar_arrive_expect_tx(br, tot);
+        bulk_g2s(st, g.g0, g.bytes, br);
+        if (n0 == 0) {
+            const size_t off[5] = {IL.stale, IL.cost, IL.post, IL.lmu, IL.lf};
+            for (int k = 0; k < 5; ++k)
+                if (gi[k].bytes) bulk_g2s(st + L.rows_bytes + off[k], gi[k].g0, gi[k].bytes, br);
+        }
     };
 
     if (threadIdx.x == 0) {
@@ -256,26 +291,56 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
         const long long b = item_b(i), n0 = item_n0(i);
         const int rows = (int)min((long long)kListRows, N - n0);
         const int s = (int)(i % kListStages);
+        unsigned char* st = smem + L.stage + s * L.stage_bytes;
+        mbar_wait(&bar[s], (unsigned)((i / kListStages) & 1));
         if (n0 == 0) {
-            // new instance: validate and build all V stream tables (warps in parallel)
-            const bool wok = warp_instance_valid(p.t, b, V, nG, nL);
-            if (wok) {
+            // new instance: validate (R-ERR) and build the V stream tables from the staged inputs
+            unsigned char* ib = st + L.rows_bytes;
+            const float* stale = reinterpret_cast<const float*>(ib + IL.stale + granules(p.t.stale + b * V, 4).off);
+            const float* cost = reinterpret_cast<const float*>(ib + IL.cost + granules(p.t.cost + b * V * nG, 4).off);
+            const float* post = reinterpret_cast<const float*>(ib + IL.post + granules(p.t.post + b * V * nG, 4).off);
+            const uint16_t* lmu = reinterpret_cast<const uint16_t*>(
+                ib + IL.lmu + granules(p.t.lam_min_units + b * V * nL, 2).off);
+            const float* lf = reinterpret_cast<const float*>(ib + IL.lf + granules(p.t.lam_factor + b * V * nL, 4).off);
+            bool vok = true;
+            for (int t = threadIdx.x; t < V; t += blockDim.x) vok &= in01(stale[t]);
+            for (int t = threadIdx.x; t < V * nG; t += blockDim.x) {
+                const float c = cost[t];
+                if (!(c >= 0.0f)) vok = false;
+                else if (!isinf(c)) vok &= in01(post[t]);
+            }
+            for (int t = threadIdx.x; t < V * nL; t += blockDim.x)
+                if (lmu[t] != kLmuPad) vok &= in01(lf[t]);
+            ok = __syncthreads_and(vok) != 0;
+            if (ok) {
                 for (int v = warp; v < V; v += nw) {
-                    warp_load_stream(sin, p.t, b * V + v, nG, nL);
+                    if (lane < nG) {
+                        sin->cost[lane] = cost[v * nG + lane];
+                        sin->post[lane] = post[v * nG + lane];
+                    }
+                    if (lane < nL) {
+                        sin->lf[lane] = lf[v * nL + lane];
+                        sin->lmu[lane] = lmu[v * nL + lane];
+                    }
+                    const bool f = lane >= nG || fast_dividend(cost[v * nG + lane]);
+                    const unsigned all = __ballot_sync(0xffffffffu, f);
+                    if (lane == 0) {
+                        sin->stale = stale[v];
+                        sin->fast = all == 0xffffffffu;
+                    }
+                    __syncwarp();
                     Tabs T = carve_tabs(tabs + v * tb, U);
                     warp_build_tables<GM>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc);
                 }
+            } else if (threadIdx.x == 0) {
+                flag_data_error(p.st);
             }
-            ok = wok;
-            if (!ok && threadIdx.x == 0) flag_data_error(p.st);
             __syncthreads();
         }
-        mbar_wait(&bar[s], (unsigned)((i / kListStages) & 1));
         const uint16_t* src = p.alloc + (b * N + n0) * J;
-        const uint16_t* rs = reinterpret_cast<const uint16_t*>(smem + L.stage + s * L.stage_bytes +
-                                                                granules(src, 2).off);
+        const uint16_t* rs = reinterpret_cast<const uint16_t*>(st + granules(src, 2).off);
         uint8_t* cdst = p.out_cfg ? p.out_cfg + (b * N + n0) * V : nullptr;
-        uint8_t* cst = smem + L.cfgbuf + (cdst ? granules(cdst, 1).off : 0);
+        uint8_t* cst = smem + L.cfgbuf + (i & 1) * L.cfg_bytes + (cdst ? granules(cdst, 1).off : 0);
         const size_t off_tvc = a16((size_t)(U + 1));
         for (int r = threadIdx.x; r < rows; r += kListThreads) {
             // (ri, rt) of stream v is one 32-bit word (alloc is 4-byte aligned, J even)
@@ -289,7 +354,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
                 const unsigned pr = row[v];
                 int ri = (int)(pr & 0xFFFFu), rt = (int)(pr >> 16);
                 tot += ri + rt;
-                rok &= (ri <= U) & (rt <= U);
+                rok &= max(ri, rt) <= U;
                 ri = min(ri, U);
                 rt = min(rt, U);
                 const uint2 vc = reinterpret_cast<const uint2*>(tp + off_tvc)[rt * kSlots + tp[ri]];
@@ -307,15 +372,10 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
             p.out_sum[o] = S;
             if (p.out_mean) p.out_mean[o] = rok ? mean_q32(S, V) : 0.0f;
         }
-        __syncthreads();   // stage s consumed, config bytes staged
+        __syncthreads();   // stage s consumed; config bytes of this chunk staged
         if (threadIdx.x == 0 && i + kListStages < items) issue(i + kListStages);
-        if (cdst) {
-            store_from_smem(cdst, cst, (size_t)rows * V);
-            __syncthreads();
-        }
+        if (cdst) store_from_smem(cdst, cst, (size_t)rows * V);   // buffer (i & 1): reused after the next barrier
     }
-    (void)misc;
-    (void)lane;
 }
 
 int resident_grid(ekya_handle* h, const void* fn, int threads, size_t smem, long long work) {
@@ -372,7 +432,7 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     p.out_mean = out_mean;
     p.out_cfg = out_cfg;
     if (reinterpret_cast<uintptr_t>(alloc) & 3) return EKYA_ERR_ARG;
-    size_t smem = list_layout(d.units, d.n_streams).total;
+    size_t smem = list_layout(d.units, d.n_streams, d.n_gamma, d.n_lambda).total;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0 || n_alloc == 0) return EKYA_OK;
     auto kern = pick_gm(d.n_gamma, list_kernel<8>, list_kernel<16>, list_kernel<24>, list_kernel<32>);

@@ -156,7 +156,7 @@ __device__ __forceinline__ void gacc_finish(const GammaAcc& a, unsigned long lon
 }
 
 struct ScratchLayout {
-    size_t bars, sim, ps, pn, mu, sums, cnt, assign, chg, misc, total;
+    size_t bars, sim, ps, pn, mu, sums, cnt, assign, chg, dcache, misc, total;
 };
 __host__ __device__ inline ScratchLayout scratch_layout(int H, int Hc, int C, int K, bool cluster) {
     ScratchLayout L;
@@ -171,6 +171,7 @@ __host__ __device__ inline ScratchLayout scratch_layout(int H, int Hc, int C, in
     L.cnt = o;    o += cluster ? al16((size_t)(kProfThreads / 32) * K * 4) : 0;
     L.assign = o; o += cluster ? al16((size_t)H * 4) : 0;
     L.chg = o;
+    L.dcache = o; o += cluster ? (size_t)8 * kProfThreads * 4 : 0;
     L.misc = o;   o += 64;
     L.total = o;
     return L;
@@ -324,7 +325,7 @@ __device__ __forceinline__ void dist_n(const float (&x)[32], const float* r0, co
 // was filled) are recomputed -- an unchanged centroid has bit-identical
 // distances.  Lowest index wins ties (C19).
 __device__ __forceinline__ int nearest_cached(const float (&x)[32], const float* mu, int K, int CP, unsigned chg,
-                                              float (&dc)[8]) {
+                                              float* dcs /* this thread's cache, stride kProfThreads */) {
     unsigned m = chg;
     while (m) {   // chg is block-uniform: no divergence
         int id[4] = {-1, -1, -1, -1};
@@ -349,18 +350,15 @@ __device__ __forceinline__ int nearest_cached(const float (&x)[32], const float*
             default: dist_n<4>(x, r0, r1, r2, r3, CP, s); break;
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (id[k] == j) dc[j] = s[k];
-        }
+        for (int k = 0; k < 4; ++k)
+            if (k < n) dcs[id[k] * kProfThreads] = s[k];
     }
     int best = 0;
-    float bd = dc[0];
-#pragma unroll
-    for (int j = 1; j < 8; ++j) {
-        if (j < K && dc[j] < bd) {
-            bd = dc[j];
+    float bd = dcs[0];
+    for (int j = 1; j < K; ++j) {
+        const float dj = dcs[j * kProfThreads];
+        if (dj < bd) {
+            bd = dj;
             best = j;
         }
     }
@@ -414,6 +412,7 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
     int* assign = reinterpret_cast<int*>(scratch + S.assign);
     int* misc = reinterpret_cast<int*>(scratch + S.misc);   // [2] query cluster, [3..4] changed-centroid masks
     const bool cache = REG && K <= 8;
+    float* dcache = reinterpret_cast<float*>(scratch + S.dcache);   // [8][kProfThreads] distance cache
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kProfThreads / 32;
     const long long Q = P.p.n_query;
@@ -455,9 +454,7 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
         if (H > 0) {
             // own window's histogram in registers (REG: H <= threads, C <= 32), zero padded
             float xr[32];
-            float dc[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) dc[j] = 0.0f;
+            float* dc = dcache + threadIdx.x;
             if (REG) {
                 const int h = threadIdx.x;
 #pragma unroll
