@@ -344,8 +344,9 @@ def run_ours(args, rank, world, local_rank):
     timer = KernelTimer()
     barrier()
     torch.cuda.synchronize()
-    l0 = h.launch_count()
+    c0 = h.counters()
     with ClockSampler(local_rank) as clk:
+        time.sleep(0.3)            # let the sampler start before the timed region
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
@@ -354,7 +355,9 @@ def run_ours(args, rank, world, local_rank):
         t1.record()
         torch.cuda.synchronize()
     barrier()
-    launches = h.launch_count() - l0
+    c1 = h.counters()
+    launches = c1["launches"] - c0["launches"]
+    lloyd_passes = c1["lloyd_passes"] - c0["lloyd_passes"]
     ms = t0.elapsed_time(t1)
     per = timer.totals_ms()
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -370,13 +373,20 @@ def run_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return
-    peak, peak_kind, _ = measured_peaks()
+    peak, peak_kind, mp = measured_peaks()
+    sm_mhz = float(mp.get("sm_max_mhz", 1965.0))
+    # FP32 issue peak for the ALU-bound CLUSTER kernel: 148 SMs x 128 FP32 lanes x clock,
+    # one flop per FSUB/FMUL/FADD (no FMA is allowed by the arithmetic contract)
+    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
     total_units = w.allocations() * world * args.steps
     value = total_units / (ms / 1000.0)
     rows_out = {}
     bytes_of = {"eval_grid": w.grid_bytes(), "eval_list": w.list_bytes(), "profile_radius": w.profile_bytes(),
                 "profile_cluster": w.profile_bytes(), "thief_steepest": w.thief_bytes(),
                 "thief_literal": w.thief_bytes()}
+    pc = w.pcfg
+    cluster_flops = lloyd_passes / max(1, args.steps) * pc.n_hist * pc.k * pc.n_class * 3
+    roof = {}
     for k, t in per.items():
         avg = t / args.steps
         r = {"ms_per_launch": avg, "share": t / ms}
@@ -384,6 +394,16 @@ def run_ours(args, rank, world, local_rank):
             gbs = bytes_of[k] / (avg / 1000.0) / 1e9
             r["algorithmic_gb_per_s"] = gbs
             r["hbm_frac"] = gbs / peak
+            roof[k] = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                       "peak_source": peak_kind, "algorithmic_bytes_per_launch": bytes_of[k]}
+        if k == "profile_cluster":
+            tfs = cluster_flops / (avg / 1000.0) / 1e12
+            r["algorithmic_tflop_per_s"] = tfs
+            r["alu_frac"] = tfs / alu_peak
+            r["lloyd_passes_per_query"] = lloyd_passes / max(1, args.steps) / w.Q
+            roof[k] = {"bound": "alu", "achieved": tfs, "peak": alu_peak, "unit": "TFLOP/s", "frac": tfs / alu_peak,
+                       "peak_source": f"derived: 148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (DESIGN.md 13)",
+                       "algorithmic_flops_per_launch": cluster_flops}
         if k.startswith("thief"):
             r["schedules_per_s"] = w.B * world / (avg / 1000.0)
         if k.startswith("profile"):
@@ -393,29 +413,27 @@ def run_ours(args, rank, world, local_rank):
         if k == "eval_list":
             r["allocation_vectors_per_s"] = w.B * w.N * world / (avg / 1000.0)
         rows_out[k] = r
-    dom = max((k for k in per if k in bytes_of and not k.startswith("thief")), key=lambda k: per[k])
-    dom_avg = per[dom] / args.steps
-    achieved = bytes_of[dom] / (dom_avg / 1000.0) / 1e9
-    traffic = None
+    dom = max((k for k in per if k in roof), key=lambda k: per[k])
+    roofline = dict(roof[dom])
+    roofline["kernel"] = dom
+    roofline["traffic"] = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(dom)
+            roofline["traffic"] = json.load(f).get(dom)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-based generator, paper shapes)",
         "config": config_block(w, args),
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                     "algorithmic_bytes_per_launch": bytes_of[dom]},
+        "roofline": roofline,
         "rows": rows_out,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
     if e2e is not None:
         line["e2e"] = e2e
-    if args.cpu_baseline and world == 1 or (args.cpu_baseline and rank == 0):
+    if args.cpu_baseline and world == 1:
         import oracle
         oracle.build()
         dt, units, desc = oracle_sample(args.ref_inst, args.ref_query)
@@ -472,7 +490,7 @@ def run_e2e(ek, h, w, T, rows, P, O, args, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n-inst", type=int, default=synth.CONFIG4.n_inst)
@@ -480,8 +498,8 @@ def main():
     ap.add_argument("--n-query", type=int, default=synth.CONFIG3.n_query)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
-    ap.add_argument("--ref-inst", type=int, default=48)
-    ap.add_argument("--ref-query", type=int, default=32)
+    ap.add_argument("--ref-inst", type=int, default=384)
+    ap.add_argument("--ref-query", type=int, default=192)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", "0"))

@@ -71,6 +71,11 @@ void ekya_destroy(ekya_handle* h);
 int  ekya_last_error(ekya_handle* h);
 /* Number of kernels this handle has launched so far (for launch accounting). */
 uint64_t ekya_launch_count(const ekya_handle* h);
+/* Telemetry (synchronises): out[0] = kernels launched, out[1] = cumulative
+ * CLUSTER-mode Lloyd assignment passes (initial assignment + iterations, summed
+ * over queries) -- the unit of the CLUSTER kernel's algorithmic work.  Writes
+ * min(n, 2) values. */
+int ekya_counters(ekya_handle* h, uint64_t* out, int n);
 const char* ekya_version(void);
 
 /* Problem statement of a batch of scheduling instances (Eq. 1, P:876-973;

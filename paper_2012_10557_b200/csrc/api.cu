@@ -81,13 +81,23 @@ int ekya_last_error(ekya_handle* h) {
     DevState st;
     if (cudaMemcpy(&st, h->dstate, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) return EKYA_ERR_CUDA;
     if (st.err) {
-        cudaMemset(h->dstate, 0, sizeof(DevState));
+        cudaMemset(&h->dstate->err, 0, sizeof(unsigned));
         return EKYA_ERR_DATA;
     }
     return EKYA_OK;
 }
 
 uint64_t ekya_launch_count(const ekya_handle* h) { return h ? h->launches : 0; }
+
+int ekya_counters(ekya_handle* h, uint64_t* out, int n) {
+    if (!h || !out || n < 0) return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return EKYA_ERR_CUDA;
+    DevState st;
+    if (cudaMemcpy(&st, h->dstate, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) return EKYA_ERR_CUDA;
+    const uint64_t v[2] = {h->launches, st.lloyd_passes};
+    for (int i = 0; i < n && i < 2; ++i) out[i] = v[i];
+    return EKYA_OK;
+}
 
 int ekya_eval_allocations(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int mode,
                           int32_t n_alloc, const uint16_t* alloc, uint64_t* out_sum_q32,

@@ -22,8 +22,10 @@ constexpr int kMaxLambda = 7;
 constexpr unsigned kErrData = 1u;
 
 struct DevState {
-    unsigned int err;       // OR of kErr* bits
-    unsigned int pad[15];
+    unsigned int err;                   // OR of kErr* bits
+    unsigned int pad0;
+    unsigned long long lloyd_passes;    // CLUSTER assignment passes (telemetry)
+    unsigned int pad[12];
 };
 
 __device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }

@@ -250,8 +250,10 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     const long long nch = (N + kListRows - 1) / kListRows;
     const long long nb_local = d.n_inst > blockIdx.x ? (d.n_inst - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const long long items = nb_local * nch;
-    auto item_b = [&](long long i) { return (long long)blockIdx.x + (i / nch) * gridDim.x; };
-    auto item_n0 = [&](long long i) { return (i % nch) * kListRows; };
+    // items fit 32-bit index math (items <= B * nch / gridDim.x)
+    const unsigned unch = (unsigned)nch;
+    auto item_b = [&](long long i) { return (long long)blockIdx.x + (long long)((unsigned)i / unch) * gridDim.x; };
+    auto item_n0 = [&](long long i) { return (long long)((unsigned)i % unch) * kListRows; };
     // leader thread: one row chunk (+ the instance inputs with its first chunk)
     auto issue = [&](long long i) {
         const long long b = item_b(i), n0 = item_n0(i);

@@ -491,7 +491,9 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
                 for (int j = 0; j < nh; ++j) move(h0 + j, -1, __shfl_sync(0xffffffffu, a, j), hs);
             }
             __syncthreads();
+            int passes = 1;
             for (int it = 0; it < P.p.max_iter; ++it) {
+                ++passes;
                 // centroid update from the exact sums (empty cluster keeps its centroid)
                 for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
                     const int ci = t / C, c = t - ci * C;
@@ -533,6 +535,7 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
                 }
                 if (!__syncthreads_or(changed)) break;
             }
+            if (threadIdx.x == 0) atomicAdd(&P.st->lloyd_passes, (unsigned long long)passes);
             // the query joins its nearest centroid: lane i computes distance to centroid i
             if (warp == 0) {
                 unsigned long long key = ~0ULL;

@@ -55,30 +55,33 @@ struct ThiefParams {
     size_t warp_bytes;   // shared bytes per warp
 };
 
+// Per-stream record rec[v][8] (Q32 units): [0] current value, [1] up (inference
+// +D), [2] up (training +D), [3] down (inference -D), [4] down (training -D),
+// [5] move with thief = training (training +D, inference -D), [6] move with
+// thief = inference (inference +D, training -D); kInvalid where the victim has
+// fewer than D units.
 struct WarpState {
-    unsigned long long* cur;     // [V]  Q32 value of each stream now
-    long long* up;               // [J]
-    long long* dn;               // [J]  kInvalid if alloc < D
-    long long* mv;               // [J]  same-stream move with thief j; kInvalid if victim < D
+    long long* rec;              // [V][8]
     int* alloc;                  // [J]
     int* lthr;                   // [V][8] lambda* breakpoints (INT_MAX = unused)
     float* lfac;                 // [V][8] factor of lambda* at the breakpoint (-1 = none)
+    __device__ __forceinline__ long long cur(int v) const { return rec[v * 8]; }
+    __device__ __forceinline__ long long up(int j) const { return rec[(j >> 1) * 8 + 1 + (j & 1)]; }
+    __device__ __forceinline__ long long dn(int j) const { return rec[(j >> 1) * 8 + 3 + (j & 1)]; }
+    __device__ __forceinline__ long long mv(int j) const { return rec[(j >> 1) * 8 + 6 - (j & 1)]; }
 };
 
 __host__ __device__ inline size_t thief_warp_bytes(int V) {
     const size_t J = 2 * (size_t)V;
-    size_t b = 8 * (size_t)V + 8 * 3 * J + 4 * J + 2 * 4 * 8 * (size_t)V;
+    size_t b = 8 * 8 * (size_t)V + 4 * J + 2 * 4 * 8 * (size_t)V;
     return (b + 15) & ~size_t(15);
 }
 
 __device__ inline WarpState carve(unsigned char* base, int V) {
     const int J = 2 * V;
     WarpState w;
-    w.cur = reinterpret_cast<unsigned long long*>(base);
-    w.up = reinterpret_cast<long long*>(w.cur + V);
-    w.dn = w.up + J;
-    w.mv = w.dn + J;
-    w.alloc = reinterpret_cast<int*>(w.mv + J);
+    w.rec = reinterpret_cast<long long*>(base);
+    w.alloc = reinterpret_cast<int*>(w.rec + 8 * V);
     w.lthr = w.alloc + J;
     w.lfac = reinterpret_cast<float*>(w.lthr + 8 * V);
     return w;
@@ -168,24 +171,15 @@ __device__ __forceinline__ void update_stream(const InstView& in, const WarpStat
         const float f = __shfl_sync(FULL, fk, km & 7u);
         fac[k] = km ? f : -1.0f;
     }
-    // lanes 0..6 each produce one of the seven entries:
+    // lanes 0..6 each produce one of the seven record entries, no divergence:
     // lane: 0 cur (rt,ri) 1 (rt,ri+D) 2 (rt+D,ri) 3 (rt,ri-D) 4 (rt-D,ri) 5 (rt+D,ri-D) 6 (rt-D,ri+D)
-    if (lane < 7) {
-        const float Ga = (lane == 2 || lane == 5) ? G[2] : (lane == 4 || lane == 6) ? G[0] : G[1];
-        const float fb = (lane == 1 || lane == 6) ? fac[2] : (lane == 3 || lane == 5) ? fac[0] : fac[1];
-        const unsigned long long val = fb < 0.0f ? 0ULL : q32(fmul(fb, Ga));
-        const unsigned long long c = fac[1] < 0.0f ? 0ULL : q32(fmul(fac[1], G[1]));
-        const long long dv = (long long)val - (long long)c;
-        switch (lane) {
-            case 0: S.cur[v] = c; break;
-            case 1: S.up[2 * v] = dv; break;                                   // inference +D
-            case 2: S.up[2 * v + 1] = dv; break;                               // training  +D
-            case 3: S.dn[2 * v] = ri >= D ? dv : kInvalid; break;              // inference -D
-            case 4: S.dn[2 * v + 1] = rt >= D ? dv : kInvalid; break;          // training  -D
-            case 5: S.mv[2 * v + 1] = ri >= D ? dv : kInvalid; break;          // thief = training
-            case 6: S.mv[2 * v] = rt >= D ? dv : kInvalid; break;              // thief = inference
-        }
-    }
+    const float Ga = (lane == 2 || lane == 5) ? G[2] : (lane == 4 || lane == 6) ? G[0] : G[1];
+    const float fb = (lane == 1 || lane == 6) ? fac[2] : (lane == 3 || lane == 5) ? fac[0] : fac[1];
+    const long long val = fb < 0.0f ? 0LL : (long long)q32(fmul(fb, Ga));
+    const long long c = fac[1] < 0.0f ? 0LL : (long long)q32(fmul(fac[1], G[1]));
+    const bool valid = (lane == 3 || lane == 5) ? ri >= D : (lane == 4 || lane == 6) ? rt >= D : true;
+    const long long out = lane == 0 ? c : (valid ? val - c : kInvalid);
+    if (lane < 7) S.rec[v * 8 + lane] = out;
     __syncwarp();
 }
 
@@ -211,14 +205,17 @@ __device__ uint8_t stream_cfg(const InstView& in, int v, int ri, int rt, const e
 
 __device__ __forceinline__ bool lit_cond(const WarpState& S, int t, int w, int J) {
     if (w >= J || w == t) return false;
-    if ((w >> 1) == (t >> 1)) return S.mv[t] != kInvalid && S.mv[t] > 0;
-    const long long dn = S.dn[w];
-    return dn != kInvalid && S.up[t] + dn > 0;
+    if ((w >> 1) == (t >> 1)) {
+        const long long m = S.mv(t);
+        return m != kInvalid && m > 0;
+    }
+    const long long dn = S.dn(w);
+    return dn != kInvalid && S.up(t) + dn > 0;
 }
 
 __device__ __forceinline__ unsigned long long stream_down_key(const WarpState& S, int v) {
     unsigned long long k = 0;
-    const long long d0 = S.dn[2 * v], d1 = S.dn[2 * v + 1];
+    const long long d0 = S.dn(2 * v), d1 = S.dn(2 * v + 1);
     if (d0 != kInvalid) k = dkey(d0, 2 * v);
     if (d1 != kInvalid) {
         const unsigned long long kk = dkey(d1, 2 * v + 1);
@@ -301,11 +298,11 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
                 long long tot = 0;
                 int w = -1;
                 if (ck) {
-                    tot = S.up[t] + key_delta(ck);
+                    tot = S.up(t) + key_delta(ck);
                     w = key_job(ck);
                     have = true;
                 }
-                const long long m = S.mv[t];
+                const long long m = S.mv(t);
                 if (m != kInvalid) {
                     const int ws = t ^ 1;
                     if (!have || m > tot || (m == tot && ws < w)) {
@@ -366,7 +363,7 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
 
     // ---- decision output (A6) ----
     unsigned long long part = 0;
-    for (int v = lane; v < V; v += 32) part += S.cur[v];
+    for (int v = lane; v < V; v += 32) part += (unsigned long long)S.cur(v);
     const unsigned long long sum = shfl_sum_u64(part);
     for (int j = lane; j < J; j += 32) p.out_alloc[b * J + j] = (uint16_t)S.alloc[j];
     for (int v = 0; v < V; ++v) {

@@ -25,7 +25,7 @@ PROFILE_RADIUS, PROFILE_CLUSTER = 0, 1
 LAMBDA_NONE = 7
 SYMBOLS = ["ekya_create", "ekya_destroy", "ekya_last_error", "ekya_launch_count", "ekya_version",
            "ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate",
-           "ekya_comm_unique_id", "ekya_comm_init", "ekya_gather_decisions"]
+           "ekya_comm_unique_id", "ekya_comm_init", "ekya_gather_decisions", "ekya_counters"]
 
 
 class EkyaError(RuntimeError):
@@ -75,6 +75,8 @@ def load_library(path: str = LIB_PATH):
     L.ekya_last_error.restype = ctypes.c_int
     L.ekya_launch_count.argtypes = [P]
     L.ekya_launch_count.restype = U64
+    L.ekya_counters.argtypes = [P, P, ctypes.c_int]
+    L.ekya_counters.restype = ctypes.c_int
     L.ekya_version.argtypes = []
     L.ekya_version.restype = ctypes.c_char_p
     L.ekya_eval_allocations.argtypes = [P, ctypes.POINTER(Dims), ctypes.POINTER(Tables), ctypes.c_int,
@@ -150,6 +152,11 @@ class Handle:
 
     def launch_count(self) -> int:
         return int(load_library().ekya_launch_count(self._h))
+
+    def counters(self) -> dict:
+        buf = (ctypes.c_uint64 * 2)()
+        _check(load_library().ekya_counters(self._h, ctypes.cast(buf, ctypes.c_void_p), 2), "ekya_counters")
+        return {"launches": int(buf[0]), "lloyd_passes": int(buf[1])}
 
 
 def make_dims(n_inst, n_streams, n_gamma, n_lambda, units, steal_units, unit_gpu_seconds, a_min):

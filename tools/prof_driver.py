@@ -11,10 +11,10 @@ import bench  # noqa: E402
 from paper_2012_10557_b200 import ekya  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--n-inst", type=int, default=8192)
+ap.add_argument("--n-inst", type=int, default=65536)
 ap.add_argument("--n-alloc", type=int, default=4096)
-ap.add_argument("--n-query", type=int, default=8192)
-ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--n-query", type=int, default=65536)
+ap.add_argument("--reps", type=int, default=1)
 a = ap.parse_args()
 torch.cuda.set_device(0)
 h = ekya.Handle(0)
