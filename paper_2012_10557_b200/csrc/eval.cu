@@ -24,10 +24,10 @@ namespace ekya {
 
 namespace {
 
-constexpr int kGridWarps = 16;
-constexpr int kListThreads = 512;
-constexpr int kListRows = 512;      // rows per pipeline stage
-constexpr int kListStages = 4;
+constexpr int kGridWarps = 32;
+constexpr int kListThreads = 1024;
+constexpr int kListRows = 1024;     // rows per pipeline stage
+constexpr int kListStages = 3;
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -79,47 +79,36 @@ struct EvalParams {
 // ------------------------------------------------------------------------
 // GRID
 // ------------------------------------------------------------------------
-// Cell-position tables, shared by every stream (the triangle depends only on U):
+// Cell-position table, shared by every stream (the triangle depends only on U):
 // for each of the 4 alignments phi of a stream's first cell within a 16-byte
-// quad, quad k of the stream covers local cells 4k-phi .. 4k-phi+3 and
-// ci[phi][k][j] = (8*rt << 16) | ri of cell 4k-phi+j (0 outside the stream).
+// quad, quad k of the stream starts at local cell c = 4k - phi and
+// qs[phi][k] = (rt << 16) | ri of max(c, 0); the quad's other cells follow by
+// stepping along the row (and wrapping to the next row).
 __host__ __device__ inline size_t cellinfo_quads(int U) {
     const long long NC = (long long)(U + 1) * (U + 2) / 2;
     return (size_t)((NC + 3) / 4 + 1);
 }
-constexpr int kCellInfoMaxU = 109;   // 4 phases x quads x 16 B <= ~96 KB
 
 template <int GM>
-__global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) {
+__global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) {   // <= 64 regs
     extern __shared__ __align__(128) unsigned char smem[];
     const ekya_dims& d = p.d;
     const int U = d.units, nG = d.n_gamma, nL = d.n_lambda, V = d.n_streams;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool use_ci = U <= kCellInfoMaxU;
     const size_t nq_tab = cellinfo_quads(U);
-    uint4* ci = reinterpret_cast<uint4*>(smem);
-    unsigned char* mine = smem + (use_ci ? 4 * nq_tab * sizeof(uint4) : 0) + (size_t)warp * p.warp_bytes;
+    unsigned* qs = reinterpret_cast<unsigned*>(smem);
+    unsigned char* mine = smem + a16(4 * nq_tab * sizeof(unsigned)) + (size_t)warp * p.warp_bytes;
     StreamIn* sin = reinterpret_cast<StreamIn*>(mine);
     Tabs T = carve_tabs(mine + a16(sizeof(StreamIn)), U);
     const int NC = (U + 1) * (U + 2) / 2;
 
-    if (use_ci) {
-        for (int t = threadIdx.x; t < (int)(4 * nq_tab); t += blockDim.x) {
-            const int phi = t / (int)nq_tab, k = t - phi * (int)nq_tab;
-            unsigned e[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int c = 4 * k - phi + j;
-                e[j] = 0;
-                if (c >= 0 && c < NC) {
-                    const int rt = row_of(c, U);
-                    e[j] = ((unsigned)(rt * kSlots) << 16) | (unsigned)(c - rowstart(rt, U));
-                }
-            }
-            ci[t] = make_uint4(e[0], e[1], e[2], e[3]);
-        }
-        __syncthreads();
+    for (int t = threadIdx.x; t < (int)(4 * nq_tab); t += blockDim.x) {
+        const int phi = t / (int)nq_tab, k = t - phi * (int)nq_tab;
+        const int c = min(max(4 * k - phi, 0), NC - 1);
+        const int rt = row_of(c, U);
+        qs[t] = ((unsigned)rt << 16) | (unsigned)(c - rowstart(rt, U));
     }
+    __syncthreads();
 
     const long long nwarps = (long long)gridDim.x * kGridWarps;
     // one warp per instance (validated once), its V streams in turn
@@ -141,24 +130,21 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
             const int phi = (int)(f0 & 3);
             const long long q0 = f0 >> 2;
             const int nq = (int)(((f1 + 3) >> 2) - q0);
-            const uint4* cit = ci + (size_t)phi * nq_tab;
+            const unsigned* qst = qs + (size_t)phi * nq_tab;
             for (int k = lane; k < nq; k += 32) {
                 const long long fq = (q0 + k) << 2;
                 const int c0 = 4 * k - phi;
+                // (rt, ri) of the quad's cells: the first from the table, then along the row
                 unsigned e[4];
-                if (use_ci) {
-                    const uint4 u = cit[k];
-                    e[0] = u.x; e[1] = u.y; e[2] = u.z; e[3] = u.w;
-                } else {
-                    const int cs = max(c0, 0);
-                    int rt = row_of(cs, U), ri = cs - rowstart(rt, U);
+                {
+                    const unsigned s0 = qst[k];
+                    int rt = (int)(s0 >> 16), ri = (int)(s0 & 0xFFFFu);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const int c = c0 + j;
-                        e[j] = 0;
-                        if (c >= cs && c < NC) {
-                            e[j] = ((unsigned)(rt * kSlots) << 16) | (unsigned)ri;
-                            if (++ri > U - rt) { ++rt; ri = 0; }
+                        e[j] = ((unsigned)(rt * kSlots) << 16) | (unsigned)ri;
+                        if (c0 + j >= 0 && ++ri > U - rt) {
+                            rt = min(rt + 1, U);   // past the last cell: stay in range (never stored)
+                            ri = 0;
                         }
                     }
                 }
@@ -221,7 +207,7 @@ __host__ __device__ inline ListLayout list_layout(int U, int V, int nG, int nL) 
     ListLayout L;
     const int J = 2 * V;
     size_t o = 0;
-    L.sin = o;    o += a16(sizeof(StreamIn)) * (kListThreads / 32);
+    L.sin = o;    o += a16(sizeof(StreamIn)) * (size_t)(kListThreads / 32);
     L.tabs = o;   o += tab_bytes(U) * V;
     L.rows_bytes = a16((size_t)kListRows * J * 2) + 16;
     L.stage_bytes = L.rows_bytes + inst_layout(V, nG, nL).total;
@@ -241,7 +227,6 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kListThreads / 32;
     const ListLayout L = list_layout(U, V, nG, nL);
     const InstLayout IL = inst_layout(V, nG, nL);
-    StreamIn* sin = reinterpret_cast<StreamIn*>(smem + L.sin + warp * a16(sizeof(StreamIn)));
     unsigned char* tabs = smem + L.tabs;
     const size_t tb = tab_bytes(U);
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bars);
@@ -315,24 +300,29 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
                 if (lmu[t] != kLmuPad) vok &= in01(lf[t]);
             ok = __syncthreads_and(vok) != 0;
             if (ok) {
-                for (int v = warp; v < V; v += nw) {
+                // warp tasks = (stream, block of 32 r_train rows): V x ceil((U+1)/32) tasks
+                const int nblk = (U + 32) / 32;
+                for (int task = warp; task < V * nblk; task += nw) {
+                    const int v = task / nblk, blk = task - v * nblk;
+                    StreamIn* si = reinterpret_cast<StreamIn*>(smem + L.sin + (size_t)warp * a16(sizeof(StreamIn)));
                     if (lane < nG) {
-                        sin->cost[lane] = cost[v * nG + lane];
-                        sin->post[lane] = post[v * nG + lane];
+                        si->cost[lane] = cost[v * nG + lane];
+                        si->post[lane] = post[v * nG + lane];
                     }
                     if (lane < nL) {
-                        sin->lf[lane] = lf[v * nL + lane];
-                        sin->lmu[lane] = lmu[v * nL + lane];
+                        si->lf[lane] = lf[v * nL + lane];
+                        si->lmu[lane] = lmu[v * nL + lane];
                     }
                     const bool f = lane >= nG || fast_dividend(cost[v * nG + lane]);
                     const unsigned all = __ballot_sync(0xffffffffu, f);
                     if (lane == 0) {
-                        sin->stale = stale[v];
-                        sin->fast = all == 0xffffffffu;
+                        si->stale = stale[v];
+                        si->fast = all == 0xffffffffu;
                     }
                     __syncwarp();
                     Tabs T = carve_tabs(tabs + v * tb, U);
-                    warp_build_tables<GM>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc);
+                    warp_build_tables<GM>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc, blk * 32,
+                                          min(U + 1, blk * 32 + 32), blk == 0);
                 }
             } else if (threadIdx.x == 0) {
                 flag_data_error(p.st);
@@ -344,30 +334,31 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
         uint8_t* cdst = p.out_cfg ? p.out_cfg + (b * N + n0) * V : nullptr;
         uint8_t* cst = smem + L.cfgbuf + (i & 1) * L.cfg_bytes + (cdst ? granules(cdst, 1).off : 0);
         const size_t off_tvc = a16((size_t)(U + 1));
+        const unsigned UU = (unsigned)U | ((unsigned)U << 16);
         for (int r = threadIdx.x; r < rows; r += kListThreads) {
-            // (ri, rt) of stream v is one 32-bit word (alloc is 4-byte aligned, J even)
+            // (ri, rt) of stream v is one 32-bit word (alloc is 4-byte aligned, J even);
+            // both halves are clamped to U with one SIMD min, and any clamp marks the row bad
             const unsigned* row = reinterpret_cast<const unsigned*>(rs + (size_t)r * J);
-            bool rok = ok;
+            unsigned bad = 0;
             int tot = 0;
             unsigned long long S = 0;
             const unsigned char* tp = tabs;
             uint8_t* cr = cst + (size_t)r * V;
+#pragma unroll 2
             for (int v = 0; v < V; ++v, tp += tb) {
                 const unsigned pr = row[v];
-                int ri = (int)(pr & 0xFFFFu), rt = (int)(pr >> 16);
+                const unsigned pc = __vminu2(pr, UU);
+                bad |= pr ^ pc;
+                const int ri = (int)(pc & 0xFFFFu), rt = (int)(pc >> 16);
                 tot += ri + rt;
-                rok &= max(ri, rt) <= U;
-                ri = min(ri, U);
-                rt = min(rt, U);
                 const uint2 vc = reinterpret_cast<const uint2*>(tp + off_tvc)[rt * kSlots + tp[ri]];
                 S += q32(__uint_as_float(vc.x));
-                if (cdst) cr[v] = (uint8_t)vc.y;
+                cr[v] = (uint8_t)vc.y;
             }
-            rok &= tot <= U;                     // Eq. 1 constraint 2
-            if (!rok) {                          // R-ERR: zero the row
+            const bool rok = ok && bad == 0 && tot <= U;   // Eq. 1 constraint 2
+            if (!rok) {                                     // R-ERR: zero the row
                 S = 0;
-                if (cdst)
-                    for (int v = 0; v < V; ++v) cr[v] = 0;
+                for (int v = 0; v < V; ++v) cr[v] = 0;
                 if (ok) flag_data_error(p.st);
             }
             const long long o = b * N + n0 + r;
@@ -409,7 +400,7 @@ int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, f
     p.out_grid_cfg = out_grid_cfg;
     p.warp_bytes = a16(sizeof(StreamIn)) + tab_bytes(d.units);
     const int warps = kGridWarps;
-    size_t smem = p.warp_bytes * warps + (d.units <= kCellInfoMaxU ? 4 * cellinfo_quads(d.units) * 16 : 0);
+    size_t smem = p.warp_bytes * warps + a16(4 * cellinfo_quads(d.units) * sizeof(unsigned));
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0) return EKYA_OK;
     auto kern = pick_gm(d.n_gamma, grid_kernel<8>, grid_kernel<16>, grid_kernel<24>, grid_kernel<32>);

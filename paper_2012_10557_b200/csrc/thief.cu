@@ -65,6 +65,8 @@ struct WarpState {
     int* alloc;                  // [J]
     int* lthr;                   // [V][8] lambda* breakpoints (INT_MAX = unused)
     float* lfac;                 // [V][8] factor of lambda* at the breakpoint (-1 = none)
+    float* gc;                   // [V][4] G*(rt-D), G*(rt), G*(rt+D) cached for rt = grt[v]
+    int* grt;                    // [V]    (-1 = empty)
     __device__ __forceinline__ long long cur(int v) const { return rec[v * 8]; }
     __device__ __forceinline__ long long up(int j) const { return rec[(j >> 1) * 8 + 1 + (j & 1)]; }
     __device__ __forceinline__ long long dn(int j) const { return rec[(j >> 1) * 8 + 3 + (j & 1)]; }
@@ -73,7 +75,7 @@ struct WarpState {
 
 __host__ __device__ inline size_t thief_warp_bytes(int V) {
     const size_t J = 2 * (size_t)V;
-    size_t b = 8 * 8 * (size_t)V + 4 * J + 2 * 4 * 8 * (size_t)V;
+    size_t b = 8 * 8 * (size_t)V + 4 * J + 2 * 4 * 8 * (size_t)V + 4 * 4 * (size_t)V + 4 * (size_t)V;
     return (b + 15) & ~size_t(15);
 }
 
@@ -84,6 +86,8 @@ __device__ inline WarpState carve(unsigned char* base, int V) {
     w.alloc = reinterpret_cast<int*>(w.rec + 8 * V);
     w.lthr = w.alloc + J;
     w.lfac = reinterpret_cast<float*>(w.lthr + 8 * V);
+    w.gc = w.lfac + 8 * V;
+    w.grt = reinterpret_cast<int*>(w.gc + 4 * V);
     return w;
 }
 
@@ -152,24 +156,43 @@ __device__ __forceinline__ void update_stream(const InstView& in, const WarpStat
     }
     const int tk = lane < 8 ? S.lthr[v * 8 + lane] : INT_MAX;
     const float fk = lane < 8 ? S.lfac[v * 8 + lane] : -1.0f;
-    float G[3], fac[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int r = rt + D * (k - 1);
+    // G*(r): lane g evaluates rule 2 for config g, REDUX max; values are >= 0 or
+    // the -1 sentinel, so signed-int order of the bits = float order
+    auto gstar = [&](int r) -> float {
         float g = -1.0f;
         if (lane == 0) g = stale;
         else if (lane <= nG) {
             float w;
             if (window_acc(stale, post, cost, r, d.unit_gpu_seconds, &w)) g = w;
         }
-        // g is >= 0 or the -1 sentinel: signed-int order of the bits = float order
         const int m = __reduce_max_sync(FULL, __float_as_int(g));
-        G[k] = r < 0 ? -1.0f : __int_as_float(m);
+        return r < 0 ? -1.0f : __int_as_float(m);
+    };
+    // G* at rt-D, rt, rt+D, reusing the stream's cached values when rt moved by D
+    const int crt = S.grt[v];
+    float G[3];
+    if (crt == rt) {
+        G[0] = S.gc[v * 4]; G[1] = S.gc[v * 4 + 1]; G[2] = S.gc[v * 4 + 2];
+    } else if (crt >= 0 && crt == rt - D) {
+        G[0] = S.gc[v * 4 + 1]; G[1] = S.gc[v * 4 + 2]; G[2] = gstar(rt + D);
+    } else if (crt >= 0 && crt == rt + D) {
+        G[2] = S.gc[v * 4 + 1]; G[1] = S.gc[v * 4]; G[0] = gstar(rt - D);
+    } else {
+        G[0] = gstar(rt - D); G[1] = gstar(rt); G[2] = gstar(rt + D);
+    }
+    float fac[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
         const int ri2 = ri + D * (k - 1);
         const unsigned key = (ri2 >= 0 && tk <= ri2) ? ((unsigned)(tk + 1) << 3) | (unsigned)lane : 0u;
         const unsigned km = __reduce_max_sync(FULL, key);
         const float f = __shfl_sync(FULL, fk, km & 7u);
         fac[k] = km ? f : -1.0f;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        S.gc[v * 4] = G[0]; S.gc[v * 4 + 1] = G[1]; S.gc[v * 4 + 2] = G[2];
+        S.grt[v] = rt;
     }
     // lanes 0..6 each produce one of the seven record entries, no divergence:
     // lane: 0 cur (rt,ri) 1 (rt,ri+D) 2 (rt+D,ri) 3 (rt,ri-D) 4 (rt-D,ri) 5 (rt+D,ri-D) 6 (rt-D,ri+D)
@@ -267,6 +290,7 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
         S.alloc[2 * v] = share - rt;
     }
     for (int v = 0; v < V; ++v) init_ladder(in, S, v, d);
+    for (int v = lane; v < V; v += 32) S.grt[v] = -1;
     __syncwarp();
     for (int v = 0; v < V; ++v) update_stream(in, S, v, d);
 
