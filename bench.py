@@ -371,6 +371,7 @@ def run_ours(args, rank, world, local_rank):
     if args.e2e_steps > 0:
         e2e = run_e2e(ek, h, w, T, rows, P, O, args, world)
 
+    context = run_context(ek, h, dev, args) if rank == 0 and args.context else None
     if rank != 0:
         return
     peak, peak_kind, mp = measured_peaks()
@@ -433,6 +434,8 @@ def run_ours(args, rank, world, local_rank):
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if context is not None:
+        line["context"] = context
     if args.cpu_baseline and world == 1:
         import oracle
         oracle.build()
@@ -440,6 +443,47 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = {"value": units / dt, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
                                 "seconds": dt}
     print(json.dumps(line), flush=True)
+
+
+def run_context(ek, h, dev, args):
+    """Context numbers beside the step (not part of `value`): single-instance thief
+    latency at config 2 (the paper's 9.4 s for 10 streams x 8 GPUs x 18 configs,
+    P:1294, was a host-side scheduler on other hardware) and config-5-shaped
+    (V=100, U=800) thief throughput on one GPU."""
+    out = {}
+    c2 = synth.SchedConfig(**{**synth.CONFIG2.__dict__, "n_inst": 1})
+    T2 = synth.sched_tables(c2, device=dev)
+    a2 = (c2.units, c2.steal_units, c2.unit_gpu_seconds, c2.a_min)
+    for name, mode in (("steepest", ek.THIEF_STEEPEST), ("literal", ek.THIEF_LITERAL)):
+        for _ in range(3):
+            ek.thief_schedule(h, T2, *a2, mode=mode)
+        ts = []
+        for _ in range(20):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ek.thief_schedule(h, T2, *a2, mode=mode)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        out[f"config2_single_instance_thief_{name}_ms"] = float(np.median(ts))
+    out["paper_thief_latency_s"] = {"value": 9.4, "cite": "P:1294, 10 streams x 8 GPUs x 18 configs, "
+                                    "host-side scheduler (PyTorch + Ray on AWS p3, P:1321)"}
+    n5 = args.context_v100
+    c5 = synth.SchedConfig(**{**synth.CONFIG5.__dict__, "n_inst": n5})
+    T5 = synth.sched_tables(c5, device=dev)
+    a5 = (c5.units, c5.steal_units, c5.unit_gpu_seconds, c5.a_min)
+    for name, mode in (("steepest", ek.THIEF_STEEPEST), ("literal", ek.THIEF_LITERAL)):
+        ek.thief_schedule(h, T5, *a5, mode=mode)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ek.thief_schedule(h, T5, *a5, mode=mode)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        out[f"config5_shape_thief_{name}"] = {"instances": n5, "ms": ms, "schedules_per_s": n5 / (ms / 1000.0)}
+    return out
 
 
 def run_e2e(ek, h, w, T, rows, P, O, args, world):
@@ -498,6 +542,8 @@ def main():
     ap.add_argument("--n-query", type=int, default=synth.CONFIG3.n_query)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-context", dest="context", action="store_false")
+    ap.add_argument("--context-v100", type=int, default=16384)
     ap.add_argument("--ref-inst", type=int, default=384)
     ap.add_argument("--ref-query", type=int, default=192)
     args = ap.parse_args()

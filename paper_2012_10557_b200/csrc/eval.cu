@@ -62,6 +62,42 @@ __device__ __forceinline__ Tabs carve_tabs(unsigned char* p, int U) {
     return t;
 }
 
+// Instance inputs (stale, cost, post, lam_min_units, lam_factor of one
+// instance) staged by the TMA alongside the instance's first row chunk.
+struct InstLayout {
+    size_t stale, cost, post, lmu, lf, total;
+};
+__host__ __device__ inline InstLayout inst_layout(int V, int nG, int nL) {
+    InstLayout L;
+    size_t o = 0;
+    L.stale = o; o += a16((size_t)V * 4) + 16;
+    L.cost = o;  o += a16((size_t)V * nG * 4) + 16;
+    L.post = o;  o += a16((size_t)V * nG * 4) + 16;
+    L.lmu = o;   o += a16((size_t)V * nL * 2) + 16;
+    L.lf = o;    o += a16((size_t)V * nL * 4) + 16;
+    L.total = o;
+    return L;
+}
+
+struct ListLayout {
+    size_t sin, tabs, stage, cfgbuf, bars, total, rows_bytes, stage_bytes, cfg_bytes;
+};
+__host__ __device__ inline ListLayout list_layout(int U, int V, int nG, int nL) {
+    ListLayout L;
+    const int J = 2 * V;
+    size_t o = 0;
+    L.sin = o;    o += a16(sizeof(StreamIn)) * (size_t)(kListThreads / 32);
+    L.tabs = o;   o += tab_bytes(U) * V;
+    L.rows_bytes = a16((size_t)kListRows * J * 2) + 16;
+    L.stage_bytes = L.rows_bytes + inst_layout(V, nG, nL).total;
+    L.stage = o;  o += L.stage_bytes * kListStages;
+    L.cfg_bytes = a16((size_t)kListRows * V) + 16;
+    L.cfgbuf = o; o += L.cfg_bytes * 2;
+    L.bars = o;   o += 8 * kListStages;
+    L.total = o;
+    return L;
+}
+
 struct EvalParams {
     ekya_dims d;
     ekya_tables t;
@@ -74,6 +110,9 @@ struct EvalParams {
     float* out_mean;
     uint8_t* out_cfg;
     size_t warp_bytes;   // GRID: shared bytes per warp
+    ListLayout L;        // LIST: shared-memory layout (host-computed, read from the param space)
+    InstLayout IL;
+    size_t tb;           // LIST: bytes per stream table
 };
 
 // ------------------------------------------------------------------------
@@ -183,52 +222,16 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
 // ------------------------------------------------------------------------
 // LIST
 // ------------------------------------------------------------------------
-// Instance inputs (stale, cost, post, lam_min_units, lam_factor of one
-// instance) staged by the TMA alongside the instance's first row chunk.
-struct InstLayout {
-    size_t stale, cost, post, lmu, lf, total;
-};
-__host__ __device__ inline InstLayout inst_layout(int V, int nG, int nL) {
-    InstLayout L;
-    size_t o = 0;
-    L.stale = o; o += a16((size_t)V * 4) + 16;
-    L.cost = o;  o += a16((size_t)V * nG * 4) + 16;
-    L.post = o;  o += a16((size_t)V * nG * 4) + 16;
-    L.lmu = o;   o += a16((size_t)V * nL * 2) + 16;
-    L.lf = o;    o += a16((size_t)V * nL * 4) + 16;
-    L.total = o;
-    return L;
-}
-
-struct ListLayout {
-    size_t sin, tabs, stage, cfgbuf, bars, total, rows_bytes, stage_bytes, cfg_bytes;
-};
-__host__ __device__ inline ListLayout list_layout(int U, int V, int nG, int nL) {
-    ListLayout L;
-    const int J = 2 * V;
-    size_t o = 0;
-    L.sin = o;    o += a16(sizeof(StreamIn)) * (size_t)(kListThreads / 32);
-    L.tabs = o;   o += tab_bytes(U) * V;
-    L.rows_bytes = a16((size_t)kListRows * J * 2) + 16;
-    L.stage_bytes = L.rows_bytes + inst_layout(V, nG, nL).total;
-    L.stage = o;  o += L.stage_bytes * kListStages;
-    L.cfg_bytes = a16((size_t)kListRows * V) + 16;
-    L.cfgbuf = o; o += L.cfg_bytes * 2;
-    L.bars = o;   o += 8 * kListStages;
-    L.total = o;
-    return L;
-}
-
 template <int GM>
 __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const ekya_dims& d = p.d;
     const int U = d.units, nG = d.n_gamma, nL = d.n_lambda, V = d.n_streams, J = 2 * V;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kListThreads / 32;
-    const ListLayout L = list_layout(U, V, nG, nL);
-    const InstLayout IL = inst_layout(V, nG, nL);
+    const ListLayout& L = p.L;
+    const InstLayout& IL = p.IL;
     unsigned char* tabs = smem + L.tabs;
-    const size_t tb = tab_bytes(U);
+    const size_t tb = p.tb;
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bars);
 
     const long long N = p.n_alloc;
@@ -321,8 +324,15 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
                     }
                     __syncwarp();
                     Tabs T = carve_tabs(tabs + v * tb, U);
-                    warp_build_tables<GM>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc, blk * 32,
-                                          min(U + 1, blk * 32 + 32), blk == 0);
+                    const int r1 = min(U + 1, blk * 32 + 32);
+                    warp_build_tables<GM>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc, blk * 32, r1,
+                                          blk == 0);
+                    // LIST needs the exact Q32 value, not the float: entry = Q32 | cfg << 40 (Q32 <= 2^32)
+                    unsigned long long* q = reinterpret_cast<unsigned long long*>(T.tvc);
+                    for (int e = blk * 32 * kSlots + lane; e < r1 * kSlots; e += 32) {
+                        const uint2 vc = T.tvc[e];
+                        q[e] = q32(__uint_as_float(vc.x)) | ((unsigned long long)(vc.y & 0xFFu) << 40);
+                    }
                 }
             } else if (threadIdx.x == 0) {
                 flag_data_error(p.st);
@@ -351,9 +361,9 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
                 bad |= pr ^ pc;
                 const int ri = (int)(pc & 0xFFFFu), rt = (int)(pc >> 16);
                 tot += ri + rt;
-                const uint2 vc = reinterpret_cast<const uint2*>(tp + off_tvc)[rt * kSlots + tp[ri]];
-                S += q32(__uint_as_float(vc.x));
-                cr[v] = (uint8_t)vc.y;
+                const unsigned long long e = reinterpret_cast<const unsigned long long*>(tp + off_tvc)[rt * kSlots + tp[ri]];
+                S += e & 0xFFFFFFFFFFull;
+                cr[v] = (uint8_t)(e >> 40);
             }
             const bool rok = ok && bad == 0 && tot <= U;   // Eq. 1 constraint 2
             if (!rok) {                                     // R-ERR: zero the row
@@ -425,7 +435,10 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     p.out_mean = out_mean;
     p.out_cfg = out_cfg;
     if (reinterpret_cast<uintptr_t>(alloc) & 3) return EKYA_ERR_ARG;
-    size_t smem = list_layout(d.units, d.n_streams, d.n_gamma, d.n_lambda).total;
+    p.L = list_layout(d.units, d.n_streams, d.n_gamma, d.n_lambda);
+    p.IL = inst_layout(d.n_streams, d.n_gamma, d.n_lambda);
+    p.tb = tab_bytes(d.units);
+    size_t smem = p.L.total;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0 || n_alloc == 0) return EKYA_OK;
     auto kern = pick_gm(d.n_gamma, list_kernel<8>, list_kernel<16>, list_kernel<24>, list_kernel<32>);

@@ -293,20 +293,23 @@ __device__ __forceinline__ int nearest_reg(const float (&x)[32], const float* mu
     return best;
 }
 
-// Squared distances of x (registers, zero padded) to N centroid rows, all N
+// Squared distances of x (registers, zero padded) to N <= 8 centroid rows, all N
 // chains interleaved for ILP; padded classes contribute fl(0-0)^2 = +0 (exact).
 template <int N>
-__device__ __forceinline__ void dist_n(const float (&x)[32], const float* r0, const float* r1, const float* r2,
-                                       const float* r3, int CP, float (&s)[4]) {
-    const float* rows[4] = {r0, r1, r2, r3};
+__device__ __forceinline__ void dist_n(const float (&x)[32], const float* mu, const int (&id)[8], int CP,
+                                       float (&s)[8]) {
+    const float4* rp[N];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) s[k] = 0.0f;
+    for (int k = 0; k < N; ++k) {
+        s[k] = 0.0f;
+        rp[k] = reinterpret_cast<const float4*>(mu + id[k] * CP);
+    }
 #pragma unroll
     for (int c4 = 0; c4 < 8; ++c4) {
         if (c4 * 4 < CP) {
 #pragma unroll
             for (int k = 0; k < N; ++k) {
-                const float4 m = *reinterpret_cast<const float4*>(rows[k] + c4 * 4);
+                const float4 m = rp[k][c4];
                 const float d0 = fsub(x[c4 * 4 + 0], m.x);
                 s[k] = fadd(s[k], fmul(d0, d0));
                 const float d1 = fsub(x[c4 * 4 + 1], m.y);
@@ -323,31 +326,30 @@ __device__ __forceinline__ void dist_n(const float (&x)[32], const float* r0, co
 // Nearest of K <= 8 centroids with a per-thread distance cache: only the
 // centroids in `chg` (those whose coordinates changed bitwise since the cache
 // was filled) are recomputed -- an unchanged centroid has bit-identical
-// distances.  Lowest index wins ties (C19).
+// distances -- all of them in one interleaved pass.  Lowest index wins ties (C19).
 __device__ __forceinline__ int nearest_cached(const float (&x)[32], const float* mu, int K, int CP, unsigned chg,
-                                              float* dcs /* this thread's cache, stride kProfThreads */) {
-    unsigned m = chg;
-    while (m) {   // chg is block-uniform: no divergence
-        int id[4] = {-1, -1, -1, -1};
-        int n = 0;
+                                           float* dcs /* this thread's cache, stride kProfThreads */) {
+    // changed centroids in groups of <= 4 interleaved chains (5..8 split evenly);
+    unsigned m = chg;   // block-uniform: no divergence
+    while (m) {
+        const int left = __popc(m);
+        const int n = left <= 4 ? left : (left + 1) / 2;
+        int id[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) id[k] = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            if (m) {
+            if (k < n) {
                 id[k] = __ffs(m) - 1;
                 m &= m - 1;
-                ++n;
             }
         }
-        float s[4];
-        const float* r0 = mu + max(id[0], 0) * CP;
-        const float* r1 = mu + max(id[1], 0) * CP;
-        const float* r2 = mu + max(id[2], 0) * CP;
-        const float* r3 = mu + max(id[3], 0) * CP;
+        float s[8];
         switch (n) {
-            case 1: dist_n<1>(x, r0, r1, r2, r3, CP, s); break;
-            case 2: dist_n<2>(x, r0, r1, r2, r3, CP, s); break;
-            case 3: dist_n<3>(x, r0, r1, r2, r3, CP, s); break;
-            default: dist_n<4>(x, r0, r1, r2, r3, CP, s); break;
+            case 1: dist_n<1>(x, mu, id, CP, s); break;
+            case 2: dist_n<2>(x, mu, id, CP, s); break;
+            case 3: dist_n<3>(x, mu, id, CP, s); break;
+            default: dist_n<4>(x, mu, id, CP, s); break;
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -478,22 +480,50 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
             if (threadIdx.x == 0) misc[3] = misc[4] = 0;
             __syncthreads();
             const unsigned all_k = K >= 32 ? 0xffffffffu : ((1u << K) - 1u);
-            // initial assignment; each warp accumulates its own windows
-            for (int h0 = warp * 32; h0 < H; h0 += kProfThreads) {
-                const int h = h0 + lane;
-                int a = 0;
-                if (h < H) {
-                    a = cache ? nearest_cached(xr, mu, K, CP, all_k, dc)
-                              : nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
-                    assign[h] = a;
+            // Lloyd passes (C19, R-CL): pass 0 assigns from the initial centroids and
+            // accumulates the exact sums; pass p >= 1 follows the centroid update of
+            // iteration p-1 and moves only the windows whose cluster changed.  One
+            // call site for the distance code (I-cache).
+            unsigned chg = all_k;
+            int passes = 0;
+            for (;;) {
+                int changed = 0;
+                for (int h0 = warp * 32; h0 < H; h0 += kProfThreads) {
+                    const int h = h0 + lane;
+                    int oa = -1, na = 0;
+                    if (h < H) {
+                        na = cache ? nearest_cached(xr, mu, K, CP, chg, dc)
+                                   : nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
+                        if (passes > 0) oa = assign[h];
+                        assign[h] = na;
+                    }
+                    if (passes == 0) {
+                        // counts by ballot, sums by one row per window (lanes over classes)
+                        const int nh = min(32, H - h0);
+                        for (int ci = 0; ci < K; ++ci) {
+                            const unsigned bm = __ballot_sync(0xffffffffu, h < H && na == ci);
+                            if (lane == 0) mycnt[ci] += __popc(bm);
+                        }
+                        for (int j = 0; j < nh; ++j) {
+                            const int aj = __shfl_sync(0xffffffffu, na, j);
+                            const float* row = hs + (size_t)(h0 + j) * C;
+                            unsigned long long* dst = mypart + aj * C;
+                            for (int c = lane; c < C; c += 32) dst[c] += q32(row[c]);
+                        }
+                    } else {
+                        unsigned m = __ballot_sync(0xffffffffu, h < H && na != oa);
+                        changed |= m != 0;
+                        while (m) {
+                            const int j = __ffs(m) - 1;
+                            m &= m - 1;
+                            move(h0 + j, __shfl_sync(0xffffffffu, oa, j), __shfl_sync(0xffffffffu, na, j), hs);
+                        }
+                    }
                 }
-                const int nh = min(32, H - h0);
-                for (int j = 0; j < nh; ++j) move(h0 + j, -1, __shfl_sync(0xffffffffu, a, j), hs);
-            }
-            __syncthreads();
-            int passes = 1;
-            for (int it = 0; it < P.p.max_iter; ++it) {
+                const int any = __syncthreads_or(changed);
+                const int it = passes;   // iteration whose centroid update comes next
                 ++passes;
+                if ((it > 0 && !any) || it >= P.p.max_iter) break;
                 // centroid update from the exact sums (empty cluster keeps its centroid)
                 for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
                     const int ci = t / C, c = t - ci * C;
@@ -512,28 +542,8 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
                     }
                 }
                 __syncthreads();
-                const unsigned chg = (unsigned)misc[3 + (it & 1)];
+                chg = (unsigned)misc[3 + (it & 1)];
                 if (threadIdx.x == 0) misc[3 + ((it + 1) & 1)] = 0;
-                // reassign; each warp moves its own changed windows between clusters
-                int changed = 0;
-                for (int h0 = warp * 32; h0 < H; h0 += kProfThreads) {
-                    const int h = h0 + lane;
-                    int oa = 0, na = 0;
-                    if (h < H) {
-                        na = cache ? nearest_cached(xr, mu, K, CP, chg, dc)
-                                   : nearest_c<REG>(xr, hs + (size_t)h * C, mu, K, C, CP);
-                        oa = assign[h];
-                        assign[h] = na;
-                    }
-                    unsigned m = __ballot_sync(0xffffffffu, na != oa);
-                    changed |= m != 0;
-                    while (m) {
-                        const int j = __ffs(m) - 1;
-                        m &= m - 1;
-                        move(h0 + j, __shfl_sync(0xffffffffu, oa, j), __shfl_sync(0xffffffffu, na, j), hs);
-                    }
-                }
-                if (!__syncthreads_or(changed)) break;
             }
             if (threadIdx.x == 0) atomicAdd(&P.st->lloyd_passes, (unsigned long long)passes);
             // the query joins its nearest centroid: lane i computes distance to centroid i

@@ -31,6 +31,7 @@
 #include <climits>
 
 #include "launch.h"
+#include "stream_tables.cuh"
 
 namespace ekya {
 
@@ -52,7 +53,9 @@ struct ThiefParams {
     float* out_mean;
     uint32_t* out_steps;
     int warps;           // warps per CTA
-    size_t warp_bytes;   // shared bytes per warp
+    size_t warp_bytes;   // shared bytes per warp (state + staged tables)
+    size_t state_bytes;  // shared bytes of the per-warp state
+    int stage;           // stage stale/cost/post of the instance in shared memory
 };
 
 // Per-stream record rec[v][8] (Q32 units): [0] current value, [1] up (inference
@@ -129,13 +132,13 @@ __device__ void init_ladder(const InstView& in, const WarpState& S, int v, const
         int t = INT_MAX;
         float f = -1.0f;
         if (lane < nL) {
-            const float stale = __ldg(in.stale + v);
-            const uint16_t m = __ldg(in.lmu + (size_t)v * nL + lane);
-            const float acc = fmul(stale, __ldg(in.lf + (size_t)v * nL + lane));
+            const float stale = in.stale[v];
+            const uint16_t m = in.lmu[(size_t)v * nL + lane];
+            const float acc = fmul(stale, in.lf[(size_t)v * nL + lane]);
             if (m != kLmuPad && acc >= d.a_min) {
                 t = m;
                 const int l = lambda_star(stale, in.lmu + (size_t)v * nL, in.lf + (size_t)v * nL, nL, m, d.a_min);
-                f = __ldg(in.lf + (size_t)v * nL + l);
+                f = in.lf[(size_t)v * nL + l];
             }
         }
         S.lthr[v * 8 + lane] = t;
@@ -144,27 +147,35 @@ __device__ void init_ladder(const InstView& in, const WarpState& S, int v, const
 }
 
 // Warp-collective update of stream v's entries in the state arrays.
-__device__ __forceinline__ void update_stream(const InstView& in, const WarpState& S, int v, const ekya_dims& d) {
+__device__ __forceinline__ void update_stream(const InstView& in, const WarpState& S, int v, const ekya_dims& d,
+                                              bool fast) {
     const int lane = threadIdx.x & 31;
     const int D = d.steal_units, nG = d.n_gamma;
     const int ri = S.alloc[2 * v], rt = S.alloc[2 * v + 1];
-    const float stale = __ldg(in.stale + v);
+    const float stale = in.stale[v];
     float cost = 0.0f, post = 0.0f;
     if (lane >= 1 && lane <= nG) {
-        cost = __ldg(in.cost + (size_t)v * nG + lane - 1);
-        post = __ldg(in.post + (size_t)v * nG + lane - 1);
+        cost = in.cost[(size_t)v * nG + lane - 1];
+        post = in.post[(size_t)v * nG + lane - 1];
     }
     const int tk = lane < 8 ? S.lthr[v * 8 + lane] : INT_MAX;
     const float fk = lane < 8 ? S.lfac[v * 8 + lane] : -1.0f;
+    const bool mine = lane >= 1 && lane <= nG;
     // G*(r): lane g evaluates rule 2 for config g, REDUX max; values are >= 0 or
-    // the -1 sentinel, so signed-int order of the bits = float order
+    // the -1 sentinel, so signed-int order of the bits = float order.  The divisor
+    // fl(r uT) is shared by the warp: with `fast` the division is the exact
+    // shared-reciprocal fast path (stream_tables.cuh), branch-free.
     auto gstar = [&](int r) -> float {
-        float g = -1.0f;
-        if (lane == 0) g = stale;
-        else if (lane <= nG) {
-            float w;
-            if (window_acc(stale, post, cost, r, d.unit_gpu_seconds, &w)) g = w;
+        const float den = fmul(__int2float_rn(r), d.unit_gpu_seconds);
+        float f;
+        if (fast) {
+            const SharedDiv dv(den);
+            f = dv.div(cost);
+        } else {
+            f = mine && r >= 1 ? fdiv(cost, den) : 2.0f;
         }
+        const float w = fsub(post, fmul(f, fsub(post, stale)));
+        const float g = lane == 0 ? stale : (mine && r >= 1 && f <= 1.0f ? w : -1.0f);
         const int m = __reduce_max_sync(FULL, __float_as_int(g));
         return r < 0 ? -1.0f : __int_as_float(m);
     };
@@ -209,21 +220,27 @@ __device__ __forceinline__ void update_stream(const InstView& in, const WarpStat
 // Warp-collective: exact argmax config byte of stream v at its final split.
 __device__ uint8_t stream_cfg(const InstView& in, int v, int ri, int rt, const ekya_dims& d) {
     const int lane = threadIdx.x & 31, nG = d.n_gamma, nL = d.n_lambda;
-    const float stale = __ldg(in.stale + v);
+    const float stale = in.stale[v];
     const int l = lambda_star(stale, in.lmu + (size_t)v * nL, in.lf + (size_t)v * nL, nL, ri, d.a_min);
     if (l < 0) return (uint8_t)(kLambdaNone << 5);
-    const float fac = __ldg(in.lf + (size_t)v * nL + l);
+    const float fac = in.lf[(size_t)v * nL + l];
     float a = -1.0f;
     if (lane == 0) a = fmul(fac, stale);
     else if (lane <= nG) {
         float w;
-        if (window_acc(stale, __ldg(in.post + (size_t)v * nG + lane - 1),
-                       __ldg(in.cost + (size_t)v * nG + lane - 1), rt, d.unit_gpu_seconds, &w))
+        if (window_acc(stale, in.post[(size_t)v * nG + lane - 1], in.cost[(size_t)v * nG + lane - 1], rt,
+                       d.unit_gpu_seconds, &w))
             a = fmul(fac, w);
     }
     const int m = __reduce_max_sync(FULL, __float_as_int(a));
     const unsigned hits = __ballot_sync(FULL, __float_as_int(a) == m);
     return (uint8_t)((__ffs(hits) - 1) | (l << 5));
+}
+
+__device__ __forceinline__ bool uT_fast(const ekya_dims& d) {
+    const float lo = d.unit_gpu_seconds;
+    const float hi = fmul(__int2float_rn(d.units + d.steal_units), d.unit_gpu_seconds);
+    return lo >= 8.67361738e-19f && hi <= 1.15292150e18f;   // [2^-60, 2^60]
 }
 
 __device__ __forceinline__ bool lit_cond(const WarpState& S, int t, int w, int J) {
@@ -253,11 +270,12 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
     const int V = d.n_streams, J = 2 * V, D = d.steal_units, U = d.units, nG = d.n_gamma, nL = d.n_lambda;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const WarpState S = carve(smem + warp * p.warp_bytes, V);
+    float* staged = reinterpret_cast<float*>(smem + warp * p.warp_bytes + p.state_bytes);
     const long long b = (long long)blockIdx.x * p.warps + warp;
     if (b >= d.n_inst) return;
 
-    const InstView in{p.t.stale + b * V, p.t.cost + b * V * nG, p.t.post + b * V * nG,
-                      p.t.lam_min_units + b * V * nL, p.t.lam_factor + b * V * nL};
+    InstView in{p.t.stale + b * V, p.t.cost + b * V * nG, p.t.post + b * V * nG,
+                p.t.lam_min_units + b * V * nL, p.t.lam_factor + b * V * nL};
 
     // ---- validity (R-ERR) ----
     bool ok = true;
@@ -270,6 +288,24 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
     for (int i = lane; i < V * nL; i += 32)
         if (__ldg(in.lmu + i) != kLmuPad) ok &= in01(__ldg(in.lf + i));
     ok = __all_sync(FULL, ok);
+    // exact shared-reciprocal division applies to every cost and every fl(r uT), r <= U + D
+    bool fast = uT_fast(d);
+    for (int i = lane; i < V * nG; i += 32) fast &= fast_dividend(__ldg(in.cost + i));
+    fast = __all_sync(FULL, fast);
+    if (p.stage && ok) {   // stale, cost, post into this warp's shared memory
+        float* st = staged;
+        float* co = st + V;
+        float* po = co + V * nG;
+        for (int i = lane; i < V; i += 32) st[i] = __ldg(in.stale + i);
+        for (int i = lane; i < V * nG; i += 32) {
+            co[i] = __ldg(in.cost + i);
+            po[i] = __ldg(in.post + i);
+        }
+        __syncwarp();
+        in.stale = st;
+        in.cost = co;
+        in.post = po;
+    }
     if (!ok) {
         for (int j = lane; j < J; j += 32) p.out_alloc[b * J + j] = 0;
         for (int v = lane; v < V; v += 32) p.out_cfg[b * V + v] = 0;
@@ -292,7 +328,7 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
     for (int v = 0; v < V; ++v) init_ladder(in, S, v, d);
     for (int v = lane; v < V; v += 32) S.grt[v] = -1;
     __syncwarp();
-    for (int v = 0; v < V; ++v) update_stream(in, S, v, d);
+    for (int v = 0; v < V; ++v) update_stream(in, S, v, d, fast);
 
     unsigned steps = 0;
     if (p.mode == EKYA_THIEF_STEEPEST) {
@@ -353,8 +389,8 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
                 S.alloc[t] += D;
             }
             __syncwarp();
-            update_stream(in, S, t >> 1, d);
-            if ((w >> 1) != (t >> 1)) update_stream(in, S, w >> 1, d);
+            update_stream(in, S, t >> 1, d, fast);
+            if ((w >> 1) != (t >> 1)) update_stream(in, S, w >> 1, d, fast);
             if (++steps >= max_steps) {
                 if (lane == 0) flag_data_error(p.st);
                 break;
@@ -376,8 +412,8 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
                         S.alloc[t] += D;
                     }
                     __syncwarp();
-                    update_stream(in, S, t >> 1, d);
-                    if ((w >> 1) != (t >> 1)) update_stream(in, S, w >> 1, d);
+                    update_stream(in, S, t >> 1, d, fast);
+                    if ((w >> 1) != (t >> 1)) update_stream(in, S, w >> 1, d, fast);
                     ++steps;
                 } while (lit_cond(S, t, w, J));
                 pos = w + 1;
@@ -418,7 +454,10 @@ int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int m
     p.out_mean = out_mean;
     p.out_steps = out_steps;
     p.warps = kThiefThreads / 32;
-    p.warp_bytes = thief_warp_bytes(d.n_streams);
+    p.state_bytes = thief_warp_bytes(d.n_streams);
+    const size_t tbytes = ((size_t)d.n_streams * (2 * d.n_gamma + 1) * 4 + 15) & ~size_t(15);
+    p.stage = tbytes <= 8192;
+    p.warp_bytes = p.state_bytes + (p.stage ? tbytes : 0);
     size_t smem = p.warp_bytes * p.warps;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0) return EKYA_OK;
