@@ -32,6 +32,7 @@ namespace {
 
 constexpr int kProfThreads = 512;
 constexpr int kStages = 2;
+constexpr int kRadiusStages = 2;
 
 struct ProfParams {
     ekya_profile_dims p;
@@ -627,12 +628,16 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
     if (p.mode == EKYA_PROFILE_RADIUS) {
         const size_t scratch_fixed = scratch_layout(0, 0, C, 0, false).total;
         const size_t per_window = (size_t)(C + G) * 4 + 1;
-        // two stages of Hc windows each
-        long long hc = (long long)((budget - scratch_fixed - 2 * (stage_layout(C, G, 0, true).total + 64)) /
-                                   (2 * per_window));
+        // kRadiusStages stages of Hc windows: a query is split into equal chunks so
+        // that several chunks are always in flight while one is being computed
+        const int NS = kRadiusStages;
+        long long hc = (long long)((budget - scratch_fixed - NS * (stage_layout(C, G, 0, true).total + 64)) /
+                                   (NS * per_window));
         if (hc < 1) return EKYA_ERR_SHAPE;
-        P.Hc = (int)std::min<long long>(hc, H);
-        P.stages = kStages;
+        hc = std::min<long long>(hc, H);
+        const long long nch = (H + hc - 1) / hc;
+        P.Hc = (int)((H + nch - 1) / nch);
+        P.stages = NS;
         P.stage_bytes = stage_layout(C, G, P.Hc, true).total;
         size_t smem = P.stages * P.stage_bytes + scratch_layout(H, P.Hc, C, 0, false).total;
         if (smem > budget) return EKYA_ERR_SHAPE;
@@ -643,6 +648,7 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
         if (H >= 65536 || K > 32) return EKYA_ERR_LIMIT;
         const size_t scratch = scratch_layout(H, H, C, K, true).total;
         P.Hc = H;
+        const bool reg = (H <= kProfThreads) && (C <= 32);
         // prefer two stages with the accuracy tile staged, then fewer
         int cfgs[4][2] = {{2, 1}, {2, 0}, {1, 1}, {1, 0}};
         size_t smem = 0;
@@ -660,7 +666,6 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
             }
         }
         if (!found) return EKYA_ERR_SHAPE;
-        const bool reg = (H <= kProfThreads) && (C <= 32);
         auto kern = reg ? cluster_kernel<true> : cluster_kernel<false>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return EKYA_ERR_CUDA;
