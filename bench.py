@@ -409,9 +409,9 @@ def run_ours(args, rank, world, local_rank):
             r["schedules_per_s"] = w.B * world / (avg / 1000.0)
         if k.startswith("profile"):
             r["queries_per_s"] = w.Q * world / (avg / 1000.0)
-        if k == "eval_grid":
+        if k.startswith("eval_grid"):
             r["cells_per_s"] = w.B * w.V * w.nc * world / (avg / 1000.0)
-        if k == "eval_list":
+        if k.endswith("list"):
             r["allocation_vectors_per_s"] = w.B * w.N * world / (avg / 1000.0)
         rows_out[k] = r
     dom = max((k for k in per if k in roof), key=lambda k: per[k])
