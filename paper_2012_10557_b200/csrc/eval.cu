@@ -345,6 +345,8 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
         uint8_t* cst = smem + L.cfgbuf + (i & 1) * L.cfg_bytes + (cdst ? granules(cdst, 1).off : 0);
         const size_t off_tvc = a16((size_t)(U + 1));
         const unsigned UU = (unsigned)U | ((unsigned)U << 16);
+        const bool pairs = (V % 2 == 0) && (reinterpret_cast<uintptr_t>(rs) % 8 == 0) &&
+                           (reinterpret_cast<uintptr_t>(cst) % 2 == 0);
         for (int r = threadIdx.x; r < rows; r += kListThreads) {
             // (ri, rt) of stream v is one 32-bit word (alloc is 4-byte aligned, J even);
             // both halves are clamped to U with one SIMD min, and any clamp marks the row bad
@@ -354,16 +356,29 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
             unsigned long long S = 0;
             const unsigned char* tp = tabs;
             uint8_t* cr = cst + (size_t)r * V;
-#pragma unroll 2
-            for (int v = 0; v < V; ++v, tp += tb) {
-                const unsigned pr = row[v];
+            // one stream's lookup: clamp, validity, table entry (Q32 | cfg << 40)
+            auto look = [&](unsigned pr, const unsigned char* t) -> unsigned long long {
                 const unsigned pc = __vminu2(pr, UU);
                 bad |= pr ^ pc;
                 const int ri = (int)(pc & 0xFFFFu), rt = (int)(pc >> 16);
                 tot += ri + rt;
-                const unsigned long long e = reinterpret_cast<const unsigned long long*>(tp + off_tvc)[rt * kSlots + tp[ri]];
-                S += e & 0xFFFFFFFFFFull;
-                cr[v] = (uint8_t)(e >> 40);
+                return reinterpret_cast<const unsigned long long*>(t + off_tvc)[rt * kSlots + t[ri]];
+            };
+            if (pairs) {   // two streams per 8-byte row load and per 2-byte config store
+                const uint2* row2 = reinterpret_cast<const uint2*>(row);
+                uint16_t* cr2 = reinterpret_cast<uint16_t*>(cr);
+                for (int v2 = 0; v2 < V / 2; ++v2, tp += 2 * tb) {
+                    const uint2 pr = row2[v2];
+                    const unsigned long long e0 = look(pr.x, tp), e1 = look(pr.y, tp + tb);
+                    S += (e0 & 0xFFFFFFFFFFull) + (e1 & 0xFFFFFFFFFFull);
+                    cr2[v2] = (uint16_t)((unsigned)(e0 >> 40) | ((unsigned)(e1 >> 40) << 8));
+                }
+            } else {
+                for (int v = 0; v < V; ++v, tp += tb) {
+                    const unsigned long long e = look(row[v], tp);
+                    S += e & 0xFFFFFFFFFFull;
+                    cr[v] = (uint8_t)(e >> 40);
+                }
             }
             const bool rok = ok && bad == 0 && tot <= U;   // Eq. 1 constraint 2
             if (!rok) {                                     // R-ERR: zero the row

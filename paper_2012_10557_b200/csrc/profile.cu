@@ -31,7 +31,6 @@ namespace ekya {
 namespace {
 
 constexpr int kProfThreads = 512;
-constexpr int kStages = 2;
 constexpr int kRadiusStages = 2;
 
 struct ProfParams {
