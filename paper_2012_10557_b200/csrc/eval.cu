@@ -26,8 +26,6 @@ namespace {
 
 constexpr int kGridWarps = 32;
 constexpr int kListThreads = 1024;
-constexpr int kListRows = 1024;     // rows per pipeline stage
-constexpr int kListStages = 3;
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -63,7 +61,7 @@ __device__ __forceinline__ Tabs carve_tabs(unsigned char* p, int U) {
 }
 
 // Instance inputs (stale, cost, post, lam_min_units, lam_factor of one
-// instance) staged by the TMA alongside the instance's first row chunk.
+// instance), staged by the TMA one instance ahead (double buffer).
 struct InstLayout {
     size_t stale, cost, post, lmu, lf, total;
 };
@@ -75,25 +73,21 @@ __host__ __device__ inline InstLayout inst_layout(int V, int nG, int nL) {
     L.post = o;  o += a16((size_t)V * nG * 4) + 16;
     L.lmu = o;   o += a16((size_t)V * nL * 2) + 16;
     L.lf = o;    o += a16((size_t)V * nL * 4) + 16;
-    L.total = o;
+    L.total = a16(o);
     return L;
 }
 
 struct ListLayout {
-    size_t sin, tabs, stage, cfgbuf, bars, total, rows_bytes, stage_bytes, cfg_bytes;
+    size_t sin, tabs, inst, bars, total, inst_bytes;
 };
 __host__ __device__ inline ListLayout list_layout(int U, int V, int nG, int nL) {
     ListLayout L;
-    const int J = 2 * V;
     size_t o = 0;
     L.sin = o;    o += a16(sizeof(StreamIn)) * (size_t)(kListThreads / 32);
     L.tabs = o;   o += tab_bytes(U) * V;
-    L.rows_bytes = a16((size_t)kListRows * J * 2) + 16;
-    L.stage_bytes = L.rows_bytes + inst_layout(V, nG, nL).total;
-    L.stage = o;  o += L.stage_bytes * kListStages;
-    L.cfg_bytes = a16((size_t)kListRows * V) + 16;
-    L.cfgbuf = o; o += L.cfg_bytes * 2;
-    L.bars = o;   o += 8 * kListStages;
+    L.inst_bytes = inst_layout(V, nG, nL).total;
+    L.inst = o;   o += 2 * L.inst_bytes;
+    L.bars = o;   o += 16;
     L.total = o;
     return L;
 }
@@ -233,166 +227,145 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     unsigned char* tabs = smem + L.tabs;
     const size_t tb = p.tb;
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bars);
-
     const long long N = p.n_alloc;
-    const long long nch = (N + kListRows - 1) / kListRows;
-    const long long nb_local = d.n_inst > blockIdx.x ? (d.n_inst - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const long long items = nb_local * nch;
-    // items fit 32-bit index math (items <= B * nch / gridDim.x)
-    const unsigned unch = (unsigned)nch;
-    auto item_b = [&](long long i) { return (long long)blockIdx.x + (long long)((unsigned)i / unch) * gridDim.x; };
-    auto item_n0 = [&](long long i) { return (long long)((unsigned)i % unch) * kListRows; };
-    // leader thread: one row chunk (+ the instance inputs with its first chunk)
-    auto issue = [&](long long i) {
-        const long long b = item_b(i), n0 = item_n0(i);
-        const long long rows = min((long long)kListRows, N - n0);
-        unsigned char* st = smem + L.stage + (i % kListStages) * L.stage_bytes;
-        unsigned long long* br = &bar[i % kListStages];
-        const Granules g = granules(p.alloc + (b * N + n0) * J, (size_t)rows * J * 2);
-        unsigned tot = g.bytes;
-        Granules gi[5];
-        if (n0 == 0) {
-            gi[0] = granules(p.t.stale + b * V, (size_t)V * 4);
-            gi[1] = granules(p.t.cost + b * V * nG, (size_t)V * nG * 4);
-            gi[2] = granules(p.t.post + b * V * nG, (size_t)V * nG * 4);
-            gi[3] = granules(p.t.lam_min_units + b * V * nL, (size_t)V * nL * 2);
-            gi[4] = granules(p.t.lam_factor + b * V * nL, (size_t)V * nL * 4);
-            for (int k = 0; k < 5; ++k) tot += gi[k].bytes;
-        }
-        mbar_arrive_expect_tx(br, tot);
-        bulk_g2s(st, g.g0, g.bytes, br);
-        if (n0 == 0) {
-            const size_t off[5] = {IL.stale, IL.cost, IL.post, IL.lmu, IL.lf};
-            for (int k = 0; k < 5; ++k)
-                if (gi[k].bytes) bulk_g2s(st + L.rows_bytes + off[k], gi[k].g0, gi[k].bytes, br);
-        }
+
+    // leader thread: TMA the inputs of instance b into buffer k, and prefetch its
+    // allocation rows into L2 (they are then read with plain coalesced loads)
+    auto issue = [&](long long b, int k) {
+        unsigned char* dst = smem + L.inst + k * L.inst_bytes;
+        const Granules g[5] = {granules(p.t.stale + b * V, (size_t)V * 4),
+                               granules(p.t.cost + b * V * nG, (size_t)V * nG * 4),
+                               granules(p.t.post + b * V * nG, (size_t)V * nG * 4),
+                               granules(p.t.lam_min_units + b * V * nL, (size_t)V * nL * 2),
+                               granules(p.t.lam_factor + b * V * nL, (size_t)V * nL * 4)};
+        const size_t off[5] = {IL.stale, IL.cost, IL.post, IL.lmu, IL.lf};
+        unsigned tot = 0;
+        for (int i = 0; i < 5; ++i) tot += g[i].bytes;
+        mbar_arrive_expect_tx(&bar[k], tot);
+        for (int i = 0; i < 5; ++i)
+            if (g[i].bytes) bulk_g2s(dst + off[i], g[i].g0, g[i].bytes, &bar[k]);
+        const Granules gr = granules(p.alloc + b * N * J, (size_t)N * J * 2);
+        for (unsigned o = 0; o < gr.bytes; o += (1u << 20))
+            bulk_prefetch_l2(gr.g0 + o, min(gr.bytes - o, 1u << 20));
     };
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kListStages; ++s) mbar_init(&bar[s], 1);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
         fence_barrier_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (long long i = 0; i < kListStages && i < items; ++i) issue(i);
+    if (threadIdx.x == 0 && blockIdx.x < d.n_inst) issue(blockIdx.x, 0);
 
-    bool ok = true;
-    for (long long i = 0; i < items; ++i) {
-        const long long b = item_b(i), n0 = item_n0(i);
-        const int rows = (int)min((long long)kListRows, N - n0);
-        const int s = (int)(i % kListStages);
-        unsigned char* st = smem + L.stage + s * L.stage_bytes;
-        mbar_wait(&bar[s], (unsigned)((i / kListStages) & 1));
-        if (n0 == 0) {
-            // new instance: validate (R-ERR) and build the V stream tables from the staged inputs
-            unsigned char* ib = st + L.rows_bytes;
-            const float* stale = reinterpret_cast<const float*>(ib + IL.stale + granules(p.t.stale + b * V, 4).off);
-            const float* cost = reinterpret_cast<const float*>(ib + IL.cost + granules(p.t.cost + b * V * nG, 4).off);
-            const float* post = reinterpret_cast<const float*>(ib + IL.post + granules(p.t.post + b * V * nG, 4).off);
-            const uint16_t* lmu = reinterpret_cast<const uint16_t*>(
-                ib + IL.lmu + granules(p.t.lam_min_units + b * V * nL, 2).off);
-            const float* lf = reinterpret_cast<const float*>(ib + IL.lf + granules(p.t.lam_factor + b * V * nL, 4).off);
-            bool vok = true;
-            for (int t = threadIdx.x; t < V; t += blockDim.x) vok &= in01(stale[t]);
-            for (int t = threadIdx.x; t < V * nG; t += blockDim.x) {
-                const float c = cost[t];
-                if (!(c >= 0.0f)) vok = false;
-                else if (!isinf(c)) vok &= in01(post[t]);
-            }
-            for (int t = threadIdx.x; t < V * nL; t += blockDim.x)
-                if (lmu[t] != kLmuPad) vok &= in01(lf[t]);
-            ok = __syncthreads_and(vok) != 0;
-            if (ok) {
-                // warp tasks = (stream, block of 32 r_train rows): V x ceil((U+1)/32) tasks
-                const int nblk = (U + 32) / 32;
-                for (int task = warp; task < V * nblk; task += nw) {
-                    const int v = task / nblk, blk = task - v * nblk;
-                    StreamIn* si = reinterpret_cast<StreamIn*>(smem + L.sin + (size_t)warp * a16(sizeof(StreamIn)));
-                    if (lane < nG) {
-                        si->cost[lane] = cost[v * nG + lane];
-                        si->post[lane] = post[v * nG + lane];
-                    }
-                    if (lane < nL) {
-                        si->lf[lane] = lf[v * nL + lane];
-                        si->lmu[lane] = lmu[v * nL + lane];
-                    }
-                    const bool f = lane >= nG || fast_dividend(cost[v * nG + lane]);
-                    const unsigned all = __ballot_sync(0xffffffffu, f);
-                    if (lane == 0) {
-                        si->stale = stale[v];
-                        si->fast = all == 0xffffffffu;
-                    }
-                    __syncwarp();
-                    Tabs T = carve_tabs(tabs + v * tb, U);
-                    const int r1 = min(U + 1, blk * 32 + 32);
-                    warp_build_tables<GM>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc, blk * 32, r1,
-                                          blk == 0);
-                    // LIST needs the exact Q32 value, not the float: entry = Q32 | cfg << 40 (Q32 <= 2^32)
-                    unsigned long long* q = reinterpret_cast<unsigned long long*>(T.tvc);
-                    for (int e = blk * 32 * kSlots + lane; e < r1 * kSlots; e += 32) {
-                        const uint2 vc = T.tvc[e];
-                        q[e] = q32(__uint_as_float(vc.x)) | ((unsigned long long)(vc.y & 0xFFu) << 40);
-                    }
-                }
-            } else if (threadIdx.x == 0) {
-                flag_data_error(p.st);
-            }
-            __syncthreads();
+    const unsigned UU = (unsigned)U | ((unsigned)U << 16);
+    const bool pairs = (V % 2 == 0) && (reinterpret_cast<uintptr_t>(p.alloc) % 8 == 0) &&
+                       (!p.out_cfg || reinterpret_cast<uintptr_t>(p.out_cfg) % 2 == 0);
+    const size_t off_tvc = a16((size_t)(U + 1));
+    int j = 0;
+    for (long long b = blockIdx.x; b < d.n_inst; b += gridDim.x, ++j) {
+        const int k = j & 1;
+        if (threadIdx.x == 0 && b + gridDim.x < d.n_inst) issue(b + gridDim.x, k ^ 1);
+        mbar_wait(&bar[k], (unsigned)((j >> 1) & 1));
+        // ---- validate (R-ERR) and build the V stream tables from the staged inputs ----
+        unsigned char* ib = smem + L.inst + k * L.inst_bytes;
+        const float* stale = reinterpret_cast<const float*>(ib + IL.stale + granules(p.t.stale + b * V, 4).off);
+        const float* cost = reinterpret_cast<const float*>(ib + IL.cost + granules(p.t.cost + b * V * nG, 4).off);
+        const float* post = reinterpret_cast<const float*>(ib + IL.post + granules(p.t.post + b * V * nG, 4).off);
+        const uint16_t* lmu =
+            reinterpret_cast<const uint16_t*>(ib + IL.lmu + granules(p.t.lam_min_units + b * V * nL, 2).off);
+        const float* lf = reinterpret_cast<const float*>(ib + IL.lf + granules(p.t.lam_factor + b * V * nL, 4).off);
+        bool vok = true;
+        for (int t = threadIdx.x; t < V; t += blockDim.x) vok &= in01(stale[t]);
+        for (int t = threadIdx.x; t < V * nG; t += blockDim.x) {
+            const float c = cost[t];
+            if (!(c >= 0.0f)) vok = false;
+            else if (!isinf(c)) vok &= in01(post[t]);
         }
-        const uint16_t* src = p.alloc + (b * N + n0) * J;
-        const uint16_t* rs = reinterpret_cast<const uint16_t*>(st + granules(src, 2).off);
-        uint8_t* cdst = p.out_cfg ? p.out_cfg + (b * N + n0) * V : nullptr;
-        uint8_t* cst = smem + L.cfgbuf + (i & 1) * L.cfg_bytes + (cdst ? granules(cdst, 1).off : 0);
-        const size_t off_tvc = a16((size_t)(U + 1));
-        const unsigned UU = (unsigned)U | ((unsigned)U << 16);
-        const bool pairs = (V % 2 == 0) && (reinterpret_cast<uintptr_t>(rs) % 8 == 0) &&
-                           (reinterpret_cast<uintptr_t>(cst) % 2 == 0);
-        for (int r = threadIdx.x; r < rows; r += kListThreads) {
-            // (ri, rt) of stream v is one 32-bit word (alloc is 4-byte aligned, J even);
-            // both halves are clamped to U with one SIMD min, and any clamp marks the row bad
-            const unsigned* row = reinterpret_cast<const unsigned*>(rs + (size_t)r * J);
-            unsigned bad = 0;
+        for (int t = threadIdx.x; t < V * nL; t += blockDim.x)
+            if (lmu[t] != kLmuPad) vok &= in01(lf[t]);
+        const bool ok = __syncthreads_and(vok) != 0;
+        if (ok) {
+            // warp tasks = (stream, block of 32 r_train rows): V x ceil((U+1)/32) tasks
+            const int nblk = (U + 32) / 32;
+            StreamIn* si = reinterpret_cast<StreamIn*>(smem + L.sin + (size_t)warp * a16(sizeof(StreamIn)));
+            for (int task = warp; task < V * nblk; task += nw) {
+                const int v = task / nblk, blk = task - v * nblk;
+                if (lane < nG) {
+                    si->cost[lane] = cost[v * nG + lane];
+                    si->post[lane] = post[v * nG + lane];
+                    si->diff[lane] = fsub(post[v * nG + lane], stale[v]);
+                }
+                if (lane < nL) {
+                    si->lf[lane] = lf[v * nL + lane];
+                    si->lmu[lane] = lmu[v * nL + lane];
+                }
+                const bool f = lane >= nG || fast_dividend(cost[v * nG + lane]);
+                const unsigned all = __ballot_sync(0xffffffffu, f);
+                if (lane == 0) {
+                    si->stale = stale[v];
+                    si->fast = all == 0xffffffffu;
+                }
+                __syncwarp();
+                Tabs T = carve_tabs(tabs + v * tb, U);
+                const int r1 = min(U + 1, blk * 32 + 32);
+                warp_build_tables<GM>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc, blk * 32, r1,
+                                      blk == 0);
+                // LIST needs the exact Q32 value, not the float: entry = Q32 | cfg << 40 (Q32 <= 2^32)
+                unsigned long long* q = reinterpret_cast<unsigned long long*>(T.tvc);
+                for (int e = blk * 32 * kSlots + lane; e < r1 * kSlots; e += 32) {
+                    const uint2 vc = T.tvc[e];
+                    q[e] = q32(__uint_as_float(vc.x)) | ((unsigned long long)(vc.y & 0xFFu) << 40);
+                }
+                __syncwarp();
+            }
+        } else if (threadIdx.x == 0) {
+            flag_data_error(p.st);
+        }
+        __syncthreads();
+        // ---- rows: one thread per allocation vector, read straight from global (L2) ----
+        for (long long r = threadIdx.x; r < N; r += kListThreads) {
+            const long long o = b * N + r;
+            const uint16_t* rowp = p.alloc + o * J;
+            bool bad = false;
             int tot = 0;
             unsigned long long S = 0;
             const unsigned char* tp = tabs;
-            uint8_t* cr = cst + (size_t)r * V;
-            // one stream's lookup: clamp, validity, table entry (Q32 | cfg << 40)
             auto look = [&](unsigned pr, const unsigned char* t) -> unsigned long long {
-                const unsigned pc = __vminu2(pr, UU);
-                bad |= pr ^ pc;
+                const unsigned pc = __vminu2(pr, UU);   // clamp both halves to U; any clamp = bad row
+                bad |= pr != pc;
                 const int ri = (int)(pc & 0xFFFFu), rt = (int)(pc >> 16);
                 tot += ri + rt;
                 return reinterpret_cast<const unsigned long long*>(t + off_tvc)[rt * kSlots + t[ri]];
             };
             if (pairs) {   // two streams per 8-byte row load and per 2-byte config store
-                const uint2* row2 = reinterpret_cast<const uint2*>(row);
-                uint16_t* cr2 = reinterpret_cast<uint16_t*>(cr);
+                const uint2* row2 = reinterpret_cast<const uint2*>(rowp);
+                uint16_t* cr2 = p.out_cfg ? reinterpret_cast<uint16_t*>(p.out_cfg + o * V) : nullptr;
                 for (int v2 = 0; v2 < V / 2; ++v2, tp += 2 * tb) {
-                    const uint2 pr = row2[v2];
+                    const uint2 pr = __ldg(row2 + v2);
                     const unsigned long long e0 = look(pr.x, tp), e1 = look(pr.y, tp + tb);
                     S += (e0 & 0xFFFFFFFFFFull) + (e1 & 0xFFFFFFFFFFull);
-                    cr2[v2] = (uint16_t)((unsigned)(e0 >> 40) | ((unsigned)(e1 >> 40) << 8));
+                    if (cr2) cr2[v2] = (uint16_t)((unsigned)(e0 >> 40) | ((unsigned)(e1 >> 40) << 8));
                 }
             } else {
+                const unsigned* row = reinterpret_cast<const unsigned*>(rowp);
+                uint8_t* cr = p.out_cfg ? p.out_cfg + o * V : nullptr;
                 for (int v = 0; v < V; ++v, tp += tb) {
-                    const unsigned long long e = look(row[v], tp);
+                    const unsigned long long e = look(__ldg(row + v), tp);
                     S += e & 0xFFFFFFFFFFull;
-                    cr[v] = (uint8_t)(e >> 40);
+                    if (cr) cr[v] = (uint8_t)(e >> 40);
                 }
             }
-            const bool rok = ok && bad == 0 && tot <= U;   // Eq. 1 constraint 2
-            if (!rok) {                                     // R-ERR: zero the row
+            const bool rok = ok && !bad && tot <= U;   // Eq. 1 constraint 2
+            if (!rok) {                                 // R-ERR: zero the row
                 S = 0;
-                for (int v = 0; v < V; ++v) cr[v] = 0;
+                if (p.out_cfg)
+                    for (int v = 0; v < V; ++v) p.out_cfg[o * V + v] = 0;
                 if (ok) flag_data_error(p.st);
             }
-            const long long o = b * N + n0 + r;
             p.out_sum[o] = S;
             if (p.out_mean) p.out_mean[o] = rok ? mean_q32(S, V) : 0.0f;
         }
-        __syncthreads();   // stage s consumed; config bytes of this chunk staged
-        if (threadIdx.x == 0 && i + kListStages < items) issue(i + kListStages);
-        if (cdst) store_from_smem(cdst, cst, (size_t)rows * V);   // buffer (i & 1): reused after the next barrier
+        __syncthreads();   // tables and input buffer k are free again
     }
 }
 
