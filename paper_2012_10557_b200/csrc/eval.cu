@@ -78,13 +78,16 @@ __host__ __device__ inline InstLayout inst_layout(int V, int nG, int nL) {
 }
 
 struct ListLayout {
-    size_t sin, tabs, inst, bars, total, inst_bytes;
+    size_t sin, tabs, tabset, inst, bars, total, inst_bytes;
+    int ntabs;   // 2 = double-buffered table sets (build of instance j+1 overlaps rows of j)
 };
-__host__ __device__ inline ListLayout list_layout(int U, int V, int nG, int nL) {
+__host__ __device__ inline ListLayout list_layout(int U, int V, int nG, int nL, int ntabs) {
     ListLayout L;
     size_t o = 0;
+    L.ntabs = ntabs;
     L.sin = o;    o += a16(sizeof(StreamIn)) * (size_t)(kListThreads / 32);
-    L.tabs = o;   o += tab_bytes(U) * V;
+    L.tabset = tab_bytes(U) * V;
+    L.tabs = o;   o += L.tabset * ntabs;
     L.inst_bytes = inst_layout(V, nG, nL).total;
     L.inst = o;   o += 2 * L.inst_bytes;
     L.bars = o;   o += 16;
@@ -104,9 +107,11 @@ struct EvalParams {
     float* out_mean;
     uint8_t* out_cfg;
     size_t warp_bytes;   // GRID: shared bytes per warp
+    int grid_qs;         // GRID: 1 = cell-position table staged in shared memory
     ListLayout L;        // LIST: shared-memory layout (host-computed, read from the param space)
     InstLayout IL;
     size_t tb;           // LIST: bytes per stream table
+    double rcp_v;        // LIST: RN(1 / V), for the exact mean
 };
 
 // ------------------------------------------------------------------------
@@ -129,13 +134,14 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
     const int U = d.units, nG = d.n_gamma, nL = d.n_lambda, V = d.n_streams;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t nq_tab = cellinfo_quads(U);
+    const bool use_qs = p.grid_qs != 0;   // position table in shared memory (small U)
     unsigned* qs = reinterpret_cast<unsigned*>(smem);
-    unsigned char* mine = smem + a16(4 * nq_tab * sizeof(unsigned)) + (size_t)warp * p.warp_bytes;
+    unsigned char* mine = smem + (use_qs ? a16(4 * nq_tab * sizeof(unsigned)) : 0) + (size_t)warp * p.warp_bytes;
     StreamIn* sin = reinterpret_cast<StreamIn*>(mine);
     Tabs T = carve_tabs(mine + a16(sizeof(StreamIn)), U);
     const int NC = (U + 1) * (U + 2) / 2;
 
-    for (int t = threadIdx.x; t < (int)(4 * nq_tab); t += blockDim.x) {
+    for (int t = threadIdx.x; use_qs && t < (int)(4 * nq_tab); t += blockDim.x) {
         const int phi = t / (int)nq_tab, k = t - phi * (int)nq_tab;
         const int c = min(max(4 * k - phi, 0), NC - 1);
         const int rt = row_of(c, U);
@@ -143,9 +149,10 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
     }
     __syncthreads();
 
-    const long long nwarps = (long long)gridDim.x * kGridWarps;
+    const int cta_warps = blockDim.x >> 5;
+    const long long nwarps = (long long)gridDim.x * cta_warps;
     // one warp per instance (validated once), its V streams in turn
-    for (long long b = (long long)blockIdx.x * kGridWarps + warp; b < d.n_inst; b += nwarps) {
+    for (long long b = (long long)blockIdx.x * cta_warps + warp; b < d.n_inst; b += nwarps) {
         const bool ok = warp_instance_valid(p.t, b, V, nG, nL);
         if (!ok && lane == 0) flag_data_error(p.st);
         for (int v = 0; v < V; ++v) {
@@ -170,8 +177,16 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
                 // (rt, ri) of the quad's cells: the first from the table, then along the row
                 unsigned e[4];
                 {
-                    const unsigned s0 = qst[k];
-                    int rt = (int)(s0 >> 16), ri = (int)(s0 & 0xFFFFu);
+                    int rt, ri;
+                    if (use_qs) {
+                        const unsigned s0 = qst[k];
+                        rt = (int)(s0 >> 16);
+                        ri = (int)(s0 & 0xFFFFu);
+                    } else {
+                        const int c = max(c0, 0);
+                        rt = row_of(c, U);
+                        ri = c - rowstart(rt, U);
+                    }
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         e[j] = ((unsigned)(rt * kSlots) << 16) | (unsigned)ri;
@@ -224,49 +239,40 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kListThreads / 32;
     const ListLayout& L = p.L;
     const InstLayout& IL = p.IL;
-    unsigned char* tabs = smem + L.tabs;
     const size_t tb = p.tb;
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bars);
-    const long long N = p.n_alloc;
+    const long long N = p.n_alloc, B = d.n_inst, g = gridDim.x;
 
-    // leader thread: TMA the inputs of instance b into buffer k, and prefetch its
-    // allocation rows into L2 (they are then read with plain coalesced loads)
-    auto issue = [&](long long b, int k) {
+    // leader thread: TMA the inputs of instance b into input buffer k
+    auto issue_inputs = [&](long long b, int k) {
         unsigned char* dst = smem + L.inst + k * L.inst_bytes;
-        const Granules g[5] = {granules(p.t.stale + b * V, (size_t)V * 4),
-                               granules(p.t.cost + b * V * nG, (size_t)V * nG * 4),
-                               granules(p.t.post + b * V * nG, (size_t)V * nG * 4),
-                               granules(p.t.lam_min_units + b * V * nL, (size_t)V * nL * 2),
-                               granules(p.t.lam_factor + b * V * nL, (size_t)V * nL * 4)};
+        const Granules gs[5] = {granules(p.t.stale + b * V, (size_t)V * 4),
+                                granules(p.t.cost + b * V * nG, (size_t)V * nG * 4),
+                                granules(p.t.post + b * V * nG, (size_t)V * nG * 4),
+                                granules(p.t.lam_min_units + b * V * nL, (size_t)V * nL * 2),
+                                granules(p.t.lam_factor + b * V * nL, (size_t)V * nL * 4)};
         const size_t off[5] = {IL.stale, IL.cost, IL.post, IL.lmu, IL.lf};
         unsigned tot = 0;
-        for (int i = 0; i < 5; ++i) tot += g[i].bytes;
+        for (int i = 0; i < 5; ++i) tot += gs[i].bytes;
         mbar_arrive_expect_tx(&bar[k], tot);
         for (int i = 0; i < 5; ++i)
-            if (g[i].bytes) bulk_g2s(dst + off[i], g[i].g0, g[i].bytes, &bar[k]);
+            if (gs[i].bytes) bulk_g2s(dst + off[i], gs[i].g0, gs[i].bytes, &bar[k]);
+    };
+    // leader thread: bulk-prefetch instance b's allocation rows into L2 (they are
+    // then read with plain coalesced loads)
+    auto prefetch_rows = [&](long long b) {
         const Granules gr = granules(p.alloc + b * N * J, (size_t)N * J * 2);
-        for (unsigned o = 0; o < gr.bytes; o += (1u << 20))
-            bulk_prefetch_l2(gr.g0 + o, min(gr.bytes - o, 1u << 20));
+        for (unsigned o = 0; o < gr.bytes; o += (1u << 20)) bulk_prefetch_l2(gr.g0 + o, min(gr.bytes - o, 1u << 20));
     };
 
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && blockIdx.x < d.n_inst) issue(blockIdx.x, 0);
-
-    const unsigned UU = (unsigned)U | ((unsigned)U << 16);
-    const bool pairs = (V % 2 == 0) && (reinterpret_cast<uintptr_t>(p.alloc) % 8 == 0) &&
-                       (!p.out_cfg || reinterpret_cast<uintptr_t>(p.out_cfg) % 2 == 0);
-    const size_t off_tvc = a16((size_t)(U + 1));
-    int j = 0;
-    for (long long b = blockIdx.x; b < d.n_inst; b += gridDim.x, ++j) {
-        const int k = j & 1;
-        if (threadIdx.x == 0 && b + gridDim.x < d.n_inst) issue(b + gridDim.x, k ^ 1);
+    // Validate (R-ERR) and build the V stream tables of instance b (the j-th
+    // instance of this CTA, inputs in buffer j & 1) into table set `tabs`:
+    // warp tasks = (stream, block of 32 r_train rows).  Returns this thread's
+    // share of the validity test; the tables are built regardless (an invalid
+    // instance's rows are zeroed, so its tables are never read).
+    auto build = [&](long long b, long long j, unsigned char* tabs) -> bool {
+        const int k = (int)(j & 1);
         mbar_wait(&bar[k], (unsigned)((j >> 1) & 1));
-        // ---- validate (R-ERR) and build the V stream tables from the staged inputs ----
         unsigned char* ib = smem + L.inst + k * L.inst_bytes;
         const float* stale = reinterpret_cast<const float*>(ib + IL.stale + granules(p.t.stale + b * V, 4).off);
         const float* cost = reinterpret_cast<const float*>(ib + IL.cost + granules(p.t.cost + b * V * nG, 4).off);
@@ -283,46 +289,44 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
         }
         for (int t = threadIdx.x; t < V * nL; t += blockDim.x)
             if (lmu[t] != kLmuPad) vok &= in01(lf[t]);
-        const bool ok = __syncthreads_and(vok) != 0;
-        if (ok) {
-            // warp tasks = (stream, block of 32 r_train rows): V x ceil((U+1)/32) tasks
-            const int nblk = (U + 32) / 32;
-            StreamIn* si = reinterpret_cast<StreamIn*>(smem + L.sin + (size_t)warp * a16(sizeof(StreamIn)));
-            for (int task = warp; task < V * nblk; task += nw) {
-                const int v = task / nblk, blk = task - v * nblk;
-                if (lane < nG) {
-                    si->cost[lane] = cost[v * nG + lane];
-                    si->post[lane] = post[v * nG + lane];
-                    si->diff[lane] = fsub(post[v * nG + lane], stale[v]);
-                }
-                if (lane < nL) {
-                    si->lf[lane] = lf[v * nL + lane];
-                    si->lmu[lane] = lmu[v * nL + lane];
-                }
-                const bool f = lane >= nG || fast_dividend(cost[v * nG + lane]);
-                const unsigned all = __ballot_sync(0xffffffffu, f);
-                if (lane == 0) {
-                    si->stale = stale[v];
-                    si->fast = all == 0xffffffffu;
-                }
-                __syncwarp();
-                Tabs T = carve_tabs(tabs + v * tb, U);
-                const int r1 = min(U + 1, blk * 32 + 32);
-                warp_build_tables<GM>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc, blk * 32, r1,
-                                      blk == 0);
-                // LIST needs the exact Q32 value, not the float: entry = Q32 | cfg << 40 (Q32 <= 2^32)
-                unsigned long long* q = reinterpret_cast<unsigned long long*>(T.tvc);
-                for (int e = blk * 32 * kSlots + lane; e < r1 * kSlots; e += 32) {
-                    const uint2 vc = T.tvc[e];
-                    q[e] = q32(__uint_as_float(vc.x)) | ((unsigned long long)(vc.y & 0xFFu) << 40);
-                }
-                __syncwarp();
+        const int nblk = (U + 32) / 32;
+        StreamIn* si = reinterpret_cast<StreamIn*>(smem + L.sin + (size_t)warp * a16(sizeof(StreamIn)));
+        for (int task = warp; task < V * nblk; task += nw) {
+            const int v = task / nblk, blk = task - v * nblk;
+            if (lane < nG) {
+                si->cost[lane] = cost[v * nG + lane];
+                si->post[lane] = post[v * nG + lane];
+                si->diff[lane] = fsub(post[v * nG + lane], stale[v]);
             }
-        } else if (threadIdx.x == 0) {
-            flag_data_error(p.st);
+            if (lane < nL) {
+                si->lf[lane] = lf[v * nL + lane];
+                si->lmu[lane] = lmu[v * nL + lane];
+            }
+            const bool f = lane >= nG || fast_dividend(cost[v * nG + lane]);
+            const unsigned all = __ballot_sync(0xffffffffu, f);
+            if (lane == 0) {
+                si->stale = stale[v];
+                si->fast = all == 0xffffffffu;
+            }
+            __syncwarp();
+            unsigned char* tv = tabs + v * tb;
+            const int r1 = min(U + 1, blk * 32 + 32);
+            // entries = exact Q32(value) | config << 40: LIST sums the exact values
+            warp_build_tables<GM>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
+                                  reinterpret_cast<unsigned long long*>(tv + a16((size_t)(U + 1))), blk * 32, r1,
+                                  blk == 0);
         }
-        __syncthreads();
-        // ---- rows: one thread per allocation vector, read straight from global (L2) ----
+        return vok;
+    };
+
+    const unsigned UU = (unsigned)U | ((unsigned)U << 16);
+    const bool pairs = (V % 2 == 0) && (reinterpret_cast<uintptr_t>(p.alloc) % 8 == 0) &&
+                       (!p.out_cfg || reinterpret_cast<uintptr_t>(p.out_cfg) % 2 == 0);
+    const size_t off_tvc = a16((size_t)(U + 1));
+    const double rcp_v = p.rcp_v, dv = (double)V;
+
+    // One thread per allocation row of instance b, read straight from global (L2).
+    auto rows = [&](long long b, const unsigned char* tabs, bool ok) {
         for (long long r = threadIdx.x; r < N; r += kListThreads) {
             const long long o = b * N + r;
             const uint16_t* rowp = p.alloc + o * J;
@@ -363,9 +367,66 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
                 if (ok) flag_data_error(p.st);
             }
             p.out_sum[o] = S;
-            if (p.out_mean) p.out_mean[o] = rok ? mean_q32(S, V) : 0.0f;
+            if (p.out_mean) {
+                // mean = (float)((double)S / (V 2^32)): S / V by the correctly rounded
+                // reciprocal rcp_v = RN(1/V) and one exact-residual correction (Markstein:
+                // RN(q0 + r rcp_v) = RN(S / V) for q0 within 1 ulp; S < 2^53, no
+                // over/underflow), then the exact power-of-two scale
+                const double a = __ull2double_rn(S);
+                const double q0 = __dmul_rn(a, rcp_v);
+                const double q = __fma_rn(__fma_rn(-dv, q0, a), rcp_v, q0);
+                p.out_mean[o] = rok ? __double2float_rn(__dmul_rn(q, 2.3283064365386963e-10)) : 0.0f;
+            }
         }
-        __syncthreads();   // tables and input buffer k are free again
+    };
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const long long b0 = blockIdx.x;
+    if (b0 >= B) return;
+    // Double-buffered table sets (ntabs == 2): while the rows of this CTA's
+    // instance j stream, the tables of instance j+1 are built -- odd warps build
+    // first and even warps stream first, so the issue-bound build overlaps the
+    // memory-bound rows inside the SM; inputs are staged two instances ahead.
+    // Single set (large V x U): build j, barrier, rows j.  Step j = -1 (double
+    // buffering only) builds instance 0.  One call site each for build and rows.
+    const bool dbl = L.ntabs == 2;
+    const int ahead = dbl ? 2 : 1;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < ahead; ++i)
+            if (b0 + i * g < B) issue_inputs(b0 + i * g, i);
+    bool ok = true;
+    for (long long j = dbl ? -1 : 0; b0 + j * g < B; ++j) {
+        const long long b = b0 + j * g, jb = dbl ? j + 1 : j, bb = b0 + jb * g;   // rows of b, build of bb
+        if (threadIdx.x == 0) {
+            // inputs of instance jb+1 (unless the prologue staged them) into buffer (jb+1) & 1,
+            // which held instance jb-1, built before the last barrier
+            if (jb + 1 >= ahead && bb + g < B) issue_inputs(bb + g, (int)((jb + 1) & 1));
+            if (bb < B) prefetch_rows(bb);
+        }
+        bool vn = true;
+        for (int ph = 0; ph < 2; ++ph) {
+            const bool do_rows = dbl ? ((ph ^ (warp & 1)) != 0) : ph == 1;
+            if (do_rows) {
+                if (j >= 0) rows(b, smem + L.tabs + (dbl ? (j & 1) : 0) * L.tabset, ok);
+            } else if (bb < B) {
+                vn = build(bb, jb, smem + L.tabs + (dbl ? (jb & 1) : 0) * L.tabset);
+            }
+            if (!dbl && ph == 0) {
+                ok = __syncthreads_and(vn) != 0;
+                if (!ok && threadIdx.x == 0) flag_data_error(p.st);
+            }
+        }
+        if (dbl) {   // also frees table set j & 1 and input buffer jb & 1
+            ok = __syncthreads_and(vn) != 0;
+            if (bb < B && !ok && threadIdx.x == 0) flag_data_error(p.st);
+        } else {
+            __syncthreads();   // tables and input buffer j & 1 are free again
+        }
     }
 }
 
@@ -387,7 +448,7 @@ F* pick_gm(int nG, F* k8, F* k16, F* k24, F* k32) {
 
 int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, float* out_grid,
                      uint8_t* out_grid_cfg, cudaStream_t s) {
-    if (d.units > 4094) return EKYA_ERR_SHAPE;
+    if (d.units > 4094) return EKYA_ERR_SHAPE;   // rt * kSlots must fit 16 bits
     if ((reinterpret_cast<uintptr_t>(out_grid) & 15) || (reinterpret_cast<uintptr_t>(out_grid_cfg) & 3))
         return EKYA_ERR_ARG;
     EvalParams p{};
@@ -397,15 +458,21 @@ int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, f
     p.out_grid = out_grid;
     p.out_grid_cfg = out_grid_cfg;
     p.warp_bytes = a16(sizeof(StreamIn)) + tab_bytes(d.units);
-    const int warps = kGridWarps;
-    size_t smem = p.warp_bytes * warps + a16(4 * cellinfo_quads(d.units) * sizeof(unsigned));
-    if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
+    // the position table (16 B per 4 cells of a stream) is staged only while it
+    // leaves room for all warps' tables; beyond that each quad locates its row
+    // arithmetically, and large U runs fewer warps per CTA (>= 1)
+    const size_t qsb = a16(4 * cellinfo_quads(d.units) * sizeof(unsigned));
+    p.grid_qs = qsb + p.warp_bytes * kGridWarps <= h->smem_optin;
+    const size_t avail = h->smem_optin - (p.grid_qs ? qsb : 0);
+    const int warps = (int)std::min<size_t>(kGridWarps, avail / p.warp_bytes);
+    if (warps < 1) return EKYA_ERR_SHAPE;
+    const size_t smem = p.warp_bytes * warps + (p.grid_qs ? qsb : 0);
     if (d.n_inst == 0) return EKYA_OK;
     auto kern = pick_gm(d.n_gamma, grid_kernel<8>, grid_kernel<16>, grid_kernel<24>, grid_kernel<32>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
-    int grid = resident_grid(h, (const void*)kern, kGridWarps * 32, smem, (d.n_inst + warps - 1) / warps);
-    kern<<<grid, kGridWarps * 32, smem, s>>>(p);
+    int grid = resident_grid(h, (const void*)kern, warps * 32, smem, (d.n_inst + warps - 1) / warps);
+    kern<<<grid, warps * 32, smem, s>>>(p);
     h->launches++;
     return cuda_status(cudaGetLastError());
 }
@@ -423,9 +490,11 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     p.out_mean = out_mean;
     p.out_cfg = out_cfg;
     if (reinterpret_cast<uintptr_t>(alloc) & 3) return EKYA_ERR_ARG;
-    p.L = list_layout(d.units, d.n_streams, d.n_gamma, d.n_lambda);
+    p.L = list_layout(d.units, d.n_streams, d.n_gamma, d.n_lambda, 2);
+    if (p.L.total > h->smem_optin) p.L = list_layout(d.units, d.n_streams, d.n_gamma, d.n_lambda, 1);
     p.IL = inst_layout(d.n_streams, d.n_gamma, d.n_lambda);
     p.tb = tab_bytes(d.units);
+    p.rcp_v = 1.0 / (double)d.n_streams;
     size_t smem = p.L.total;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0 || n_alloc == 0) return EKYA_OK;

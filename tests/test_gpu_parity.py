@@ -57,6 +57,12 @@ SCHED_CASES = [
     ("nogamma", variant(synth.CONFIG2, n_inst=16, n_gamma=0)),
     ("u1", variant(synth.CONFIG1, n_inst=32, units=1)),
     ("odd", variant(synth.CONFIG2, n_inst=37, n_streams=7, n_gamma=31, n_lambda=5, units=53, a_min=0.0)),
+    # > 4 instances per CTA: every mbarrier phase of LIST's two input buffers
+    ("c1-many", variant(synth.CONFIG1, n_inst=1200)),
+    # V x (U+1) too large for two LIST table sets in shared memory: the single-set path
+    ("wide", variant(synth.CONFIG2, n_inst=20, n_streams=20, units=120)),
+    # GRID beyond the staged position table (row located arithmetically), fewer warps per CTA
+    ("bigU", variant(synth.CONFIG2, n_inst=6, n_streams=3, units=800)),
 ]
 
 

@@ -14,6 +14,8 @@ which = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 torch.cuda.set_device(0)
 dev = torch.device("cuda", 0)
+if os.environ.get("KBENCH_LIB"):   # A/B a variant build (tools only; the product loads LIB_PATH)
+    ekya.load_library(os.environ["KBENCH_LIB"])
 h = ekya.Handle(0)
 w = bench.Workload(synth.CONFIG4.n_inst, synth.CONFIG4.n_alloc, synth.CONFIG3.n_query)
 if which in ("cluster", "radius"):
@@ -57,4 +59,4 @@ for _ in range(reps):
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 assert h.last_error() == 0
-print(which, os.environ.get("EKYA_CLUSTER_OCC", "-"), "ms", sorted(ts)[len(ts) // 2], "min", min(ts))
+print(which, os.path.basename(os.environ.get("KBENCH_LIB", "libekya.so")), "ms", sorted(ts)[len(ts) // 2], "min", min(ts))
