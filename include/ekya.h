@@ -112,14 +112,16 @@ typedef struct {
  *   allocation vectors alloc[b][n][0..2V) (u16 units, job order C10), the
  *   exact objective out_sum_q32[b][n] = sum_v Q32(value_v) (u64), optionally
  *   out_mean[b][n] = (float)(S / (V 2^32)) and out_cfg[b][n][v].  Requires the
- *   per-instance tables (V*(U+1)*(5*nL+1) bytes) to fit in 200 KB of shared
- *   memory, else EKYA_ERR_SHAPE.
+ *   per-instance tables, V * (65 (U+1) + 16) bytes, plus ~14 KB of staging to fit
+ *   in the device's opt-in shared memory per block (227 KB on B200: V (U+1) <~
+ *   3300), else EKYA_ERR_SHAPE.
  * mode EKYA_EVAL_GRID: for each (b, v) and every split with r_train + r_infer
  *   <= U, out_grid[b][v][c] = value of stream v alone (f32) and
  *   out_grid_cfg[b][v][c] = its argmax config byte, cell c = rowstart(rt) + ri,
  *   rowstart(rt) = rt*(U+1) - rt*(rt-1)/2, i.e. (U+1)(U+2)/2 cells per stream
  *   (north star "for every v, gamma, lambda and (r_train, r_infer) ... per-stream
- *   argmax").  U <= 4094 in GRID mode.
+ *   argmax").  GRID needs one stream's tables, 65 (U+1) + ~450 bytes, in shared
+ *   memory (U <~ 3400 on B200), else EKYA_ERR_SHAPE.
  * Outputs not used by the mode may be NULL; out_mean/out_cfg/out_grid_cfg are
  * optional.
  * ------------------------------------------------------------------------- */

@@ -9,12 +9,16 @@
 // each warp store is a contiguous 128-byte (f32) / 32-byte (u8) run.  Bound by
 // the 5 B/cell output stream to HBM.
 //
-// LIST: one persistent CTA per SM walks its instances; for each instance the 8
-// warps build the V stream tables in parallel, and the instance's allocation
-// rows stream through a two-stage shared-memory pipeline fed by TMA bulk copies
-// (cp.async.bulk + mbarrier), one thread per row: V table lookups, exact Q32
-// sum, mean and config bytes (staged in shared memory and written with 16-byte
-// vector stores).
+// LIST: one persistent 32-warp CTA per SM walks its instances.  Instance
+// inputs arrive by TMA bulk copy (cp.async.bulk + mbarrier) two instances
+// ahead and each instance's allocation rows are bulk-prefetched into L2 one
+// instance ahead.  With two table sets in shared memory, step j builds instance
+// j+1's V stream tables -- (stream, 32-row block) warp tasks, entries = exact
+// Q32 value | config byte -- while instance j's rows are evaluated in 32-row
+// chunks, both pulled from one shared task counter (interleaved 1:1).  A row
+// is one thread: 8-byte pair loads, one SIMD min clamps both halves (any clamp
+// marks the row bad), V table lookups, an add-with-carry exact sum, the mean
+// by a correctly rounded reciprocal, 2-byte config stores.
 #include <algorithm>
 
 #include "launch.h"
@@ -90,7 +94,7 @@ __host__ __device__ inline ListLayout list_layout(int U, int V, int nG, int nL, 
     L.tabs = o;   o += L.tabset * ntabs;
     L.inst_bytes = inst_layout(V, nG, nL).total;
     L.inst = o;   o += 2 * L.inst_bytes;
-    L.bars = o;   o += 16;
+    L.bars = o;   o += 32;   // 2 mbarriers + 2 task counters
     L.total = o;
     return L;
 }
@@ -231,17 +235,32 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
 // ------------------------------------------------------------------------
 // LIST
 // ------------------------------------------------------------------------
+// Sum of V LIST entries (Q32 | cfg << 56): low words by an add-with-carry chain
+// into the high words; bits 0..23 of the high accumulator hold the Q32 bit-32
+// count plus carries (< 2V), the config bytes land in bits 24..31 and are dropped.
+struct Q32Sum {
+    unsigned lo = 0, hi = 0;
+    __device__ __forceinline__ void add(uint2 e) {
+        asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(lo), "+r"(hi) : "r"(e.x), "r"(e.y));
+    }
+    __device__ __forceinline__ unsigned long long value() const {
+        return ((unsigned long long)(hi & 0xFFFFFFu) << 32) | lo;
+    }
+};
+
 template <int GM>
 __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const ekya_dims& d = p.d;
     const int U = d.units, nG = d.n_gamma, nL = d.n_lambda, V = d.n_streams, J = 2 * V;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kListThreads / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const ListLayout& L = p.L;
     const InstLayout& IL = p.IL;
-    const size_t tb = p.tb;
+    const int tb = (int)p.tb;
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bars);
-    const long long N = p.n_alloc, B = d.n_inst, g = gridDim.x;
+    int* ctr = reinterpret_cast<int*>(smem + L.bars + 16);   // task counters, one per phase parity
+    const int N = p.n_alloc;
+    const long long B = d.n_inst, g = gridDim.x;
 
     // leader thread: TMA the inputs of instance b into input buffer k
     auto issue_inputs = [&](long long b, int k) {
@@ -265,135 +284,173 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
         for (unsigned o = 0; o < gr.bytes; o += (1u << 20)) bulk_prefetch_l2(gr.g0 + o, min(gr.bytes - o, 1u << 20));
     };
 
-    // Validate (R-ERR) and build the V stream tables of instance b (the j-th
-    // instance of this CTA, inputs in buffer j & 1) into table set `tabs`:
-    // warp tasks = (stream, block of 32 r_train rows).  Returns this thread's
-    // share of the validity test; the tables are built regardless (an invalid
-    // instance's rows are zeroed, so its tables are never read).
-    auto build = [&](long long b, long long j, unsigned char* tabs) -> bool {
-        const int k = (int)(j & 1);
-        mbar_wait(&bar[k], (unsigned)((j >> 1) & 1));
-        unsigned char* ib = smem + L.inst + k * L.inst_bytes;
-        const float* stale = reinterpret_cast<const float*>(ib + IL.stale + granules(p.t.stale + b * V, 4).off);
-        const float* cost = reinterpret_cast<const float*>(ib + IL.cost + granules(p.t.cost + b * V * nG, 4).off);
-        const float* post = reinterpret_cast<const float*>(ib + IL.post + granules(p.t.post + b * V * nG, 4).off);
-        const uint16_t* lmu =
-            reinterpret_cast<const uint16_t*>(ib + IL.lmu + granules(p.t.lam_min_units + b * V * nL, 2).off);
-        const float* lf = reinterpret_cast<const float*>(ib + IL.lf + granules(p.t.lam_factor + b * V * nL, 4).off);
+    // Staged inputs of instance b (the j-th of this CTA: buffer j & 1).
+    struct Staged {
+        const float *stale, *cost, *post, *lf;
+        const uint16_t* lmu;
+    };
+    auto staged = [&](long long b, long long j) {
+        unsigned char* ib = smem + L.inst + (j & 1) * L.inst_bytes;
+        Staged S;
+        S.stale = reinterpret_cast<const float*>(ib + IL.stale + granules(p.t.stale + b * V, 4).off);
+        S.cost = reinterpret_cast<const float*>(ib + IL.cost + granules(p.t.cost + b * V * nG, 4).off);
+        S.post = reinterpret_cast<const float*>(ib + IL.post + granules(p.t.post + b * V * nG, 4).off);
+        S.lmu = reinterpret_cast<const uint16_t*>(ib + IL.lmu + granules(p.t.lam_min_units + b * V * nL, 2).off);
+        S.lf = reinterpret_cast<const float*>(ib + IL.lf + granules(p.t.lam_factor + b * V * nL, 4).off);
+        return S;
+    };
+    // Wait for instance b's inputs and test them (R-ERR): this thread's share.
+    auto validate = [&](long long b, long long j) -> bool {
+        mbar_wait(&bar[j & 1], (unsigned)((j >> 1) & 1));
+        const Staged S = staged(b, j);
         bool vok = true;
-        for (int t = threadIdx.x; t < V; t += blockDim.x) vok &= in01(stale[t]);
+        for (int t = threadIdx.x; t < V; t += blockDim.x) vok &= in01(S.stale[t]);
         for (int t = threadIdx.x; t < V * nG; t += blockDim.x) {
-            const float c = cost[t];
+            const float c = S.cost[t];
             if (!(c >= 0.0f)) vok = false;
-            else if (!isinf(c)) vok &= in01(post[t]);
+            else if (!isinf(c)) vok &= in01(S.post[t]);
         }
         for (int t = threadIdx.x; t < V * nL; t += blockDim.x)
-            if (lmu[t] != kLmuPad) vok &= in01(lf[t]);
-        const int nblk = (U + 32) / 32;
-        StreamIn* si = reinterpret_cast<StreamIn*>(smem + L.sin + (size_t)warp * a16(sizeof(StreamIn)));
-        for (int task = warp; task < V * nblk; task += nw) {
-            const int v = task / nblk, blk = task - v * nblk;
-            if (lane < nG) {
-                si->cost[lane] = cost[v * nG + lane];
-                si->post[lane] = post[v * nG + lane];
-                si->diff[lane] = fsub(post[v * nG + lane], stale[v]);
-            }
-            if (lane < nL) {
-                si->lf[lane] = lf[v * nL + lane];
-                si->lmu[lane] = lmu[v * nL + lane];
-            }
-            const bool f = lane >= nG || fast_dividend(cost[v * nG + lane]);
-            const unsigned all = __ballot_sync(0xffffffffu, f);
-            if (lane == 0) {
-                si->stale = stale[v];
-                si->fast = all == 0xffffffffu;
-            }
-            __syncwarp();
-            unsigned char* tv = tabs + v * tb;
-            const int r1 = min(U + 1, blk * 32 + 32);
-            // entries = exact Q32(value) | config << 40: LIST sums the exact values
-            warp_build_tables<GM>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
-                                  reinterpret_cast<unsigned long long*>(tv + a16((size_t)(U + 1))), blk * 32, r1,
-                                  blk == 0);
-        }
+            if (S.lmu[t] != kLmuPad) vok &= in01(S.lf[t]);
         return vok;
+    };
+    // Build task `task` = (stream v, block of 32 r_train rows) of instance b into
+    // table set `tabs` (built regardless of validity: an invalid instance's rows
+    // are zeroed, so its tables are never read).
+    const int nblk = (U + 32) / 32;
+    StreamIn* si = reinterpret_cast<StreamIn*>(smem + L.sin + (size_t)warp * a16(sizeof(StreamIn)));
+    auto build_task = [&](long long b, long long j, unsigned char* tabs, int task) {
+        const Staged S = staged(b, j);
+        const int v = task / nblk, blk = task - v * nblk;
+        if (lane < nG) {
+            si->cost[lane] = S.cost[v * nG + lane];
+            si->post[lane] = S.post[v * nG + lane];
+            si->diff[lane] = fsub(S.post[v * nG + lane], S.stale[v]);
+        }
+        if (lane < nL) {
+            si->lf[lane] = S.lf[v * nL + lane];
+            si->lmu[lane] = S.lmu[v * nL + lane];
+        }
+        const bool f = lane >= nG || fast_dividend(S.cost[v * nG + lane]);
+        const unsigned all = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) {
+            si->stale = S.stale[v];
+            si->fast = all == 0xffffffffu;
+        }
+        __syncwarp();
+        unsigned char* tv = tabs + v * tb;
+        const int r1 = min(U + 1, blk * 32 + 32);
+        warp_build_tables<GM>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
+                              reinterpret_cast<unsigned long long*>(tv + a16((size_t)(U + 1))), blk * 32, r1,
+                              blk == 0);
     };
 
     const unsigned UU = (unsigned)U | ((unsigned)U << 16);
     const bool pairs = (V % 2 == 0) && (reinterpret_cast<uintptr_t>(p.alloc) % 8 == 0) &&
                        (!p.out_cfg || reinterpret_cast<uintptr_t>(p.out_cfg) % 2 == 0);
-    const size_t off_tvc = a16((size_t)(U + 1));
-    const double rcp_v = p.rcp_v, dv = (double)V;
+    const int off_tvc = (int)a16((size_t)(U + 1));
+    // Row chunk c of instance b: rows 32c + lane, one thread per allocation row,
+    // read straight from global (L2).
+    auto row_chunk = [&](long long b, const unsigned char* tabs, bool ok, int c) {
+        const int r = c * 32 + lane;
+        if (r >= N) return;
+        const long long o = b * N + r;
+        unsigned dev = 0;   // any bit set: some r_train / r_infer > U (clamped)
+        int tot = 0;
+        Q32Sum S;
+        const unsigned char* tp = tabs;
+        auto look = [&](unsigned pr, const unsigned char* t) -> uint2 {
+            const unsigned pc = __vminu2(pr, UU);   // clamp both halves to U
+            dev |= pr ^ pc;
+            const int ri = (int)(pc & 0xFFFFu), rt = (int)(pc >> 16);
+            tot += ri + rt;
+            return reinterpret_cast<const uint2*>(t + off_tvc)[rt * kSlots + t[ri]];
+        };
+        if (pairs) {   // two streams per 8-byte row load and per 2-byte config store
+            const uint2* row2 = reinterpret_cast<const uint2*>(p.alloc) + o * (V / 2);
+            uint16_t* cr2 = p.out_cfg ? reinterpret_cast<uint16_t*>(p.out_cfg) + o * (V / 2) : nullptr;
+            for (int v2 = 0; v2 < V / 2; ++v2, tp += 2 * tb) {
+                const uint2 pr = __ldg(row2 + v2);
+                const uint2 e0 = look(pr.x, tp), e1 = look(pr.y, tp + tb);
+                S.add(e0);
+                S.add(e1);
+                if (cr2) cr2[v2] = (uint16_t)__byte_perm(e0.y, e1.y, 0x0073);
+            }
+        } else {
+            const unsigned* row = reinterpret_cast<const unsigned*>(p.alloc) + o * V;
+            uint8_t* cr = p.out_cfg ? p.out_cfg + o * V : nullptr;
+            for (int v = 0; v < V; ++v, tp += tb) {
+                const uint2 e = look(__ldg(row + v), tp);
+                S.add(e);
+                if (cr) cr[v] = (uint8_t)(e.y >> 24);
+            }
+        }
+        const bool rok = ok && dev == 0 && tot <= U;   // Eq. 1 constraint 2
+        unsigned long long s = S.value();
+        if (!rok) {                                     // R-ERR: zero the row
+            s = 0;
+            if (p.out_cfg)
+                for (int v = 0; v < V; ++v) p.out_cfg[o * V + v] = 0;
+            if (ok) flag_data_error(p.st);
+        }
+        p.out_sum[o] = s;
+        if (p.out_mean) {
+            // mean = (float)((double)s / (V 2^32)): s / V by the correctly rounded
+            // reciprocal rcp_v = RN(1/V) and one exact-residual correction (Markstein:
+            // RN(q0 + r rcp_v) = RN(s / V) for q0 within 1 ulp; s < 2^53, no
+            // over/underflow), then the exact power-of-two scale
+            const double a = __ull2double_rn(s);
+            const double q0 = __dmul_rn(a, p.rcp_v);
+            const double q = __fma_rn(__fma_rn(-(double)V, q0, a), p.rcp_v, q0);
+            p.out_mean[o] = rok ? __double2float_rn(__dmul_rn(q, 2.3283064365386963e-10)) : 0.0f;
+        }
+    };
 
-    // One thread per allocation row of instance b, read straight from global (L2).
-    auto rows = [&](long long b, const unsigned char* tabs, bool ok) {
-        for (long long r = threadIdx.x; r < N; r += kListThreads) {
-            const long long o = b * N + r;
-            const uint16_t* rowp = p.alloc + o * J;
-            bool bad = false;
-            int tot = 0;
-            unsigned long long S = 0;
-            const unsigned char* tp = tabs;
-            auto look = [&](unsigned pr, const unsigned char* t) -> unsigned long long {
-                const unsigned pc = __vminu2(pr, UU);   // clamp both halves to U; any clamp = bad row
-                bad |= pr != pc;
-                const int ri = (int)(pc & 0xFFFFu), rt = (int)(pc >> 16);
-                tot += ri + rt;
-                return reinterpret_cast<const unsigned long long*>(t + off_tvc)[rt * kSlots + t[ri]];
-            };
-            if (pairs) {   // two streams per 8-byte row load and per 2-byte config store
-                const uint2* row2 = reinterpret_cast<const uint2*>(rowp);
-                uint16_t* cr2 = p.out_cfg ? reinterpret_cast<uint16_t*>(p.out_cfg + o * V) : nullptr;
-                for (int v2 = 0; v2 < V / 2; ++v2, tp += 2 * tb) {
-                    const uint2 pr = __ldg(row2 + v2);
-                    const unsigned long long e0 = look(pr.x, tp), e1 = look(pr.y, tp + tb);
-                    S += (e0 & 0xFFFFFFFFFFull) + (e1 & 0xFFFFFFFFFFull);
-                    if (cr2) cr2[v2] = (uint16_t)((unsigned)(e0 >> 40) | ((unsigned)(e1 >> 40) << 8));
-                }
+    // Dynamic task queue of one phase: n_build build tasks of instance bb (into
+    // table set tb_build) and n_rows row chunks of instance b, interleaved 1:1
+    // while both last so that the issue-bound builds and the memory-bound row
+    // chunks share the SM; warps pull tasks from a shared counter.
+    int phase = 0;
+    auto run_phase = [&](long long bb, long long jb, unsigned char* tabs_build, int n_build, long long b,
+                         const unsigned char* tabs_rows, bool ok, int n_rows) {
+        int* c = ctr + (phase & 1);
+        if (threadIdx.x == 0) ctr[(phase + 1) & 1] = 0;   // used by the previous phase (ended by a barrier)
+        ++phase;
+        const int m = min(n_build, n_rows), total = n_build + n_rows;
+        for (;;) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(c, 1);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= total) break;
+            bool is_build;
+            int idx;
+            if (t < 2 * m) {
+                is_build = (t & 1) == 0;
+                idx = t >> 1;
             } else {
-                const unsigned* row = reinterpret_cast<const unsigned*>(rowp);
-                uint8_t* cr = p.out_cfg ? p.out_cfg + o * V : nullptr;
-                for (int v = 0; v < V; ++v, tp += tb) {
-                    const unsigned long long e = look(__ldg(row + v), tp);
-                    S += e & 0xFFFFFFFFFFull;
-                    if (cr) cr[v] = (uint8_t)(e >> 40);
-                }
+                is_build = n_build > n_rows;
+                idx = t - m;
             }
-            const bool rok = ok && !bad && tot <= U;   // Eq. 1 constraint 2
-            if (!rok) {                                 // R-ERR: zero the row
-                S = 0;
-                if (p.out_cfg)
-                    for (int v = 0; v < V; ++v) p.out_cfg[o * V + v] = 0;
-                if (ok) flag_data_error(p.st);
-            }
-            p.out_sum[o] = S;
-            if (p.out_mean) {
-                // mean = (float)((double)S / (V 2^32)): S / V by the correctly rounded
-                // reciprocal rcp_v = RN(1/V) and one exact-residual correction (Markstein:
-                // RN(q0 + r rcp_v) = RN(S / V) for q0 within 1 ulp; S < 2^53, no
-                // over/underflow), then the exact power-of-two scale
-                const double a = __ull2double_rn(S);
-                const double q0 = __dmul_rn(a, rcp_v);
-                const double q = __fma_rn(__fma_rn(-dv, q0, a), rcp_v, q0);
-                p.out_mean[o] = rok ? __double2float_rn(__dmul_rn(q, 2.3283064365386963e-10)) : 0.0f;
-            }
+            if (is_build) build_task(bb, jb, tabs_build, idx);
+            else row_chunk(b, tabs_rows, ok, idx);
         }
     };
 
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        ctr[0] = 0;
+        ctr[1] = 0;
         fence_barrier_init();
     }
     __syncthreads();
     const long long b0 = blockIdx.x;
     if (b0 >= B) return;
-    // Double-buffered table sets (ntabs == 2): while the rows of this CTA's
-    // instance j stream, the tables of instance j+1 are built -- odd warps build
-    // first and even warps stream first, so the issue-bound build overlaps the
-    // memory-bound rows inside the SM; inputs are staged two instances ahead.
-    // Single set (large V x U): build j, barrier, rows j.  Step j = -1 (double
-    // buffering only) builds instance 0.  One call site each for build and rows.
+    const int n_build = V * nblk, n_chunks = (N + 31) / 32;
+    // Double-buffered table sets (ntabs == 2): the phase of step j builds
+    // instance j+1's tables while instance j's rows stream; inputs are staged two
+    // instances ahead.  Single set (large V x U): build j | barrier | rows j.
+    // Step j = -1 (double buffering only) builds instance 0.
     const bool dbl = L.ntabs == 2;
     const int ahead = dbl ? 2 : 1;
     if (threadIdx.x == 0)
@@ -408,23 +465,19 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
             if (jb + 1 >= ahead && bb + g < B) issue_inputs(bb + g, (int)((jb + 1) & 1));
             if (bb < B) prefetch_rows(bb);
         }
-        bool vn = true;
-        for (int ph = 0; ph < 2; ++ph) {
-            const bool do_rows = dbl ? ((ph ^ (warp & 1)) != 0) : ph == 1;
-            if (do_rows) {
-                if (j >= 0) rows(b, smem + L.tabs + (dbl ? (j & 1) : 0) * L.tabset, ok);
-            } else if (bb < B) {
-                vn = build(bb, jb, smem + L.tabs + (dbl ? (jb & 1) : 0) * L.tabset);
-            }
-            if (!dbl && ph == 0) {
-                ok = __syncthreads_and(vn) != 0;
-                if (!ok && threadIdx.x == 0) flag_data_error(p.st);
-            }
-        }
-        if (dbl) {   // also frees table set j & 1 and input buffer jb & 1
-            ok = __syncthreads_and(vn) != 0;
-            if (bb < B && !ok && threadIdx.x == 0) flag_data_error(p.st);
+        const bool has_next = bb < B;
+        const bool vn = has_next ? validate(bb, jb) : true;
+        unsigned char* tabs_b = smem + L.tabs + (dbl ? (jb & 1) : 0) * L.tabset;
+        const unsigned char* tabs_r = smem + L.tabs + (dbl ? (j & 1) : 0) * L.tabset;
+        if (dbl) {
+            run_phase(bb, jb, tabs_b, has_next ? n_build : 0, b, tabs_r, ok, j >= 0 ? n_chunks : 0);
+            ok = __syncthreads_and(vn) != 0;   // also frees table set j & 1 and input buffer jb & 1
+            if (has_next && !ok && threadIdx.x == 0) flag_data_error(p.st);
         } else {
+            run_phase(bb, jb, tabs_b, n_build, b, tabs_r, true, 0);
+            ok = __syncthreads_and(vn) != 0;
+            if (!ok && threadIdx.x == 0) flag_data_error(p.st);
+            run_phase(bb, jb, tabs_b, 0, b, tabs_r, ok, n_chunks);
             __syncthreads();   // tables and input buffer j & 1 are free again
         }
     }
