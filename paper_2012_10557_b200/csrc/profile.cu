@@ -23,6 +23,7 @@
 // associative.
 #include <algorithm>
 #include <cfloat>
+#include <cstring>
 
 #include "launch.h"
 
@@ -583,6 +584,417 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
     }
 }
 
+// ------------------------------------------------------------------------
+// CLUSTER, several queries per SM (the shape of BASELINE config 3)
+// ------------------------------------------------------------------------
+// Lloyd's algorithm is a chain of short block-wide phases per pass (distances,
+// moves, barrier, centroid update, barrier); with one query per SM the SM idles
+// in every serial phase.  Here a 256-thread CTA owns one query at a time and
+// kC2Ctas CTAs share each SM, so one query's serial phases overlap the others'
+// distance work.  Each thread owns two windows (h = t and t + 256); their
+// squared distances are computed together as packed f32x2 pairs (one FADD2 /
+// FMUL2 / FFMA2 per class and centroid for both windows), reading the
+// histograms from the staged tile (row stride C words: conflict-free for odd C)
+// and each centroid as a float4 broadcast.  The per-thread distance registers
+// double as a cache: only centroids whose coordinates changed bitwise are
+// recomputed.  The history tile is single-buffered: the next query's TMA is
+// issued as soon as this query's Lloyd passes are done, overlapping the
+// accuracy reduction, which reads the accuracy tile from L2 (bulk-prefetched
+// when the query was issued).
+constexpr int kC2Threads = 256;
+constexpr int kC2Ctas = 4;
+constexpr int kC2Kmax = 8;
+
+using u64 = unsigned long long;
+
+// packed binary32 pairs (lo = window t, hi = window t + 256); each op is one
+// IEEE rounding per half, round-to-nearest-even, subnormals kept
+__device__ __forceinline__ u64 pk2(float a, float b) {
+    u64 d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float lo2(u64 x) { return __uint_as_float((unsigned)x); }
+__device__ __forceinline__ float hi2(u64 x) { return __uint_as_float((unsigned)(x >> 32)); }
+// s + fl(fl(x - m)^2) for both halves.  The accumulate is written as
+// fma(sq, one, s) with `one` = (1.0f, 1.0f) known only at run time: sq * 1 is
+// exact, so this is fl(s + sq); a plain add.rn.f32x2 after mul.rn.f32x2 is
+// contracted into one FFMA2 by ptxas 12.9 even under --fmad=false, which would
+// skip the rounding of the square (rule 5).
+__device__ __forceinline__ u64 d2acc(u64 s, u64 x, float m, u64 one) {
+    u64 d, q, r;
+    const u64 mm = pk2(m, m);
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(mm));
+    asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(q) : "l"(d));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(q), "l"(one), "l"(s));
+    return r;
+}
+
+// One Lloyd pass's distances for a thread's two windows (packed): s[k] is
+// recomputed for every centroid k in `chg` (ALL: every centroid), the others
+// keep their cached values.  Classes in chunks of 4; the padded classes of the
+// last chunk read x = 0 against the zero-padded centroid, adding fl(0 - 0)^2 = +0.
+template <int KT, int KS, bool ALL>
+__device__ __forceinline__ void c2_dists(u64 (&s)[KS], const float* x0, const float* x1, const float* mu, int C,
+                                         int CP, int K, unsigned chg, u64 one) {
+#pragma unroll
+    for (int k = 0; k < KS; ++k)
+        if ((KT > 0 || k < K) && (ALL || ((chg >> k) & 1u))) s[k] = 0ULL;
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+        const int cb = c4 * 4;
+        if (cb >= C) break;
+        u64 xp[4];
+        if (cb + 4 <= C) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) xp[j] = pk2(x0[cb + j], x1[cb + j]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const bool in = cb + j < C;
+                xp[j] = pk2(in ? x0[cb + j] : 0.0f, in ? x1[cb + j] : 0.0f);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+            if ((KT > 0 || k < K) && (ALL || ((chg >> k) & 1u))) {
+                const float4 m = *reinterpret_cast<const float4*>(mu + k * CP + cb);
+                s[k] = d2acc(s[k], xp[0], m.x, one);
+                s[k] = d2acc(s[k], xp[1], m.y, one);
+                s[k] = d2acc(s[k], xp[2], m.z, one);
+                s[k] = d2acc(s[k], xp[3], m.w, one);
+            }
+        }
+    }
+}
+
+// Exact Q32 sums as two 32-bit shared counters: v = hi * 2^16 + lo with
+// lo < 2^16 and hi <= 2^16, so each half of a sum over <= 65,535 windows fits 32
+// bits; adds and subtracts are native 32-bit shared atomics (the 64-bit shared
+// atomic is a CAS loop on sm_100a) and wrap-around arithmetic gives the exact
+// non-negative result.
+__device__ __forceinline__ void sum16_add(unsigned* lo, unsigned* hi, u64 v) {
+    atomicAdd(lo, (unsigned)(v & 0xFFFFu));
+    atomicAdd(hi, (unsigned)(v >> 16));
+}
+__device__ __forceinline__ void sum16_sub(unsigned* lo, unsigned* hi, u64 v) {
+    atomicSub(lo, (unsigned)(v & 0xFFFFu));
+    atomicSub(hi, (unsigned)(v >> 16));
+}
+// red.shared.add.u32 at a shared-window address
+__device__ __forceinline__ void red_add_shared(unsigned addr, unsigned v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ u64 sum16_get(const unsigned* lo, const unsigned* hi) {
+    return ((u64)*hi << 16) + *lo;
+}
+
+struct C2Layout {
+    size_t bar, misc, cf, hist, mu, sums, cnt, dummy, total, cf_slot;
+};
+__host__ __device__ inline C2Layout c2_layout(int H, int C, int G, int K) {
+    C2Layout L;
+    const int CP = (C + 3) & ~3;
+    size_t o = 0;
+    L.bar = o;    o += 16;
+    L.misc = o;   o += 48;
+    L.cf_slot = al16((size_t)C * 4) + 16 + al16((size_t)G * 4) + 16;   // [cur][fallback] granule-staged
+    L.cf = o;     o += 2 * L.cf_slot;
+    L.hist = o;   o += al16((size_t)H * C * 4) + 16;
+    L.mu = o;     o += al16((size_t)K * CP * 4);
+    // Lloyd: cluster sums lo[K][C], hi[K][C] (u32); afterwards the same space holds
+    // the similar-window list (u16[H]) and the per-gamma sums lo[G], hi[G], n[G]
+    const size_t lloyd = (size_t)K * C * 8, gam = al16((size_t)H * 2) + (size_t)G * 12;
+    L.sums = o;   o += al16(lloyd > gam ? lloyd : gam);
+    L.cnt = o;    o += al16((size_t)K * 4);
+    L.dummy = o;  o += 128;   // sink of the lanes beyond column C
+    L.total = o;
+    return L;
+}
+
+struct C2Params {
+    ProfParams P;
+    C2Layout L;
+    u64 one2;   // (1.0f, 1.0f), opaque to the compiler
+};
+
+// KT > 0: K == KT known at compile time; KT == 0: runtime K <= kC2Kmax.
+// CT > 0: C == CT known at compile time (immediate-offset loads, no class guards).
+template <int KT, int CT>
+__global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __grid_constant__ C2Params A) {
+    constexpr int KS = KT > 0 ? KT : kC2Kmax;   // distance registers per window
+    extern __shared__ __align__(128) unsigned char smem[];
+    const ProfParams& P = A.P;
+    const C2Layout& L = A.L;
+    const int H = P.p.n_hist, G = P.p.n_gamma, K = KT > 0 ? KT : P.p.k;
+    const int C = CT > 0 ? CT : P.p.n_class;
+    const int CP = (C + 3) & ~3;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bar);
+    int* misc = reinterpret_cast<int*>(smem + L.misc);   // [0..1] changed-centroid masks, [2] query cluster,
+                                                         // [3] similar-window count
+    float* mu = reinterpret_cast<float*>(smem + L.mu);
+    unsigned* slo = reinterpret_cast<unsigned*>(smem + L.sums);
+    unsigned* shi = slo + K * C;
+    int* cnt = reinterpret_cast<int*>(smem + L.cnt);
+    uint16_t* list = reinterpret_cast<uint16_t*>(smem + L.sums);
+    unsigned* glo = reinterpret_cast<unsigned*>(smem + L.sums + al16((size_t)H * 2));
+    unsigned* ghi = glo + G;
+    int* gnn = reinterpret_cast<int*>(ghi + G);
+    const long long Q = P.p.n_query;
+    const long long items = Q > blockIdx.x ? (Q - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const u64 one = A.one2;
+    // this lane's counter address = cbase + cluster * cstride (+ choff for the high half)
+    const bool lane_c = lane < C;
+    const unsigned cbase = lane_c ? smem_addr(slo) + 4u * (unsigned)lane : smem_addr(smem + L.dummy) + 4u * (unsigned)lane;
+    const unsigned cstride = lane_c ? (unsigned)(C * 4) : 0u, choff = lane_c ? (unsigned)(K * C * 4) : 0u;
+
+    // leader: TMA the history tile (+ cur, fallback into slot j & 1) of this CTA's j-th query and
+    // bulk-prefetch its accuracy tile into L2
+    auto issue = [&](long long j) {
+        const long long q = blockIdx.x + j * gridDim.x;
+        unsigned char* cf = smem + L.cf + (j & 1) * L.cf_slot;
+        const Granules gc = granules(P.cur + q * C, (size_t)C * 4);
+        const Granules gf = granules(P.fallback + q * G, (size_t)G * 4);
+        const Granules gh = granules(P.hist + (size_t)q * H * C, (size_t)H * C * 4);
+        mbar_arrive_expect_tx(bar, gc.bytes + gf.bytes + gh.bytes);
+        bulk_g2s(cf, gc.g0, gc.bytes, bar);
+        bulk_g2s(cf + al16((size_t)C * 4) + 16, gf.g0, gf.bytes, bar);
+        bulk_g2s(smem + L.hist, gh.g0, gh.bytes, bar);
+        const Granules ga = granules(P.acc + (size_t)q * H * G, (size_t)H * G * 4);
+        for (unsigned o = 0; o < ga.bytes; o += (1u << 20)) bulk_prefetch_l2(ga.g0 + o, min(ga.bytes - o, 1u << 20));
+    };
+
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid == 0 && items > 0) issue(0);
+
+    const int h0 = tid, h1 = tid + kC2Threads;
+    const bool v0 = h0 < H, v1 = h1 < H;
+    for (long long i = 0; i < items; ++i) {
+        const long long q = blockIdx.x + i * gridDim.x;
+        const unsigned char* cf = smem + L.cf + (i & 1) * L.cf_slot;
+        const float* cur = reinterpret_cast<const float*>(cf + granules(P.cur + q * C, 4).off);
+        const float* fb = reinterpret_cast<const float*>(cf + al16((size_t)C * 4) + 16 +
+                                                        granules(P.fallback + q * G, 4).off);
+        const float* hs = reinterpret_cast<const float*>(smem + L.hist +
+                                                         granules(P.hist + (size_t)q * H * C, 4).off);
+        const float* x0 = hs + (size_t)(v0 ? h0 : 0) * C;
+        const float* x1 = hs + (size_t)(v1 ? h1 : (v0 ? h0 : 0)) * C;
+        for (int t = tid; t < 2 * K * C; t += kC2Threads) slo[t] = 0u;
+        for (int t = tid; t < K; t += kC2Threads) cnt[t] = 0;
+        if (tid == 0) misc[0] = misc[1] = misc[3] = 0;
+        mbar_wait(bar, (unsigned)(i & 1));
+        bool ok = true;
+        for (int c = tid; c < C; c += kC2Threads) ok &= in01(cur[c]);
+        if (v0)
+            for (int c = 0; c < C; ++c) ok &= in01(x0[c]);
+        if (v1)
+            for (int c = 0; c < C; ++c) ok &= in01(x1[c]);
+        // initial centroids mu_i = h_floor(iH/K) (C19), zero padded to CP columns
+        for (int t = tid; t < K * CP; t += kC2Threads) {
+            const int ci = t / CP, c = t - ci * CP;
+            mu[t] = c < C ? hs[(size_t)(((long long)ci * H) / K) * C + c] : 0.0f;
+        }
+        __syncthreads();
+
+        u64 s[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) s[k] = 0ULL;
+        const unsigned all_k = (1u << K) - 1u;
+        unsigned chg = all_k;
+        int oa0 = -1, oa1 = -1, na0 = 0, na1 = 0;
+        int passes = 0;
+        for (;;) {
+            // distances of both windows to every changed centroid (rule 5 order: class ascending)
+            if (KT > 0 && chg == all_k) c2_dists<KT, KS, true>(s, x0, x1, mu, C, CP, K, chg, one);
+            else c2_dists<KT, KS, false>(s, x0, x1, mu, C, CP, K, chg, one);
+            // nearest centroid, lowest index on ties (C19)
+            {
+                float b0 = lo2(s[0]), b1 = hi2(s[0]);
+                na0 = 0;
+                na1 = 0;
+#pragma unroll
+                for (int k = 1; k < KS; ++k) {
+                    if (KT > 0 || k < K) {
+                        const float d0 = lo2(s[k]), d1 = hi2(s[k]);
+                        if (d0 < b0) { b0 = d0; na0 = k; }
+                        if (d1 < b1) { b1 = d1; na1 = k; }
+                    }
+                }
+            }
+            // exact cluster sums: windows whose cluster changed (pass 0: all, entering from
+            // "none") move between the shared counters; lane c carries column c (C <= 32; lanes
+            // >= C read past their row, inside shared memory, and add into a private dummy word)
+            const unsigned bm0 = __ballot_sync(0xffffffffu, v0 && na0 != oa0);
+            const unsigned bm1 = __ballot_sync(0xffffffffu, v1 && na1 != oa1);
+            if (passes == 0) {
+                for (int k = 0; k < K; ++k) {
+                    const int n = __popc(__ballot_sync(0xffffffffu, v0 && na0 == k)) +
+                                  __popc(__ballot_sync(0xffffffffu, v1 && na1 == k));
+                    if (lane == 0 && n) atomicAdd(&cnt[k], n);
+                }
+#pragma unroll
+                for (int sl = 0; sl < 2; ++sl) {
+                    // the valid windows of a slot are the low lanes: no mask walk
+                    const float* rows = hs + (size_t)(warp * 32 + sl * kC2Threads) * C + lane;
+                    const int nav = sl ? na1 : na0;
+                    const int nh = __popc(sl ? bm1 : bm0);
+#pragma unroll 2
+                    for (int j = 0; j < nh; ++j) {
+                        const int n = __shfl_sync(0xffffffffu, nav, j);
+                        const u64 v = q32(rows[j * C]);
+                        const unsigned a = cbase + (unsigned)n * cstride;
+                        red_add_shared(a, (unsigned)v & 0xFFFFu);
+                        red_add_shared(a + choff, (unsigned)(v >> 16));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int sl = 0; sl < 2; ++sl) {
+                    const float* rows = hs + (size_t)(warp * 32 + sl * kC2Threads) * C + lane;
+                    const int oav = sl ? oa1 : oa0, nav = sl ? na1 : na0;
+                    for (unsigned m = sl ? bm1 : bm0; m; m &= m - 1) {
+                        const int j = __ffs(m) - 1;
+                        const int o = __shfl_sync(0xffffffffu, oav, j);
+                        const int n = __shfl_sync(0xffffffffu, nav, j);
+                        const u64 v = q32(rows[j * C]);
+                        const unsigned lo = (unsigned)v & 0xFFFFu, hi = (unsigned)(v >> 16);
+                        const unsigned ao = cbase + (unsigned)o * cstride, an = cbase + (unsigned)n * cstride;
+                        red_add_shared(ao, 0u - lo);
+                        red_add_shared(ao + choff, 0u - hi);
+                        red_add_shared(an, lo);
+                        red_add_shared(an + choff, hi);
+                        if (lane == 0) {
+                            atomicSub(&cnt[o], 1);
+                            atomicAdd(&cnt[n], 1);
+                        }
+                    }
+                }
+            }
+            oa0 = na0;
+            oa1 = na1;
+            const int any = __syncthreads_or((bm0 | bm1) != 0);
+            const int it = passes++;
+            if ((it > 0 && !any) || it >= P.p.max_iter) break;
+            // centroid update from the exact sums (empty cluster keeps its centroid)
+            for (int t = tid; t < K * C; t += kC2Threads) {
+                const int ci = t / C, c = t - ci * C;
+                const int n = cnt[ci];
+                if (n > 0) {
+                    const float nm = mean_q32(sum16_get(&slo[t], &shi[t]), n);
+                    if (__float_as_uint(nm) != __float_as_uint(mu[ci * CP + c])) {
+                        mu[ci * CP + c] = nm;
+                        atomicOr(reinterpret_cast<unsigned*>(&misc[it & 1]), 1u << ci);
+                    }
+                }
+            }
+            __syncthreads();
+            chg = (unsigned)misc[it & 1];
+            if (tid == 0) misc[(it + 1) & 1] = 0;
+        }
+        // the history tile is free: stream the next query's while this one finishes
+        if (tid == 0) {
+            atomicAdd(&P.st->lloyd_passes, (unsigned long long)passes);
+            if (i + 1 < items) issue(i + 1);
+        }
+        // the query joins its nearest centroid: lane i computes distance to centroid i
+        if (warp == 0) {
+            unsigned long long key = ~0ULL;
+            for (int ci = lane; ci < K; ci += 32) {
+                const float d = dist2_mem(cur, mu + ci * CP, C);
+                const unsigned long long kk = ((unsigned long long)__float_as_uint(d) << 8) | (unsigned)ci;
+                key = kk < key ? kk : key;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+                key = y < key ? y : key;
+            }
+            if (lane == 0) misc[2] = (int)(key & 0xFF);
+        }
+        // validate the whole accuracy tile (NaN = unmeasured, else in [0, 1]; R-ERR)
+        {
+            const float* at = P.acc + (size_t)q * H * G;
+            const long long n = (long long)H * G;
+            if ((reinterpret_cast<uintptr_t>(at) & 15) == 0) {
+                const float4* a4 = reinterpret_cast<const float4*>(at);
+                for (long long t = tid; t < n / 4; t += kC2Threads) {
+                    const float4 x = __ldg(a4 + t);
+                    ok &= !(x.x < 0.0f) && !(x.x > 1.0f) && !(x.y < 0.0f) && !(x.y > 1.0f) &&
+                          !(x.z < 0.0f) && !(x.z > 1.0f) && !(x.w < 0.0f) && !(x.w > 1.0f);
+                }
+                for (long long t = (n & ~3LL) + tid; t < n; t += kC2Threads) {
+                    const float x = __ldg(at + t);
+                    ok &= !(x < 0.0f) && !(x > 1.0f);
+                }
+            } else {
+                for (long long t = tid; t < n; t += kC2Threads) {
+                    const float x = __ldg(at + t);
+                    ok &= !(x < 0.0f) && !(x > 1.0f);
+                }
+            }
+        }
+        __syncthreads();   // misc[2] visible; the cluster sums are dead: their space holds the list
+        const int qc = misc[2];
+        for (int t = tid; t < 3 * G; t += kC2Threads) glo[t] = 0u;
+        // compact list of the query cluster's windows (any order: the sums are exact integers)
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+            const bool in = sl ? (v1 && na1 == qc) : (v0 && na0 == qc);
+            const unsigned bm = __ballot_sync(0xffffffffu, in);
+            int base = 0;
+            if (lane == 0 && bm) base = atomicAdd(&misc[3], __popc(bm));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (in) list[base + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)(sl ? h1 : h0);
+        }
+        __syncthreads();
+        // per-gamma exact sums over the similar, measured windows: thread t owns gamma t % G and
+        // list entries t / G (mod ngrp); the accuracy tile comes from L2
+        {
+            const int ns = misc[3];
+            const int ngrp = kC2Threads / G, g = tid % G, grp = tid / G;
+            if (grp < ngrp) {
+                const float* acc = P.acc + (size_t)q * H * G + g;
+                u64 gs = 0;
+                int gn = 0;
+#pragma unroll 4
+                for (int e = grp; e < ns; e += ngrp) {
+                    const float x = __ldg(acc + (size_t)list[e] * G);
+                    if (x == x) {
+                        gs += q32(x);
+                        gn += 1;
+                    }
+                }
+                if (gn) {
+                    sum16_add(&glo[g], &ghi[g], gs);
+                    atomicAdd(&gnn[g], gn);
+                }
+            }
+        }
+        ok = __syncthreads_and(ok) != 0;
+        if (!ok && tid == 0) flag_data_error(P.st);
+        if (P.out_cluster) {
+            int* oc = P.out_cluster + q * (H + 1);
+            if (v0) oc[h0] = ok ? na0 : 0;
+            if (v1) oc[h1] = ok ? na1 : 0;
+            if (tid == 0) oc[H] = ok ? qc : 0;
+        }
+        for (int g = tid; g < G; g += kC2Threads) {
+            int n = gnn[g];
+            float est = 0.0f;
+            if (!ok) n = 0;
+            else est = n > 0 ? mean_q32(sum16_get(&glo[g], &ghi[g]), n) : fb[g];
+            P.out_est[q * G + g] = est;
+            P.out_n[q * G + g] = n;
+        }
+        __syncthreads();   // sums, list and the cur/fallback slot are free again
+    }
+}
+
 // queries with an empty history: every estimate is the caller's fallback
 __global__ void no_history_kernel(ProfParams P) {
     const long long QG = (long long)P.p.n_query * P.p.n_gamma;
@@ -645,6 +1057,26 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
         radius_kernel<<<(unsigned)grid, kProfThreads, smem, s>>>(P);
     } else {
         if (H >= 65536 || K > 32) return EKYA_ERR_LIMIT;
+        if (H <= 2 * kC2Threads && C <= 32 && K <= kC2Kmax && G <= kC2Threads &&
+            c2_layout(H, C, G, K).total <= budget) {
+            C2Params A{};
+            A.P = P;
+            A.L = c2_layout(H, C, G, K);
+            const float one = 1.0f;
+            unsigned ob;
+            memcpy(&ob, &one, 4);
+            A.one2 = ((unsigned long long)ob << 32) | ob;
+            const size_t smem = A.L.total;
+            auto k2 = (K == 5 && C == 27) ? cluster2_kernel<5, 27> : cluster2_kernel<0, 0>;
+            e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return EKYA_ERR_CUDA;
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2, kC2Threads, smem);
+            grid = std::min<long long>(p.n_query, (long long)h->sm_count * std::max(per_sm, 1));
+            k2<<<(unsigned)grid, kC2Threads, smem, s>>>(A);
+            h->launches++;
+            return cuda_status(cudaGetLastError());
+        }
         const size_t scratch = scratch_layout(H, H, C, K, true).total;
         P.Hc = H;
         const bool reg = (H <= kProfThreads) && (C <= 32);

@@ -243,6 +243,37 @@ def test_profile_bitexact(h, name, pc, mode):
         assert_eq(cl, ocl, "clusters")
 
 
+CLUSTER_EDGE = [
+    # (name, config, k, max_iter): window counts at the 2-windows-per-thread boundaries of the
+    # multi-query CLUSTER kernel, k at its register-cache limits, capped iteration counts
+    ("h256-k8", synth.ProfileConfig("p", 40, 256, 27, 18), 8, 100),
+    ("h257-k1", synth.ProfileConfig("p", 40, 257, 27, 18), 1, 100),
+    ("h512-k5", synth.ProfileConfig("p", 24, 512, 27, 18), 5, 100),
+    ("h513-k5", synth.ProfileConfig("p", 12, 513, 27, 18), 5, 100),
+    ("h500-k5-iter0", synth.ProfileConfig("p", 30, 500, 27, 18), 5, 0),
+    ("h500-k5-iter1", synth.ProfileConfig("p", 30, 500, 27, 18), 5, 1),
+    ("h500-k7-iter3", synth.ProfileConfig("p", 30, 500, 27, 18), 7, 3),
+    ("c32-g1", synth.ProfileConfig("p", 20, 300, 32, 1), 5, 100),
+    ("c1-g40", synth.ProfileConfig("p", 20, 90, 1, 40), 3, 100),
+    ("k9-fallback", synth.ProfileConfig("p", 10, 500, 27, 18), 9, 100),
+    ("h3-k5", synth.ProfileConfig("p", 10, 3, 27, 18), 5, 100),
+]
+
+
+@pytest.mark.parametrize("name,pc,k,it", CLUSTER_EDGE, ids=[c[0] for c in CLUSTER_EDGE])
+def test_cluster_edges_bitexact(h, name, pc, k, it):
+    P = synth.profile_inputs(pc)
+    Pd = {kk: v.cuda() for kk, v in P.items()}
+    est, n, cl = ek().profile_estimate(h, Pd["cur"], Pd["hist"], Pd["hist_acc"], Pd["fallback"], mode=1, k=k,
+                                       max_iter=it, with_cluster=True)
+    oe, on, ocl, bad = oracle.profile(P["cur"].numpy(), P["hist"].numpy(), P["hist_acc"].numpy(),
+                                      P["fallback"].numpy(), mode=1, k=k, max_iter=it)
+    assert bad == 0 and h.last_error() == 0
+    assert_eq(cl, ocl, "clusters")
+    assert_eq(n, on, "n_similar")
+    assert_eq(est, oe, "estimate")
+
+
 def test_profile_invalid_query(h):
     pc = synth.ProfileConfig("p", 5, 50, 27, 18)
     P = synth.profile_inputs(pc)
