@@ -248,11 +248,12 @@ struct Q32Sum {
     }
 };
 
-template <int GM>
+// VT > 0: compile-time stream count (fully unrolled rows); 0: runtime V
+template <int GM, int VT>
 __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const ekya_dims& d = p.d;
-    const int U = d.units, nG = d.n_gamma, nL = d.n_lambda, V = d.n_streams, J = 2 * V;
+    const int U = d.units, nG = d.n_gamma, nL = d.n_lambda, V = VT > 0 ? VT : d.n_streams, J = 2 * V;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const ListLayout& L = p.L;
     const InstLayout& IL = p.IL;
@@ -366,7 +367,45 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
             tot += ri + rt;
             return reinterpret_cast<const uint2*>(t + off_tvc)[rt * kSlots + t[ri]];
         };
-        if (pairs) {   // two streams per 8-byte row load and per 2-byte config store
+        bool fast_ok = false;
+        if constexpr (VT > 0) {
+            // V == VT (even): the whole row in registers, fully unrolled.  One SIMD max over
+            // the row decides whether every entry is <= U; then no clamping is needed and the
+            // unit total is one packed 16x2 sum (each half <= VT U < 2^16, host-checked).
+            if (pairs) {
+                constexpr int V2 = VT / 2;
+                const uint2* row2 = reinterpret_cast<const uint2*>(p.alloc) + o * V2;
+                uint2 pr[V2];
+#pragma unroll
+                for (int v2 = 0; v2 < V2; ++v2) pr[v2] = __ldg(row2 + v2);
+                unsigned mx = 0;
+#pragma unroll
+                for (int v2 = 0; v2 < V2; ++v2) mx = __vmaxu2(mx, __vmaxu2(pr[v2].x, pr[v2].y));
+                if ((mx & 0xFFFFu) <= (unsigned)U && (mx >> 16) <= (unsigned)U) {
+                    unsigned acc = 0;
+                    uint16_t* cr2 = p.out_cfg ? reinterpret_cast<uint16_t*>(p.out_cfg) + o * V2 : nullptr;
+#pragma unroll
+                    for (int v2 = 0; v2 < V2; ++v2) {
+                        uint2 e[2];
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const unsigned w = hh ? pr[v2].y : pr[v2].x;
+                            const unsigned char* t = tabs + (2 * v2 + hh) * tb;
+                            acc += w;
+                            e[hh] = reinterpret_cast<const uint2*>(t + off_tvc)[(w >> 16) * kSlots + t[w & 0xFFFFu]];
+                            S.add(e[hh]);
+                        }
+                        if (cr2) cr2[v2] = (uint16_t)__byte_perm(e[0].y, e[1].y, 0x0073);
+                    }
+                    tot = (int)((acc & 0xFFFFu) + (acc >> 16));
+                    fast_ok = true;
+                }
+            }
+        }
+        if (fast_ok) {
+        } else if (pairs) {   // two streams per 8-byte row load and per 2-byte config store
+            S = Q32Sum();
+            tot = 0;
             const uint2* row2 = reinterpret_cast<const uint2*>(p.alloc) + o * (V / 2);
             uint16_t* cr2 = p.out_cfg ? reinterpret_cast<uint16_t*>(p.out_cfg) + o * (V / 2) : nullptr;
             for (int v2 = 0; v2 < V / 2; ++v2, tp += 2 * tb) {
@@ -377,6 +416,8 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
                 if (cr2) cr2[v2] = (uint16_t)__byte_perm(e0.y, e1.y, 0x0073);
             }
         } else {
+            S = Q32Sum();
+            tot = 0;
             const unsigned* row = reinterpret_cast<const unsigned*>(p.alloc) + o * V;
             uint8_t* cr = p.out_cfg ? p.out_cfg + o * V : nullptr;
             for (int v = 0; v < V; ++v, tp += tb) {
@@ -493,10 +534,11 @@ int resident_grid(ekya_handle* h, const void* fn, int threads, size_t smem, long
 
 }  // namespace
 
+// register slots for {none} + Gamma: the paper's |Gamma| = 18 gets an exact fit
 template <typename F>
-F* pick_gm(int nG, F* k8, F* k16, F* k24, F* k32) {
+F* pick_gm(int nG, F* k8, F* k16, F* k19, F* k24, F* k32) {
     const int g1 = nG + 1;
-    return g1 <= 8 ? k8 : g1 <= 16 ? k16 : g1 <= 24 ? k24 : k32;
+    return g1 <= 8 ? k8 : g1 <= 16 ? k16 : g1 <= 19 ? k19 : g1 <= 24 ? k24 : k32;
 }
 
 int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, float* out_grid,
@@ -521,7 +563,7 @@ int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, f
     if (warps < 1) return EKYA_ERR_SHAPE;
     const size_t smem = p.warp_bytes * warps + (p.grid_qs ? qsb : 0);
     if (d.n_inst == 0) return EKYA_OK;
-    auto kern = pick_gm(d.n_gamma, grid_kernel<8>, grid_kernel<16>, grid_kernel<24>, grid_kernel<32>);
+    auto kern = pick_gm(d.n_gamma, grid_kernel<8>, grid_kernel<16>, grid_kernel<19>, grid_kernel<24>, grid_kernel<32>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
     int grid = resident_grid(h, (const void*)kern, warps * 32, smem, (d.n_inst + warps - 1) / warps);
@@ -551,7 +593,11 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     size_t smem = p.L.total;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0 || n_alloc == 0) return EKYA_OK;
-    auto kern = pick_gm(d.n_gamma, list_kernel<8>, list_kernel<16>, list_kernel<24>, list_kernel<32>);
+    // the paper's shape (V = 10 streams, |Gamma| = 18) gets the unrolled-row kernel
+    auto kern = (d.n_streams == 10 && d.n_gamma + 1 <= 19 && d.n_gamma + 1 > 16 && 10 * d.units < 65536)
+                    ? list_kernel<19, 10>
+                    : pick_gm(d.n_gamma, list_kernel<8, 0>, list_kernel<16, 0>, list_kernel<19, 0>, list_kernel<24, 0>,
+                              list_kernel<32, 0>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
     int grid = resident_grid(h, (const void*)kern, kListThreads, smem, d.n_inst);

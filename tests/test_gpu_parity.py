@@ -136,10 +136,13 @@ def test_list_invalid_rows_and_data_errors(h):
     rows = synth.list_allocs(cfg, 40)
     rows[0, 3, 4] = cfg.units + 1                      # entry > U
     rows[1, 7, 0] = int(rows[1, 7, 0]) + 3             # sum > U
+    rows[2, 11, 19] = 65535                            # largest u16 entry (no out-of-table read)
+    rows[2, 12, 0] = cfg.units                         # one stream takes every unit: valid
+    rows[2, 12, 1:] = 0
     s, mean, c = ek().eval_list(h, Td, rows.cuda(), *args(cfg))
     assert h.last_error() == -6
     os_, om, ocf, bad = oracle.eval_list(inst, rows.numpy())
-    assert bad == 2 + 40
+    assert bad == 3 + 40
     assert_eq(s, os_, "sum_q32")
     assert_eq(mean, om, "mean")
     assert_eq(c, ocf, "cfg")

@@ -17,7 +17,8 @@ dev = torch.device("cuda", 0)
 if os.environ.get("KBENCH_LIB"):   # A/B a variant build (tools only; the product loads LIB_PATH)
     ekya.load_library(os.environ["KBENCH_LIB"])
 h = ekya.Handle(0)
-w = bench.Workload(synth.CONFIG4.n_inst, synth.CONFIG4.n_alloc, synth.CONFIG3.n_query)
+w = bench.Workload(int(os.environ.get("KB_B", synth.CONFIG4.n_inst)), int(os.environ.get("KB_N", synth.CONFIG4.n_alloc)),
+                   synth.CONFIG3.n_query)
 if which in ("cluster", "radius"):
     p = w.pcfg
     P = {}
