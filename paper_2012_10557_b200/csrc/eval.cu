@@ -116,6 +116,7 @@ struct EvalParams {
     InstLayout IL;
     size_t tb;           // LIST: bytes per stream table
     double rcp_v;        // LIST: RN(1 / V), for the exact mean
+    int build_rows;      // LIST: r_train rows per table-build task (multiple of 32)
 };
 
 // ------------------------------------------------------------------------
@@ -131,7 +132,8 @@ __host__ __device__ inline size_t cellinfo_quads(int U) {
     return (size_t)((NC + 3) / 4 + 1);
 }
 
-template <int GM>
+// NGT / NLT > 0: |Gamma| / |Lambda| fixed at compile time (table build without guards)
+template <int GM, int NGT, int NLT>
 __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) {   // <= 64 regs
     extern __shared__ __align__(128) unsigned char smem[];
     const ekya_dims& d = p.d;
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
             const long long item = b * V + v;
             if (ok) {
                 warp_load_stream(sin, p.t, item, nG, nL);
-                warp_build_tables<GM>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc);
+                warp_build_tables<GM, NGT, NLT>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc);
             }
             // Flat write of the stream's cells [f0, f0 + NC) in aligned quads of 4
             // cells: one 16-B value store + one 4-B config store per quad (the
@@ -248,8 +250,8 @@ struct Q32Sum {
     }
 };
 
-// VT > 0: compile-time stream count (fully unrolled rows); 0: runtime V
-template <int GM, int VT>
+// VT > 0: compile-time stream count (fully unrolled rows); 0: runtime V.  NGT / NLT as GRID.
+template <int GM, int VT, int NGT, int NLT>
 __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const ekya_dims& d = p.d;
@@ -318,15 +320,14 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     // Build task `task` = (stream v, block of 32 r_train rows) of instance b into
     // table set `tabs` (built regardless of validity: an invalid instance's rows
     // are zeroed, so its tables are never read).
-    const int nblk = (U + 32) / 32;
+    const int brows = p.build_rows, nblk = (U + brows) / brows;   // r_train rows per build task
     StreamIn* si = reinterpret_cast<StreamIn*>(smem + L.sin + (size_t)warp * a16(sizeof(StreamIn)));
     auto build_task = [&](long long b, long long j, unsigned char* tabs, int task) {
         const Staged S = staged(b, j);
         const int v = task / nblk, blk = task - v * nblk;
         if (lane < nG) {
-            si->cost[lane] = S.cost[v * nG + lane];
-            si->post[lane] = S.post[v * nG + lane];
-            si->diff[lane] = fsub(S.post[v * nG + lane], S.stale[v]);
+            const float post = S.post[v * nG + lane];
+            si->cpd[lane] = make_float4(S.cost[v * nG + lane], post, fsub(post, S.stale[v]), 0.0f);
         }
         if (lane < nL) {
             si->lf[lane] = S.lf[v * nL + lane];
@@ -340,9 +341,9 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
         }
         __syncwarp();
         unsigned char* tv = tabs + v * tb;
-        const int r1 = min(U + 1, blk * 32 + 32);
-        warp_build_tables<GM>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
-                              reinterpret_cast<unsigned long long*>(tv + a16((size_t)(U + 1))), blk * 32, r1,
+        const int r1 = min(U + 1, blk * brows + brows);
+        warp_build_tables<GM, NGT, NLT>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
+                              reinterpret_cast<unsigned long long*>(tv + a16((size_t)(U + 1))), blk * brows, r1,
                               blk == 0);
     };
 
@@ -563,7 +564,11 @@ int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, f
     if (warps < 1) return EKYA_ERR_SHAPE;
     const size_t smem = p.warp_bytes * warps + (p.grid_qs ? qsb : 0);
     if (d.n_inst == 0) return EKYA_OK;
-    auto kern = pick_gm(d.n_gamma, grid_kernel<8>, grid_kernel<16>, grid_kernel<19>, grid_kernel<24>, grid_kernel<32>);
+    // the paper's shape (|Gamma| = 18, |Lambda| = 5) gets a guard-free table build
+    auto kern = (d.n_gamma == 18 && d.n_lambda == 5)
+                    ? grid_kernel<19, 18, 0>
+                    : pick_gm(d.n_gamma, grid_kernel<8, 0, 0>, grid_kernel<16, 0, 0>, grid_kernel<19, 0, 0>,
+                              grid_kernel<24, 0, 0>, grid_kernel<32, 0, 0>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
     int grid = resident_grid(h, (const void*)kern, warps * 32, smem, (d.n_inst + warps - 1) / warps);
@@ -590,14 +595,18 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     p.IL = inst_layout(d.n_streams, d.n_gamma, d.n_lambda);
     p.tb = tab_bytes(d.units);
     p.rcp_v = 1.0 / (double)d.n_streams;
+    // Many rows per instance: one build task per stream (staging and the lambda ladder done
+    // once, all r_train rows in one warp) -- the row chunks keep every warp busy meanwhile.
+    // Few rows: 32-row build tasks, so that the build itself spreads over the CTA's warps.
+    p.build_rows = n_alloc >= 1024 ? ((d.units + 32) / 32) * 32 : 32;
     size_t smem = p.L.total;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0 || n_alloc == 0) return EKYA_OK;
-    // the paper's shape (V = 10 streams, |Gamma| = 18) gets the unrolled-row kernel
-    auto kern = (d.n_streams == 10 && d.n_gamma + 1 <= 19 && d.n_gamma + 1 > 16 && 10 * d.units < 65536)
-                    ? list_kernel<19, 10>
-                    : pick_gm(d.n_gamma, list_kernel<8, 0>, list_kernel<16, 0>, list_kernel<19, 0>, list_kernel<24, 0>,
-                              list_kernel<32, 0>);
+    // the paper's shape (V = 10 streams, |Gamma| = 18, |Lambda| = 5) gets the unrolled-row kernel
+    auto kern = (d.n_streams == 10 && d.n_gamma == 18 && d.n_lambda == 5 && 10 * d.units < 65536)
+                    ? list_kernel<19, 10, 18, 0>
+                    : pick_gm(d.n_gamma, list_kernel<8, 0, 0, 0>, list_kernel<16, 0, 0, 0>, list_kernel<19, 0, 0, 0>,
+                              list_kernel<24, 0, 0, 0>, list_kernel<32, 0, 0, 0>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
     int grid = resident_grid(h, (const void*)kern, kListThreads, smem, d.n_inst);
