@@ -190,6 +190,7 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.first = threading.Event()
 
     def __enter__(self):
         try:
@@ -205,6 +206,13 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+            self.first.set()
+
+    def wait_first(self, timeout=10.0):
+        """Block until the sampler has produced its first line (nvidia-smi can take
+        over a second to start), so the timed region is covered from its start."""
+        if self.proc:
+            self.first.wait(timeout)
 
     def __exit__(self, *a):
         if self.proc:
@@ -346,7 +354,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     c0 = h.counters()
     with ClockSampler(local_rank) as clk:
-        time.sleep(0.3)            # let the sampler start before the timed region
+        clk.wait_first()           # the sampler is running before the timed region starts
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()

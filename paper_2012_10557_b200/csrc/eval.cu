@@ -124,9 +124,11 @@ struct EvalParams {
 // ------------------------------------------------------------------------
 // Cell-position table, shared by every stream (the triangle depends only on U):
 // for each of the 4 alignments phi of a stream's first cell within a 16-byte
-// quad, quad k of the stream starts at local cell c = 4k - phi and
-// qs[phi][k] = (rt << 16) | ri of max(c, 0); the quad's other cells follow by
-// stepping along the row (and wrapping to the next row).
+// quad, quad k of the stream covers local cells c = 4k - phi + j (j < 4) and
+// qs[phi][k] holds their (rt, ri) as bytes (U <= 255): .x = cells 0, 1 and
+// .y = cells 2, 3, each cell ri | rt << 8 (cells outside the stream clamped to
+// its first / last cell, never stored).  Larger U: (rt, ri) of the quad's first
+// cell is located arithmetically and the others follow along the row.
 __host__ __device__ inline size_t cellinfo_quads(int U) {
     const long long NC = (long long)(U + 1) * (U + 2) / 2;
     return (size_t)((NC + 3) / 4 + 1);
@@ -140,18 +142,22 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
     const int U = d.units, nG = d.n_gamma, nL = d.n_lambda, V = d.n_streams;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t nq_tab = cellinfo_quads(U);
-    const bool use_qs = p.grid_qs != 0;   // position table in shared memory (small U)
-    unsigned* qs = reinterpret_cast<unsigned*>(smem);
-    unsigned char* mine = smem + (use_qs ? a16(4 * nq_tab * sizeof(unsigned)) : 0) + (size_t)warp * p.warp_bytes;
+    const bool use_qs = p.grid_qs != 0;   // byte position table in shared memory (U <= 255)
+    uint2* qs = reinterpret_cast<uint2*>(smem);
+    unsigned char* mine = smem + (use_qs ? a16(4 * nq_tab * sizeof(uint2)) : 0) + (size_t)warp * p.warp_bytes;
     StreamIn* sin = reinterpret_cast<StreamIn*>(mine);
     Tabs T = carve_tabs(mine + a16(sizeof(StreamIn)), U);
     const int NC = (U + 1) * (U + 2) / 2;
 
     for (int t = threadIdx.x; use_qs && t < (int)(4 * nq_tab); t += blockDim.x) {
         const int phi = t / (int)nq_tab, k = t - phi * (int)nq_tab;
-        const int c = min(max(4 * k - phi, 0), NC - 1);
-        const int rt = row_of(c, U);
-        qs[t] = ((unsigned)rt << 16) | (unsigned)(c - rowstart(rt, U));
+        unsigned w[2] = {0u, 0u};
+        for (int j = 0; j < 4; ++j) {
+            const int c = min(max(4 * k - phi + j, 0), NC - 1);
+            const int rt = row_of(c, U);
+            w[j >> 1] |= ((unsigned)(c - rowstart(rt, U)) | ((unsigned)rt << 8)) << (16 * (j & 1));
+        }
+        qs[t] = make_uint2(w[0], w[1]);
     }
     __syncthreads();
 
@@ -176,23 +182,23 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
             const int phi = (int)(f0 & 3);
             const long long q0 = f0 >> 2;
             const int nq = (int)(((f1 + 3) >> 2) - q0);
-            const unsigned* qst = qs + (size_t)phi * nq_tab;
+            const uint2* qst = qs + (size_t)phi * nq_tab;
             for (int k = lane; k < nq; k += 32) {
                 const long long fq = (q0 + k) << 2;
                 const int c0 = 4 * k - phi;
-                // (rt, ri) of the quad's cells: the first from the table, then along the row
+                // (rt, ri) of the quad's cells as (rt * kSlots) << 16 | ri
                 unsigned e[4];
-                {
-                    int rt, ri;
-                    if (use_qs) {
-                        const unsigned s0 = qst[k];
-                        rt = (int)(s0 >> 16);
-                        ri = (int)(s0 & 0xFFFFu);
-                    } else {
-                        const int c = max(c0, 0);
-                        rt = row_of(c, U);
-                        ri = c - rowstart(rt, U);
+                if (use_qs) {
+                    const uint2 s2 = qst[k];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const unsigned wj = (j < 2 ? s2.x : s2.y) >> (16 * (j & 1));
+                        e[j] = ((wj & 0xFF00u) << 11) | (wj & 0xFFu);   // rt * 8 << 16 | ri
                     }
+                } else {
+                    const int c = max(c0, 0);
+                    int rt = row_of(c, U);
+                    int ri = c - rowstart(rt, U);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         e[j] = ((unsigned)(rt * kSlots) << 16) | (unsigned)ri;
@@ -557,8 +563,8 @@ int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, f
     // the position table (16 B per 4 cells of a stream) is staged only while it
     // leaves room for all warps' tables; beyond that each quad locates its row
     // arithmetically, and large U runs fewer warps per CTA (>= 1)
-    const size_t qsb = a16(4 * cellinfo_quads(d.units) * sizeof(unsigned));
-    p.grid_qs = qsb + p.warp_bytes * kGridWarps <= h->smem_optin;
+    const size_t qsb = a16(4 * cellinfo_quads(d.units) * sizeof(uint2));
+    p.grid_qs = d.units <= 255 && qsb + p.warp_bytes * kGridWarps <= h->smem_optin;
     const size_t avail = h->smem_optin - (p.grid_qs ? qsb : 0);
     const int warps = (int)std::min<size_t>(kGridWarps, avail / p.warp_bytes);
     if (warps < 1) return EKYA_ERR_SHAPE;
