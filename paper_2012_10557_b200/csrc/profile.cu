@@ -1,8 +1,9 @@
 // profile.cu -- ekya_profile_estimate: the class-distribution-similarity
 // accuracy estimator (draft appendix).
 //
-// Both modes run one persistent CTA (512 threads) per SM that walks its
-// queries through a two-stage shared-memory pipeline fed by the TMA bulk-copy
+// RADIUS and the general CLUSTER kernel run one persistent CTA (512 threads)
+// per SM that walks its queries through a two-stage shared-memory pipeline fed
+// by the TMA bulk-copy
 // engine (cp.async.bulk + mbarrier): while the CTA computes query j, the
 // history histograms / accuracies of query j+1 are in flight, so HBM streams
 // continuously and no thread stalls on a global load.
@@ -15,12 +16,14 @@
 // Queries whose history does not fit a stage are processed in window chunks.
 //
 // CLUSTER (ALU-bound): Lloyd's algorithm (C19) per query on the staged
-// history.  Each thread keeps its window's histogram in registers across
-// iterations and reads centroids as float4 broadcasts; cluster sums are exact
-// Q32 integers maintained INCREMENTALLY (only windows whose assignment changed
-// are moved between clusters, with 64-bit shared atomics), which is
-// bit-identical to the oracle's full recomputation because integer addition is
-// associative.
+// history.  The bench shape (H <= 512, C <= 32, k <= 8) runs cluster2_kernel:
+// four 256-thread CTAs per SM, one query each, packed f32x2 distances with a
+// changed-centroid register cache and exact cluster sums in shared 32-bit
+// counter pairs (see the comment above the kernel).  Other shapes run
+// cluster_kernel: one 512-thread CTA per SM, window rows in registers or shared
+// memory, per-warp exact partial sums.  Both maintain the sums INCREMENTALLY
+// (only windows whose assignment changed are moved), which is bit-identical to
+// the oracle's full recomputation because integer addition is associative.
 #include <algorithm>
 #include <cfloat>
 #include <cstring>
@@ -597,10 +600,13 @@ __global__ void __launch_bounds__(kProfThreads, 1) cluster_kernel(ProfParams P) 
 // histograms from the staged tile (row stride C words: conflict-free for odd C)
 // and each centroid as a float4 broadcast.  The per-thread distance registers
 // double as a cache: only centroids whose coordinates changed bitwise are
-// recomputed.  The history tile is single-buffered: the next query's TMA is
-// issued as soon as this query's Lloyd passes are done, overlapping the
-// accuracy reduction, which reads the accuracy tile from L2 (bulk-prefetched
-// when the query was issued).
+// recomputed.  Exact cluster sums are shared 32-bit counter pairs moved with
+// red.shared only for windows that changed cluster; the similar windows of the
+// query's cluster are compacted into a list for the accuracy reduction.  The
+// history tile is single-buffered (4 CTAs x 56 KB fill the SM): the next
+// query's TMA is issued as soon as this query's Lloyd passes are done,
+// overlapping the accuracy reduction, which reads the accuracy tile from L2
+// (bulk-prefetched when the query was issued).
 constexpr int kC2Threads = 256;
 constexpr int kC2Ctas = 4;
 constexpr int kC2Kmax = 8;

@@ -264,6 +264,9 @@ __device__ __forceinline__ unsigned long long stream_down_key(const WarpState& S
     return k;
 }
 
+// MODE: EKYA_THIEF_STEEPEST or EKYA_THIEF_LITERAL (one kernel per mode keeps the hot loop's
+// code small)
+template <int MODE>
 __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const ekya_dims& d = p.d;
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
     for (int v = 0; v < V; ++v) update_stream(in, S, v, d, fast);
 
     unsigned steps = 0;
-    if (p.mode == EKYA_THIEF_STEEPEST) {
+    if (MODE == EKYA_THIEF_STEEPEST) {
         const unsigned max_steps = 1u << 26;
         for (;;) {
             // per-stream best down, top-2 by stream
@@ -461,11 +464,12 @@ int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int m
     size_t smem = p.warp_bytes * p.warps;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0) return EKYA_OK;
-    cudaError_t e = cudaFuncSetAttribute(thief_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = mode == EKYA_THIEF_STEEPEST ? thief_kernel<EKYA_THIEF_STEEPEST> : thief_kernel<EKYA_THIEF_LITERAL>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
     long long grid = (d.n_inst + p.warps - 1) / p.warps;
     if (grid > 0x7fffffffLL) return EKYA_ERR_SHAPE;
-    thief_kernel<<<(unsigned)grid, kThiefThreads, smem, s>>>(p);
+    kern<<<(unsigned)grid, kThiefThreads, smem, s>>>(p);
     h->launches++;
     return cuda_status(cudaGetLastError());
 }
