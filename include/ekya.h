@@ -112,7 +112,7 @@ typedef struct {
  *   allocation vectors alloc[b][n][0..2V) (u16 units, job order C10), the
  *   exact objective out_sum_q32[b][n] = sum_v Q32(value_v) (u64), optionally
  *   out_mean[b][n] = (float)(S / (V 2^32)) and out_cfg[b][n][v].  Requires the
- *   per-instance tables, V * (65 (U+1) + 16) bytes, plus ~14 KB of staging to fit
+ *   per-instance tables, V * (73 (U+1) + 32) bytes, plus ~20 KB of staging to fit
  *   in the device's opt-in shared memory per block (227 KB on B200: V (U+1) <~
  *   3300), else EKYA_ERR_SHAPE.
  * mode EKYA_EVAL_GRID: for each (b, v) and every split with r_train + r_infer

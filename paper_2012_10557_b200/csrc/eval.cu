@@ -33,9 +33,9 @@ constexpr int kListThreads = 1024;
 
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// per-stream table footprint: lad[U+1] + tvc[U+1][8] (uint2)
-__host__ __device__ inline size_t tab_bytes(int U) {
-    return a16((size_t)(U + 1)) + a16((size_t)(U + 1) * kSlots * 8);
+// per-stream table footprint: lad[U+1] + tvc[U+1][rs] (8-byte entries)
+__host__ __device__ inline size_t tab_bytes(int U, int rs = kSlots) {
+    return a16((size_t)(U + 1)) + a16((size_t)(U + 1) * rs * 8);
 }
 
 // first cell of row rt of a stream's triangle
@@ -90,7 +90,7 @@ __host__ __device__ inline ListLayout list_layout(int U, int V, int nG, int nL, 
     size_t o = 0;
     L.ntabs = ntabs;
     L.sin = o;    o += a16(sizeof(StreamIn)) * (size_t)(kListThreads / 32);
-    L.tabset = tab_bytes(U) * V;
+    L.tabset = tab_bytes(U, kListRow) * V;
     L.tabs = o;   o += L.tabset * ntabs;
     L.inst_bytes = inst_layout(V, nG, nL).total;
     L.inst = o;   o += 2 * L.inst_bytes;
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
         __syncwarp();
         unsigned char* tv = tabs + v * tb;
         const int r1 = min(U + 1, blk * brows + brows);
-        warp_build_tables<GM, NGT, NLT>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
+        warp_build_tables<GM, NGT, NLT, kListRow>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
                               reinterpret_cast<unsigned long long*>(tv + a16((size_t)(U + 1))), blk * brows, r1,
                               blk == 0);
     };
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
             dev |= pr ^ pc;
             const int ri = (int)(pc & 0xFFFFu), rt = (int)(pc >> 16);
             tot += ri + rt;
-            return reinterpret_cast<const uint2*>(t + off_tvc)[rt * kSlots + t[ri]];
+            return reinterpret_cast<const uint2*>(t + off_tvc)[rt * kListRow + t[ri]];
         };
         bool fast_ok = false;
         if constexpr (VT > 0) {
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
                             const unsigned w = hh ? pr[v2].y : pr[v2].x;
                             const unsigned char* t = tabs + (2 * v2 + hh) * tb;
                             acc += w;
-                            e[hh] = reinterpret_cast<const uint2*>(t + off_tvc)[(w >> 16) * kSlots + t[w & 0xFFFFu]];
+                            e[hh] = reinterpret_cast<const uint2*>(t + off_tvc)[(w >> 16) * kListRow + t[w & 0xFFFFu]];
                             S.add(e[hh]);
                         }
                         if (cr2) cr2[v2] = (uint16_t)__byte_perm(e[0].y, e[1].y, 0x0073);
@@ -599,7 +599,7 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     p.L = list_layout(d.units, d.n_streams, d.n_gamma, d.n_lambda, 2);
     if (p.L.total > h->smem_optin) p.L = list_layout(d.units, d.n_streams, d.n_gamma, d.n_lambda, 1);
     p.IL = inst_layout(d.n_streams, d.n_gamma, d.n_lambda);
-    p.tb = tab_bytes(d.units);
+    p.tb = tab_bytes(d.units, kListRow);
     p.rcp_v = 1.0 / (double)d.n_streams;
     // Many rows per instance: one build task per stream (staging and the lambda ladder done
     // once, all r_train rows in one warp) -- the row chunks keep every warp busy meanwhile.
