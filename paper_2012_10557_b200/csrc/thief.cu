@@ -66,8 +66,9 @@ struct ThiefParams {
 struct WarpState {
     long long* rec;              // [V][8]
     int* alloc;                  // [J]
-    int* lthr;                   // [V][8] lambda* breakpoints (INT_MAX = unused)
-    float* lfac;                 // [V][8] factor of lambda* at the breakpoint (-1 = none)
+    int* lthr;                   // [V][8] lambda* breakpoints, ascending (INT_MAX = unused)
+    float* lfac;                 // [V][8] factor of lambda* at the breakpoint
+    int* lidx;                   // [V][8] index of lambda* at the breakpoint
     float* gc;                   // [V][4] G*(rt-D), G*(rt), G*(rt+D) cached for rt = grt[v]
     int* grt;                    // [V]    (-1 = empty)
     __device__ __forceinline__ long long cur(int v) const { return rec[v * 8]; }
@@ -78,7 +79,7 @@ struct WarpState {
 
 __host__ __device__ inline size_t thief_warp_bytes(int V) {
     const size_t J = 2 * (size_t)V;
-    size_t b = 8 * 8 * (size_t)V + 4 * J + 2 * 4 * 8 * (size_t)V + 4 * 4 * (size_t)V + 4 * (size_t)V;
+    size_t b = 8 * 8 * (size_t)V + 4 * J + 3 * 4 * 8 * (size_t)V + 4 * 4 * (size_t)V + 4 * (size_t)V;
     return (b + 15) & ~size_t(15);
 }
 
@@ -89,7 +90,8 @@ __device__ inline WarpState carve(unsigned char* base, int V) {
     w.alloc = reinterpret_cast<int*>(w.rec + 8 * V);
     w.lthr = w.alloc + J;
     w.lfac = reinterpret_cast<float*>(w.lthr + 8 * V);
-    w.gc = w.lfac + 8 * V;
+    w.lidx = reinterpret_cast<int*>(w.lfac + 8 * V);
+    w.gc = reinterpret_cast<float*>(w.lidx + 8 * V);
     w.grt = reinterpret_cast<int*>(w.gc + 4 * V);
     return w;
 }
@@ -120,30 +122,57 @@ struct InstView {
     const float* post;
     const uint16_t* lmu;    // [V][nL]
     const float* lf;
+    const float4* cpd;      // [V][nG] staged (cost, post, fl(post - stale), 0), or NULL
+    // (cost, post, fl(post - stale)) of config g (0-based) of stream v
+    __device__ __forceinline__ float4 get(int v, int g, int nG) const {
+        if (cpd) return cpd[v * nG + g];
+        const float c = cost[(size_t)v * nG + g], po = post[(size_t)v * nG + g];
+        return make_float4(c, po, fsub(po, stale[v]), 0.0f);
+    }
 };
 
-// Warp-collective, once per stream: lambda* breakpoints.  lambda*(ri) depends
-// only on {admissible l : lmu_l <= ri}, which equals the set at
-// t* = max{lmu_l admissible, lmu_l <= ri}; so lane k stores t_k = lmu_k (if
-// admissible) and the factor of lambda*(t_k).
+// Warp-collective, once per stream: lambda* ladder (Alg. 2 lines 3-4, rule 3).
+// lambda*(ri) depends only on the admissible set {l : t_l <= ri} (t_l = lmu_l if
+// fl(stale f_l) >= a_MIN, else never), which equals the set at the largest
+// t_l <= ri; so the thresholds are stored ascending (ties: lambda order) with
+// lambda*(t) and its factor, and a lookup is one ballot over lanes 0..7: the
+// lanes with t <= ri form a prefix and its last lane holds lambda*(ri).
 __device__ void init_ladder(const InstView& in, const WarpState& S, int v, const ekya_dims& d) {
     const int lane = threadIdx.x & 31, nL = d.n_lambda;
-    if (lane < 8) {
-        int t = INT_MAX;
-        float f = -1.0f;
-        if (lane < nL) {
-            const float stale = in.stale[v];
-            const uint16_t m = in.lmu[(size_t)v * nL + lane];
-            const float acc = fmul(stale, in.lf[(size_t)v * nL + lane]);
-            if (m != kLmuPad && acc >= d.a_min) {
-                t = m;
-                const int l = lambda_star(stale, in.lmu + (size_t)v * nL, in.lf + (size_t)v * nL, nL, m, d.a_min);
-                f = in.lf[(size_t)v * nL + l];
-            }
-        }
-        S.lthr[v * 8 + lane] = t;
-        S.lfac[v * 8 + lane] = f;
+    int t = INT_MAX;
+    float acc = 0.0f, f = 0.0f;
+    if (lane < nL) {
+        const uint16_t m = in.lmu[(size_t)v * nL + lane];
+        f = in.lf[(size_t)v * nL + lane];
+        acc = fmul(in.stale[v], f);
+        if (m != kLmuPad && acc >= d.a_min) t = m;
     }
+    // lambda*(t) over {l : t_l <= t}: highest accuracy, lowest index on ties
+    int best = -1, rank = 0;
+    float bacc = 0.0f;
+    for (int l = 0; l < nL; ++l) {
+        const int tl = __shfl_sync(FULL, t, l);
+        const float al = __shfl_sync(FULL, acc, l);
+        if (tl <= t && (best < 0 || al > bacc)) {
+            best = l;
+            bacc = al;
+        }
+        rank += (tl < t || (tl == t && l < lane)) ? 1 : 0;
+    }
+    const float fb = __shfl_sync(FULL, f, best < 0 ? 0 : best);
+    if (lane < 8) {
+        // unused / inadmissible lambdas sort last (t = INT_MAX) and are never reached
+        const int pos = lane < nL ? rank : lane;
+        S.lthr[v * 8 + pos] = t;
+        S.lfac[v * 8 + pos] = fb;
+        S.lidx[v * 8 + pos] = best;
+    }
+}
+
+// lambda* ladder lookup of stream v at ri: slot of lambda*(ri) in the ladder, -1 if none
+__device__ __forceinline__ int ladder_slot(int tk, int ri) {
+    const unsigned m = __ballot_sync(FULL, (threadIdx.x & 31) < 8 && tk <= ri);
+    return 31 - __clz(m);   // -1 when m == 0
 }
 
 // Warp-collective update of stream v's entries in the state arrays.
@@ -153,10 +182,12 @@ __device__ __forceinline__ void update_stream(const InstView& in, const WarpStat
     const int D = d.steal_units, nG = d.n_gamma;
     const int ri = S.alloc[2 * v], rt = S.alloc[2 * v + 1];
     const float stale = in.stale[v];
-    float cost = 0.0f, post = 0.0f;
+    float cost = 0.0f, post = 0.0f, diff = 0.0f;
     if (lane >= 1 && lane <= nG) {
-        cost = in.cost[(size_t)v * nG + lane - 1];
-        post = in.post[(size_t)v * nG + lane - 1];
+        const float4 c = in.get(v, lane - 1, nG);
+        cost = c.x;
+        post = c.y;
+        diff = c.z;
     }
     const int tk = lane < 8 ? S.lthr[v * 8 + lane] : INT_MAX;
     const float fk = lane < 8 ? S.lfac[v * 8 + lane] : -1.0f;
@@ -174,7 +205,7 @@ __device__ __forceinline__ void update_stream(const InstView& in, const WarpStat
         } else {
             f = mine && r >= 1 ? fdiv(cost, den) : 2.0f;
         }
-        const float w = fsub(post, fmul(f, fsub(post, stale)));
+        const float w = fsub(post, fmul(f, diff));
         const float g = lane == 0 ? stale : (mine && r >= 1 && f <= 1.0f ? w : -1.0f);
         const int m = __reduce_max_sync(FULL, __float_as_int(g));
         return r < 0 ? -1.0f : __int_as_float(m);
@@ -195,10 +226,9 @@ __device__ __forceinline__ void update_stream(const InstView& in, const WarpStat
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const int ri2 = ri + D * (k - 1);
-        const unsigned key = (ri2 >= 0 && tk <= ri2) ? ((unsigned)(tk + 1) << 3) | (unsigned)lane : 0u;
-        const unsigned km = __reduce_max_sync(FULL, key);
-        const float f = __shfl_sync(FULL, fk, km & 7u);
-        fac[k] = km ? f : -1.0f;
+        const int sl = ladder_slot(tk, ri2);   // ri2 < 0 never reaches a threshold (t >= 0)
+        const float f = __shfl_sync(FULL, fk, sl < 0 ? 0 : sl);
+        fac[k] = sl >= 0 ? f : -1.0f;
     }
     __syncwarp();
     if (lane == 0) {
@@ -218,19 +248,20 @@ __device__ __forceinline__ void update_stream(const InstView& in, const WarpStat
 }
 
 // Warp-collective: exact argmax config byte of stream v at its final split.
-__device__ uint8_t stream_cfg(const InstView& in, int v, int ri, int rt, const ekya_dims& d) {
-    const int lane = threadIdx.x & 31, nG = d.n_gamma, nL = d.n_lambda;
+__device__ uint8_t stream_cfg(const InstView& in, const WarpState& S, int v, int ri, int rt, const ekya_dims& d) {
+    const int lane = threadIdx.x & 31, nG = d.n_gamma;
+    const int tk = lane < 8 ? S.lthr[v * 8 + lane] : INT_MAX;
+    const int sl = ladder_slot(tk, ri);
+    if (sl < 0) return (uint8_t)(kLambdaNone << 5);
+    const int l = S.lidx[v * 8 + sl];
+    const float fac = S.lfac[v * 8 + sl];
     const float stale = in.stale[v];
-    const int l = lambda_star(stale, in.lmu + (size_t)v * nL, in.lf + (size_t)v * nL, nL, ri, d.a_min);
-    if (l < 0) return (uint8_t)(kLambdaNone << 5);
-    const float fac = in.lf[(size_t)v * nL + l];
     float a = -1.0f;
     if (lane == 0) a = fmul(fac, stale);
     else if (lane <= nG) {
+        const float4 c = in.get(v, lane - 1, nG);
         float w;
-        if (window_acc(stale, in.post[(size_t)v * nG + lane - 1], in.cost[(size_t)v * nG + lane - 1], rt,
-                       d.unit_gpu_seconds, &w))
-            a = fmul(fac, w);
+        if (window_acc(stale, c.y, c.x, rt, d.unit_gpu_seconds, &w)) a = fmul(fac, w);
     }
     const int m = __reduce_max_sync(FULL, __float_as_int(a));
     const unsigned hits = __ballot_sync(FULL, __float_as_int(a) == m);
@@ -267,7 +298,7 @@ __device__ __forceinline__ unsigned long long stream_down_key(const WarpState& S
 // MODE: EKYA_THIEF_STEEPEST or EKYA_THIEF_LITERAL (one kernel per mode keeps the hot loop's
 // code small)
 template <int MODE>
-__global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
+__global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const ekya_dims& d = p.d;
     const int V = d.n_streams, J = 2 * V, D = d.steal_units, U = d.units, nG = d.n_gamma, nL = d.n_lambda;
@@ -278,7 +309,7 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
     if (b >= d.n_inst) return;
 
     InstView in{p.t.stale + b * V, p.t.cost + b * V * nG, p.t.post + b * V * nG,
-                p.t.lam_min_units + b * V * nL, p.t.lam_factor + b * V * nL};
+                p.t.lam_min_units + b * V * nL, p.t.lam_factor + b * V * nL, nullptr};
 
     // ---- validity (R-ERR) ----
     bool ok = true;
@@ -295,19 +326,17 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
     bool fast = uT_fast(d);
     for (int i = lane; i < V * nG; i += 32) fast &= fast_dividend(__ldg(in.cost + i));
     fast = __all_sync(FULL, fast);
-    if (p.stage && ok) {   // stale, cost, post into this warp's shared memory
-        float* st = staged;
-        float* co = st + V;
-        float* po = co + V * nG;
+    if (p.stage && ok) {   // stale and (cost, post, post - stale) into this warp's shared memory
+        float4* cpd = reinterpret_cast<float4*>(staged);
+        float* st = reinterpret_cast<float*>(cpd + V * nG);
         for (int i = lane; i < V; i += 32) st[i] = __ldg(in.stale + i);
         for (int i = lane; i < V * nG; i += 32) {
-            co[i] = __ldg(in.cost + i);
-            po[i] = __ldg(in.post + i);
+            const float c = __ldg(in.cost + i), po = __ldg(in.post + i);
+            cpd[i] = make_float4(c, po, fsub(po, __ldg(in.stale + i / nG)), 0.0f);
         }
         __syncwarp();
         in.stale = st;
-        in.cost = co;
-        in.post = po;
+        in.cpd = cpd;
     }
     if (!ok) {
         for (int j = lane; j < J; j += 32) p.out_alloc[b * J + j] = 0;
@@ -430,7 +459,7 @@ __global__ void __launch_bounds__(kThiefThreads) thief_kernel(ThiefParams p) {
     const unsigned long long sum = shfl_sum_u64(part);
     for (int j = lane; j < J; j += 32) p.out_alloc[b * J + j] = (uint16_t)S.alloc[j];
     for (int v = 0; v < V; ++v) {
-        const uint8_t c = stream_cfg(in, v, S.alloc[2 * v], S.alloc[2 * v + 1], d);
+        const uint8_t c = stream_cfg(in, S, v, S.alloc[2 * v], S.alloc[2 * v + 1], d);
         if (lane == 0) p.out_cfg[b * V + v] = c;
     }
     if (lane == 0) {
@@ -458,7 +487,7 @@ int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int m
     p.out_steps = out_steps;
     p.warps = kThiefThreads / 32;
     p.state_bytes = thief_warp_bytes(d.n_streams);
-    const size_t tbytes = ((size_t)d.n_streams * (2 * d.n_gamma + 1) * 4 + 15) & ~size_t(15);
+    const size_t tbytes = ((size_t)d.n_streams * (4 * d.n_gamma + 1) * 4 + 15) & ~size_t(15);
     p.stage = tbytes <= 8192;
     p.warp_bytes = p.state_bytes + (p.stage ? tbytes : 0);
     size_t smem = p.warp_bytes * p.warps;
