@@ -257,7 +257,9 @@ struct Q32Sum {
 };
 
 // VT > 0: compile-time stream count (fully unrolled rows); 0: runtime V.  NGT / NLT as GRID.
-template <int GM, int VT, int NGT, int NLT>
+// UT > 0: the tables are laid out for U = UT (>= the runtime U), so every per-stream table
+// offset is a compile-time constant.
+template <int GM, int VT, int NGT, int NLT, int UT>
 __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const ekya_dims& d = p.d;
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const ListLayout& L = p.L;
     const InstLayout& IL = p.IL;
-    const int tb = (int)p.tb;
+    const int tb = UT > 0 ? (int)tab_bytes(UT, kListRow) : (int)p.tb;
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bars);
     int* ctr = reinterpret_cast<int*>(smem + L.bars + 16);   // task counters, one per phase parity
     const int N = p.n_alloc;
@@ -348,19 +350,18 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
         __syncwarp();
         unsigned char* tv = tabs + v * tb;
         const int r1 = min(U + 1, blk * brows + brows);
-        warp_build_tables<GM, NGT, NLT, kListRow>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
-                              reinterpret_cast<unsigned long long*>(tv + a16((size_t)(U + 1))), blk * brows, r1,
+        warp_build_tables<GM, NGT, NLT, kListRow, 8>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
+                              reinterpret_cast<unsigned long long*>(tv + a16((size_t)((UT > 0 ? UT : U) + 1))), blk * brows, r1,
                               blk == 0);
     };
 
     const unsigned UU = (unsigned)U | ((unsigned)U << 16);
     const bool pairs = (V % 2 == 0) && (reinterpret_cast<uintptr_t>(p.alloc) % 8 == 0) &&
                        (!p.out_cfg || reinterpret_cast<uintptr_t>(p.out_cfg) % 2 == 0);
-    const int off_tvc = (int)a16((size_t)(U + 1));
-    // Row chunk c of instance b: rows 32c + lane, one thread per allocation row,
-    // read straight from global (L2).
-    auto row_chunk = [&](long long b, const unsigned char* tabs, bool ok, int c) {
-        const int r = c * 32 + lane;
+    const int off_tvc = (int)a16((size_t)((UT > 0 ? UT : U) + 1));   // lad[] precedes the entries
+    constexpr int kRowBytes = kListRow * 8;
+    // Allocation row r of instance b: one thread per row, read straight from global (L2).
+    auto row_one = [&](long long b, const unsigned char* tabs, bool ok, int r) {
         if (r >= N) return;
         const long long o = b * N + r;
         unsigned dev = 0;   // any bit set: some r_train / r_infer > U (clamped)
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
             dev |= pr ^ pc;
             const int ri = (int)(pc & 0xFFFFu), rt = (int)(pc >> 16);
             tot += ri + rt;
-            return reinterpret_cast<const uint2*>(t + off_tvc)[rt * kListRow + t[ri]];
+            return *reinterpret_cast<const uint2*>(t + off_tvc + rt * kRowBytes + t[ri]);
         };
         bool fast_ok = false;
         if constexpr (VT > 0) {
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
                             const unsigned w = hh ? pr[v2].y : pr[v2].x;
                             const unsigned char* t = tabs + (2 * v2 + hh) * tb;
                             acc += w;
-                            e[hh] = reinterpret_cast<const uint2*>(t + off_tvc)[(w >> 16) * kListRow + t[w & 0xFFFFu]];
+                            e[hh] = *reinterpret_cast<const uint2*>(t + off_tvc + (w >> 16) * kRowBytes + t[w & 0xFFFFu]);
                             S.add(e[hh]);
                         }
                         if (cr2) cr2[v2] = (uint16_t)__byte_perm(e[0].y, e[1].y, 0x0073);
@@ -454,6 +455,13 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
         }
     };
 
+    // Row task c: rows 64c + lane and 64c + 32 + lane (two rows per thread halve the
+    // task-queue traffic per row)
+    auto row_chunk = [&](long long b, const unsigned char* tabs, bool ok, int c) {
+        row_one(b, tabs, ok, c * 64 + lane);
+        row_one(b, tabs, ok, c * 64 + 32 + lane);
+    };
+
     // Dynamic task queue of one phase: n_build build tasks of instance bb (into
     // table set tb_build) and n_rows row chunks of instance b, interleaved 1:1
     // while both last so that the issue-bound builds and the memory-bound row
@@ -494,7 +502,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     __syncthreads();
     const long long b0 = blockIdx.x;
     if (b0 >= B) return;
-    const int n_build = V * nblk, n_chunks = (N + 31) / 32;
+    const int n_build = V * nblk, n_chunks = (N + 63) / 64;
     // Double-buffered table sets (ntabs == 2): the phase of step j builds
     // instance j+1's tables while instance j's rows stream; inputs are staged two
     // instances ahead.  Single set (large V x U): build j | barrier | rows j.
@@ -596,10 +604,15 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     p.out_mean = out_mean;
     p.out_cfg = out_cfg;
     if (reinterpret_cast<uintptr_t>(alloc) & 3) return EKYA_ERR_ARG;
-    p.L = list_layout(d.units, d.n_streams, d.n_gamma, d.n_lambda, 2);
-    if (p.L.total > h->smem_optin) p.L = list_layout(d.units, d.n_streams, d.n_gamma, d.n_lambda, 1);
+    // the paper's shape (V = 10 streams, |Gamma| = 18, |Lambda| = 5, U <= 80) gets the
+    // unrolled-row kernel with tables laid out for U = 80 (compile-time offsets)
+    constexpr int kFastU = 80;
+    const bool fast = d.n_streams == 10 && d.n_gamma == 18 && d.n_lambda == 5 && d.units <= kFastU;
+    const int lu = fast ? kFastU : d.units;   // table layout
+    p.L = list_layout(lu, d.n_streams, d.n_gamma, d.n_lambda, 2);
+    if (p.L.total > h->smem_optin) p.L = list_layout(lu, d.n_streams, d.n_gamma, d.n_lambda, 1);
     p.IL = inst_layout(d.n_streams, d.n_gamma, d.n_lambda);
-    p.tb = tab_bytes(d.units, kListRow);
+    p.tb = tab_bytes(lu, kListRow);
     p.rcp_v = 1.0 / (double)d.n_streams;
     // Many rows per instance: one build task per stream (staging and the lambda ladder done
     // once, all r_train rows in one warp) -- the row chunks keep every warp busy meanwhile.
@@ -608,11 +621,9 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     size_t smem = p.L.total;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0 || n_alloc == 0) return EKYA_OK;
-    // the paper's shape (V = 10 streams, |Gamma| = 18, |Lambda| = 5) gets the unrolled-row kernel
-    auto kern = (d.n_streams == 10 && d.n_gamma == 18 && d.n_lambda == 5 && 10 * d.units < 65536)
-                    ? list_kernel<19, 10, 18, 0>
-                    : pick_gm(d.n_gamma, list_kernel<8, 0, 0, 0>, list_kernel<16, 0, 0, 0>, list_kernel<19, 0, 0, 0>,
-                              list_kernel<24, 0, 0, 0>, list_kernel<32, 0, 0, 0>);
+    auto kern = fast ? list_kernel<19, 10, 18, 0, kFastU>
+                     : pick_gm(d.n_gamma, list_kernel<8, 0, 0, 0, 0>, list_kernel<16, 0, 0, 0, 0>,
+                               list_kernel<19, 0, 0, 0, 0>, list_kernel<24, 0, 0, 0, 0>, list_kernel<32, 0, 0, 0, 0>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
     int grid = resident_grid(h, (const void*)kern, kListThreads, smem, d.n_inst);

@@ -167,7 +167,7 @@ __host__ __device__ inline ScratchLayout scratch_layout(int H, int Hc, int C, in
     const int CP = (C + 3) & ~3;
     size_t o = 0;
     L.bars = o;   o += 64;
-    L.sim = o;    o += al16((size_t)(cluster ? H : Hc) + 1);
+    L.sim = o;    o += al16(cluster ? (size_t)H + 1 : 2 * (size_t)Hc + 2);   // CLUSTER: flags; RADIUS: u16 list
     L.ps = o;     o += al16((size_t)kProfThreads * 8);
     L.pn = o;     o += al16((size_t)kProfThreads * 4);
     L.mu = o;     o += cluster ? al16((size_t)K * CP * 4) : 0;
@@ -214,12 +214,20 @@ __global__ void __launch_bounds__(kProfThreads, 1) radius_kernel(ProfParams P) {
             issue_item(P, smem + (i % NS) * P.stage_bytes, &bar[i % NS], item_q(i), h0, min(Hc, H - h0), true, L);
         }
     }
+    // similar windows of the current chunk, compacted (any order: the sums are exact integers)
+    uint16_t* list = reinterpret_cast<uint16_t*>(sim);
+    int* nsim = reinterpret_cast<int*>(scratch + S.misc);   // [2] counters, by chunk parity
+    if (threadIdx.x < 2) nsim[threadIdx.x] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     GammaAcc a;
     bool ok = true;
     for (long long i = 0; i < items; ++i) {
         const int s = (int)(i % NS);
         const long long q = item_q(i);
         const int h0 = item_h0(i), hn = min(Hc, H - h0);
+        int* cnt = nsim + (i & 1);
+        if (threadIdx.x == 0) nsim[(i + 1) & 1] = 0;   // last used by chunk i - 1 (ended by a barrier)
         mbar_wait(&bar[s], (unsigned)((i / NS) & 1));
         const StagePtrs sp = stage_ptrs(P, smem + s * P.stage_bytes, q, h0, true, L);
         if (h0 == 0) {
@@ -227,26 +235,72 @@ __global__ void __launch_bounds__(kProfThreads, 1) radius_kernel(ProfParams P) {
             ok = true;
             for (int c = threadIdx.x; c < C; c += blockDim.x) ok &= in01(sp.cur[c]);
         }
-        for (int h = threadIdx.x; h < hn; h += blockDim.x) {
-            const float* row = sp.hist + (size_t)h * C;
-            float d2 = 0.0f;
-            for (int c = 0; c < C; ++c) {
-                float x = row[c];
-                ok &= in01(x);
-                float diff = fsub(sp.cur[c], x);
-                d2 = fadd(d2, fmul(diff, diff));
+        // rule 5 distance per window; range check folded into a running min / max (a NaN
+        // element makes d2 NaN, caught below); similar windows appended to the list
+        for (int hw = warp * 32; hw < hn; hw += blockDim.x) {
+            const int h = hw + lane;
+            bool in = false;
+            if (h < hn) {
+                const float* row = sp.hist + (size_t)h * C;
+                float d2 = 0.0f, lo = 1.0f, hi = 0.0f;
+                for (int c = 0; c < C; ++c) {
+                    const float x = row[c];
+                    lo = fminf(lo, x);
+                    hi = fmaxf(hi, x);
+                    const float diff = fsub(sp.cur[c], x);
+                    d2 = fadd(d2, fmul(diff, diff));
+                }
+                ok &= lo >= 0.0f && hi <= 1.0f && d2 == d2;
+                in = __fsqrt_rn(d2) <= tau;
             }
-            sim[h] = __fsqrt_rn(d2) <= tau;
+            const unsigned m = __ballot_sync(0xffffffffu, in);
+            int base = 0;
+            if (lane == 0 && m) base = atomicAdd(cnt, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (in) list[base + __popc(m & ((1u << lane) - 1u))] = (uint16_t)h;
+        }
+        // the accuracy tile: NaN (unmeasured) or in [0, 1] (fminf / fmaxf ignore NaN)
+        {
+            float lo = 1.0f, hi = 0.0f;
+            const int n = hn * G;
+            if ((reinterpret_cast<uintptr_t>(sp.acc) & 15) == 0) {
+                const float4* a4 = reinterpret_cast<const float4*>(sp.acc);
+                for (int t = threadIdx.x; t < n / 4; t += blockDim.x) {
+                    const float4 x = a4[t];
+                    lo = fminf(fminf(lo, x.x), fminf(x.y, fminf(x.z, x.w)));
+                    hi = fmaxf(fmaxf(hi, x.x), fmaxf(x.y, fmaxf(x.z, x.w)));
+                }
+                for (int t = (n & ~3) + threadIdx.x; t < n; t += blockDim.x) {
+                    lo = fminf(lo, sp.acc[t]);
+                    hi = fmaxf(hi, sp.acc[t]);
+                }
+            } else {
+                for (int t = threadIdx.x; t < n; t += blockDim.x) {
+                    lo = fminf(lo, sp.acc[t]);
+                    hi = fmaxf(hi, sp.acc[t]);
+                }
+            }
+            ok &= lo >= 0.0f && hi <= 1.0f;
         }
         __syncthreads();
-        ok &= gacc_add(a, sp.acc, sim, hn, G);
+        // exact per-gamma sums over the similar, measured windows
+        if (a.grp < a.ngrp) {
+            const int ns = *cnt;
+            for (int e = a.grp; e < ns; e += a.ngrp) {
+                const float x = sp.acc[(size_t)list[e] * G + a.g];
+                if (x == x) {
+                    a.s += q32(x);
+                    a.n += 1;
+                }
+            }
+        }
         const bool last = h0 + hn >= H;
         if (last) {
             ok = __syncthreads_and(ok) != 0;
             if (!ok && threadIdx.x == 0) flag_data_error(P.st);
             gacc_finish(a, ps, pn, sp.fb, P, q, ok);
         }
-        __syncthreads();   // stage s and sim[] are free again
+        __syncthreads();   // stage s and the list are free again
         if (threadIdx.x == 0 && i + NS < items) {
             int h1 = item_h0(i + NS);
             issue_item(P, smem + s * P.stage_bytes, &bar[s], item_q(i + NS), h1, min(Hc, H - h1), true, L);
@@ -1044,7 +1098,7 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
     cudaError_t e;
     if (p.mode == EKYA_PROFILE_RADIUS) {
         const size_t scratch_fixed = scratch_layout(0, 0, C, 0, false).total;
-        const size_t per_window = (size_t)(C + G) * 4 + 1;
+        const size_t per_window = (size_t)(C + G) * 4 + 2;
         // kRadiusStages stages of Hc windows: a query is split into equal chunks so
         // that several chunks are always in flight while one is being computed
         const int NS = kRadiusStages;

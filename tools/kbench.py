@@ -44,7 +44,15 @@ else:
         rows = torch.empty((w.B, w.N, w.J), dtype=torch.uint16, device=dev)
         for b0 in range(0, w.B, 1024):
             rows[b0:b0 + 1024] = synth.list_allocs(w.cfg, w.N, b0, min(w.B, b0 + 1024), device=dev)
-        fn = lambda: ekya.eval_list(h, T, rows, *args)
+        if os.environ.get("KB_OUT"):   # subset of LIST outputs, e.g. "sum" or "sum,mean"
+            outs = os.environ["KB_OUT"].split(",")
+            dims, tabs = ekya.dims_from(T, *args), ekya.make_tables(**T)
+            ls = torch.empty((w.B, w.N), dtype=torch.uint64, device=dev)
+            lm = torch.empty((w.B, w.N), dtype=torch.float32, device=dev) if "mean" in outs else None
+            lc = torch.empty((w.B, w.N, w.V), dtype=torch.uint8, device=dev) if "cfg" in outs else None
+            fn = lambda: ekya.ekya_eval_allocations(h, dims, tabs, ekya.EVAL_LIST, w.N, rows, ls, lm, lc)
+        else:
+            fn = lambda: ekya.eval_list(h, T, rows, *args)
     else:
         mode = ekya.THIEF_STEEPEST if which == "steepest" else ekya.THIEF_LITERAL
         fn = lambda: ekya.thief_schedule(h, T, *args, mode=mode)
