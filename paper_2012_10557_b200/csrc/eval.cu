@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
             const long long item = b * V + v;
             if (ok) {
                 warp_load_stream(sin, p.t, item, nG, nL);
-                warp_build_tables<GM, NGT, NLT>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc);
+                warp_build_tables<GM, NGT, NLT, kSlots, 8>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc);
             }
             // Flat write of the stream's cells [f0, f0 + NC) in aligned quads of 4
             // cells: one 16-B value store + one 4-B config store per quad (the
@@ -186,34 +186,39 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
             for (int k = lane; k < nq; k += 32) {
                 const long long fq = (q0 + k) << 2;
                 const int c0 = 4 * k - phi;
-                // (rt, ri) of the quad's cells as (rt * kSlots) << 16 | ri
-                unsigned e[4];
+                // (rt, ri) of the quad's four cells
+                int ri[4], rt[4];
                 if (use_qs) {
                     const uint2 s2 = qst[k];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const unsigned wj = (j < 2 ? s2.x : s2.y) >> (16 * (j & 1));
-                        e[j] = ((wj & 0xFF00u) << 11) | (wj & 0xFFu);   // rt * 8 << 16 | ri
+                        const unsigned wj = j < 2 ? s2.x : s2.y;
+                        ri[j] = (int)__byte_perm(wj, 0u, 0x4440u + 2u * (j & 1));
+                        rt[j] = (int)__byte_perm(wj, 0u, 0x4441u + 2u * (j & 1));
                     }
                 } else {
                     const int c = max(c0, 0);
-                    int rt = row_of(c, U);
-                    int ri = c - rowstart(rt, U);
+                    int r_t = row_of(c, U);
+                    int r_i = c - rowstart(r_t, U);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        e[j] = ((unsigned)(rt * kSlots) << 16) | (unsigned)ri;
-                        if (c0 + j >= 0 && ++ri > U - rt) {
-                            rt = min(rt + 1, U);   // past the last cell: stay in range (never stored)
-                            ri = 0;
+                        rt[j] = r_t;
+                        ri[j] = r_i;
+                        if (c0 + j >= 0 && ++r_i > U - r_t) {
+                            r_t = min(r_t + 1, U);   // past the last cell: stay in range (never stored)
+                            r_i = 0;
                         }
                     }
                 }
                 float v4[4];
                 unsigned cfg4 = 0;
                 if (ok) {
+                    // lad[] holds byte offsets of lambda* within a row: the entry of (rt, ri)
+                    // is rt * 64 + lad[ri] bytes into tvc
+                    const unsigned char* tv = reinterpret_cast<const unsigned char*>(T.tvc);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const uint2 vc = T.tvc[(e[j] >> 16) + T.lad[e[j] & 0xFFFFu]];
+                        const uint2 vc = *reinterpret_cast<const uint2*>(tv + rt[j] * (kSlots * 8) + T.lad[ri[j]]);
                         v4[j] = __uint_as_float(vc.x);
                         cfg4 |= vc.y << (8 * j);
                     }
