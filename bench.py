@@ -494,25 +494,80 @@ def run_context(ek, h, dev, args):
     return out
 
 
+class ChunkOut:
+    """Outputs of instances [b0, b1) and queries [q0, q1): views into the full buffers."""
+
+    def __init__(self, O, b0, b1, q0, q1):
+        self.grid, self.grid_cfg = O.grid[b0:b1], O.grid_cfg[b0:b1]
+        self.lsum, self.lmean, self.lcfg = O.lsum[b0:b1], O.lmean[b0:b1], O.lcfg[b0:b1]
+        self.dec = [{k: d[k][b0:b1] for k in ("alloc", "cfg", "sum", "mean", "steps")} for d in O.dec]
+        self.est = [e[q0:q1] for e in O.est]
+        self.n = [n[q0:q1] for n in O.n]
+
+
 def run_e2e(ek, h, w, T, rows, P, O, args, world):
-    """Same step through the public API, inputs copied from pinned host memory
-    and the decisions/estimates/objectives read back, every step."""
-    host_in = {("T", k): v.cpu().pin_memory() for k, v in T.items()}
-    host_in[("rows", "")] = rows.cpu().pin_memory()
-    for k, v in P.items():
-        host_in[("P", k)] = v.cpu().pin_memory()
-    outs = [O.dec[0]["buf"], O.dec[1]["buf"], O.est[0], O.n[0], O.est[1], O.n[1], O.lsum, O.lmean]
-    host_out = [torch.empty(o.shape, dtype=o.dtype, pin_memory=True) for o in outs]
-    h2d = sum(v.numel() * v.element_size() for v in host_in.values())
-    d2h = sum(o.numel() * o.element_size() for o in outs)
+    """Same step through the public API with HOST buffers: every step copies its inputs
+    from pinned host memory and reads the decisions / estimates / objectives back.  The
+    batch is split into chunks pipelined over three CUDA streams (host->device copy of
+    chunk c+1 and device->host copy of chunk c-1 overlap the kernels of chunk c); the
+    timed region spans all of it, copies included."""
+    C = max(1, min(args.e2e_chunks, w.B, w.Q))
+    bnd = [(w.B * c // C, w.B * (c + 1) // C, w.Q * c // C, w.Q * (c + 1) // C) for c in range(C)]
+    host_T = {k: v.cpu().pin_memory() for k, v in T.items()}
+    host_rows = rows.cpu().pin_memory()
+    host_P = {k: v.cpu().pin_memory() for k, v in P.items()}
+
+    def outs_of(o):   # (device view, per-instance?) of every array read back
+        arr = [o.dec[0][k] for k in ("sum", "mean", "steps", "alloc", "cfg")]
+        arr += [o.dec[1][k] for k in ("sum", "mean", "steps", "alloc", "cfg")]
+        arr += [o.lsum, o.lmean]
+        q = [o.est[0], o.n[0], o.est[1], o.n[1]]
+        return arr, q
+
+    full_b, full_q = outs_of(O)
+    host_b = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in full_b]
+    host_q = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in full_q]
+    h2d = sum(v.numel() * v.element_size() for v in list(host_T.values()) + [host_rows] + list(host_P.values()))
+    d2h = sum(x.numel() * x.element_size() for x in full_b + full_q)
+    s_in, s_comp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event()
+    comp_done = [None] * C
+    out_done = [None] * C
 
     def e2e_step():
-        for (grp, k), v in host_in.items():
-            dst = T[k] if grp == "T" else rows if grp == "rows" else P[k]
-            dst.copy_(v, non_blocking=True)
-        run_step(ek, h, w, T, rows, P, O)
-        for o, ho in zip(outs, host_out):
-            ho.copy_(o, non_blocking=True)
+        in_ready = []
+        for c, (b0, b1, q0, q1) in enumerate(bnd):
+            with torch.cuda.stream(s_in):
+                if comp_done[c] is not None:       # the previous step's kernels of chunk c read these
+                    s_in.wait_event(comp_done[c])
+                for k in T:
+                    T[k][b0:b1].copy_(host_T[k][b0:b1], non_blocking=True)
+                rows[b0:b1].copy_(host_rows[b0:b1], non_blocking=True)
+                for k in P:
+                    P[k][q0:q1].copy_(host_P[k][q0:q1], non_blocking=True)
+                e = ev()
+                e.record(s_in)
+                in_ready.append(e)
+        for c, (b0, b1, q0, q1) in enumerate(bnd):
+            with torch.cuda.stream(s_comp):
+                s_comp.wait_event(in_ready[c])
+                if out_done[c] is not None:        # the previous step's read-back of chunk c
+                    s_comp.wait_event(out_done[c])
+                wc = Workload(b1 - b0, w.N, q1 - q0)
+                run_step(ek, h, wc, {k: v[b0:b1] for k, v in T.items()}, rows[b0:b1],
+                         {k: v[q0:q1] for k, v in P.items()}, ChunkOut(O, b0, b1, q0, q1))
+                e = ev()
+                e.record(s_comp)
+                comp_done[c] = e
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(comp_done[c])
+                for x, hx in zip(full_b, host_b):
+                    hx[b0:b1].copy_(x[b0:b1], non_blocking=True)
+                for x, hx in zip(full_q, host_q):
+                    hx[q0:q1].copy_(x[q0:q1], non_blocking=True)
+                e = ev()
+                e.record(s_out)
+                out_done[c] = e
 
     e2e_step()
     torch.cuda.synchronize()
@@ -521,10 +576,15 @@ def run_e2e(ek, h, w, T, rows, P, O, args, world):
         dist.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
+    cur = torch.cuda.current_stream()
+    t0.record(cur)
+    for st in (s_in, s_comp, s_out):
+        st.wait_event(t0)
     for _ in range(args.e2e_steps):
         e2e_step()
-    t1.record()
+    for st in (s_in, s_comp, s_out):
+        cur.wait_stream(st)
+    t1.record(cur)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=rows.device)
@@ -534,7 +594,7 @@ def run_e2e(ek, h, w, T, rows, P, O, args, world):
     ms = float(ms_t.item())
     return {"value": w.allocations() * world * args.e2e_steps / (ms / 1000.0), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": ms / args.e2e_steps, "steps": args.e2e_steps,
+            "ms_per_step": ms / args.e2e_steps, "steps": args.e2e_steps, "chunks": C,
             "read_back": "thief decisions (both modes), profile estimates+counts (both modes), LIST objectives "
                          "(sum_q32, mean); GRID/LIST config tables stay device-resident"}
 
@@ -549,6 +609,7 @@ def main():
     ap.add_argument("--n-alloc", type=int, default=synth.CONFIG4.n_alloc)
     ap.add_argument("--n-query", type=int, default=synth.CONFIG3.n_query)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunks", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-context", dest="context", action="store_false")
     ap.add_argument("--context-v100", type=int, default=16384)
