@@ -749,6 +749,49 @@ __device__ __forceinline__ u64 sum16_get(const unsigned* lo, const unsigned* hi)
     return ((u64)*hi << 16) + *lo;
 }
 
+// The changed centroids' distances for N = popcount(chg) < K: the N centroid
+// indices (ascending) are gathered first, so the class loop is straight-line code
+// over N accumulators (no per-(chunk, centroid) branch), then scattered into the
+// cache with compile-time selects.
+template <int N, int KS>
+__device__ __forceinline__ void c2_dists_n(u64 (&s)[KS], const float* x0, const float* x1, const float* mu, int C,
+                                           int CP, unsigned chg, u64 one) {
+    int idx[N];
+    unsigned m = chg;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        idx[j] = __ffs(m) - 1;
+        m &= m - 1;
+    }
+    u64 acc[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc[j] = 0ULL;
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+        const int cb = c4 * 4;
+        if (cb >= C) break;
+        u64 xp[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool in = cb + j < C;
+            xp[j] = pk2(in ? x0[cb + j] : 0.0f, in ? x1[cb + j] : 0.0f);
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const float4 mm = *reinterpret_cast<const float4*>(mu + idx[j] * CP + cb);
+            acc[j] = d2acc(acc[j], xp[0], mm.x, one);
+            acc[j] = d2acc(acc[j], xp[1], mm.y, one);
+            acc[j] = d2acc(acc[j], xp[2], mm.z, one);
+            acc[j] = d2acc(acc[j], xp[3], mm.w, one);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < KS; ++k)
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            if (idx[j] == k) s[k] = acc[j];
+}
+
 struct C2Layout {
     size_t bar, misc, cf, hist, mu, sums, cnt, dummy, total, cf_slot;
 };
@@ -870,8 +913,19 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
         int passes = 0;
         for (;;) {
             // distances of both windows to every changed centroid (rule 5 order: class ascending)
-            if (KT > 0 && chg == all_k) c2_dists<KT, KS, true>(s, x0, x1, mu, C, CP, K, chg, one);
-            else c2_dists<KT, KS, false>(s, x0, x1, mu, C, CP, K, chg, one);
+            if constexpr (KT == 5) {
+                switch (__popc(chg)) {
+                    case 0: break;   // nothing moved: the cache is exact
+                    case 1: c2_dists_n<1, KS>(s, x0, x1, mu, C, CP, chg, one); break;
+                    case 2: c2_dists_n<2, KS>(s, x0, x1, mu, C, CP, chg, one); break;
+                    case 3: c2_dists_n<3, KS>(s, x0, x1, mu, C, CP, chg, one); break;
+                    case 4: c2_dists_n<4, KS>(s, x0, x1, mu, C, CP, chg, one); break;
+                    default: c2_dists<KT, KS, true>(s, x0, x1, mu, C, CP, K, chg, one); break;
+                }
+            } else {
+                if (KT > 0 && chg == all_k) c2_dists<KT, KS, true>(s, x0, x1, mu, C, CP, K, chg, one);
+                else c2_dists<KT, KS, false>(s, x0, x1, mu, C, CP, K, chg, one);
+            }
             // nearest centroid, lowest index on ties (C19)
             {
                 float b0 = lo2(s[0]), b1 = hi2(s[0]);
