@@ -694,9 +694,12 @@ __device__ __forceinline__ u64 d2acc(u64 s, u64 x, float m, u64 one) {
 // recomputed for every centroid k in `chg` (ALL: every centroid), the others
 // keep their cached values.  Classes in chunks of 4; the padded classes of the
 // last chunk read x = 0 against the zero-padded centroid, adding fl(0 - 0)^2 = +0.
-template <int KT, int KS, bool ALL>
+// CK: also fold every loaded histogram value into the running [lo, hi] range (first pass:
+// the input check of R-ERR; fminf / fmaxf ignore NaN, which poisons the distances instead)
+template <int KT, int KS, bool ALL, bool CK = false>
 __device__ __forceinline__ void c2_dists(u64 (&s)[KS], const float* x0, const float* x1, const float* mu, int C,
-                                         int CP, int K, unsigned chg, u64 one) {
+                                         int CP, int K, unsigned chg, u64 one, float* lo = nullptr,
+                                         float* hi = nullptr) {
 #pragma unroll
     for (int k = 0; k < KS; ++k)
         if ((KT > 0 || k < K) && (ALL || ((chg >> k) & 1u))) s[k] = 0ULL;
@@ -707,12 +710,24 @@ __device__ __forceinline__ void c2_dists(u64 (&s)[KS], const float* x0, const fl
         u64 xp[4];
         if (cb + 4 <= C) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) xp[j] = pk2(x0[cb + j], x1[cb + j]);
+            for (int j = 0; j < 4; ++j) {
+                const float a = x0[cb + j], b = x1[cb + j];
+                if (CK) {
+                    *lo = fminf(*lo, fminf(a, b));
+                    *hi = fmaxf(*hi, fmaxf(a, b));
+                }
+                xp[j] = pk2(a, b);
+            }
         } else {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const bool in = cb + j < C;
-                xp[j] = pk2(in ? x0[cb + j] : 0.0f, in ? x1[cb + j] : 0.0f);
+                const float a = in ? x0[cb + j] : 0.0f, b = in ? x1[cb + j] : 0.0f;
+                if (CK) {
+                    *lo = fminf(*lo, fminf(a, b));
+                    *hi = fmaxf(*hi, fmaxf(a, b));
+                }
+                xp[j] = pk2(a, b);
             }
         }
 #pragma unroll
@@ -893,10 +908,12 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
         mbar_wait(bar, (unsigned)(i & 1));
         bool ok = true;
         for (int c = tid; c < C; c += kC2Threads) ok &= in01(cur[c]);
-        if (v0)
-            for (int c = 0; c < C; ++c) ok &= in01(x0[c]);
-        if (v1)
-            for (int c = 0; c < C; ++c) ok &= in01(x1[c]);
+        if (KT != 5) {   // K = 5: checked during the first pass's distances
+            if (v0)
+                for (int c = 0; c < C; ++c) ok &= in01(x0[c]);
+            if (v1)
+                for (int c = 0; c < C; ++c) ok &= in01(x1[c]);
+        }
         // initial centroids mu_i = h_floor(iH/K) (C19), zero padded to CP columns
         for (int t = tid; t < K * CP; t += kC2Threads) {
             const int ci = t / CP, c = t - ci * CP;
@@ -914,7 +931,14 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
         for (;;) {
             // distances of both windows to every changed centroid (rule 5 order: class ascending)
             if constexpr (KT == 5) {
-                switch (__popc(chg)) {
+                if (passes == 0) {
+                    // all K distances from the initial centroids, checking every histogram
+                    // value on the way; a NaN value makes both windows' distances NaN.  Lanes
+                    // without a second (or any) window read a duplicate row: still a real row.
+                    float lo = 1.0f, hi = 0.0f;
+                    c2_dists<KT, KS, true, true>(s, x0, x1, mu, C, CP, K, chg, one, &lo, &hi);
+                    ok &= lo >= 0.0f && hi <= 1.0f && lo2(s[0]) == lo2(s[0]) && hi2(s[0]) == hi2(s[0]);
+                } else switch (__popc(chg)) {
                     case 0: break;   // nothing moved: the cache is exact
                     case 1: c2_dists_n<1, KS>(s, x0, x1, mu, C, CP, chg, one); break;
                     case 2: c2_dists_n<2, KS>(s, x0, x1, mu, C, CP, chg, one); break;
@@ -946,25 +970,31 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
             const unsigned bm0 = __ballot_sync(0xffffffffu, v0 && na0 != oa0);
             const unsigned bm1 = __ballot_sync(0xffffffffu, v1 && na1 != oa1);
             if (passes == 0) {
+                // every window enters its first cluster: per cluster, the warp's members (ballot
+                // masks) are summed in registers -- low and high halves separately, so the
+                // shared counters keep each window's exact (v mod 2^16, v / 2^16) split that
+                // later moves subtract -- then one pair of shared adds per cluster and lane
+                const float* r0 = hs + (size_t)(warp * 32) * C + lane;
+                const float* r1 = r0 + (size_t)kC2Threads * C;
                 for (int k = 0; k < K; ++k) {
-                    const int n = __popc(__ballot_sync(0xffffffffu, v0 && na0 == k)) +
-                                  __popc(__ballot_sync(0xffffffffu, v1 && na1 == k));
-                    if (lane == 0 && n) atomicAdd(&cnt[k], n);
-                }
-#pragma unroll
-                for (int sl = 0; sl < 2; ++sl) {
-                    // the valid windows of a slot are the low lanes: no mask walk
-                    const float* rows = hs + (size_t)(warp * 32 + sl * kC2Threads) * C + lane;
-                    const int nav = sl ? na1 : na0;
-                    const int nh = __popc(sl ? bm1 : bm0);
-#pragma unroll 2
-                    for (int j = 0; j < nh; ++j) {
-                        const int n = __shfl_sync(0xffffffffu, nav, j);
-                        const u64 v = q32(rows[j * C]);
-                        const unsigned a = cbase + (unsigned)n * cstride;
-                        red_add_shared(a, (unsigned)v & 0xFFFFu);
-                        red_add_shared(a + choff, (unsigned)(v >> 16));
+                    const unsigned b0 = __ballot_sync(0xffffffffu, v0 && na0 == k);
+                    const unsigned b1 = __ballot_sync(0xffffffffu, v1 && na1 == k);
+                    if ((b0 | b1) == 0) continue;
+                    if (lane == 0) atomicAdd(&cnt[k], __popc(b0) + __popc(b1));
+                    unsigned alo = 0, ahi = 0;
+                    for (unsigned m = b0; m; m &= m - 1) {
+                        const u64 v = q32(r0[(__ffs(m) - 1) * C]);
+                        alo += (unsigned)v & 0xFFFFu;
+                        ahi += (unsigned)(v >> 16);
                     }
+                    for (unsigned m = b1; m; m &= m - 1) {
+                        const u64 v = q32(r1[(__ffs(m) - 1) * C]);
+                        alo += (unsigned)v & 0xFFFFu;
+                        ahi += (unsigned)(v >> 16);
+                    }
+                    const unsigned a = cbase + (unsigned)k * cstride;
+                    red_add_shared(a, alo);
+                    red_add_shared(a + choff, ahi);
                 }
             } else {
 #pragma unroll

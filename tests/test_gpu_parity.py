@@ -282,12 +282,14 @@ def test_profile_invalid_query(h):
     P = synth.profile_inputs(pc)
     P["hist"][2, 7, 3] = -0.5
     P["hist_acc"][4, 1, 1] = 2.0
+    P["hist"][1, 49, 26] = float("nan")       # last class of the last window
+    P["hist"][3, 0, 0] = float("inf")
     Pd = {k: v.cuda() for k, v in P.items()}
     for mode in (0, 1):
         est, n, _ = ek().profile_estimate(h, Pd["cur"], Pd["hist"], Pd["hist_acc"], Pd["fallback"], mode=mode)
         oe, on, _, bad = oracle.profile(*(P[k].numpy() for k in ("cur", "hist", "hist_acc", "fallback")),
                                         mode=mode)
-        assert bad == 2 and h.last_error() == -6
+        assert bad == 4 and h.last_error() == -6
         assert_eq(est, oe, "estimate")
         assert_eq(n, on, "n")
 
