@@ -585,7 +585,7 @@ int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, f
     if (d.n_inst == 0) return EKYA_OK;
     // the paper's shape (|Gamma| = 18, |Lambda| = 5) gets a guard-free table build
     auto kern = (d.n_gamma == 18 && d.n_lambda == 5)
-                    ? grid_kernel<19, 18, 0>
+                    ? grid_kernel<19, 18, 5>
                     : pick_gm(d.n_gamma, grid_kernel<8, 0, 0>, grid_kernel<16, 0, 0>, grid_kernel<19, 0, 0>,
                               grid_kernel<24, 0, 0>, grid_kernel<32, 0, 0>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -626,7 +626,7 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     size_t smem = p.L.total;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0 || n_alloc == 0) return EKYA_OK;
-    auto kern = fast ? list_kernel<19, 10, 18, 0, kFastU>
+    auto kern = fast ? list_kernel<19, 10, 18, 5, kFastU>
                      : pick_gm(d.n_gamma, list_kernel<8, 0, 0, 0, 0>, list_kernel<16, 0, 0, 0, 0>,
                                list_kernel<19, 0, 0, 0, 0>, list_kernel<24, 0, 0, 0, 0>, list_kernel<32, 0, 0, 0, 0>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
