@@ -359,3 +359,47 @@ def test_config3_full_batch_sampled(h):
             assert_eq(n[q:q + 1], on, f"n q={q}")
             if mode == 1:
                 assert_eq(cl[q:q + 1], ocl, f"cluster q={q}")
+
+
+def adversarial_ties(n_inst=24):
+    """Config-2 instances edited so the config choice hits every tie path: duplicated
+    gamma (exact ties -> lowest index), 1-ulp neighbours (near ties inside 2^-21), a zero
+    and a subnormal lambda factor (zero / subnormal products), post == stale (ties with the
+    no-retraining choice)."""
+    cfg = variant(synth.CONFIG2, n_inst=n_inst, a_min=0.0)   # a_MIN = 0 admits zero-accuracy lambdas
+    T = synth.sched_tables(cfg)
+    cost, post, stale, lf = T["cost"], T["post"], T["stale"], T["lam_factor"]
+    cost[:, 0, 1:4] = cost[:, 0, 0:1]
+    post[:, 0, 1:4] = post[:, 0, 0:1]
+    p1 = post[:, 1, 0:1]
+    post[:, 1, 1:2] = torch.nextafter(p1, torch.ones_like(p1))
+    post[:, 1, 2:3] = torch.nextafter(p1, torch.zeros_like(p1))
+    cost[:, 1, 1:3] = cost[:, 1, 0:1]
+    lf[:, 2, :] = 0.0
+    lf[:, 3, 1:] = 1e-39
+    post[:, 4, :] = stale[:, 4:5]
+    cost[:, 5, :] = cost[:, 5, 0:1]            # every gamma the same cost, posts differ
+    return cfg, T
+
+
+def test_ties_grid_list_thief_bitexact(h):
+    cfg, T = adversarial_ties()
+    inst = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            *args(cfg))
+    Td = {k: v.cuda() for k, v in T.items()}
+    grid, gcfg = ek().eval_grid(h, Td, *args(cfg))
+    og, ocfg, bad = oracle.eval_grid(inst)
+    assert bad == 0 and h.last_error() == 0
+    assert_eq(grid, og, "grid values")
+    assert_eq(gcfg, ocfg, "grid configs")
+    rows = synth.list_allocs(cfg, 4096)        # the many-rows LIST path (one build task per stream)
+    s, mean, c = ek().eval_list(h, Td, rows.cuda(), *args(cfg))
+    os_, om, ocf, _ = oracle.eval_list(inst, rows.numpy())
+    assert_eq(s, os_, "list sum")
+    assert_eq(c, ocf, "list cfg")
+    for mode in (0, 1):
+        a, cc, ts, tm, st = ek().thief_schedule(h, Td, *args(cfg), mode=mode)
+        oa, oc, osum, omean, osteps, _ = oracle.thief(inst, mode)
+        assert_eq(a, oa, f"thief alloc {mode}")
+        assert_eq(cc, oc, f"thief cfg {mode}")
+        assert_eq(ts, osum, f"thief sum {mode}")
