@@ -53,6 +53,17 @@ __device__ __forceinline__ int row_of(int c, int U) {
     return r;
 }
 
+__device__ __forceinline__ unsigned ld_shared_u8(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_shared_v2(unsigned a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+
 struct Tabs {
     uint8_t* lad;
     uint2* tvc;
@@ -183,7 +194,9 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
             const long long q0 = f0 >> 2;
             const int nq = (int)(((f1 + 3) >> 2) - q0);
             const uint2* qst = qs + (size_t)phi * nq_tab;
-            for (int k = lane; k < nq; k += 32) {
+            // one quad, any position / validity (edge quads shared with the neighbouring
+            // streams, invalid instances, large U without the position table)
+            auto quad_generic = [&](int k) {
                 const long long fq = (q0 + k) << 2;
                 const int c0 = 4 * k - phi;
                 // (rt, ri) of the quad's four cells
@@ -239,6 +252,42 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
                         }
                     }
                 }
+            };
+            // quads whose four cells all belong to this stream
+            const int k_lo = phi ? 1 : 0, k_hi = (NC + phi) / 4;
+            if (ok && use_qs) {
+                // interior quads: table entry -> 4 x (lambda* byte offset, entry) through 32-bit
+                // shared addresses, one 16-byte value store and one 4-byte config store, with
+                // pointers advanced by 32 quads per step
+                const unsigned lad_s = smem_addr(T.lad), tvc_s = smem_addr(T.tvc);
+                int k = k_lo + lane;
+                const uint2* qp = qst + k;
+                float4* gp = reinterpret_cast<float4*>(p.out_grid + ((q0 + k) << 2));
+                unsigned* cp = p.out_grid_cfg ? reinterpret_cast<unsigned*>(p.out_grid_cfg + ((q0 + k) << 2)) : nullptr;
+                for (; k < k_hi; k += 32, qp += 32, gp += 32) {
+                    const uint2 s2 = *qp;
+                    float v4[4];
+                    unsigned cfg4 = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const unsigned wj = j < 2 ? s2.x : s2.y;
+                        const unsigned ri = __byte_perm(wj, 0u, 0x4440u + 2u * (j & 1));
+                        const unsigned rt = __byte_perm(wj, 0u, 0x4441u + 2u * (j & 1));
+                        const unsigned lad8 = ld_shared_u8(lad_s + ri);
+                        const uint2 vc = ld_shared_v2(tvc_s + rt * (kSlots * 8) + lad8);
+                        v4[j] = __uint_as_float(vc.x);
+                        cfg4 |= vc.y << (8 * j);
+                    }
+                    *gp = make_float4(v4[0], v4[1], v4[2], v4[3]);
+                    if (cp) {
+                        *cp = cfg4;
+                        cp += 32;
+                    }
+                }
+                if (lane == 0 && k_lo > 0) quad_generic(0);
+                for (int kk = k_hi + lane; kk < nq; kk += 32) quad_generic(kk);
+            } else {
+                for (int kk = lane; kk < nq; kk += 32) quad_generic(kk);
             }
             __syncwarp();
         }
