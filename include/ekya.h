@@ -120,7 +120,7 @@ typedef struct {
  *   out_grid_cfg[b][v][c] = its argmax config byte, cell c = rowstart(rt) + ri,
  *   rowstart(rt) = rt*(U+1) - rt*(rt-1)/2, i.e. (U+1)(U+2)/2 cells per stream
  *   (north star "for every v, gamma, lambda and (r_train, r_infer) ... per-stream
- *   argmax").  GRID needs one stream's tables, 65 (U+1) + ~450 bytes, in shared
+ *   argmax").  GRID needs one stream's tables, 68 (U+1) + ~600 bytes, in shared
  *   memory (U <~ 3400 on B200), else EKYA_ERR_SHAPE.  GRID writes whole 16-byte
  *   value quads: out_grid must be 16-byte aligned and out_grid_cfg 4-byte
  *   aligned; LIST reads rows as 4/8-byte words: alloc must be 4-byte aligned

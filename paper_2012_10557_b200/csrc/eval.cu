@@ -34,6 +34,10 @@ constexpr int kListThreads = 1024;
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // per-stream table footprint: lad[U+1] + tvc[U+1][rs] (8-byte entries)
+// GRID: lad[U+1] (u32 byte offsets of the lambda blocks) + tvc[8][U+1] (lambda-major)
+__host__ __device__ inline size_t grid_tab_bytes(int U) {
+    return a16((size_t)(U + 1) * 4) + a16((size_t)(U + 1) * kSlots * 8);
+}
 __host__ __device__ inline size_t tab_bytes(int U, int rs = kSlots) {
     return a16((size_t)(U + 1)) + a16((size_t)(U + 1) * rs * 8);
 }
@@ -58,10 +62,26 @@ __device__ __forceinline__ unsigned ld_shared_u8(unsigned a) {
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
+__device__ __forceinline__ unsigned ld_shared_u32(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint2 ld_shared_v2(unsigned a) {
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
     return v;
+}
+
+struct GridTabs {
+    uint32_t* lad;
+    uint2* tvc;
+};
+__device__ __forceinline__ GridTabs carve_grid_tabs(unsigned char* p, int U) {
+    GridTabs t;
+    t.lad = reinterpret_cast<uint32_t*>(p);
+    t.tvc = reinterpret_cast<uint2*>(p + a16((size_t)(U + 1) * 4));
+    return t;
 }
 
 struct Tabs {
@@ -157,7 +177,7 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
     uint2* qs = reinterpret_cast<uint2*>(smem);
     unsigned char* mine = smem + (use_qs ? a16(4 * nq_tab * sizeof(uint2)) : 0) + (size_t)warp * p.warp_bytes;
     StreamIn* sin = reinterpret_cast<StreamIn*>(mine);
-    Tabs T = carve_tabs(mine + a16(sizeof(StreamIn)), U);
+    GridTabs T = carve_grid_tabs(mine + a16(sizeof(StreamIn)), U);
     const int NC = (U + 1) * (U + 2) / 2;
 
     for (int t = threadIdx.x; use_qs && t < (int)(4 * nq_tab); t += blockDim.x) {
@@ -182,7 +202,8 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
             const long long item = b * V + v;
             if (ok) {
                 warp_load_stream(sin, p.t, item, nG, nL);
-                warp_build_tables<GM, NGT, NLT, kSlots, 8>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad, T.tvc);
+                warp_build_tables<GM, NGT, NLT, kSlots, 1, true>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad,
+                                                                 T.tvc);
             }
             // Flat write of the stream's cells [f0, f0 + NC) in aligned quads of 4
             // cells: one 16-B value store + one 4-B config store per quad (the
@@ -226,12 +247,12 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
                 float v4[4];
                 unsigned cfg4 = 0;
                 if (ok) {
-                    // lad[] holds byte offsets of lambda* within a row: the entry of (rt, ri)
-                    // is rt * 64 + lad[ri] bytes into tvc
+                    // lad[] holds the byte offset of lambda*'s block: the entry of (rt, ri) is
+                    // lad[ri] + rt * 8 bytes into tvc
                     const unsigned char* tv = reinterpret_cast<const unsigned char*>(T.tvc);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const uint2 vc = *reinterpret_cast<const uint2*>(tv + rt[j] * (kSlots * 8) + T.lad[ri[j]]);
+                        const uint2 vc = *reinterpret_cast<const uint2*>(tv + T.lad[ri[j]] + rt[j] * 8);
                         v4[j] = __uint_as_float(vc.x);
                         cfg4 |= vc.y << (8 * j);
                     }
@@ -273,8 +294,8 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
                         const unsigned wj = j < 2 ? s2.x : s2.y;
                         const unsigned ri = __byte_perm(wj, 0u, 0x4440u + 2u * (j & 1));
                         const unsigned rt = __byte_perm(wj, 0u, 0x4441u + 2u * (j & 1));
-                        const unsigned lad8 = ld_shared_u8(lad_s + ri);
-                        const uint2 vc = ld_shared_v2(tvc_s + rt * (kSlots * 8) + lad8);
+                        const unsigned lo = ld_shared_u32(lad_s + 4 * ri);
+                        const uint2 vc = ld_shared_v2(tvc_s + lo + rt * 8);
                         v4[j] = __uint_as_float(vc.x);
                         cfg4 |= vc.y << (8 * j);
                     }
@@ -621,7 +642,7 @@ int launch_eval_grid(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, f
     p.st = h->dstate;
     p.out_grid = out_grid;
     p.out_grid_cfg = out_grid_cfg;
-    p.warp_bytes = a16(sizeof(StreamIn)) + tab_bytes(d.units);
+    p.warp_bytes = a16(sizeof(StreamIn)) + grid_tab_bytes(d.units);
     // the position table (16 B per 4 cells of a stream) is staged only while it
     // leaves room for all warps' tables; beyond that each quad locates its row
     // arithmetically, and large U runs fewer warps per CTA (>= 1)
