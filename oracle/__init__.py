@@ -95,6 +95,14 @@ def lib():
         L.orc_bruteforce.argtypes = [ctypes.POINTER(Dims), P, P, P, P, P, P, P, P]
         L.orc_profile.restype = ctypes.c_int64
         L.orc_profile.argtypes = [ctypes.POINTER(ProfileDims), P, P, P, P, P, P, P]
+        L.orc_quantize_frac.argtypes = [ctypes.c_int64, ctypes.c_int32]
+        L.orc_quantize_frac.restype = ctypes.c_int32
+        L.orc_pack.argtypes = [ctypes.c_int32, P, ctypes.c_int32, P, P]
+        L.orc_pack.restype = ctypes.c_int64
+        L.orc_place.argtypes = [ctypes.c_int32] * 4 + [P] * 6
+        L.orc_place.restype = ctypes.c_int64
+        L.orc_checkpoint.argtypes = [ctypes.c_int64] + [P] * 8
+        L.orc_checkpoint.restype = ctypes.c_int64
     return _lib
 
 
@@ -296,3 +304,46 @@ def profile(cur, hist, hist_acc, fallback, mode=RADIUS, tau=0.2, k=5, max_iter=1
     if bad < 0:
         raise ValueError("oracle: invalid profile dims")
     return est, n, (cl if mode == CLUSTER else None), int(bad)
+
+
+Q_ONE = 65536   # one GPU in quanta of 2^-16 GPU (placement outputs)
+
+
+def quantize_frac(r: int, units: int) -> int:
+    """PL1: fractional GPU share r/U quantized down to 2^-k, in 2^-16 quanta."""
+    return int(lib().orc_quantize_frac(int(r), int(units)))
+
+
+def pack(q, gpus: int):
+    """S:333-339 first-fit decreasing of demands q (2^-16 GPU quanta); returns (gpu per job, load)."""
+    q = _c(q, np.uint32).reshape(-1)
+    g = np.zeros(q.size, np.int16)
+    load = np.zeros(gpus, np.uint32)
+    lib().orc_pack(q.size, _p(q), gpus, _p(g), _p(load))
+    return g, load
+
+
+def place(alloc, units: int, gpus: int):
+    """Placement onto GPUs (readings PL1-PL3).  alloc [B][J] u16.
+    Returns piece_job [B][J+G] u16, piece_q [B][J+G] u32, piece_gpu [B][J+G] i16,
+    n_pieces [B] u16, gpu_load [B][G] u32, bad."""
+    alloc = _c(alloc, np.uint16)
+    B, J = alloc.shape
+    P = J + gpus
+    pj = np.zeros((B, P), np.uint16)
+    pq = np.zeros((B, P), np.uint32)
+    pg = np.zeros((B, P), np.int16)
+    npc = np.zeros(B, np.uint16)
+    load = np.zeros((B, gpus), np.uint32)
+    bad = lib().orc_place(B, J, units, gpus, _p(alloc), _p(pj), _p(pq), _p(pg), _p(npc), _p(load))
+    if bad < 0:
+        raise ValueError("oracle: invalid placement dims")
+    return pj, pq, pg, npc, load, int(bad)
+
+
+def checkpoint(tau, t, T, a, a_star, A, delta_ckpt):
+    """Checkpoint decision (draft P:62-81, reading CK1): (tau-t)(a*-a) > delta A."""
+    arrs = [_c(x, np.float32).reshape(-1) for x in (tau, t, T, a, a_star, A, delta_ckpt)]
+    out = np.zeros(arrs[0].size, np.uint8)
+    bad = lib().orc_checkpoint(arrs[0].size, *(_p(x) for x in arrs), _p(out))
+    return out, int(bad)

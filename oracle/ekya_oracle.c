@@ -605,3 +605,139 @@ int64_t orc_profile(const orc_profile_dims* p, const float* cur, const float* hi
     free(cnt);
     return bad;
 }
+
+/* ========================================================================
+ * NEXT-4: placement onto GPUs and the checkpoint decision.
+ * ======================================================================== */
+
+/* PL1: the fractional part r/U of a GPU (0 < r < U) quantized DOWN to the largest
+ * inverse power of two 2^-k, k >= 1 ("quantizes the allocations to inverse powers of
+ * two (e.g. 1/2, 1/4, 1/8)"; "largest value 2^(-k) <= share, round down; never
+ * over-subscribes").  Exact integer test: 2^-k <= r/U  <=>  U <= r 2^k.
+ * Returned in quanta of 2^-16 GPU; U <= 65534 < 2^16 guarantees k <= 16. */
+int32_t orc_quantize_frac(int64_t r, int32_t U)
+{
+    if (r <= 0 || r >= U) return 0;
+    int k = 1;
+    while ((r << k) < (int64_t)U) ++k;
+    return (int32_t)(ORC_Q_ONE >> k);
+}
+
+typedef struct { int32_t job, piece; uint32_t q; } orc_piece;
+
+/* descending demand, then ascending job id, then piece index */
+static int orc_piece_cmp(const void* x, const void* y)
+{
+    const orc_piece* a = (const orc_piece*)x;
+    const orc_piece* b = (const orc_piece*)y;
+    if (a->q != b->q) return a->q > b->q ? -1 : 1;
+    if (a->job != b->job) return a->job < b->job ? -1 : 1;
+    return a->piece < b->piece ? -1 : (a->piece > b->piece);
+}
+
+/* PL2 first-fit decreasing of `np` pieces already sorted by orc_piece_cmp onto `gpus`
+ * GPUs of capacity one GPU (ORC_Q_ONE quanta): each piece goes to the lowest-index GPU it
+ * still fits in, else it is unplaced (-1). */
+static void orc_ffd(const orc_piece* pc, int32_t np, int32_t gpus, int16_t* gpu_out, uint32_t* load)
+{
+    for (int32_t g = 0; g < gpus; ++g) load[g] = 0;
+    for (int32_t i = 0; i < np; ++i) {
+        gpu_out[i] = -1;
+        for (int32_t g = 0; g < gpus; ++g) {
+            if (load[g] + pc[i].q <= ORC_Q_ONE) { gpu_out[i] = (int16_t)g; load[g] += pc[i].q; break; }
+        }
+    }
+}
+
+/* S:333-339 pack() on its own (pinned with the spec's examples): demands in quanta,
+ * job ids = input order; outputs per input job its GPU (-1 unplaced) and the loads. */
+int64_t orc_pack(int32_t n, const uint32_t* q, int32_t gpus, int16_t* gpu_of_job, uint32_t* load)
+{
+    if (n < 0 || gpus < 1) return -1;
+    orc_piece* pc = (orc_piece*)malloc(sizeof(orc_piece) * (size_t)(n > 0 ? n : 1));
+    int16_t* go = (int16_t*)malloc(sizeof(int16_t) * (size_t)(n > 0 ? n : 1));
+    for (int32_t i = 0; i < n; ++i) { pc[i].job = i; pc[i].piece = 0; pc[i].q = q[i]; }
+    qsort(pc, (size_t)n, sizeof(orc_piece), orc_piece_cmp);
+    orc_ffd(pc, n, gpus, go, load);
+    for (int32_t i = 0; i < n; ++i) gpu_of_job[pc[i].job] = go[i];
+    free(pc);
+    free(go);
+    return 0;
+}
+
+/* Placement of every instance's job allocations (units) onto `gpus` GPUs.
+ * PL1: job j with a_j units holds a_j G / U GPUs (delta = G/U GPU per unit):
+ *      floor(a_j G / U) whole GPUs, each a piece of one GPU, plus the remainder
+ *      quantized down to 2^-k (orc_quantize_frac) as one more piece if non-zero.
+ * PL2: pieces sorted by descending demand, ties by job id then piece index;
+ *      first fit over GPUs 0..G-1 (capacity one GPU, in quanta); a piece that fits
+ *      nowhere is unplaced (gpu -1).
+ * PL3: outputs per instance: the sorted pieces (job, quanta, gpu) -- at most J + G
+ *      of them when sum a_j <= U -- their count, and the per-GPU load in quanta.
+ * Rows with sum a_j > U are data errors (R-ERR): zero pieces, counted. */
+int64_t orc_place(int32_t n_inst, int32_t n_jobs, int32_t units, int32_t gpus, const uint16_t* alloc,
+                  uint16_t* piece_job, uint32_t* piece_q, int16_t* piece_gpu, uint16_t* n_pieces,
+                  uint32_t* gpu_load)
+{
+    if (n_inst < 0 || n_jobs < 1 || units < 1 || units > 65534 || gpus < 1) return -1;
+    const int32_t P = n_jobs + gpus;
+    orc_piece* pc = (orc_piece*)malloc(sizeof(orc_piece) * (size_t)P);
+    uint32_t* load = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)gpus);
+    int64_t bad = 0;
+    for (int64_t b = 0; b < n_inst; ++b) {
+        const uint16_t* a = alloc + b * n_jobs;
+        int64_t tot = 0;
+        for (int32_t j = 0; j < n_jobs; ++j) tot += a[j];
+        int32_t np = 0;
+        if (tot > units) {
+            ++bad;
+        } else {
+            for (int32_t j = 0; j < n_jobs; ++j) {
+                const int64_t share = (int64_t)a[j] * gpus;           /* in 1/U GPU */
+                const int64_t whole = share / units, r = share % units;
+                for (int64_t w = 0; w < whole; ++w) {
+                    pc[np].job = j; pc[np].piece = (int32_t)w; pc[np].q = ORC_Q_ONE; ++np;
+                }
+                const int32_t fq = orc_quantize_frac(r, units);
+                if (fq > 0) {
+                    pc[np].job = j; pc[np].piece = (int32_t)whole; pc[np].q = (uint32_t)fq; ++np;
+                }
+            }
+            qsort(pc, (size_t)np, sizeof(orc_piece), orc_piece_cmp);
+        }
+        orc_ffd(pc, np, gpus, piece_gpu + b * P, load);
+        for (int32_t i = 0; i < P; ++i) {
+            piece_job[b * P + i] = i < np ? (uint16_t)pc[i].job : 0;
+            piece_q[b * P + i] = i < np ? pc[i].q : 0;
+            if (i >= np) piece_gpu[b * P + i] = -1;
+        }
+        n_pieces[b] = (uint16_t)np;
+        if (gpu_load)
+            for (int32_t g = 0; g < gpus; ++g) gpu_load[b * gpus + g] = load[g];
+    }
+    free(pc);
+    free(load);
+    return bad;
+}
+
+/* CK1: checkpoint now iff acc > base_acc (draft P:74-81) with
+ *   base_acc = ((tau-t) a + (T-tau) A) / T,  acc = ((tau-t) a* + (T-tau-delta) A) / T,
+ * i.e. (tau-t)(a*-a) > delta A ("equivalently"): evaluated in that form, one
+ * binary32 rounding per operation.  Elements violating 0 <= t <= tau <= T, T > 0,
+ * accuracies in [0,1], delta >= 0 are data errors (decision 0, counted). */
+int64_t orc_checkpoint(int64_t n, const float* tau, const float* t, const float* T, const float* a,
+                       const float* a_star, const float* A, const float* delta_ckpt, uint8_t* out)
+{
+    int64_t bad = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const int ok = T[i] > 0.0f && t[i] >= 0.0f && t[i] <= tau[i] && tau[i] <= T[i] &&
+                       orc_in01(a[i]) && orc_in01(a_star[i]) && orc_in01(A[i]) && delta_ckpt[i] >= 0.0f;
+        if (!ok) { ++bad; out[i] = 0; continue; }
+        const float rem = tau[i] - t[i];
+        const float gain = a_star[i] - a[i];
+        const float lhs = rem * gain;
+        const float rhs = delta_ckpt[i] * A[i];
+        out[i] = lhs > rhs;
+    }
+    return bad;
+}

@@ -69,6 +69,17 @@ int64_t orc_profile(const orc_profile_dims* p, const float* cur, const float* hi
                     const float* hist_acc, const float* fallback,
                     float* out_est, int32_t* out_n, int32_t* out_cluster);
 
+/* ---- NEXT-4: placement of decisions onto GPUs and the
+ *      checkpoint decision (draft P:62-81); readings PL1-PL3, CK1 ---- */
+#define ORC_Q_ONE 65536   /* one GPU in quanta of 2^-16 GPU */
+int32_t orc_quantize_frac(int64_t r, int32_t U);   /* largest 2^-k (k >= 1) <= r/U, in quanta */
+int64_t orc_pack(int32_t n, const uint32_t* q, int32_t gpus, int16_t* gpu_of_job, uint32_t* load);
+int64_t orc_place(int32_t n_inst, int32_t n_jobs, int32_t units, int32_t gpus, const uint16_t* alloc,
+                  uint16_t* piece_job, uint32_t* piece_q, int16_t* piece_gpu, uint16_t* n_pieces,
+                  uint32_t* gpu_load);
+int64_t orc_checkpoint(int64_t n, const float* tau, const float* t, const float* T, const float* a,
+                       const float* a_star, const float* A, const float* delta_ckpt, uint8_t* out);
+
 #ifdef __cplusplus
 }
 #endif

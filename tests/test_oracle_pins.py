@@ -524,3 +524,118 @@ def test_cluster_on_synth_converges_to_fixed_point():
         for h in range(500):
             d = {i: ((P["hist"][q, h] - mu[i]) ** 2).sum() for i in present}
             assert d[a[h]] <= min(d.values()) + 1e-6
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: placement onto GPUs and checkpointing
+# ---------------------------------------------------------------------------
+def test_quantize_spec_examples():
+    """0.5 -> 0.5, 0.3 -> 0.25, 1.0 -> 1.0 (a whole GPU)."""
+    Q = oracle.Q_ONE
+    assert oracle.quantize_frac(5, 10) == Q // 2
+    assert oracle.quantize_frac(3, 10) == Q // 4
+    pj, pq, pg, npc, load, bad = oracle.place(np.array([[10]], np.uint16), 10, 1)
+    assert npc[0] == 1 and pq[0, 0] == Q and pg[0, 0] == 0 and bad == 0
+
+
+def test_quantize_is_largest_inverse_power_of_two_below():
+    """Exact-rational definition: 2^-k <= r/U < 2^-(k-1), k >= 1, for every r < U."""
+    from fractions import Fraction
+    rng = np.random.default_rng(11)
+    for U in [1, 2, 3, 7, 10, 80, 800, 65534]:
+        for r in set(list(range(1, min(U, 40))) + list(rng.integers(1, max(2, U), 40))):
+            if not 0 < r < U:
+                continue
+            q = Fraction(oracle.quantize_frac(int(r), U), oracle.Q_ONE)
+            x = Fraction(int(r), U)
+            assert q <= x < 2 * q and q.numerator == 1 and (q.denominator & (q.denominator - 1)) == 0
+
+
+def test_pack_spec_examples():
+    """S:337-339 (first-fit decreasing)."""
+    Q = oracle.Q_ONE
+    g, load = oracle.pack(np.array([Q // 2] * 4), 2)
+    assert sorted(g.tolist()) == [0, 0, 1, 1] and load.tolist() == [Q, Q]
+    g, load = oracle.pack(np.array([Q // 2, Q // 4, Q // 4, Q // 4, Q // 4, Q // 2]), 2)
+    assert (g >= 0).all() and load.tolist() == [Q, Q]
+    g, load = oracle.pack(np.array([Q, Q, Q // 2]), 2)
+    assert g.tolist() == [0, 1, -1]
+
+
+def test_pack_invariants_fuzzed():
+    """Per-GPU load <= 1 GPU; every unplaced piece fits no GPU's final free space; with
+    power-of-two pieces whose total fits, first-fit decreasing places all of them."""
+    Q = oracle.Q_ONE
+    rng = np.random.default_rng(12)
+    for _ in range(300):
+        n, G = int(rng.integers(1, 30)), int(rng.integers(1, 9))
+        q = (Q >> rng.integers(0, 8, n)).astype(np.uint32)
+        g, load = oracle.pack(q, G)
+        assert (load <= Q).all()
+        for i in np.flatnonzero(g < 0):
+            assert (load + q[i] > Q).all()
+        for gg in range(G):
+            assert load[gg] == q[g == gg].sum()
+        if q.sum() <= G * Q:
+            assert (g >= 0).all()
+
+
+def test_place_pieces_follow_pl1():
+    """PL1 exactly (fractions): floor(a G / U) whole GPUs plus the remainder quantized down;
+    total quantized <= total share; everything placed when sum a <= U (power-of-two pieces)."""
+    from fractions import Fraction
+    rng = np.random.default_rng(13)
+    for _ in range(200):
+        J, U, G = int(rng.integers(1, 24)), int(rng.integers(1, 200)), int(rng.integers(1, 12))
+        w = rng.integers(0, 5, J)
+        a = np.floor(w / max(1, w.sum()) * U).astype(np.uint16)
+        pj, pq, pg, npc, load, bad = oracle.place(a[None, :], U, G)
+        assert bad == 0
+        n = int(npc[0])
+        assert n <= J + G and (pg[0, :n] >= 0).all()
+        for j in range(J):
+            share = Fraction(int(a[j]) * G, U)
+            got = [Fraction(int(x), oracle.Q_ONE) for x in pq[0, :n][pj[0, :n] == j]]
+            whole = [x for x in got if x == 1]
+            frac = [x for x in got if x < 1]
+            assert len(whole) == int(share)
+            rem = share - int(share)
+            assert len(frac) == (1 if rem > 0 else 0)
+            if frac:
+                assert frac[0] <= rem < 2 * frac[0]
+        assert sum(int(x) for x in pq[0, :n]) <= sum(int(x) for x in a) * G * oracle.Q_ONE // U + 1
+    pj, pq, pg, npc, load, bad = oracle.place(np.array([[9, 9]], np.uint16), 16, 2)
+    assert bad == 1 and npc[0] == 0                    # sum > U: data error
+
+
+def test_checkpoint_spec_examples():
+    """S:347-349."""
+    out, bad = oracle.checkpoint([30], [20], [100], [0.5], [0.6], [0.9], [0.0])
+    assert out[0] == 1 and bad == 0                    # free checkpoint with any gain
+    out, bad = oracle.checkpoint([30], [20], [100], [0.5], [0.6], [0.9], [2.0])
+    assert out[0] == 0                                 # 10 * 0.1 = 1.0 > 1.8 is false
+    out, bad = oracle.checkpoint([30], [20], [100], [0.7], [0.7], [0.9], [0.5])
+    assert out[0] == 0                                 # a* = a, positive cost
+
+
+def test_checkpoint_matches_the_averaged_accuracy_form():
+    """acc > base_acc in exact rationals agrees with the oracle's simplified form
+    wherever the two sides differ by more than 1e-5 (rounding can only flip near ties)."""
+    from fractions import Fraction as F
+    rng = np.random.default_rng(14)
+    n = 4000
+    T = rng.uniform(10, 300, n).astype(np.float32)
+    tau = (T * rng.uniform(0, 1, n)).astype(np.float32)
+    t = (tau * rng.uniform(0, 1, n)).astype(np.float32)
+    a, ast, A = (rng.uniform(0, 1, n).astype(np.float32) for _ in range(3))
+    dl = rng.uniform(0, 20, n).astype(np.float32)
+    out, bad = oracle.checkpoint(tau, t, T, a, ast, A, dl)
+    assert bad == 0
+    for i in range(n):
+        Ti, ti, taui = F(float(T[i])), F(float(t[i])), F(float(tau[i]))
+        base = ((taui - ti) * F(float(a[i])) + (Ti - taui) * F(float(A[i]))) / Ti
+        acc = ((taui - ti) * F(float(ast[i])) + (Ti - taui - F(float(dl[i]))) * F(float(A[i]))) / Ti
+        if abs(acc - base) > F(1, 100000):
+            assert out[i] == (acc > base)
+    out, bad = oracle.checkpoint([10], [20], [100], [0.5], [0.6], [0.9], [1.0])
+    assert bad == 1 and out[0] == 0                    # t > tau: data error
