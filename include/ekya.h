@@ -192,6 +192,37 @@ int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p,
  * ekya_gather_decisions: root_buf[r*bytes_per_rank ...] <- rank r's `local`
  *   (device pointers; root_buf used on the root only), enqueued on `stream`.
  * ------------------------------------------------------------------------- */
+/* ---------------------------------------------------------------------------
+ * ekya_place -- placement of scheduling decisions onto discrete GPUs (SURVEY 8(f)
+ * NEXT-4; "quantizes the allocations to inverse powers of two ...
+ * allocates jobs to GPUs in descending order of demands").
+ * alloc [B][n_jobs] u16: units per job (e.g. ekya_thief_schedule's out_alloc),
+ *   U = units, G = gpus (one unit = G/U GPU).  Readings:
+ *   PL1 job j holds a_j G / U GPUs exactly: floor(a_j G / U) whole-GPU pieces plus
+ *       the remainder r/U quantized DOWN to the largest 2^-k (k >= 1), as one more
+ *       piece; demands in quanta of 2^-16 GPU (a whole GPU = 65536).
+ *   PL2 first-fit decreasing: pieces by descending demand, ties by job then piece,
+ *       each to the lowest-index GPU with room (capacity 65536), else unplaced.
+ *   PL3 per instance, in that order: out_piece_job [B][n_jobs+G] u16,
+ *       out_piece_q [B][n_jobs+G] u32, out_piece_gpu [B][n_jobs+G] i16 (-1 =
+ *       unplaced or unused), out_n_pieces [B] u16, out_gpu_load [B][G] u32 (quanta;
+ *       may be NULL).  Slots past n_pieces: job 0, 0 quanta, gpu -1.
+ *   A row with sum a_j > U is a data error (R-ERR): zero pieces, error word set.
+ * Limits: 1 <= U <= 65534, 1 <= G <= 128, n_jobs + G <= 4096 (EKYA_ERR_LIMIT).
+ *
+ * ekya_checkpoint_decide -- the checkpoint decision of draft P:62-81 for n
+ * independent (stream, time) points: out[i] = 1 iff acc > base_acc,
+ * evaluated as fl(fl(tau-t) fl(a*-a)) > fl(delta A) (reading CK1; the averaged
+ * accuracies differ by that amount over T).  Points violating 0 <= t <= tau <= T,
+ * T > 0, accuracies in [0,1] or delta >= 0 are data errors (out = 0).
+ * ------------------------------------------------------------------------- */
+int ekya_place(ekya_handle* h, int32_t n_inst, int32_t n_jobs, int32_t units, int32_t gpus,
+               const uint16_t* alloc, uint16_t* out_piece_job, uint32_t* out_piece_q, int16_t* out_piece_gpu,
+               uint16_t* out_n_pieces, uint32_t* out_gpu_load, ekya_stream_t stream);
+int ekya_checkpoint_decide(ekya_handle* h, int64_t n, const float* tau, const float* t, const float* T,
+                           const float* a, const float* a_star, const float* A, const float* delta_ckpt,
+                           uint8_t* out, ekya_stream_t stream);
+
 int ekya_comm_unique_id(void* out_id_128_bytes);
 int ekya_comm_init(ekya_handle* h, const void* id_128_bytes, int nranks, int rank);
 int ekya_gather_decisions(ekya_handle* h, const void* local, size_t bytes_per_rank,

@@ -155,4 +155,28 @@ int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p, const floa
                           reinterpret_cast<cudaStream_t>(stream));
 }
 
+int ekya_place(ekya_handle* h, int32_t n_inst, int32_t n_jobs, int32_t units, int32_t gpus,
+               const uint16_t* alloc, uint16_t* out_piece_job, uint32_t* out_piece_q, int16_t* out_piece_gpu,
+               uint16_t* out_n_pieces, uint32_t* out_gpu_load, ekya_stream_t stream) {
+    if (!h) return EKYA_ERR_ARG;
+    if (n_inst < 0 || n_jobs < 1) return EKYA_ERR_SHAPE;
+    if (units < 1 || units > 65534 || gpus < 1 || gpus > 128 || n_jobs + gpus > 4096) return EKYA_ERR_LIMIT;
+    if (n_inst > 0 && (!alloc || !out_piece_job || !out_piece_q || !out_piece_gpu || !out_n_pieces))
+        return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    return launch_place(h, n_inst, n_jobs, units, gpus, alloc, out_piece_job, out_piece_q, out_piece_gpu,
+                        out_n_pieces, out_gpu_load, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ekya_checkpoint_decide(ekya_handle* h, int64_t n, const float* tau, const float* t, const float* T,
+                           const float* a, const float* a_star, const float* A, const float* delta_ckpt,
+                           uint8_t* out, ekya_stream_t stream) {
+    if (!h) return EKYA_ERR_ARG;
+    if (n < 0) return EKYA_ERR_SHAPE;
+    if (n > 0 && (!tau || !t || !T || !a || !a_star || !A || !delta_ckpt || !out)) return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    return launch_checkpoint(h, (long long)n, tau, t, T, a, a_star, A, delta_ckpt, out,
+                             reinterpret_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

@@ -57,11 +57,6 @@ __device__ __forceinline__ int row_of(int c, int U) {
     return r;
 }
 
-__device__ __forceinline__ unsigned ld_shared_u8(unsigned a) {
-    unsigned v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
 __device__ __forceinline__ unsigned ld_shared_u32(unsigned a) {
     unsigned v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -88,12 +83,6 @@ struct Tabs {
     uint8_t* lad;
     uint2* tvc;
 };
-__device__ __forceinline__ Tabs carve_tabs(unsigned char* p, int U) {
-    Tabs t;
-    t.lad = p;
-    t.tvc = reinterpret_cast<uint2*>(p + a16((size_t)(U + 1)));
-    return t;
-}
 
 // Instance inputs (stale, cost, post, lam_min_units, lam_factor of one
 // instance), staged by the TMA one instance ahead (double buffer).

@@ -33,6 +33,13 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
                    const float* hist_acc, const float* fallback, float* out_est, int32_t* out_n,
                    int32_t* out_cluster, cudaStream_t s);
 
+int launch_place(ekya_handle* h, int32_t n_inst, int32_t n_jobs, int32_t units, int32_t gpus,
+                 const uint16_t* alloc, uint16_t* piece_job, uint32_t* piece_q, int16_t* piece_gpu,
+                 uint16_t* n_pieces, uint32_t* gpu_load, cudaStream_t s);
+int launch_checkpoint(ekya_handle* h, long long n, const float* tau, const float* t, const float* T,
+                      const float* a, const float* a_star, const float* A, const float* delta, uint8_t* out,
+                      cudaStream_t s);
+
 inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? EKYA_OK : EKYA_ERR_CUDA; }
 
 }  // namespace ekya

@@ -752,10 +752,6 @@ __device__ __forceinline__ void sum16_add(unsigned* lo, unsigned* hi, u64 v) {
     atomicAdd(lo, (unsigned)(v & 0xFFFFu));
     atomicAdd(hi, (unsigned)(v >> 16));
 }
-__device__ __forceinline__ void sum16_sub(unsigned* lo, unsigned* hi, u64 v) {
-    atomicSub(lo, (unsigned)(v & 0xFFFFu));
-    atomicSub(hi, (unsigned)(v >> 16));
-}
 // red.shared.add.u32 at a shared-window address
 __device__ __forceinline__ void red_add_shared(unsigned addr, unsigned v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");

@@ -25,7 +25,8 @@ PROFILE_RADIUS, PROFILE_CLUSTER = 0, 1
 LAMBDA_NONE = 7
 SYMBOLS = ["ekya_create", "ekya_destroy", "ekya_last_error", "ekya_launch_count", "ekya_version",
            "ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate",
-           "ekya_comm_unique_id", "ekya_comm_init", "ekya_gather_decisions", "ekya_counters"]
+           "ekya_comm_unique_id", "ekya_comm_init", "ekya_gather_decisions", "ekya_counters", "ekya_place",
+           "ekya_checkpoint_decide"]
 
 
 class EkyaError(RuntimeError):
@@ -87,6 +88,10 @@ def load_library(path: str = LIB_PATH):
     L.ekya_thief_schedule.restype = ctypes.c_int
     L.ekya_profile_estimate.argtypes = [P, ctypes.POINTER(ProfileDims), P, P, P, P, P, P, P, P]
     L.ekya_profile_estimate.restype = ctypes.c_int
+    L.ekya_place.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P]
+    L.ekya_place.restype = ctypes.c_int
+    L.ekya_checkpoint_decide.argtypes = [P, ctypes.c_int64] + [P] * 8 + [P]
+    L.ekya_checkpoint_decide.restype = ctypes.c_int
     L.ekya_comm_unique_id.argtypes = [P]
     L.ekya_comm_unique_id.restype = ctypes.c_int
     L.ekya_comm_init.argtypes = [P, P, ctypes.c_int, ctypes.c_int]
@@ -218,6 +223,27 @@ def ekya_profile_estimate(h: Handle, pdims: ProfileDims, cur, hist, hist_acc, fa
     _check(code, "ekya_profile_estimate")
 
 
+def ekya_place(h: Handle, units: int, gpus: int, alloc, out_piece_job, out_piece_q, out_piece_gpu, out_n_pieces,
+               out_gpu_load=None, stream=None):
+    L = load_library()
+    B, J = alloc.shape
+    code = L.ekya_place(h.ptr, B, J, units, gpus, _ptr(alloc, torch.uint16, "alloc"),
+                        _ptr(out_piece_job, torch.uint16, "out_piece_job"),
+                        _ptr(out_piece_q, torch.uint32, "out_piece_q"),
+                        _ptr(out_piece_gpu, torch.int16, "out_piece_gpu"),
+                        _ptr(out_n_pieces, torch.uint16, "out_n_pieces"),
+                        _ptr(out_gpu_load, torch.uint32, "out_gpu_load", True), _stream(stream))
+    _check(code, "ekya_place")
+
+
+def ekya_checkpoint_decide(h: Handle, tau, t, T, a, a_star, A, delta_ckpt, out, stream=None):
+    L = load_library()
+    args = [_ptr(x, torch.float32, nm) for x, nm in ((tau, "tau"), (t, "t"), (T, "T"), (a, "a"),
+                                                   (a_star, "a_star"), (A, "A"), (delta_ckpt, "delta_ckpt"))]
+    code = L.ekya_checkpoint_decide(h.ptr, out.numel(), *args, _ptr(out, torch.uint8, "out"), _stream(stream))
+    _check(code, "ekya_checkpoint_decide")
+
+
 def ekya_comm_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(load_library().ekya_comm_unique_id(buf), "ekya_comm_unique_id")
@@ -297,3 +323,24 @@ def profile_estimate(h, cur, hist, hist_acc, fallback, mode=PROFILE_RADIUS, tau=
     cl = torch.empty((Q, H + 1), dtype=torch.int32, device=cur.device) if with_cluster else None
     ekya_profile_estimate(h, pd, cur, hist, hist_acc, fallback, est, n, cl, stream=stream)
     return est, n, cl
+
+
+def place(h, alloc, units, gpus, stream=None):
+    """Placement of allocations (units) onto `gpus` GPUs; returns (piece_job, piece_q,
+    piece_gpu, n_pieces, gpu_load) as device tensors (include/ekya.h ekya_place)."""
+    B, J = alloc.shape
+    dev = alloc.device
+    P = J + gpus
+    pj = torch.empty((B, P), dtype=torch.uint16, device=dev)
+    pq = torch.empty((B, P), dtype=torch.uint32, device=dev)
+    pg = torch.empty((B, P), dtype=torch.int16, device=dev)
+    npc = torch.empty((B,), dtype=torch.uint16, device=dev)
+    load = torch.empty((B, gpus), dtype=torch.uint32, device=dev)
+    ekya_place(h, units, gpus, alloc, pj, pq, pg, npc, load, stream=stream)
+    return pj, pq, pg, npc, load
+
+
+def checkpoint_decide(h, tau, t, T, a, a_star, A, delta_ckpt, stream=None):
+    out = torch.empty(tau.shape, dtype=torch.uint8, device=tau.device)
+    ekya_checkpoint_decide(h, tau, t, T, a, a_star, A, delta_ckpt, out, stream=stream)
+    return out

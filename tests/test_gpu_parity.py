@@ -403,3 +403,63 @@ def test_ties_grid_list_thief_bitexact(h):
         assert_eq(a, oa, f"thief alloc {mode}")
         assert_eq(cc, oc, f"thief cfg {mode}")
         assert_eq(ts, osum, f"thief sum {mode}")
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: placement onto GPUs and the checkpoint decision
+# ---------------------------------------------------------------------------
+def _place_cmp(h, alloc, units, gpus):
+    pj, pq, pg, npc, load = ek().place(h, alloc.cuda(), units, gpus)
+    opj, opq, opg, onpc, oload, bad = oracle.place(alloc.numpy(), units, gpus)
+    assert_eq(npc, onpc, "n_pieces")
+    assert_eq(pj, opj, "piece_job")
+    assert_eq(pq, opq, "piece_q")
+    assert_eq(pg, opg, "piece_gpu")
+    assert_eq(load, oload, "gpu_load")
+    return bad
+
+
+@pytest.mark.parametrize("name,cfg,gpus", [("c2", variant(synth.CONFIG2, n_inst=256), 8),
+                                           ("c5", variant(synth.CONFIG5, n_inst=48), 80)],
+                         ids=["config2-8gpu", "config5-80gpu"])
+def test_place_thief_decisions_bitexact(h, name, cfg, gpus):
+    """The thief's decisions placed on the cluster's GPUs (delta = G/U GPU per unit)."""
+    Td, _ = tables(cfg)
+    a, *_ = ek().thief_schedule(h, Td, *args(cfg))
+    assert _place_cmp(h, a.cpu(), cfg.units, gpus) == 0 and h.last_error() == 0
+
+
+def test_place_random_edges_bitexact(h):
+    rng = np.random.default_rng(21)
+    for J, U, G in [(1, 1, 1), (3, 10, 2), (20, 80, 8), (7, 65534, 128), (64, 100, 100), (33, 7, 33),
+                    (200, 800, 80), (5, 3, 96)]:
+        B = 64
+        w = rng.integers(0, 6, (B, J))
+        a = np.floor(w / np.maximum(1, w.sum(1, keepdims=True)) * U).astype(np.int64)
+        a[0] = 0
+        a[1] = 0
+        a[1, 0] = U                                    # one job takes everything
+        if J > 1:
+            a[2, :2] = U                               # sum > U: data error
+        bad = _place_cmp(h, torch.from_numpy(a.astype(np.uint16)), U, G)
+        assert bad == (1 if J > 1 else 0)
+        assert h.last_error() == (-6 if bad else 0)
+
+
+def test_checkpoint_bitexact(h):
+    rng = np.random.default_rng(22)
+    n = 100_000
+    T = rng.uniform(10, 300, n).astype(np.float32)
+    tau = (T * rng.uniform(0, 1, n)).astype(np.float32)
+    t = (tau * rng.uniform(0, 1, n)).astype(np.float32)
+    a, ast, A = (rng.uniform(0, 1, n).astype(np.float32) for _ in range(3))
+    dl = rng.uniform(0, 20, n).astype(np.float32)
+    t[:5] = tau[:5] + 1.0                              # invalid: t > tau
+    A[5] = 1.5
+    dl[6] = -1.0
+    ast[7:100] = a[7:100]                              # no gain
+    dl[100:200] = 0.0
+    out = ek().checkpoint_decide(h, *(torch.from_numpy(x).cuda() for x in (tau, t, T, a, ast, A, dl)))
+    oo, bad = oracle.checkpoint(tau, t, T, a, ast, A, dl)
+    assert bad == 7 and h.last_error() == -6
+    assert_eq(out, oo, "checkpoint")
