@@ -380,6 +380,8 @@ def run_ours(args, rank, world, local_rank):
         e2e = run_e2e(ek, h, w, T, rows, P, O, args, world)
 
     context = run_context(ek, h, dev, args) if rank == 0 and args.context else None
+    if context is not None:
+        context.update(run_next4(ek, h, w, O, dev))
     if rank != 0:
         return
     peak, peak_kind, mp = measured_peaks()
@@ -450,7 +452,61 @@ def run_ours(args, rank, world, local_rank):
         dt, units, desc = oracle_sample(args.ref_inst, args.ref_query)
         line["cpu_baseline"] = {"value": units / dt, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
                                 "seconds": dt}
+        # NEXT-4 placement: the oracle on 4,096 of the step's STEEPEST decisions (one thread)
+        sample = O.dec[0]["alloc"][:4096].cpu().numpy()
+        t0 = time.perf_counter()
+        oracle.place(sample, w.U, 8)
+        line["cpu_baseline"]["next4_placement_instances_per_s"] = sample.shape[0] / (time.perf_counter() - t0)
     print(json.dumps(line), flush=True)
+
+
+def _time_ms(fn, reps=10):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def run_next4(ek, h, w, O, dev):
+    """SURVEY 8(f) NEXT-4 beside the step: placement of the step's STEEPEST decisions
+    (65,536 instances x 20 jobs) onto the 8 GPUs of config 4 (0.1 GPU per unit), and
+    checkpoint decisions for one (stream, time) point per stream."""
+    gpus = 8
+    alloc = O.dec[0]["alloc"]
+    B, J = alloc.shape
+    P = J + gpus
+    pj = torch.empty((B, P), dtype=torch.uint16, device=dev)
+    pq = torch.empty((B, P), dtype=torch.uint32, device=dev)
+    pg = torch.empty((B, P), dtype=torch.int16, device=dev)
+    npc = torch.empty((B,), dtype=torch.uint16, device=dev)
+    load = torch.empty((B, gpus), dtype=torch.uint32, device=dev)
+    ms_p = _time_ms(lambda: ek.ekya_place(h, w.U, gpus, alloc, pj, pq, pg, npc, load))
+    n = B * w.V
+    g = torch.Generator(device="cpu").manual_seed(5)
+    T = torch.full((n,), 200.0)
+    tau = T * torch.rand(n, generator=g)
+    t = tau * torch.rand(n, generator=g)
+    a, ast, A = (torch.rand(n, generator=g) for _ in range(3))
+    dl = 5.0 * torch.rand(n, generator=g)
+    xs = [x.to(dev) for x in (tau, t, T, a, ast, A, dl)]
+    out = torch.empty((n,), dtype=torch.uint8, device=dev)
+    ms_c = _time_ms(lambda: ek.ekya_checkpoint_decide(h, *xs, out))
+    assert h.last_error() == 0
+    peak, _, _ = measured_peaks()
+    bytes_p = B * (2 * J + P * 8 + 2 + 4 * gpus)     # alloc in; pieces, count, loads out
+    bytes_c = n * (7 * 4 + 1)
+    res = {"next4_placement": {"instances": B, "jobs": J, "gpus": gpus, "ms": ms_p,
+                               "instances_per_s": B / (ms_p / 1000.0),
+                               "hbm_frac": bytes_p / (ms_p / 1000.0) / 1e9 / peak},
+           "next4_checkpoint": {"points": n, "ms": ms_c, "decisions_per_s": n / (ms_c / 1000.0),
+                                "hbm_frac": bytes_c / (ms_c / 1000.0) / 1e9 / peak}}
+    return res
 
 
 def run_context(ek, h, dev, args):
