@@ -97,6 +97,10 @@ def lib():
         L.orc_profile.argtypes = [ctypes.POINTER(ProfileDims), P, P, P, P, P, P, P]
         L.orc_quantize_frac.argtypes = [ctypes.c_int64, ctypes.c_int32]
         L.orc_quantize_frac.restype = ctypes.c_int32
+        L.orc_uniform.argtypes = [ctypes.POINTER(Dims), P, P, P, P, P, ctypes.c_int32, ctypes.c_float, P, P, P, P]
+        L.orc_uniform.restype = ctypes.c_int64
+        L.orc_pareto.argtypes = [ctypes.c_int64, ctypes.c_int32, P, P, P]
+        L.orc_pareto.restype = ctypes.c_int64
         L.orc_pack.argtypes = [ctypes.c_int32, P, ctypes.c_int32, P, P]
         L.orc_pack.restype = ctypes.c_int64
         L.orc_place.argtypes = [ctypes.c_int32] * 4 + [P] * 6
@@ -347,3 +351,33 @@ def checkpoint(tau, t, T, a, a_star, A, delta_ckpt):
     out = np.zeros(arrs[0].size, np.uint8)
     bad = lib().orc_checkpoint(arrs[0].size, *(_p(x) for x in arrs), _p(out))
     return out, int(bad)
+
+
+HIGHEST_POST = -1   # uniform baseline: each stream's highest-accuracy config
+
+
+def uniform(inst: Instances, fixed_gamma: int = HIGHEST_POST, inference_weight: float = 0.5):
+    """Uniform baseline (readings U1, U2): alloc, cfg, sum, mean, bad."""
+    d = inst.dims()
+    B, V = inst.B, inst.V
+    alloc = np.zeros((B, 2 * V), np.uint16)
+    cfg = np.zeros((B, V), np.uint8)
+    s = np.zeros(B, np.uint64)
+    mean = np.zeros(B, np.float32)
+    bad = lib().orc_uniform(ctypes.byref(d), *inst.tables(), int(fixed_gamma), float(inference_weight),
+                            _p(alloc), _p(cfg), _p(s), _p(mean))
+    if bad < 0:
+        raise ValueError("oracle: invalid uniform arguments")
+    return alloc, cfg, s, mean, int(bad)
+
+
+def pareto(cost, post):
+    """Pareto-frontier mask (bit k = config k) of each set of configs (reading PR1)."""
+    cost = _c(cost, np.float32)
+    post = _c(post, np.float32)
+    n = cost.shape[-1]
+    sets = cost.size // max(1, n)
+    m = np.zeros(cost.shape[:-1], np.uint32)
+    if lib().orc_pareto(sets, n, _p(cost), _p(post), _p(m)) < 0:
+        raise ValueError("oracle: invalid pareto shape")
+    return m

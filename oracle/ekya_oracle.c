@@ -741,3 +741,107 @@ int64_t orc_checkpoint(int64_t n, const float* tau, const float* t, const float*
     }
     return bad;
 }
+
+/* ========================================================================
+ * NEXT-3: the uniform baseline and the Pareto frontier of the
+ * retraining configurations.
+ * ======================================================================== */
+
+/* U1 + U2: the uniform scheduler ("evenly splits the GPUs between video streams,
+ * and each stream evenly partitions its allocated GPUs"; "a fixed retraining
+ * configuration, and a static retraining/inference resource allocation").
+ * U1: share_v as C9; r_train = floor(fl(share fl(1 - w))), r_infer = share - r_train
+ *     (w = inference_weight in (0,1); w = 1/2 is exactly C9's fair start).
+ * U2: the retraining config is fixed: fixed_gamma >= 1 is config fixed_gamma - 1 of every
+ *     stream, 0 = no retraining, -1 = each stream's highest post-retraining accuracy
+ *     ("the configuration ... that results in the highest accuracy"; lowest index on
+ *     ties; none if the stream has no real config).  lambda* as rule 3.  Value =
+ *     fl(factor g(gamma, r_train)) when gamma is feasible at r_train (rule 1), else the
+ *     retraining does not finish within the window and the value is fl(factor stale);
+ *     no admissible lambda -> 0 (C8).  cfg reports the fixed gamma and lambda*.
+ * Returns the number of invalid instances (R-ERR: outputs zeroed). */
+int64_t orc_uniform(const orc_dims* d, const float* stale, const float* cost, const float* post,
+                    const uint16_t* lmu, const float* lf, int32_t fixed_gamma, float inference_weight,
+                    uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum, float* out_mean)
+{
+    if (!orc_dims_valid(d) || fixed_gamma < -1 || fixed_gamma > d->n_gamma ||
+        !(inference_weight > 0.0f && inference_weight < 1.0f))
+        return -1;
+    const int32_t V = d->n_streams, J = 2 * V, nG = d->n_gamma, nL = d->n_lambda;
+    int64_t bad = 0;
+    for (int64_t b = 0; b < d->n_inst; ++b) {
+        orc_inst in = orc_instance(d, b, stale, cost, post, lmu, lf);
+        if (!orc_instance_valid(d, &in)) {
+            ++bad;
+            for (int32_t j = 0; j < J; ++j) out_alloc[b * J + j] = 0;
+            for (int32_t v = 0; v < V; ++v) out_cfg[b * V + v] = 0;
+            out_sum[b] = 0;
+            if (out_mean) out_mean[b] = 0.0f;
+            continue;
+        }
+        uint64_t S = 0;
+        for (int32_t v = 0; v < V; ++v) {
+            const int32_t share = d->units / V + (v < d->units % V ? 1 : 0);
+            const float keep = 1.0f - inference_weight;
+            const float x = (float)share * keep;
+            const int32_t rt = (int32_t)floorf(x);
+            const int32_t ri = share - rt;
+            out_alloc[b * J + 2 * v] = (uint16_t)ri;
+            out_alloc[b * J + 2 * v + 1] = (uint16_t)rt;
+            const float st = in.stale[v];
+            const float* cv = in.cost + (int64_t)v * nG;
+            const float* pv = in.post + (int64_t)v * nG;
+            int g = fixed_gamma;                       /* 1-based config, 0 = none */
+            if (g < 0) {
+                g = 0;
+                float bp = 0.0f;
+                for (int k = 0; k < nG; ++k) {
+                    if (isinf(cv[k])) continue;        /* padding */
+                    if (g == 0 || pv[k] > bp) { g = k + 1; bp = pv[k]; }
+                }
+            }
+            const int l = orc_lambda_star(st, in.lmu + (int64_t)v * nL, in.lf + (int64_t)v * nL, nL, ri,
+                                          d->a_min);
+            float val = 0.0f;
+            uint8_t cfg = (uint8_t)(ORC_LAMBDA_NONE << 5);
+            if (l >= 0) {
+                const float fac = in.lf[(int64_t)v * nL + l];
+                float acc = st;
+                if (g > 0 && orc_gamma_feasible(cv[g - 1], rt, d->unit_gpu_seconds))
+                    acc = orc_window_accuracy(st, pv[g - 1], cv[g - 1], rt, d->unit_gpu_seconds);
+                val = fac * acc;
+                cfg = (uint8_t)(g | (l << 5));
+            }
+            out_cfg[b * V + v] = cfg;
+            S += orc_q32(val);
+        }
+        out_sum[b] = S;
+        if (out_mean) out_mean[b] = orc_mean_from_q32(S, V);
+    }
+    return bad;
+}
+
+/* PR1: the Pareto frontier of a stream's configurations in (cost, accuracy) (Figure 3,
+ * P:147 "Pareto boundary"): config k is on it iff no other real config k'
+ * has cost' <= cost and post' >= post with at least one strict.  Padding (cost +INF) is
+ * never on it.  Bit k of out_mask[set] (k = 0..n-1) marks config k. */
+int64_t orc_pareto(int64_t n_sets, int32_t n, const float* cost, const float* post, uint32_t* out_mask)
+{
+    if (n_sets < 0 || n < 0 || n > 32) return -1;
+    for (int64_t s = 0; s < n_sets; ++s) {
+        const float* c = cost + s * n;
+        const float* p = post + s * n;
+        uint32_t m = 0;
+        for (int32_t k = 0; k < n; ++k) {
+            if (isinf(c[k])) continue;
+            int dominated = 0;
+            for (int32_t j = 0; j < n && !dominated; ++j) {
+                if (j == k || isinf(c[j])) continue;
+                if (c[j] <= c[k] && p[j] >= p[k] && (c[j] < c[k] || p[j] > p[k])) dominated = 1;
+            }
+            if (!dominated) m |= 1u << k;
+        }
+        out_mask[s] = m;
+    }
+    return 0;
+}

@@ -80,6 +80,13 @@ int64_t orc_place(int32_t n_inst, int32_t n_jobs, int32_t units, int32_t gpus, c
 int64_t orc_checkpoint(int64_t n, const float* tau, const float* t, const float* T, const float* a,
                        const float* a_star, const float* A, const float* delta_ckpt, uint8_t* out);
 
+/* ---- NEXT-3: uniform baseline (readings U1, U2) and the
+ *      Pareto frontier of a stream's configurations (reading PR1) ---- */
+int64_t orc_uniform(const orc_dims* d, const float* stale, const float* cost, const float* post,
+                    const uint16_t* lmu, const float* lf, int32_t fixed_gamma, float inference_weight,
+                    uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum, float* out_mean);
+int64_t orc_pareto(int64_t n_sets, int32_t n, const float* cost, const float* post, uint32_t* out_mask);
+
 #ifdef __cplusplus
 }
 #endif

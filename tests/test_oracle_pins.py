@@ -639,3 +639,96 @@ def test_checkpoint_matches_the_averaged_accuracy_form():
             assert out[i] == (acc > base)
     out, bad = oracle.checkpoint([10], [20], [100], [0.5], [0.6], [0.9], [1.0])
     assert bad == 1 and out[0] == 0                    # t > tau: data error
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: uniform baseline and Pareto frontier
+# ---------------------------------------------------------------------------
+def test_uniform_allocation_spec_example():
+    """2 streams, 3 GPUs, weight 0.5 -> each job gets 0.75 GPU (3 units of 0.25)."""
+    fx, inst = table1_inst()
+    a, cfg, s, mean, bad = oracle.uniform(inst, oracle.HIGHEST_POST, 0.5)
+    assert bad == 0 and a.tolist() == [[3, 3, 3, 3]]
+    assert (a[0] * fx["delta_gpu"] == 0.75).all()
+
+
+def test_uniform_table1_picks_highest_accuracy_configs():
+    """the baseline always retrains with the highest-accuracy configuration
+    (Cfg1A, Cfg1B); at 0.75 GPU inference keeps the lambda with factor 0.75 (65% ->
+    49%, 50% -> 37.5%, below the fixture's a_MIN, so a_MIN = 0 as in the P:765 pin)."""
+    fx, inst0 = table1_inst()
+    inst = oracle.Instances(inst0.stale, inst0.cost, inst0.post, inst0.lam_min_units, inst0.lam_factor,
+                            inst0.units, 1, inst0.unit_gpu_seconds, 0.0)
+    a, cfg, s, mean, bad = oracle.uniform(inst)
+    assert [(c & 31) for c in cfg[0]] == [1, 1]          # config index 0 of each stream (Cfg1*)
+    assert [(c >> 5) for c in cfg[0]] == [1, 1]           # lambda with factor 0.75
+    # value = fl(0.75 g(Cfg1, rt = 3)) per stream, g the window average of rule 2 (pinned above)
+    val = [f32(f32(0.75) * f32(oracle.window_accuracy(fx["stale"][v], fx["post"][v][0],
+                                                       fx["cost_gpu_s"][v][0], 3, inst.unit_gpu_seconds)))
+           for v in range(2)]
+    assert int(s[0]) == sum(oracle.q32(x) for x in val)
+    # both finish inside the window (85/90 and 80/90 of it), so both beat the stale model
+    assert val[0] > f32(0.75 * fx["stale"][0]) and val[1] > f32(0.75 * fx["stale"][1])
+
+
+def test_uniform_half_weight_is_dominated_by_pickconfigs_and_thief():
+    """S:289 dominance: at w = 1/2 the uniform allocation is the thief's fair start, so
+    fixed-config value <= PickConfigs(fair) <= thief (exact integer objectives)."""
+    for cfg in (synth.CONFIG1, synth.CONFIG2):
+        c = synth.SchedConfig(**{**cfg.__dict__, "n_inst": 200})
+        inst = make_inst(c, 0, 200)
+        fair = oracle.fair(inst)
+        ts = oracle.thief(inst, oracle.STEEPEST)[2]
+        tl = oracle.thief(inst, oracle.LITERAL)[2]
+        for g in [oracle.HIGHEST_POST, 0] + list(range(1, inst.nG + 1)):
+            a, cf, s, mean, bad = oracle.uniform(inst, g, 0.5)
+            assert bad == 0
+            for b in range(200):
+                assert list(a[b]) == list(fair[b] if fair.ndim == 2 else fair)
+                pc = oracle.pickconfigs(inst, b, fair)[0]
+                assert int(s[b]) <= pc <= int(ts[b]) and pc <= int(tl[b])
+
+
+def test_uniform_weight_and_no_retraining():
+    """U1: r_train = floor(share (1 - w)); fixed config 0 (no retraining) is stale x factor."""
+    c = synth.SchedConfig(**{**synth.CONFIG2.__dict__, "n_inst": 20})
+    inst = make_inst(c, 0, 20)
+    for w in (0.1, 0.25, 0.9):
+        a, cf, s, mean, bad = oracle.uniform(inst, 0, w)
+        share = a[:, 0::2] + a[:, 1::2]
+        assert (a.sum(1) == c.units).all()
+        assert (a[:, 1::2] == np.floor(share * np.float32(1 - np.float32(w))).astype(int)).all()
+        assert ((cf & 31) == 0).all()
+        for b in range(20):
+            tot = 0
+            for v in range(c.n_streams):
+                lam = cf[b, v] >> 5
+                x = 0.0 if lam == 7 else f32(inst.lam_factor[b, v, lam]) * f32(inst.stale[b, v])
+                tot += oracle.q32(f32(x))
+            assert tot == int(s[b])
+
+
+def test_pareto_spec_examples_and_properties():
+    """singleton; equal accuracy, lower cost dominates; 20 random points = the
+    dominance definition; the frontier is a staircase (cost ascending, accuracy strictly
+    ascending) and every other point is dominated by a frontier point (Fig. 3 caption)."""
+    assert int(oracle.pareto([[10.0]], [[0.9]])[0]) == 0b1
+    assert int(oracle.pareto([[10.0, 5.0]], [[0.9, 0.9]])[0]) == 0b10
+    rng = np.random.default_rng(31)
+    for _ in range(300):
+        n = int(rng.integers(1, 32))
+        c = rng.choice([1.0, 2.0, 3.0, 5.0, 8.0], n).astype(np.float32) * rng.integers(1, 4, n)
+        p = np.round(rng.uniform(0, 1, n), 1).astype(np.float32)
+        c[rng.uniform(size=n) < 0.1] = np.inf                     # padding
+        m = int(oracle.pareto(c[None], p[None])[0])
+        on = [k for k in range(n) if m >> k & 1]
+        for k in range(n):
+            dom = any(j != k and np.isfinite(c[j]) and c[j] <= c[k] and p[j] >= p[k] and
+                      (c[j] < c[k] or p[j] > p[k]) for j in range(n))
+            assert (k in on) == (np.isfinite(c[k]) and not dom)
+        pts = sorted(set((float(c[k]), float(p[k])) for k in on))
+        for (c0, p0), (c1, p1) in zip(pts, pts[1:]):
+            assert c0 < c1 and p0 < p1
+        for k in range(n):
+            if np.isfinite(c[k]) and k not in on:
+                assert any(c[j] <= c[k] and p[j] >= p[k] for j in on)
