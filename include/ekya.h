@@ -193,6 +193,34 @@ int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p,
  *   (device pointers; root_buf used on the root only), enqueued on `stream`.
  * ------------------------------------------------------------------------- */
 /* ---------------------------------------------------------------------------
+ * ekya_uniform_schedule -- the uniform scheduler the paper compares against
+ * ("evenly splits the GPUs between video streams, and
+ * each stream evenly partitions its allocated GPUs for retraining and inference
+ * ... always picks the configuration for retraining that results in the highest
+ * accuracy"; "a fixed retraining configuration, and a static
+ * retraining/inference resource allocation").  Readings:
+ *   U1 share_v as the fair start (C9); r_train = floor(fl(share fl(1 - w))),
+ *      r_infer = share - r_train, w = inference_weight in (0,1) (w = 1/2: C9).
+ *   U2 retraining config fixed_gamma: >= 1 = config fixed_gamma-1 of every stream,
+ *      0 = no retraining, -1 = each stream's highest post accuracy (lowest index on
+ *      ties).  lambda* as rule 3; value = fl(factor g(gamma, r_train)) if gamma
+ *      finishes in the window (rule 1), else fl(factor stale); no lambda -> 0.
+ * Outputs as ekya_thief_schedule (alloc [B][2V], cfg [B][V] with the fixed gamma,
+ * exact sum [B], mean [B] or NULL).  Invalid instances: zeroed + EKYA_ERR_DATA.
+ *
+ * ekya_pareto -- Pareto frontier of each of n_sets sets of n <= 31 configurations
+ * (cost [n_sets][n], post [n_sets][n]; e.g. a table's cost/post with n_sets =
+ * B*V): bit k of out_mask[s] set iff config k is real (cost finite) and no other
+ * real config has cost' <= cost and post' >= post with one strict (P:147 Figure
+ * 3's "Pareto boundary"; reading PR1).
+ * ------------------------------------------------------------------------- */
+int ekya_uniform_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int32_t fixed_gamma,
+                          float inference_weight, uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum_q32,
+                          float* out_mean, ekya_stream_t stream);
+int ekya_pareto(ekya_handle* h, int64_t n_sets, int32_t n, const float* cost, const float* post,
+                uint32_t* out_mask, ekya_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * ekya_place -- placement of scheduling decisions onto discrete GPUs (SURVEY 8(f)
  * NEXT-4; "quantizes the allocations to inverse powers of two ...
  * allocates jobs to GPUs in descending order of demands").

@@ -155,6 +155,37 @@ int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p, const floa
                           reinterpret_cast<cudaStream_t>(stream));
 }
 
+int ekya_uniform_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int32_t fixed_gamma,
+                          float inference_weight, uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum_q32,
+                          float* out_mean, ekya_stream_t stream) {
+    if (!h) return EKYA_ERR_ARG;
+    int why = EKYA_OK;
+    if (!dims_ok(d, &why)) return why;
+    if (!tables_ok(d, t)) return EKYA_ERR_ARG;
+    if (fixed_gamma < -1 || fixed_gamma > d->n_gamma || !(inference_weight > 0.0f && inference_weight < 1.0f))
+        return EKYA_ERR_ARG;
+    if (d->n_inst > 0 && (!out_alloc || !out_cfg || !out_sum_q32)) return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    return launch_uniform(h, *d, *t, fixed_gamma, inference_weight, out_alloc, out_cfg, out_sum_q32, out_mean,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ekya_pareto(ekya_handle* h, int64_t n_sets, int32_t n, const float* cost, const float* post,
+                uint32_t* out_mask, ekya_stream_t stream) {
+    if (!h) return EKYA_ERR_ARG;
+    if (n_sets < 0 || n < 0) return EKYA_ERR_SHAPE;
+    if (n > 31) return EKYA_ERR_LIMIT;
+    if (n_sets > 0 && n > 0 && (!cost || !post || !out_mask)) return EKYA_ERR_ARG;
+    if (n_sets > 0 && n == 0) {
+        if (!out_mask) return EKYA_ERR_ARG;
+        if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+        return cudaMemsetAsync(out_mask, 0, (size_t)n_sets * 4, reinterpret_cast<cudaStream_t>(stream)) ==
+                       cudaSuccess ? EKYA_OK : EKYA_ERR_CUDA;
+    }
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    return launch_pareto(h, (long long)n_sets, n, cost, post, out_mask, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int ekya_place(ekya_handle* h, int32_t n_inst, int32_t n_jobs, int32_t units, int32_t gpus,
                const uint16_t* alloc, uint16_t* out_piece_job, uint32_t* out_piece_q, int16_t* out_piece_gpu,
                uint16_t* out_n_pieces, uint32_t* out_gpu_load, ekya_stream_t stream) {

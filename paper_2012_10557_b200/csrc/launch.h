@@ -40,6 +40,11 @@ int launch_checkpoint(ekya_handle* h, long long n, const float* tau, const float
                       const float* a, const float* a_star, const float* A, const float* delta, uint8_t* out,
                       cudaStream_t s);
 
+int launch_uniform(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int fixed_gamma, float weight,
+                   uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum, float* out_mean, cudaStream_t s);
+int launch_pareto(ekya_handle* h, long long n_sets, int n, const float* cost, const float* post,
+                  uint32_t* out_mask, cudaStream_t s);
+
 inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? EKYA_OK : EKYA_ERR_CUDA; }
 
 }  // namespace ekya

@@ -26,7 +26,7 @@ LAMBDA_NONE = 7
 SYMBOLS = ["ekya_create", "ekya_destroy", "ekya_last_error", "ekya_launch_count", "ekya_version",
            "ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate",
            "ekya_comm_unique_id", "ekya_comm_init", "ekya_gather_decisions", "ekya_counters", "ekya_place",
-           "ekya_checkpoint_decide"]
+           "ekya_checkpoint_decide", "ekya_uniform_schedule", "ekya_pareto"]
 
 
 class EkyaError(RuntimeError):
@@ -88,6 +88,11 @@ def load_library(path: str = LIB_PATH):
     L.ekya_thief_schedule.restype = ctypes.c_int
     L.ekya_profile_estimate.argtypes = [P, ctypes.POINTER(ProfileDims), P, P, P, P, P, P, P, P]
     L.ekya_profile_estimate.restype = ctypes.c_int
+    L.ekya_uniform_schedule.argtypes = [P, ctypes.POINTER(Dims), ctypes.POINTER(Tables), ctypes.c_int32,
+                                        ctypes.c_float, P, P, P, P, P]
+    L.ekya_uniform_schedule.restype = ctypes.c_int
+    L.ekya_pareto.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P, P, P, P]
+    L.ekya_pareto.restype = ctypes.c_int
     L.ekya_place.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P]
     L.ekya_place.restype = ctypes.c_int
     L.ekya_checkpoint_decide.argtypes = [P, ctypes.c_int64] + [P] * 8 + [P]
@@ -223,6 +228,27 @@ def ekya_profile_estimate(h: Handle, pdims: ProfileDims, cur, hist, hist_acc, fa
     _check(code, "ekya_profile_estimate")
 
 
+def ekya_uniform_schedule(h: Handle, dims: Dims, tables: Tables, fixed_gamma: int, inference_weight: float,
+                          out_alloc, out_cfg, out_sum_q32, out_mean=None, stream=None):
+    L = load_library()
+    code = L.ekya_uniform_schedule(h.ptr, ctypes.byref(dims), ctypes.byref(tables), int(fixed_gamma),
+                                   float(inference_weight), _ptr(out_alloc, torch.uint16, "out_alloc"),
+                                   _ptr(out_cfg, torch.uint8, "out_cfg"),
+                                   _ptr(out_sum_q32, torch.uint64, "out_sum_q32"),
+                                   _ptr(out_mean, torch.float32, "out_mean", True), _stream(stream))
+    _check(code, "ekya_uniform_schedule")
+
+
+def ekya_pareto(h: Handle, cost, post, out_mask, stream=None):
+    L = load_library()
+    n = cost.shape[-1]
+    n_sets = cost.numel() // max(1, n)
+    code = L.ekya_pareto(h.ptr, n_sets, n, _ptr(cost, torch.float32, "cost", True),
+                         _ptr(post, torch.float32, "post", True), _ptr(out_mask, torch.uint32, "out_mask"),
+                         _stream(stream))
+    _check(code, "ekya_pareto")
+
+
 def ekya_place(h: Handle, units: int, gpus: int, alloc, out_piece_job, out_piece_q, out_piece_gpu, out_n_pieces,
                out_gpu_load=None, stream=None):
     L = load_library()
@@ -343,4 +369,27 @@ def place(h, alloc, units, gpus, stream=None):
 def checkpoint_decide(h, tau, t, T, a, a_star, A, delta_ckpt, stream=None):
     out = torch.empty(tau.shape, dtype=torch.uint8, device=tau.device)
     ekya_checkpoint_decide(h, tau, t, T, a, a_star, A, delta_ckpt, out, stream=stream)
+    return out
+
+
+HIGHEST_POST = -1
+
+
+def uniform_schedule(h, tables: dict, units, steal_units, unit_gpu_seconds, a_min, fixed_gamma=HIGHEST_POST,
+                     inference_weight=0.5, stream=None):
+    dims = dims_from(tables, units, steal_units, unit_gpu_seconds, a_min)
+    B, V = dims.n_inst, dims.n_streams
+    dev = tables["stale"].device
+    alloc = torch.empty((B, 2 * V), dtype=torch.uint16, device=dev)
+    cfg = torch.empty((B, V), dtype=torch.uint8, device=dev)
+    s = torch.empty((B,), dtype=torch.uint64, device=dev)
+    mean = torch.empty((B,), dtype=torch.float32, device=dev)
+    ekya_uniform_schedule(h, dims, make_tables(**tables), fixed_gamma, inference_weight, alloc, cfg, s, mean,
+                          stream=stream)
+    return alloc, cfg, s, mean
+
+
+def pareto(h, cost, post, stream=None):
+    out = torch.empty(cost.shape[:-1], dtype=torch.uint32, device=cost.device)
+    ekya_pareto(h, cost, post, out, stream=stream)
     return out

@@ -463,3 +463,53 @@ def test_checkpoint_bitexact(h):
     oo, bad = oracle.checkpoint(tau, t, T, a, ast, A, dl)
     assert bad == 7 and h.last_error() == -6
     assert_eq(out, oo, "checkpoint")
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: uniform baseline and Pareto frontier
+# ---------------------------------------------------------------------------
+UNIFORM_CASES = [("c2-highest", variant(synth.CONFIG2, n_inst=96), -1, 0.5),
+                 ("c2-ragged-g3-w07", variant(synth.CONFIG2, n_inst=64, ragged=True), 3, 0.7),
+                 ("c2-none-w025", variant(synth.CONFIG2, n_inst=64), 0, 0.25),
+                 ("c1-g2-w09", variant(synth.CONFIG1, n_inst=300), 2, 0.9),
+                 ("odd-highest", variant(synth.CONFIG2, n_inst=37, n_streams=37, n_gamma=31, units=100), -1, 0.5),
+                 ("nogamma", variant(synth.CONFIG2, n_inst=16, n_gamma=0), -1, 0.5)]
+
+
+@pytest.mark.parametrize("name,cfg,g,w", UNIFORM_CASES, ids=[c[0] for c in UNIFORM_CASES])
+def test_uniform_bitexact(h, name, cfg, g, w):
+    Td, inst = tables(cfg)
+    a, c, s, m = ek().uniform_schedule(h, Td, *args(cfg), fixed_gamma=g, inference_weight=w)
+    oa, oc, osum, omean, bad = oracle.uniform(inst, g, w)
+    assert bad == 0 and h.last_error() == 0
+    assert_eq(a, oa, "alloc")
+    assert_eq(c, oc, "cfg")
+    assert_eq(s, osum, "sum")
+    assert_eq(m, omean, "mean")
+
+
+def test_uniform_invalid_instance_zeroed(h):
+    cfg = variant(synth.CONFIG2, n_inst=6)
+    T = synth.sched_tables(cfg)
+    T["post"][2, 1, 3] = 1.5
+    inst = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            *args(cfg))
+    a, c, s, m = ek().uniform_schedule(h, {k: v.cuda() for k, v in T.items()}, *args(cfg))
+    oa, oc, osum, omean, bad = oracle.uniform(inst)
+    assert bad == 1 and h.last_error() == -6
+    assert_eq(a, oa, "alloc")
+    assert_eq(s, osum, "sum")
+
+
+def test_pareto_bitexact(h):
+    cfg = variant(synth.CONFIG2, n_inst=512, ragged=True)
+    Td, inst = tables(cfg)
+    m = ek().pareto(h, Td["cost"], Td["post"])
+    assert_eq(m, oracle.pareto(inst.cost, inst.post), "pareto mask (tables)")
+    rng = np.random.default_rng(41)
+    for n in (1, 2, 7, 31):
+        c = (rng.choice([1.0, 2.0, 3.0, 5.0], (2000, n)) * rng.integers(1, 4, (2000, n))).astype(np.float32)
+        p = np.round(rng.uniform(0, 1, (2000, n)), 1).astype(np.float32)
+        c[rng.uniform(size=c.shape) < 0.1] = np.inf
+        m = ek().pareto(h, torch.from_numpy(c).cuda(), torch.from_numpy(p).cuda())
+        assert_eq(m, oracle.pareto(c, p), f"pareto mask n={n}")
