@@ -381,6 +381,7 @@ def run_ours(args, rank, world, local_rank):
 
     context = run_context(ek, h, dev, args) if rank == 0 and args.context else None
     if context is not None:
+        context.update(run_next3(ek, h, w, T, O, dev))
         context.update(run_next4(ek, h, w, O, dev))
     if rank != 0:
         return
@@ -471,6 +472,39 @@ def _time_ms(fn, reps=10):
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
+
+
+def run_next3(ek, h, w, T, O, dev):
+    """SURVEY 8(f) NEXT-3 beside the step: the uniform baseline (even split, each stream's
+    highest-accuracy config) on the step's 65,536 config-4 instances -- its mean
+    objective against the two thieves' (the uniform <= thief sandwich at scale) -- and the
+    Pareto frontier of every stream's 18 configurations."""
+    dims, tabs = ek.dims_from(T, *w.args), ek.make_tables(**T)
+    B, V = w.B, w.V
+    ua = torch.empty((B, 2 * V), dtype=torch.uint16, device=dev)
+    uc = torch.empty((B, V), dtype=torch.uint8, device=dev)
+    us = torch.empty((B,), dtype=torch.uint64, device=dev)
+    um = torch.empty((B,), dtype=torch.float32, device=dev)
+    ms_u = _time_ms(lambda: ek.ekya_uniform_schedule(h, dims, tabs, -1, 0.5, ua, uc, us, um))
+    mask = torch.empty((B, V), dtype=torch.uint32, device=dev)
+    ms_p = _time_ms(lambda: ek.ekya_pareto(h, T["cost"], T["post"], mask))
+    assert h.last_error() == 0
+    peak, _, _ = measured_peaks()
+    G = T["cost"].shape[2]
+    bytes_u = w.table_bytes() + B * (4 * V + V + 8 + 4)
+    bytes_p = B * V * (8 * G + 4)
+    m = mask.cpu().numpy().view(np.uint32)
+    frontier = float(np.unpackbits(m.view(np.uint8)).sum()) / m.size
+    return {"next3_uniform": {"instances": B, "ms": ms_u, "instances_per_s": B / (ms_u / 1000.0),
+                              "hbm_frac": bytes_u / (ms_u / 1000.0) / 1e9 / peak,
+                              "mean_objective_uniform": float(um.mean()),
+                              "mean_objective_thief_steepest": float(O.dec[0]["mean"].mean()),
+                              "mean_objective_thief_literal": float(O.dec[1]["mean"].mean()),
+                              "uniform_le_thief_all": bool((us.cpu().numpy().view(np.uint64) <=
+                                                            O.dec[1]["sum"].cpu().numpy().view(np.uint64)).all())},
+            "next3_pareto": {"sets": B * V, "configs": G, "ms": ms_p, "sets_per_s": B * V / (ms_p / 1000.0),
+                             "hbm_frac": bytes_p / (ms_p / 1000.0) / 1e9 / peak,
+                             "mean_frontier_size": frontier}}
 
 
 def run_next4(ek, h, w, O, dev):
