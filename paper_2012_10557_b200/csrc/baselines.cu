@@ -6,8 +6,8 @@
 // split (C9's per-stream share, inference weight w), the fixed retraining config
 // (or each stream's highest-accuracy config), lambda* (rule 3) and the window
 // average of rule 2 -- then the exact Q32 objective by a warp reduction.
-// ekya_pareto: one warp per (instance, stream) set, lane k = config k; the
-// dominance test against every other config by shuffles, the frontier by ballot.
+// ekya_pareto: one thread per (instance, stream) set, its configs in registers,
+// the O(n^2) dominance test sequential.
 #include <algorithm>
 
 #include "launch.h"
@@ -96,22 +96,29 @@ struct ParetoParams {
     uint32_t* out_mask;
 };
 
-__global__ void __launch_bounds__(kBaseWarps * 32) pareto_kernel(ParetoParams p) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = p.n;
-    for (long long s = (long long)blockIdx.x * kBaseWarps + warp; s < p.n_sets;
-         s += (long long)gridDim.x * kBaseWarps) {
-        float c = INFINITY, q = 0.0f;
-        if (lane < n) {
-            c = __ldg(p.cost + s * n + lane);
-            q = __ldg(p.post + s * n + lane);
+// one set per thread: the set's n <= 31 (cost, post) pairs in registers (NM = compile-time
+// bound), the O(n^2) dominance test sequential -- far fewer instructions than a warp per set
+template <int NM>
+__global__ void __launch_bounds__(256) pareto_kernel(ParetoParams p) {
+    const int n = p.n;
+    for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < p.n_sets;
+         s += (long long)gridDim.x * blockDim.x) {
+        float c[NM], q[NM];
+#pragma unroll
+        for (int k = 0; k < NM; ++k) {
+            c[k] = k < n ? __ldg(p.cost + s * n + k) : INFINITY;
+            q[k] = k < n ? __ldg(p.post + s * n + k) : 0.0f;
         }
-        bool dom = false;
-        for (int j = 0; j < n; ++j) {
-            const float cj = __shfl_sync(0xffffffffu, c, j), qj = __shfl_sync(0xffffffffu, q, j);
-            dom |= j != lane && !isinf(cj) && cj <= c && qj >= q && (cj < c || qj > q);
+        unsigned m = 0;
+#pragma unroll
+        for (int k = 0; k < NM; ++k) {
+            bool dom = isinf(c[k]);
+#pragma unroll
+            for (int j = 0; j < NM; ++j)
+                if (j != k) dom |= !isinf(c[j]) && c[j] <= c[k] && q[j] >= q[k] && (c[j] < c[k] || q[j] > q[k]);
+            m |= dom ? 0u : (1u << k);
         }
-        const unsigned m = __ballot_sync(0xffffffffu, lane < n && !isinf(c) && !dom);
-        if (lane == 0) p.out_mask[s] = m;
+        p.out_mask[s] = m;
     }
 }
 
@@ -133,9 +140,10 @@ int launch_pareto(ekya_handle* h, long long n_sets, int n, const float* cost, co
                   uint32_t* out_mask, cudaStream_t s) {
     if (n_sets == 0) return EKYA_OK;
     ParetoParams p{n_sets, n, cost, post, out_mask};
-    const long long need = (n_sets + kBaseWarps - 1) / kBaseWarps;
+    const long long need = (n_sets + 255) / 256;
     const int grid = (int)std::min<long long>(need, (long long)h->sm_count * 8);
-    pareto_kernel<<<grid, kBaseWarps * 32, 0, s>>>(p);
+    auto k = n <= 8 ? pareto_kernel<8> : n <= 18 ? pareto_kernel<18> : pareto_kernel<31>;
+    k<<<grid, 256, 0, s>>>(p);
     h->launches++;
     return cuda_status(cudaGetLastError());
 }
