@@ -101,6 +101,8 @@ def lib():
         L.orc_uniform.restype = ctypes.c_int64
         L.orc_pareto.argtypes = [ctypes.c_int64, ctypes.c_int32, P, P, P]
         L.orc_pareto.restype = ctypes.c_int64
+        L.orc_curve_fit.argtypes = [ctypes.c_int64, ctypes.c_int32, P, P, P, P]
+        L.orc_curve_fit.restype = ctypes.c_int64
         L.orc_pack.argtypes = [ctypes.c_int32, P, ctypes.c_int32, P, P]
         L.orc_pack.restype = ctypes.c_int64
         L.orc_place.argtypes = [ctypes.c_int32] * 4 + [P] * 6
@@ -381,3 +383,17 @@ def pareto(cost, post):
     if lib().orc_pareto(sets, n, _p(cost), _p(post), _p(m)) < 0:
         raise ValueError("oracle: invalid pareto shape")
     return m
+
+
+def curve_fit(acc, full_epochs):
+    """Micro-profiler curve fit (readings CF1-CF3): acc [S][P] at epochs 1..P, full_epochs
+    [S] -> predicted accuracy [S], params [S][3] = (alpha, c, beta2), bad."""
+    acc = _c(acc, np.float32)
+    S, Pn = acc.shape
+    ke = _c(full_epochs, np.int32).reshape(S)
+    pred = np.zeros(S, np.float32)
+    prm = np.zeros((S, 3), np.float32)
+    bad = lib().orc_curve_fit(S, Pn, _p(acc), _p(ke), _p(pred), _p(prm))
+    if bad < 0:
+        raise ValueError("oracle: invalid curve-fit shape")
+    return pred, prm, int(bad)

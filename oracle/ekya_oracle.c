@@ -845,3 +845,127 @@ int64_t orc_pareto(int64_t n_sets, int32_t n, const float* cost, const float* po
     }
     return 0;
 }
+
+/* ========================================================================
+ * NEXT-2: the micro-profiler's curve fit and extrapolation
+ * ("fit the accuracy-epoch points to the a non-linear curve model ...
+ * using a non-negative least squares solver ... extrapolate"; S:106-108,
+ * S:147-163).  Readings CF1-CF3 in DESIGN.md.
+ * ======================================================================== */
+
+/* CF1 model: accuracy(k) = 1 - (1/(beta0 k + beta1) + beta2), beta >= 0.  With
+ * alpha = 1/beta0 and c = beta1/beta0 the loss term is alpha/(k + c): for a fixed c >= 0
+ * the fit is a two-variable non-negative least squares problem in (alpha, beta2).
+ * orc_nnls2: min sum_k (alpha x_k + b - y_k)^2, alpha, b >= 0, closed form by the active
+ * set: the unconstrained solution if both >= 0, else the better of the two boundary
+ * solutions (alpha = 0, b = max(0, mean y)) and (b = 0, alpha = max(0, Sxy/Sxx)).
+ * Sums sequential in k; one binary32 rounding per operation.  Returns the SSE. */
+static float orc_sse(const float* x, const float* y, int n, float al, float b)
+{
+    float e = 0.0f;
+    for (int k = 0; k < n; ++k) {
+        const float r = al * x[k];
+        const float t = r + b;
+        const float d = t - y[k];
+        const float dd = d * d;
+        e = e + dd;
+    }
+    return e;
+}
+
+static float orc_nnls2(const float* x, const float* y, int n, float* al_out, float* b_out)
+{
+    float sx = 0.0f, sy = 0.0f, sxx = 0.0f, sxy = 0.0f;
+    for (int k = 0; k < n; ++k) {
+        sx = sx + x[k];
+        sy = sy + y[k];
+        const float xx = x[k] * x[k];
+        sxx = sxx + xx;
+        const float xy = x[k] * y[k];
+        sxy = sxy + xy;
+    }
+    const float fn = (float)n;
+    const float a1 = fn * sxx, a2 = sx * sx;
+    const float det = a1 - a2;
+    if (det > 0.0f) {
+        const float u1 = fn * sxy, u2 = sx * sy;
+        const float al = (u1 - u2) / det;
+        const float v1 = sxx * sy, v2 = sx * sxy;
+        const float b = (v1 - v2) / det;
+        if (al >= 0.0f && b >= 0.0f) {
+            *al_out = al;
+            *b_out = b;
+            return orc_sse(x, y, n, al, b);
+        }
+    }
+    /* boundary candidates (both feasible): alpha = 0, or b = 0 */
+    const float m = sy / fn;
+    const float b0 = m > 0.0f ? m : 0.0f;
+    const float e0 = orc_sse(x, y, n, 0.0f, b0);
+    const float q = sxx > 0.0f ? sxy / sxx : 0.0f;
+    const float a0 = q > 0.0f ? q : 0.0f;
+    const float e1 = orc_sse(x, y, n, a0, 0.0f);
+    if (e1 < e0) {
+        *al_out = a0;
+        *b_out = 0.0f;
+        return e1;
+    }
+    *al_out = 0.0f;
+    *b_out = b0;
+    return e0;
+}
+
+/* CF2: the non-linear parameter c over the fixed grid c_i = i/8, i = 0..256 (c in [0, 32]
+ * epochs; exact binary32 values); the lowest SSE wins, lowest i on ties.  CF3: the
+ * extrapolated accuracy at epoch K, 1 - (alpha/(K + c) + beta2), clamped to [0, 1].
+ * acc [n_sets][n_points] at epochs 1..n_points (2 <= n_points <= 32), full_epochs [n_sets]
+ * >= 1; out_pred [n_sets]; out_params [n_sets][3] = (alpha, c, beta2) or NULL.  A set
+ * with an accuracy outside [0,1] or full_epochs < 1 is a data error (pred 0). */
+#define ORC_CF_GRID 257
+int64_t orc_curve_fit(int64_t n_sets, int32_t n_points, const float* acc, const int32_t* full_epochs,
+                      float* out_pred, float* out_params)
+{
+    if (n_sets < 0 || n_points < 2 || n_points > 32) return -1;
+    int64_t bad = 0;
+    float x[32], y[32];
+    for (int64_t s = 0; s < n_sets; ++s) {
+        const float* a = acc + s * n_points;
+        int ok = full_epochs[s] >= 1;
+        for (int k = 0; k < n_points; ++k) ok &= orc_in01(a[k]);
+        if (!ok) {
+            ++bad;
+            out_pred[s] = 0.0f;
+            if (out_params) out_params[s * 3] = out_params[s * 3 + 1] = out_params[s * 3 + 2] = 0.0f;
+            continue;
+        }
+        for (int k = 0; k < n_points; ++k) y[k] = 1.0f - a[k];
+        float best = 0.0f, bal = 0.0f, bb = 0.0f, bc = 0.0f;
+        for (int i = 0; i < ORC_CF_GRID; ++i) {
+            const float c = (float)i * 0.125f;
+            for (int k = 0; k < n_points; ++k) {
+                const float den = (float)(k + 1) + c;
+                x[k] = 1.0f / den;
+            }
+            float al, b;
+            const float e = orc_nnls2(x, y, n_points, &al, &b);
+            if (i == 0 || e < best) {
+                best = e;
+                bal = al;
+                bb = b;
+                bc = c;
+            }
+        }
+        const float den = (float)full_epochs[s] + bc;
+        const float l1 = bal / den;
+        const float l = l1 + bb;
+        float p = 1.0f - l;
+        p = p < 0.0f ? 0.0f : (p > 1.0f ? 1.0f : p);
+        out_pred[s] = p;
+        if (out_params) {
+            out_params[s * 3] = bal;
+            out_params[s * 3 + 1] = bc;
+            out_params[s * 3 + 2] = bb;
+        }
+    }
+    return bad;
+}

@@ -87,6 +87,11 @@ int64_t orc_uniform(const orc_dims* d, const float* stale, const float* cost, co
                     uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum, float* out_mean);
 int64_t orc_pareto(int64_t n_sets, int32_t n, const float* cost, const float* post, uint32_t* out_mask);
 
+/* ---- NEXT-2: micro-profiler curve fit + extrapolation (
+ *      readings CF1-CF3) ---- */
+int64_t orc_curve_fit(int64_t n_sets, int32_t n_points, const float* acc, const int32_t* full_epochs,
+                      float* out_pred, float* out_params);
+
 #ifdef __cplusplus
 }
 #endif

@@ -732,3 +732,64 @@ def test_pareto_spec_examples_and_properties():
         for k in range(n):
             if np.isfinite(c[k]) and k not in on:
                 assert any(c[j] <= c[k] and p[j] >= p[k] for j in on)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: micro-profiler curve fit
+# ---------------------------------------------------------------------------
+def _curve(b0, b1, b2, k):
+    return 1.0 - (1.0 / (b0 * k + b1) + b2)
+
+
+def test_curve_fit_spec_examples():
+    """S:155 constant data -> constant fit; S:156 noiseless round trip within 1e-3 at k = 30;
+    S:161 the (0.5, 1.0, 0.1) curve at 30 epochs is 0.8375."""
+    k = np.arange(1, 6, dtype=np.float64)
+    a = np.stack([np.full(5, 0.7), _curve(0.5, 1.0, 0.1, k)]).astype(np.float32)
+    for K in (1, 5, 30, 100):
+        pred, prm, bad = oracle.curve_fit(a, np.array([K, K]))
+        assert bad == 0
+        assert pred[0] == pytest.approx(0.7, abs=1e-6)
+        assert pred[1] == pytest.approx(_curve(0.5, 1.0, 0.1, K), abs=1e-3)
+    assert _curve(0.5, 1.0, 0.1, 30) == pytest.approx(0.8375)
+
+
+def test_curve_fit_noisy_median_error():
+    """sigma = 0.02 noise on k = 1..5, median absolute error at k = 30 over 200 random
+    curves of the family < 0.058 (the paper's 5.8% median error)."""
+    rng = np.random.default_rng(51)
+    k = np.arange(1, 6, dtype=np.float64)
+    b0, b1, b2 = rng.uniform(0.2, 2.0, 200), rng.uniform(0.8, 3.0, 200), rng.uniform(0.0, 0.3, 200)
+    a = np.clip(_curve(b0[:, None], b1[:, None], b2[:, None], k) + rng.normal(0, 0.02, (200, 5)), 0, 1)
+    pred, _, bad = oracle.curve_fit(a.astype(np.float32), np.full(200, 30))
+    assert bad == 0
+    assert np.median(np.abs(pred - _curve(b0, b1, b2, 30))) < 0.058
+
+
+def test_curve_fit_nnls_and_grid_optimal():
+    """CF1-CF2 against an independent solver: for every grid c the fp64 active-set-free NNLS
+    (scipy.optimize.nnls) optimum is no better than the chosen c's by more than rounding;
+    alpha, beta2 >= 0; the extrapolation is non-decreasing in the epoch count."""
+    from scipy.optimize import nnls
+    rng = np.random.default_rng(52)
+    S = 60
+    a = np.clip(rng.uniform(0.3, 0.9, (S, 1)) + np.cumsum(rng.uniform(-0.03, 0.08, (S, 5)), 1), 0, 1)
+    a = a.astype(np.float32)
+    pred, prm, bad = oracle.curve_fit(a, np.full(S, 30))
+    assert bad == 0 and (prm[:, 0] >= 0).all() and (prm[:, 2] >= 0).all()
+    y = 1.0 - a.astype(np.float64)
+    for s in range(S):
+        def sse(c):
+            X = np.stack([1.0 / (np.arange(1, 6) + c), np.ones(5)], 1)
+            return nnls(X, y[s])[1] ** 2
+        chosen = sse(float(prm[s, 1]))
+        best = min(sse(i / 8) for i in range(257))
+        assert chosen <= best + 1e-6
+        p2, _, _ = oracle.curve_fit(a[s:s + 1], np.array([60]))
+        assert p2[0] >= pred[s] - 1e-7
+
+
+def test_curve_fit_invalid():
+    a = np.array([[0.5, 0.6, 1.2, 0.7, 0.8], [0.5, 0.6, 0.7, 0.7, 0.8]], np.float32)
+    pred, _, bad = oracle.curve_fit(a, np.array([30, 0]))
+    assert bad == 2 and (pred == 0).all()
