@@ -193,6 +193,26 @@ int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p,
  *   (device pointers; root_buf used on the root only), enqueued on `stream`.
  * ------------------------------------------------------------------------- */
 /* ---------------------------------------------------------------------------
+ * ekya_curve_fit -- the micro-profiler's accuracy extrapolation (SURVEY 8(f)
+ * NEXT-2; "fit the accuracy-epoch points to the a non-linear curve model
+ * ... using a non-negative least squares solver ... extrapolate the accuracy that
+ * would be obtained by retraining with all the data for larger number of epochs";
+ * S:106-108).  acc [n_sets][n_points]: validation accuracy after epochs
+ * 1..n_points (2 <= n_points <= 32) of each (stream, config) micro-profile;
+ * full_epochs [n_sets] (>= 1).  Readings:
+ *   CF1 model acc(k) = 1 - (1/(b0 k + b1) + b2), b >= 0, written alpha/(k + c) + b2
+ *       (alpha = 1/b0, c = b1/b0); for fixed c a two-variable NNLS in (alpha, b2),
+ *       solved in closed form (active set).
+ *   CF2 c over the grid i/8, i = 0..256; lowest residual, lowest i on ties.
+ *   CF3 out_pred = 1 - (alpha/(K + c) + b2) clamped to [0,1] (the `post` input of the
+ *       tables); out_params [n_sets][3] = (alpha, c, b2) or NULL.
+ * One binary32 rounding per operation.  Invalid sets (accuracy outside [0,1] or
+ * full_epochs < 1): outputs 0, EKYA_ERR_DATA.
+ * ------------------------------------------------------------------------- */
+int ekya_curve_fit(ekya_handle* h, int64_t n_sets, int32_t n_points, const float* acc, const int32_t* full_epochs,
+                   float* out_pred, float* out_params, ekya_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * ekya_uniform_schedule -- the uniform scheduler the paper compares against
  * ("evenly splits the GPUs between video streams, and
  * each stream evenly partitions its allocated GPUs for retraining and inference

@@ -186,6 +186,17 @@ int ekya_pareto(ekya_handle* h, int64_t n_sets, int32_t n, const float* cost, co
     return launch_pareto(h, (long long)n_sets, n, cost, post, out_mask, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int ekya_curve_fit(ekya_handle* h, int64_t n_sets, int32_t n_points, const float* acc, const int32_t* full_epochs,
+                   float* out_pred, float* out_params, ekya_stream_t stream) {
+    if (!h) return EKYA_ERR_ARG;
+    if (n_sets < 0) return EKYA_ERR_SHAPE;
+    if (n_points < 2 || n_points > 32) return EKYA_ERR_LIMIT;
+    if (n_sets > 0 && (!acc || !full_epochs || !out_pred)) return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    return launch_curve_fit(h, (long long)n_sets, n_points, acc, full_epochs, out_pred, out_params,
+                            reinterpret_cast<cudaStream_t>(stream));
+}
+
 int ekya_place(ekya_handle* h, int32_t n_inst, int32_t n_jobs, int32_t units, int32_t gpus,
                const uint16_t* alloc, uint16_t* out_piece_job, uint32_t* out_piece_q, int16_t* out_piece_gpu,
                uint16_t* out_n_pieces, uint32_t* out_gpu_load, ekya_stream_t stream) {

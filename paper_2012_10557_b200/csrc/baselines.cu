@@ -149,3 +149,156 @@ int launch_pareto(ekya_handle* h, long long n_sets, int n, const float* cost, co
 }
 
 }  // namespace ekya
+
+// ------------------------------------------------------------------------
+// NEXT-2: micro-profiler curve fit (readings CF1-CF3)
+// ------------------------------------------------------------------------
+// One thread per (stream, config) set.  For every grid value c_i = i/8 the
+// regressor x_k = 1/(k + c_i) and its sums (sum x, sum x^2, n sum x^2 - (sum x)^2)
+// do not depend on the data: each CTA computes them once into shared memory, in
+// the oracle's operation order, so a set costs sum x y, the 2x2 solve and the
+// residual sums only.  Everything is one binary32 rounding per operation.
+namespace ekya {
+
+namespace {
+
+constexpr int kCfGrid = 257;
+constexpr int kCfMaxPoints = 32;
+
+struct CurveParams {
+    long long n_sets;
+    int np;
+    const float* acc;
+    const int* full_epochs;
+    float* out_pred;
+    float* out_params;
+    DevState* st;
+};
+
+template <int NP>
+__device__ __forceinline__ float cf_sse(const float* x, const float (&y)[NP], int n, float al, float b) {
+    float e = 0.0f;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        if (NP == kCfMaxPoints && k >= n) break;
+        const float d = fsub(fadd(fmul(al, x[k]), b), y[k]);
+        e = fadd(e, fmul(d, d));
+    }
+    return e;
+}
+
+// NP: compile-time point count (5 = the paper's "say, 5" epochs), or kCfMaxPoints for a
+// runtime count
+template <int NP>
+__global__ void __launch_bounds__(256) curve_fit_kernel(CurveParams p) {
+    extern __shared__ __align__(16) float cs[];
+    const int n = NP == kCfMaxPoints ? p.np : NP;
+    float* xs = cs;                                  // [kCfGrid][n]
+    float* sxs = xs + kCfGrid * n;                   // [kCfGrid] sum x
+    float* sxxs = sxs + kCfGrid;                     // [kCfGrid] sum x^2
+    float* dets = sxxs + kCfGrid;                    // [kCfGrid] n sum x^2 - (sum x)^2
+    const float fn = __int2float_rn(n);
+    for (int i = threadIdx.x; i < kCfGrid; i += blockDim.x) {
+        const float c = fmul(__int2float_rn(i), 0.125f);
+        float sx = 0.0f, sxx = 0.0f;
+        for (int k = 0; k < n; ++k) {
+            const float x = fdiv(1.0f, fadd(__int2float_rn(k + 1), c));
+            xs[i * n + k] = x;
+            sx = fadd(sx, x);
+            sxx = fadd(sxx, fmul(x, x));
+        }
+        sxs[i] = sx;
+        sxxs[i] = sxx;
+        dets[i] = fsub(fmul(fn, sxx), fmul(sx, sx));
+    }
+    __syncthreads();
+    for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < p.n_sets;
+         s += (long long)gridDim.x * blockDim.x) {
+        const int K = p.full_epochs[s];
+        bool ok = K >= 1;
+        float y[NP];
+        float sy = 0.0f;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            if (NP == kCfMaxPoints && k >= n) break;
+            const float a = __ldg(p.acc + s * n + k);
+            ok &= in01(a);
+            y[k] = fsub(1.0f, a);
+            sy = fadd(sy, y[k]);
+        }
+        float best = 0.0f, bal = 0.0f, bb = 0.0f, bc = 0.0f;
+        for (int i = 0; i < kCfGrid; ++i) {
+            const float* x = xs + i * n;
+            float sxy = 0.0f;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                if (NP == kCfMaxPoints && k >= n) break;
+                sxy = fadd(sxy, fmul(x[k], y[k]));
+            }
+            const float sx = sxs[i], sxx = sxxs[i], det = dets[i];
+            float al = 0.0f, b = 0.0f, e = 0.0f;
+            bool done = false;
+            if (det > 0.0f) {
+                const float a1 = fdiv(fsub(fmul(fn, sxy), fmul(sx, sy)), det);
+                const float b1 = fdiv(fsub(fmul(sxx, sy), fmul(sx, sxy)), det);
+                if (a1 >= 0.0f && b1 >= 0.0f) {
+                    al = a1;
+                    b = b1;
+                    e = cf_sse<NP>(x, y, n, al, b);
+                    done = true;
+                }
+            }
+            if (!done) {
+                const float m = fdiv(sy, fn);
+                const float b0 = m > 0.0f ? m : 0.0f;
+                const float e0 = cf_sse<NP>(x, y, n, 0.0f, b0);
+                const float q = sxx > 0.0f ? fdiv(sxy, sxx) : 0.0f;
+                const float a0 = q > 0.0f ? q : 0.0f;
+                const float e1 = cf_sse<NP>(x, y, n, a0, 0.0f);
+                if (e1 < e0) {
+                    al = a0;
+                    b = 0.0f;
+                    e = e1;
+                } else {
+                    al = 0.0f;
+                    b = b0;
+                    e = e0;
+                }
+            }
+            if (i == 0 || e < best) {
+                best = e;
+                bal = al;
+                bb = b;
+                bc = fmul(__int2float_rn(i), 0.125f);
+            }
+        }
+        float pr = fsub(1.0f, fadd(fdiv(bal, fadd(__int2float_rn(K), bc)), bb));
+        pr = pr < 0.0f ? 0.0f : (pr > 1.0f ? 1.0f : pr);
+        if (!ok) flag_data_error(p.st);
+        p.out_pred[s] = ok ? pr : 0.0f;
+        if (p.out_params) {
+            p.out_params[s * 3] = ok ? bal : 0.0f;
+            p.out_params[s * 3 + 1] = ok ? bc : 0.0f;
+            p.out_params[s * 3 + 2] = ok ? bb : 0.0f;
+        }
+    }
+}
+
+}  // namespace
+
+int launch_curve_fit(ekya_handle* h, long long n_sets, int np, const float* acc, const int* full_epochs,
+                     float* out_pred, float* out_params, cudaStream_t s) {
+    if (n_sets == 0) return EKYA_OK;
+    CurveParams p{n_sets, np, acc, full_epochs, out_pred, out_params, h->dstate};
+    const size_t smem = (size_t)kCfGrid * (np + 3) * 4;
+    auto k = np == 5 ? curve_fit_kernel<5> : curve_fit_kernel<kCfMaxPoints>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return EKYA_ERR_CUDA;
+    const long long need = (n_sets + 255) / 256;
+    const int grid = (int)std::min<long long>(need, (long long)h->sm_count * 8);
+    k<<<grid, 256, smem, s>>>(p);
+    h->launches++;
+    return cuda_status(cudaGetLastError());
+}
+
+}  // namespace ekya

@@ -45,6 +45,9 @@ int launch_uniform(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int
 int launch_pareto(ekya_handle* h, long long n_sets, int n, const float* cost, const float* post,
                   uint32_t* out_mask, cudaStream_t s);
 
+int launch_curve_fit(ekya_handle* h, long long n_sets, int np, const float* acc, const int* full_epochs,
+                     float* out_pred, float* out_params, cudaStream_t s);
+
 inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? EKYA_OK : EKYA_ERR_CUDA; }
 
 }  // namespace ekya

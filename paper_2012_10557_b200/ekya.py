@@ -26,7 +26,7 @@ LAMBDA_NONE = 7
 SYMBOLS = ["ekya_create", "ekya_destroy", "ekya_last_error", "ekya_launch_count", "ekya_version",
            "ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate",
            "ekya_comm_unique_id", "ekya_comm_init", "ekya_gather_decisions", "ekya_counters", "ekya_place",
-           "ekya_checkpoint_decide", "ekya_uniform_schedule", "ekya_pareto"]
+           "ekya_checkpoint_decide", "ekya_uniform_schedule", "ekya_pareto", "ekya_curve_fit"]
 
 
 class EkyaError(RuntimeError):
@@ -93,6 +93,8 @@ def load_library(path: str = LIB_PATH):
     L.ekya_uniform_schedule.restype = ctypes.c_int
     L.ekya_pareto.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P, P, P, P]
     L.ekya_pareto.restype = ctypes.c_int
+    L.ekya_curve_fit.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P, P, P, P, P]
+    L.ekya_curve_fit.restype = ctypes.c_int
     L.ekya_place.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P]
     L.ekya_place.restype = ctypes.c_int
     L.ekya_checkpoint_decide.argtypes = [P, ctypes.c_int64] + [P] * 8 + [P]
@@ -249,6 +251,15 @@ def ekya_pareto(h: Handle, cost, post, out_mask, stream=None):
     _check(code, "ekya_pareto")
 
 
+def ekya_curve_fit(h: Handle, acc, full_epochs, out_pred, out_params=None, stream=None):
+    L = load_library()
+    S, n = acc.shape
+    code = L.ekya_curve_fit(h.ptr, S, n, _ptr(acc, torch.float32, "acc"), _ptr(full_epochs, torch.int32, "full_epochs"),
+                            _ptr(out_pred, torch.float32, "out_pred"),
+                            _ptr(out_params, torch.float32, "out_params", True), _stream(stream))
+    _check(code, "ekya_curve_fit")
+
+
 def ekya_place(h: Handle, units: int, gpus: int, alloc, out_piece_job, out_piece_q, out_piece_gpu, out_n_pieces,
                out_gpu_load=None, stream=None):
     L = load_library()
@@ -393,3 +404,13 @@ def pareto(h, cost, post, stream=None):
     out = torch.empty(cost.shape[:-1], dtype=torch.uint32, device=cost.device)
     ekya_pareto(h, cost, post, out, stream=stream)
     return out
+
+
+def curve_fit(h, acc, full_epochs, stream=None):
+    """Micro-profiler curve fit: acc [S][P] (epochs 1..P), full_epochs [S] int32 ->
+    (predicted accuracy [S], params [S][3] = (alpha, c, beta2))."""
+    S = acc.shape[0]
+    pred = torch.empty((S,), dtype=torch.float32, device=acc.device)
+    prm = torch.empty((S, 3), dtype=torch.float32, device=acc.device)
+    ekya_curve_fit(h, acc, full_epochs, pred, prm, stream=stream)
+    return pred, prm

@@ -513,3 +513,40 @@ def test_pareto_bitexact(h):
         c[rng.uniform(size=c.shape) < 0.1] = np.inf
         m = ek().pareto(h, torch.from_numpy(c).cuda(), torch.from_numpy(p).cuda())
         assert_eq(m, oracle.pareto(c, p), f"pareto mask n={n}")
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: micro-profiler curve fit
+# ---------------------------------------------------------------------------
+def curve_inputs(S, P, seed):
+    """Profile-epoch accuracies from the Optimus family plus noise (sigma 0.02),
+    some constant and some degenerate sets, and the configs' full epoch counts."""
+    rng = np.random.default_rng(seed)
+    k = np.arange(1, P + 1, dtype=np.float64)
+    b0, b1, b2 = rng.uniform(0.1, 2.0, S), rng.uniform(0.8, 3.0, S), rng.uniform(0.0, 0.3, S)
+    a = 1.0 - (1.0 / (b0[:, None] * k + b1[:, None]) + b2[:, None]) + rng.normal(0, 0.02, (S, P))
+    a[::7] = rng.uniform(0.2, 0.9, (len(a[::7]), 1))             # constant profiles
+    a[3::11] = a[3::11, ::-1]                                      # decreasing profiles
+    a = np.clip(a, 0, 1).astype(np.float32)
+    K = rng.integers(P, 60, S).astype(np.int32)
+    return a, K
+
+
+@pytest.mark.parametrize("P", [5, 2, 9])
+def test_curve_fit_bitexact(h, P):
+    a, K = curve_inputs(4000, P, 60 + P)
+    pred, prm = ek().curve_fit(h, torch.from_numpy(a).cuda(), torch.from_numpy(K).cuda())
+    op, oprm, bad = oracle.curve_fit(a, K)
+    assert bad == 0 and h.last_error() == 0
+    assert_eq(pred, op, "predicted accuracy")
+    assert_eq(prm, oprm, "params")
+
+
+def test_curve_fit_invalid(h):
+    a, K = curve_inputs(64, 5, 70)
+    a[3, 2] = 1.5
+    K[5] = 0
+    pred, prm = ek().curve_fit(h, torch.from_numpy(a).cuda(), torch.from_numpy(K).cuda())
+    op, oprm, bad = oracle.curve_fit(a, K)
+    assert bad == 2 and h.last_error() == -6
+    assert_eq(pred, op, "predicted accuracy")
