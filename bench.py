@@ -381,6 +381,7 @@ def run_ours(args, rank, world, local_rank):
 
     context = run_context(ek, h, dev, args) if rank == 0 and args.context else None
     if context is not None:
+        context.update(run_next2(ek, h, w, dev))
         context.update(run_next3(ek, h, w, T, O, dev))
         context.update(run_next4(ek, h, w, O, dev))
     if rank != 0:
@@ -505,6 +506,29 @@ def run_next3(ek, h, w, T, O, dev):
             "next3_pareto": {"sets": B * V, "configs": G, "ms": ms_p, "sets_per_s": B * V / (ms_p / 1000.0),
                              "hbm_frac": bytes_p / (ms_p / 1000.0) / 1e9 / peak,
                              "mean_frontier_size": frontier}}
+
+
+def run_next2(ek, h, w, dev):
+    """SURVEY 8(f) NEXT-2 beside the step: the micro-profiler curve fit for every
+    (stream, config) of 65,536 config-4 streams (5 profiled epochs, "say, 5"),
+    extrapolated to 30 epochs -- the `post` input of a table."""
+    S, P = w.B * w.cfg.n_gamma, 5
+    g = torch.Generator(device="cpu").manual_seed(9)
+    k = torch.arange(1, P + 1, dtype=torch.float64)
+    b0 = 0.1 + 1.9 * torch.rand(S, 1, generator=g, dtype=torch.float64)
+    b1 = 0.8 + 2.2 * torch.rand(S, 1, generator=g, dtype=torch.float64)
+    b2 = 0.3 * torch.rand(S, 1, generator=g, dtype=torch.float64)
+    a = (1.0 - (1.0 / (b0 * k + b1) + b2) + 0.02 * torch.randn(S, P, generator=g, dtype=torch.float64))
+    acc = a.clamp(0, 1).to(torch.float32).to(dev)
+    K = torch.full((S,), 30, dtype=torch.int32, device=dev)
+    pred = torch.empty((S,), dtype=torch.float32, device=dev)
+    ms = _time_ms(lambda: ek.ekya_curve_fit(h, acc, K, pred), reps=3)
+    assert h.last_error() == 0
+    # algorithmic work per set: 257 grid points x (the 2x2 NNLS + residuals over 5 points)
+    flops = S * 257 * (2 * P + 10 + 4 * P)
+    peak_alu = 148 * 128 * 1965e6 / 1e12
+    return {"next2_curve_fit": {"sets": S, "points": P, "ms": ms, "sets_per_s": S / (ms / 1000.0),
+                                "alu_frac": flops / (ms / 1000.0) / 1e12 / peak_alu}}
 
 
 def run_next4(ek, h, w, O, dev):
