@@ -34,9 +34,11 @@ constexpr int kListThreads = 1024;
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
 // per-stream table footprint: lad[U+1] + tvc[U+1][rs] (8-byte entries)
-// GRID: lad[U+1] (u32 byte offsets of the lambda blocks) + tvc[8][U+1] (lambda-major)
+// GRID: lad[U+1] (u8 lambda*, 7 = none) + tvc[8][U+1] (lambda-major).  The quads' lanes read
+// lad[4 lane + const]: byte entries keep those reads on distinct banks (4-byte entries at a
+// 16-byte stride conflicted 4-way)
 __host__ __device__ inline size_t grid_tab_bytes(int U) {
-    return a16((size_t)(U + 1) * 4) + a16((size_t)(U + 1) * kSlots * 8);
+    return a16((size_t)(U + 1)) + a16((size_t)(U + 1) * kSlots * 8);
 }
 __host__ __device__ inline size_t tab_bytes(int U, int rs = kSlots) {
     return a16((size_t)(U + 1)) + a16((size_t)(U + 1) * rs * 8);
@@ -57,9 +59,9 @@ __device__ __forceinline__ int row_of(int c, int U) {
     return r;
 }
 
-__device__ __forceinline__ unsigned ld_shared_u32(unsigned a) {
+__device__ __forceinline__ unsigned ld_shared_u8(unsigned a) {
     unsigned v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
 }
 __device__ __forceinline__ uint2 ld_shared_v2(unsigned a) {
@@ -69,13 +71,13 @@ __device__ __forceinline__ uint2 ld_shared_v2(unsigned a) {
 }
 
 struct GridTabs {
-    uint32_t* lad;
+    uint8_t* lad;
     uint2* tvc;
 };
 __device__ __forceinline__ GridTabs carve_grid_tabs(unsigned char* p, int U) {
     GridTabs t;
-    t.lad = reinterpret_cast<uint32_t*>(p);
-    t.tvc = reinterpret_cast<uint2*>(p + a16((size_t)(U + 1) * 4));
+    t.lad = p;
+    t.tvc = reinterpret_cast<uint2*>(p + a16((size_t)(U + 1)));
     return t;
 }
 
@@ -167,6 +169,7 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
     unsigned char* mine = smem + (use_qs ? a16(4 * nq_tab * sizeof(uint2)) : 0) + (size_t)warp * p.warp_bytes;
     StreamIn* sin = reinterpret_cast<StreamIn*>(mine);
     GridTabs T = carve_grid_tabs(mine + a16(sizeof(StreamIn)), U);
+    const int lblk = (U + 1) * 8;   // bytes per lambda block of tvc
     const int NC = (U + 1) * (U + 2) / 2;
 
     for (int t = threadIdx.x; use_qs && t < (int)(4 * nq_tab); t += blockDim.x) {
@@ -191,8 +194,8 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
             const long long item = b * V + v;
             if (ok) {
                 warp_load_stream(sin, p.t, item, nG, nL);
-                warp_build_tables<GM, NGT, NLT, kSlots, 1, true>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min, T.lad,
-                                                                 T.tvc);
+                warp_build_tables<GM, NGT, NLT, kSlots, 1, true, uint8_t>(sin, U, nG, nL, d.unit_gpu_seconds, d.a_min,
+                                                                          T.lad, T.tvc);
             }
             // Flat write of the stream's cells [f0, f0 + NC) in aligned quads of 4
             // cells: one 16-B value store + one 4-B config store per quad (the
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
                     const unsigned char* tv = reinterpret_cast<const unsigned char*>(T.tvc);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const uint2 vc = *reinterpret_cast<const uint2*>(tv + T.lad[ri[j]] + rt[j] * 8);
+                        const uint2 vc = *reinterpret_cast<const uint2*>(tv + T.lad[ri[j]] * lblk + rt[j] * 8);
                         v4[j] = __uint_as_float(vc.x);
                         cfg4 |= vc.y << (8 * j);
                     }
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
                         const unsigned wj = j < 2 ? s2.x : s2.y;
                         const unsigned ri = __byte_perm(wj, 0u, 0x4440u + 2u * (j & 1));
                         const unsigned rt = __byte_perm(wj, 0u, 0x4441u + 2u * (j & 1));
-                        const unsigned lo = ld_shared_u32(lad_s + 4 * ri);
+                        const unsigned lo = ld_shared_u8(lad_s + ri) * (unsigned)lblk;
                         const uint2 vc = ld_shared_v2(tvc_s + lo + rt * 8);
                         v4[j] = __uint_as_float(vc.x);
                         cfg4 |= vc.y << (8 * j);
