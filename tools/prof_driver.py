@@ -1,5 +1,5 @@
-"""Launch each hot-path kernel a few times on a reduced-but-representative batch
-(for ncu captures; timings taken under ncu are never bench values)."""
+"""Launch each hot-path kernel once at the bench sizes (for ncu captures; timings taken
+under ncu are never bench values), then each SURVEY 8(f) NEXT-row kernel once."""
 import argparse
 import os
 import sys
@@ -15,14 +15,28 @@ ap.add_argument("--n-inst", type=int, default=65536)
 ap.add_argument("--n-alloc", type=int, default=4096)
 ap.add_argument("--n-query", type=int, default=65536)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--no-next", dest="next", action="store_false")
 a = ap.parse_args()
 torch.cuda.set_device(0)
+dev = torch.device("cuda", 0)
 h = ekya.Handle(0)
 w = bench.Workload(a.n_inst, a.n_alloc, a.n_query)
-T, rows, P = bench.gen_device(w, torch.device("cuda", 0))
-O = bench.Outputs(w, torch.device("cuda", 0))
+T, rows, P = bench.gen_device(w, dev)
+O = bench.Outputs(w, dev)
 for _ in range(a.reps):
     bench.run_step(ekya, h, w, T, rows, P, O)
+if a.next:
+    B, V, G = w.B, w.V, T["cost"].shape[2]
+    S = B * G
+    acc = torch.rand((S, 5), device=dev)
+    ekya.curve_fit(h, acc, torch.full((S,), 30, dtype=torch.int32, device=dev))
+    ekya.uniform_schedule(h, T, *w.args)
+    ekya.pareto(h, T["cost"], T["post"])
+    ekya.place(h, O.dec[0]["alloc"], w.U, 8)
+    n = B * V
+    tau = torch.rand(n, device=dev) * 100
+    ekya.checkpoint_decide(h, tau, tau * 0.5, torch.full((n,), 100.0, device=dev), torch.rand(n, device=dev),
+                           torch.rand(n, device=dev), torch.rand(n, device=dev), torch.rand(n, device=dev))
 torch.cuda.synchronize()
 assert h.last_error() == 0
 print("launches", h.launch_count())

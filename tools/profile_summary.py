@@ -11,7 +11,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NAMES = [("cluster2_kernel", "profile_cluster"), ("cluster_kernel", "profile_cluster"),
          ("radius_kernel", "profile_radius"), ("grid_kernel", "eval_grid"), ("list_kernel", "eval_list"),
-         ("thief_kernel<0>", "thief_steepest"), ("thief_kernel<1>", "thief_literal")]
+         ("thief_kernel<0>", "thief_steepest"), ("thief_kernel<1>", "thief_literal"),
+         ("curve_fit_kernel", "next2_curve_fit"), ("uniform_kernel", "next3_uniform"),
+         ("pareto_kernel", "next3_pareto"), ("place_kernel", "next4_placement"),
+         ("checkpoint_kernel", "next4_checkpoint")]
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_issued.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
@@ -85,14 +88,16 @@ def main(ev, tag):
           "|---|---|---|---|---|---|---|---|"]
     step_ms = bench["ms_per_step"]
     fd = {n: d for n, d in full}
-    for n in ["profile_cluster", "profile_radius", "eval_grid", "eval_list", "thief_steepest", "thief_literal"]:
+    for n in ["profile_cluster", "profile_radius", "eval_grid", "eval_list", "thief_steepest", "thief_literal",
+              "next2_curve_fit", "next3_uniform", "next3_pareto", "next4_placement", "next4_checkpoint"]:
         ms = per.get(n, [])
         nm = sum(ms) / len(ms) if ms else float("nan")
         share = sum(ms) / tot if ms else float("nan")
-        b = bench["rows"].get(n, {})
+        b = bench["rows"].get(n, bench.get("context", {}).get(n, {}))
         d = fd.get(n, {})
         g = traffic.get(n, float("nan")) / 1e9
-        md.append(f"| {n} | {nm:.3f} | {share:.3f} | {b.get('ms_per_launch', float('nan')):.3f} | "
+        bms = b.get("ms_per_launch", b.get("ms", float("nan")))
+        md.append(f"| {n} | {nm:.3f} | {share:.3f} | {bms:.3f} | "
                   f"{b.get('share', float('nan')):.3f} | {g:.2f} | "
                   f"{d.get('sm__inst_issued.avg.pct_of_peak_sustained_active', ('',))[0]} | "
                   f"{d.get('sm__warps_active.avg.pct_of_peak_sustained_active', ('',))[0]} |")
