@@ -101,6 +101,8 @@ def lib():
         L.orc_uniform.restype = ctypes.c_int64
         L.orc_pareto.argtypes = [ctypes.c_int64, ctypes.c_int32, P, P, P]
         L.orc_pareto.restype = ctypes.c_int64
+        L.orc_window.argtypes = [ctypes.POINTER(Dims), P, P, P, P, P, ctypes.c_int32, P, P, P]
+        L.orc_window.restype = ctypes.c_int64
         L.orc_curve_fit.argtypes = [ctypes.c_int64, ctypes.c_int32, P, P, P, P]
         L.orc_curve_fit.restype = ctypes.c_int64
         L.orc_pack.argtypes = [ctypes.c_int32, P, ctypes.c_int32, P, P]
@@ -397,3 +399,18 @@ def curve_fit(acc, full_epochs):
     if bad < 0:
         raise ValueError("oracle: invalid curve-fit shape")
     return pred, prm, int(bad)
+
+
+def window(inst: Instances, mode: int = STEEPEST):
+    """The retraining window as a timeline with the thief re-invoked at each completion
+    (readings W1-W6): realized window-average accuracy [B], invocations [B], completion
+    time per stream [B][V] (1 = none), bad."""
+    d = inst.dims()
+    B, V = inst.B, inst.V
+    avg = np.zeros(B, np.float32)
+    ev = np.zeros(B, np.uint32)
+    done = np.zeros((B, V), np.float32)
+    bad = lib().orc_window(ctypes.byref(d), *inst.tables(), int(mode), _p(avg), _p(ev), _p(done))
+    if bad < 0:
+        raise ValueError("oracle: invalid window arguments")
+    return avg, ev, done, int(bad)

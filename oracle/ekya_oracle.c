@@ -969,3 +969,128 @@ int64_t orc_curve_fit(int64_t n_sets, int32_t n_points, const float* acc, const 
     }
     return bad;
 }
+
+/* ========================================================================
+ * NEXT-1: the retraining window as a timeline, with the thief
+ * re-invoked at every retraining completion ("Algorithm 1 is invoked at
+ * the beginning of each retraining window, as well as on the completion of
+ * every training job during the window to reallocate resources to the other
+ * training and inference jobs").  Readings W1-W6 in DESIGN.md.
+ * Time is the window fraction tau in [0, 1]; every step one binary32 rounding.
+ * ======================================================================== */
+/* Per instance: st_v 0 idle / 1 retraining (config g_v, remaining work R_v in cost
+ * units) / 2 done; m_v the stream's model accuracy (stale, then post of its config).
+ * Invocation at tau (W2): the residual problem is the instance's own tables with
+ *   stale' = m_v; idle: cost' = fl(cost fl(1/fl(1 - tau))) (the remaining window is
+ *   shorter, W3); retraining: only config g_v, cost' = fl(R_v fl(1/fl(1 - tau)));
+ *   done: no config.  The thief (same mode, from its fair start, Alg. 1 line 2) decides
+ *   allocations and configs for [tau, 1].
+ * W4: a stream retraining with config g at rt units finishes at
+ *   tau_v = fl(tau + fl(f fl(1 - tau))), f = rule 1's fraction of the residual
+ *   window; the next event is the earliest tau_v (1 if none).
+ * W5: inference accuracy over [tau, tau*] is fl(factor_lambda m_v) (lambda from the
+ *   thief's config, none -> 0); A_v += fl(fl(tau* - tau) fl(factor m_v)).
+ * W6: at tau*: streams with tau_v <= tau* are done (m_v = post_g); the others
+ *   retraining keep R_v = fl(R_v' fl(1 - fl(fl(tau* - tau) / fl(tau_v - tau)))) with
+ *   R_v' their residual work in cost units (idle streams starting: cost_g); a config-0
+ *   choice for a retraining stream pauses it.  At most V + 1 invocations.
+ * Outputs: out_avg[b] = fl(sum_v A_v (sequential) / V); out_events[b] = invocations;
+ * out_done[b][v] = completion time (1 if none). */
+int64_t orc_window(const orc_dims* d, const float* stale, const float* cost, const float* post,
+                   const uint16_t* lmu, const float* lf, int32_t mode, float* out_avg, uint32_t* out_events,
+                   float* out_done)
+{
+    if (!orc_dims_valid(d) || (mode != 0 && mode != 1)) return -1;
+    const int32_t V = d->n_streams, nG = d->n_gamma, nL = d->n_lambda, J = 2 * V;
+    orc_dims d1 = *d;
+    d1.n_inst = 1;
+    float* st1 = (float*)malloc(sizeof(float) * V);
+    float* c1 = (float*)malloc(sizeof(float) * (size_t)(V * nG + 1));
+    uint16_t* a1 = (uint16_t*)malloc(sizeof(uint16_t) * J);
+    uint8_t* cf1 = (uint8_t*)malloc((size_t)V);
+    float* m = (float*)malloc(sizeof(float) * V);
+    float* R = (float*)malloc(sizeof(float) * V);
+    float* A = (float*)malloc(sizeof(float) * V);
+    float* tv = (float*)malloc(sizeof(float) * V);
+    int32_t* stt = (int32_t*)malloc(sizeof(int32_t) * V);
+    int32_t* g = (int32_t*)malloc(sizeof(int32_t) * V);
+    int64_t bad = 0;
+    for (int64_t b = 0; b < d->n_inst; ++b) {
+        orc_inst in = orc_instance(d, b, stale, cost, post, lmu, lf);
+        if (!orc_instance_valid(d, &in)) {
+            ++bad;
+            out_avg[b] = 0.0f;
+            out_events[b] = 0;
+            for (int32_t v = 0; v < V; ++v) out_done[b * V + v] = 0.0f;
+            continue;
+        }
+        for (int32_t v = 0; v < V; ++v) {
+            m[v] = in.stale[v]; R[v] = 0.0f; A[v] = 0.0f; stt[v] = 0; g[v] = 0;
+            out_done[b * V + v] = 1.0f;
+        }
+        float tau = 0.0f;
+        uint32_t ev = 0;
+        while (tau < 1.0f && ev <= (uint32_t)V) {
+            const float rem = 1.0f - tau;
+            const float sc = 1.0f / rem;
+            for (int32_t v = 0; v < V; ++v) {
+                st1[v] = m[v];
+                for (int32_t k = 0; k < nG; ++k) {
+                    const float c = in.cost[(int64_t)v * nG + k];
+                    float cs = INFINITY;
+                    if (stt[v] == 0) cs = isinf(c) ? c : c * sc;
+                    else if (stt[v] == 1 && k + 1 == g[v]) cs = R[v] * sc;
+                    c1[v * nG + k] = cs;
+                }
+            }
+            uint64_t s1;
+            orc_thief(&d1, st1, c1, in.post, in.lmu, in.lf, mode, a1, cf1, &s1, NULL, NULL);
+            ++ev;
+            /* W4: completion times of the streams retraining in [tau, 1] */
+            float tnext = 1.0f;
+            for (int32_t v = 0; v < V; ++v) {
+                const int32_t gv = cf1[v] & 31, rt = a1[2 * v + 1];
+                tv[v] = 2.0f;
+                if (gv > 0) {
+                    const float f = orc_retrain_fraction(c1[v * nG + gv - 1], rt, d->unit_gpu_seconds);
+                    const float dt = f * rem;
+                    tv[v] = tau + dt;
+                    if (tv[v] < tnext) tnext = tv[v];
+                }
+            }
+            /* W5: accuracy over [tau, tnext] */
+            const float span = tnext - tau;
+            for (int32_t v = 0; v < V; ++v) {
+                const int32_t l = cf1[v] >> 5;
+                const float fac = l == ORC_LAMBDA_NONE ? 0.0f : in.lf[(int64_t)v * nL + l];
+                const float acc = fac * m[v];
+                const float seg = span * acc;
+                A[v] = A[v] + seg;
+            }
+            /* W6: completions and remaining work */
+            for (int32_t v = 0; v < V; ++v) {
+                const int32_t gv = cf1[v] & 31;
+                if (gv == 0) continue;
+                if (tv[v] <= tnext) {
+                    stt[v] = 2;
+                    m[v] = in.post[(int64_t)v * nG + gv - 1];
+                    out_done[b * V + v] = tv[v];
+                } else {
+                    const float base = stt[v] == 1 ? R[v] : in.cost[(int64_t)v * nG + gv - 1];
+                    const float q = span / (tv[v] - tau);
+                    const float keep = 1.0f - q;
+                    R[v] = base * keep;
+                    stt[v] = 1;
+                    g[v] = gv;
+                }
+            }
+            tau = tnext;
+        }
+        float sum = 0.0f;
+        for (int32_t v = 0; v < V; ++v) sum = sum + A[v];
+        out_avg[b] = sum / (float)V;
+        out_events[b] = ev;
+    }
+    free(st1); free(c1); free(a1); free(cf1); free(m); free(R); free(A); free(tv); free(stt); free(g);
+    return bad;
+}

@@ -92,6 +92,12 @@ int64_t orc_pareto(int64_t n_sets, int32_t n, const float* cost, const float* po
 int64_t orc_curve_fit(int64_t n_sets, int32_t n_points, const float* acc, const int32_t* full_epochs,
                       float* out_pred, float* out_params);
 
+/* ---- NEXT-1: the window as a timeline with re-invocation at completions (P:1022,
+ *      P:1123-1125; readings W1-W6) ---- */
+int64_t orc_window(const orc_dims* d, const float* stale, const float* cost, const float* post,
+                   const uint16_t* lmu, const float* lf, int32_t mode, float* out_avg, uint32_t* out_events,
+                   float* out_done);
+
 #ifdef __cplusplus
 }
 #endif

@@ -793,3 +793,54 @@ def test_curve_fit_invalid():
     a = np.array([[0.5, 0.6, 1.2, 0.7, 0.8], [0.5, 0.6, 0.7, 0.7, 0.8]], np.float32)
     pred, _, bad = oracle.curve_fit(a, np.array([30, 0]))
     assert bad == 2 and (pred == 0).all()
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1: the window as a timeline, thief re-invoked at each completion
+# ---------------------------------------------------------------------------
+def test_window_single_stream_closed_form():
+    """One stream, U = 4, uT = 10 GPU-s/unit, stale 0.5, one config (cost 10, post 0.9), one
+    lambda (factor 1).  The thief ends at r_train = 3 (window average 0.9 - 0.4/3 beats
+    r_train = 2's 0.7 and r_train = 1's 0.5), so retraining ends at tau = 1/3; re-invoked,
+    the stream is done (model 0.9).  Realized average = tau1 0.5 + (1 - tau1) 0.9, written
+    out in binary32 (W4-W6), and 23/30 in exact rationals."""
+    inst = oracle.Instances([[0.5]], [[[10.0]]], [[[0.9]]], [[[1]]], [[[1.0]]], 4, 1, 10.0, 0.0)
+    a, c, s, mean, steps, _ = oracle.thief(inst, oracle.STEEPEST)
+    assert a.tolist() == [[1, 3]]
+    avg, ev, done, bad = oracle.window(inst, oracle.STEEPEST)
+    f = np.float32(10.0) / (np.float32(3.0) * np.float32(10.0))
+    t1 = np.float32(0.0) + f * (np.float32(1.0) - np.float32(0.0))
+    seg1 = t1 * (np.float32(1.0) * np.float32(0.5))
+    seg2 = (np.float32(1.0) - t1) * (np.float32(1.0) * np.float32(0.9))
+    assert bad == 0 and ev[0] == 2 and done[0, 0] == t1
+    assert avg[0] == np.float32(np.float32(0.0) + seg1 + seg2) / np.float32(1.0)
+    assert avg[0] == pytest.approx(23 / 30, abs=1e-6)
+
+
+def test_window_without_retraining_is_the_thief_estimate():
+    """No retraining config finishes (all +inf): one invocation over the whole window and
+    the realized average equals the thief's estimate (W5 with tau* = 1)."""
+    c = synth.SchedConfig(**{**synth.CONFIG2.__dict__, "n_inst": 50})
+    inst = make_inst(c, 0, 50)
+    inst2 = oracle.Instances(inst.stale, np.full_like(inst.cost, np.inf), inst.post, inst.lam_min_units,
+                             inst.lam_factor, inst.units, inst.steal_units, inst.unit_gpu_seconds, inst.a_min)
+    avg, ev, done, bad = oracle.window(inst2, oracle.STEEPEST)
+    mean = oracle.thief(inst2, oracle.STEEPEST)[3]
+    assert bad == 0 and (ev == 1).all() and (done == 1).all()
+    np.testing.assert_allclose(avg, mean, atol=2e-6)
+
+
+def test_window_invariants():
+    """At most V + 1 invocations; every completion time in (0, 1]; a stream completes at most
+    once; 0 <= average <= 1; both modes; re-invocation (freed units return to inference,
+    C4(b)) does not lose to the t = 0 estimate on average over many instances."""
+    for cfg in (synth.CONFIG1, synth.CONFIG2):
+        c = synth.SchedConfig(**{**cfg.__dict__, "n_inst": 120})
+        inst = make_inst(c, 0, 120)
+        for mode in (oracle.STEEPEST, oracle.LITERAL):
+            avg, ev, done, bad = oracle.window(inst, mode)
+            assert bad == 0
+            assert (ev >= 1).all() and (ev <= inst.V + 1).all()
+            assert ((done > 0) & (done <= 1)).all()
+            assert ((avg >= 0) & (avg <= 1)).all()
+            assert avg.mean() >= oracle.thief(inst, mode)[3].mean() - 1e-3
