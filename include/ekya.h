@@ -193,6 +193,28 @@ int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p,
  *   (device pointers; root_buf used on the root only), enqueued on `stream`.
  * ------------------------------------------------------------------------- */
 /* ---------------------------------------------------------------------------
+ * ekya_window_schedule -- the retraining window as a timeline (SURVEY 8(f)
+ * NEXT-1; "Algorithm 1 is invoked at the beginning of each retraining
+ * window, as well as on the completion of every training job during the window
+ * to reallocate resources to the other training and inference jobs";
+ * P:1123-1125).  Readings W1-W6: time is the window fraction tau;
+ * at tau = 0 and at every retraining completion the thief (`mode`) re-plans the
+ * residual window on residual tables (finished streams: their new model accuracy
+ * as `stale` and no config; streams retraining: only their config, remaining
+ * work; idle streams: all configs; costs scaled by 1/(1 - tau)); a stream's
+ * inference accuracy over each interval is factor(lambda) x model accuracy.
+ * out_avg [B]: realized window-average accuracy over the streams; out_events [B]:
+ * thief invocations (<= V + 1); out_done [B][V]: completion time (1 = none).
+ * `workspace` (device, >= ekya_window_workspace_bytes(d) bytes, caller-owned)
+ * holds the residual tables and the timeline state.  V <= 127.  Invalid
+ * instances: outputs 0, EKYA_ERR_DATA.
+ * ------------------------------------------------------------------------- */
+size_t ekya_window_workspace_bytes(const ekya_dims* d);
+int ekya_window_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int mode, void* workspace,
+                         size_t workspace_bytes, float* out_avg, uint32_t* out_events, float* out_done,
+                         ekya_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * ekya_curve_fit -- the micro-profiler's accuracy extrapolation (SURVEY 8(f)
  * NEXT-2; "fit the accuracy-epoch points to the a non-linear curve model
  * ... using a non-negative least squares solver ... extrapolate the accuracy that

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libekya.so")
-SOURCES = ["api.cu", "eval.cu", "thief.cu", "profile.cu", "comm.cu", "place.cu", "baselines.cu"]
+SOURCES = ["api.cu", "eval.cu", "thief.cu", "profile.cu", "comm.cu", "place.cu", "baselines.cu", "window.cu"]
 HEADERS = ["ekya_common.cuh", "stream_tables.cuh", "launch.h"]
 
 

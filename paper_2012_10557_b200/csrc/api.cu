@@ -186,6 +186,26 @@ int ekya_pareto(ekya_handle* h, int64_t n_sets, int32_t n, const float* cost, co
     return launch_pareto(h, (long long)n_sets, n, cost, post, out_mask, reinterpret_cast<cudaStream_t>(stream));
 }
 
+size_t ekya_window_workspace_bytes(const ekya_dims* d) {
+    if (!d || d->n_inst < 0 || d->n_streams < 1) return 0;
+    return window_workspace_bytes(*d);
+}
+
+int ekya_window_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int mode, void* workspace,
+                         size_t workspace_bytes, float* out_avg, uint32_t* out_events, float* out_done,
+                         ekya_stream_t stream) {
+    if (!h) return EKYA_ERR_ARG;
+    int why = EKYA_OK;
+    if (!dims_ok(d, &why)) return why;
+    if (!tables_ok(d, t)) return EKYA_ERR_ARG;
+    if (mode != EKYA_THIEF_STEEPEST && mode != EKYA_THIEF_LITERAL) return EKYA_ERR_ARG;
+    if (d->n_streams > 127) return EKYA_ERR_LIMIT;
+    if (d->n_inst > 0 && (!out_avg || !out_events || !out_done)) return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    return launch_window(h, *d, *t, mode, workspace, workspace_bytes, out_avg, out_events, out_done,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
 int ekya_curve_fit(ekya_handle* h, int64_t n_sets, int32_t n_points, const float* acc, const int32_t* full_epochs,
                    float* out_pred, float* out_params, ekya_stream_t stream) {
     if (!h) return EKYA_ERR_ARG;

@@ -48,6 +48,10 @@ int launch_pareto(ekya_handle* h, long long n_sets, int n, const float* cost, co
 int launch_curve_fit(ekya_handle* h, long long n_sets, int np, const float* acc, const int* full_epochs,
                      float* out_pred, float* out_params, cudaStream_t s);
 
+size_t window_workspace_bytes(const ekya_dims& d);
+int launch_window(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int mode, void* ws, size_t ws_bytes,
+                  float* out_avg, uint32_t* out_events, float* out_done, cudaStream_t s);
+
 inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? EKYA_OK : EKYA_ERR_CUDA; }
 
 }  // namespace ekya

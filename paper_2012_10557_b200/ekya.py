@@ -26,7 +26,8 @@ LAMBDA_NONE = 7
 SYMBOLS = ["ekya_create", "ekya_destroy", "ekya_last_error", "ekya_launch_count", "ekya_version",
            "ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate",
            "ekya_comm_unique_id", "ekya_comm_init", "ekya_gather_decisions", "ekya_counters", "ekya_place",
-           "ekya_checkpoint_decide", "ekya_uniform_schedule", "ekya_pareto", "ekya_curve_fit"]
+           "ekya_checkpoint_decide", "ekya_uniform_schedule", "ekya_pareto", "ekya_curve_fit",
+           "ekya_window_workspace_bytes", "ekya_window_schedule"]
 
 
 class EkyaError(RuntimeError):
@@ -93,6 +94,11 @@ def load_library(path: str = LIB_PATH):
     L.ekya_uniform_schedule.restype = ctypes.c_int
     L.ekya_pareto.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P, P, P, P]
     L.ekya_pareto.restype = ctypes.c_int
+    L.ekya_window_workspace_bytes.argtypes = [ctypes.POINTER(Dims)]
+    L.ekya_window_workspace_bytes.restype = ctypes.c_size_t
+    L.ekya_window_schedule.argtypes = [P, ctypes.POINTER(Dims), ctypes.POINTER(Tables), ctypes.c_int, P,
+                                       ctypes.c_size_t, P, P, P, P]
+    L.ekya_window_schedule.restype = ctypes.c_int
     L.ekya_curve_fit.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P, P, P, P, P]
     L.ekya_curve_fit.restype = ctypes.c_int
     L.ekya_place.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P]
@@ -249,6 +255,20 @@ def ekya_pareto(h: Handle, cost, post, out_mask, stream=None):
                          _ptr(post, torch.float32, "post", True), _ptr(out_mask, torch.uint32, "out_mask"),
                          _stream(stream))
     _check(code, "ekya_pareto")
+
+
+def ekya_window_workspace_bytes(dims: Dims) -> int:
+    return int(load_library().ekya_window_workspace_bytes(ctypes.byref(dims)))
+
+
+def ekya_window_schedule(h: Handle, dims: Dims, tables: Tables, mode: int, workspace, out_avg, out_events, out_done,
+                         stream=None):
+    L = load_library()
+    code = L.ekya_window_schedule(h.ptr, ctypes.byref(dims), ctypes.byref(tables), mode,
+                                  _ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                  _ptr(out_avg, torch.float32, "out_avg"), _ptr(out_events, torch.uint32, "out_events"),
+                                  _ptr(out_done, torch.float32, "out_done"), _stream(stream))
+    _check(code, "ekya_window_schedule")
 
 
 def ekya_curve_fit(h: Handle, acc, full_epochs, out_pred, out_params=None, stream=None):
@@ -414,3 +434,16 @@ def curve_fit(h, acc, full_epochs, stream=None):
     prm = torch.empty((S, 3), dtype=torch.float32, device=acc.device)
     ekya_curve_fit(h, acc, full_epochs, pred, prm, stream=stream)
     return pred, prm
+
+
+def window_schedule(h, tables: dict, units, steal_units, unit_gpu_seconds, a_min, mode=THIEF_STEEPEST, stream=None):
+    """The window timeline with re-invocation at completions: (avg [B], events [B], done [B][V])."""
+    dims = dims_from(tables, units, steal_units, unit_gpu_seconds, a_min)
+    B, V = dims.n_inst, dims.n_streams
+    dev = tables["stale"].device
+    ws = torch.empty((max(1, ekya_window_workspace_bytes(dims)),), dtype=torch.uint8, device=dev)
+    avg = torch.empty((B,), dtype=torch.float32, device=dev)
+    ev = torch.empty((B,), dtype=torch.uint32, device=dev)
+    done = torch.empty((B, V), dtype=torch.float32, device=dev)
+    ekya_window_schedule(h, dims, make_tables(**tables), mode, ws, avg, ev, done, stream=stream)
+    return avg, ev, done

@@ -550,3 +550,38 @@ def test_curve_fit_invalid(h):
     op, oprm, bad = oracle.curve_fit(a, K)
     assert bad == 2 and h.last_error() == -6
     assert_eq(pred, op, "predicted accuracy")
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1: the window timeline with re-invocation at completions
+# ---------------------------------------------------------------------------
+WINDOW_CASES = [("c2", variant(synth.CONFIG2, n_inst=96)),
+                ("c2-ragged", variant(synth.CONFIG2, n_inst=48, ragged=True)),
+                ("c1", variant(synth.CONFIG1, n_inst=300)),
+                ("odd", variant(synth.CONFIG2, n_inst=24, n_streams=7, n_gamma=31, units=53, a_min=0.0)),
+                ("nogamma", variant(synth.CONFIG2, n_inst=16, n_gamma=0))]
+
+
+@pytest.mark.parametrize("mode", [0, 1], ids=["steepest", "literal"])
+@pytest.mark.parametrize("name,cfg", WINDOW_CASES, ids=[c[0] for c in WINDOW_CASES])
+def test_window_bitexact(h, name, cfg, mode):
+    Td, inst = tables(cfg)
+    avg, ev, done = ek().window_schedule(h, Td, *args(cfg), mode=mode)
+    oavg, oev, odone, bad = oracle.window(inst, mode)
+    assert bad == 0 and h.last_error() == 0
+    assert_eq(ev, oev, "invocations")
+    assert_eq(done, odone, "completion times")
+    assert_eq(avg, oavg, "realized average")
+
+
+def test_window_invalid_instance(h):
+    cfg = variant(synth.CONFIG2, n_inst=8)
+    T = synth.sched_tables(cfg)
+    T["cost"][5, 3, 2] = -1.0
+    inst = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            *args(cfg))
+    avg, ev, done = ek().window_schedule(h, {k: v.cuda() for k, v in T.items()}, *args(cfg))
+    oavg, oev, odone, bad = oracle.window(inst, 0)
+    assert bad == 1 and h.last_error() == -6
+    assert_eq(avg, oavg, "realized average")
+    assert_eq(done, odone, "completion times")
