@@ -381,6 +381,7 @@ def run_ours(args, rank, world, local_rank):
 
     context = run_context(ek, h, dev, args) if rank == 0 and args.context else None
     if context is not None:
+        context.update(run_next1(ek, h, w, T, O, dev))
         context.update(run_next2(ek, h, w, dev))
         context.update(run_next3(ek, h, w, T, O, dev))
         context.update(run_next4(ek, h, w, O, dev))
@@ -506,6 +507,25 @@ def run_next3(ek, h, w, T, O, dev):
             "next3_pareto": {"sets": B * V, "configs": G, "ms": ms_p, "sets_per_s": B * V / (ms_p / 1000.0),
                              "hbm_frac": bytes_p / (ms_p / 1000.0) / 1e9 / peak,
                              "mean_frontier_size": frontier}}
+
+
+def run_next1(ek, h, w, T, O, dev):
+    """SURVEY 8(f) NEXT-1 beside the step: the window timeline with the thief re-invoked at
+    every retraining completion, over the step's 65,536 config-4 instances (STEEPEST):
+    realized window-average accuracy vs the thief's t = 0 estimate."""
+    dims, tabs = ek.dims_from(T, *w.args), ek.make_tables(**T)
+    B, V = w.B, w.V
+    ws = torch.empty((ek.ekya_window_workspace_bytes(dims),), dtype=torch.uint8, device=dev)
+    avg = torch.empty((B,), dtype=torch.float32, device=dev)
+    ev = torch.empty((B,), dtype=torch.uint32, device=dev)
+    done = torch.empty((B, V), dtype=torch.float32, device=dev)
+    ms = _time_ms(lambda: ek.ekya_window_schedule(h, dims, tabs, ek.THIEF_STEEPEST, ws, avg, ev, done), reps=2)
+    assert h.last_error() == 0
+    return {"next1_window": {"instances": B, "ms": ms, "instances_per_s": B / (ms / 1000.0),
+                             "thief_invocations_per_instance": float(ev.cpu().numpy().view(np.uint32).mean()),
+                             "mean_realized_accuracy": float(avg.mean()),
+                             "mean_t0_estimate": float(O.dec[0]["mean"].mean()),
+                             "streams_retrained_frac": float((done < 1).float().mean())}}
 
 
 def run_next2(ek, h, w, dev):
