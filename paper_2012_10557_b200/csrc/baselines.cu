@@ -175,16 +175,20 @@ struct CurveParams {
     DevState* st;
 };
 
-template <int NP>
-__device__ __forceinline__ float cf_sse(const float* x, const float (&y)[NP], int n, float al, float b) {
-    float e = 0.0f;
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-        if (NP == kCfMaxPoints && k >= n) break;
-        const float d = fsub(fadd(fmul(al, x[k]), b), y[k]);
-        e = fadd(e, fmul(d, d));
+// One grid point's record in shared memory: x_0..x_{n-1}, then sum x, sum x^2, det, and the
+// refined reciprocals of det and sum x^2 with a flag saying whether they may be used.
+__host__ __device__ constexpr int cf_rec(int n) { return (n + 6 + 3) & ~3; }
+
+// a / den, correctly rounded: the shared-reciprocal fast path (SharedDiv) when |a| and den
+// lie in [2^-60, 2^60], else the full IEEE division (zeros keep their sign there)
+__device__ __forceinline__ float cf_div(float a, float den, float rden, bool den_fast) {
+    const float aa = fabsf(a);
+    if (den_fast && aa >= 8.67361738e-19f && aa <= 1.15292150e18f) {
+        const float q0 = __fmaf_rn(a, rden, 0.0f);
+        const float e = __fmaf_rn(-den, q0, a);
+        return __fmaf_rn(rden, e, q0);
     }
-    return e;
+    return fdiv(a, den);
 }
 
 // NP: compile-time point count (5 = the paper's "say, 5" epochs), or kCfMaxPoints for a
@@ -193,23 +197,29 @@ template <int NP>
 __global__ void __launch_bounds__(256) curve_fit_kernel(CurveParams p) {
     extern __shared__ __align__(16) float cs[];
     const int n = NP == kCfMaxPoints ? p.np : NP;
-    float* xs = cs;                                  // [kCfGrid][n]
-    float* sxs = xs + kCfGrid * n;                   // [kCfGrid] sum x
-    float* sxxs = sxs + kCfGrid;                     // [kCfGrid] sum x^2
-    float* dets = sxxs + kCfGrid;                    // [kCfGrid] n sum x^2 - (sum x)^2
+    const int R = cf_rec(n);
     const float fn = __int2float_rn(n);
     for (int i = threadIdx.x; i < kCfGrid; i += blockDim.x) {
+        float* rec = cs + i * R;
         const float c = fmul(__int2float_rn(i), 0.125f);
         float sx = 0.0f, sxx = 0.0f;
         for (int k = 0; k < n; ++k) {
             const float x = fdiv(1.0f, fadd(__int2float_rn(k + 1), c));
-            xs[i * n + k] = x;
+            rec[k] = x;
             sx = fadd(sx, x);
             sxx = fadd(sxx, fmul(x, x));
         }
-        sxs[i] = sx;
-        sxxs[i] = sxx;
-        dets[i] = fsub(fmul(fn, sxx), fmul(sx, sx));
+        const float det = fsub(fmul(fn, sxx), fmul(sx, sx));
+        rec[n] = sx;
+        rec[n + 1] = sxx;
+        rec[n + 2] = det;
+        // the reciprocals as SharedDiv refines them; usable for divisors in [2^-60, 2^60]
+        const float dd = det > 0.0f ? det : 1.0f;
+        const SharedDiv sd(dd), sq(sxx > 0.0f ? sxx : 1.0f);
+        rec[n + 3] = sd.r;
+        rec[n + 4] = sq.r;
+        const bool fd = det > 0.0f && fast_dividend(det) && sxx > 0.0f && fast_dividend(sxx);
+        rec[n + 5] = fd ? 1.0f : 0.0f;
     }
     __syncthreads();
     for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < p.n_sets;
@@ -226,35 +236,72 @@ __global__ void __launch_bounds__(256) curve_fit_kernel(CurveParams p) {
             y[k] = fsub(1.0f, a);
             sy = fadd(sy, y[k]);
         }
-        float best = 0.0f, bal = 0.0f, bb = 0.0f, bc = 0.0f;
+        // the alpha = 0 boundary solution does not depend on c: fl(0 x) + b0 = b0 exactly
+        const float m = fdiv(sy, fn);
+        const float b0 = m > 0.0f ? m : 0.0f;
+        float e0 = 0.0f;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            if (NP == kCfMaxPoints && k >= n) break;
+            const float d = fsub(b0, y[k]);
+            e0 = fadd(e0, fmul(d, d));
+        }
+        float best = 0.0f, bal = 0.0f, bb = 0.0f;
+        int bi = 0;
         for (int i = 0; i < kCfGrid; ++i) {
-            const float* x = xs + i * n;
+            const float* rec = cs + i * R;
+            float x[NP];
+            float sx, sxx, det, rdet, rsxx;
+            bool fd;
+            if constexpr (NP == 5) {
+                const float4 r0 = *reinterpret_cast<const float4*>(rec);
+                const float4 r1 = *reinterpret_cast<const float4*>(rec + 4);
+                const float4 r2 = *reinterpret_cast<const float4*>(rec + 8);
+                x[0] = r0.x, x[1] = r0.y, x[2] = r0.z, x[3] = r0.w, x[4] = r1.x;
+                sx = r1.y, sxx = r1.z, det = r1.w, rdet = r2.x, rsxx = r2.y, fd = r2.z != 0.0f;
+            } else {
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                    if (NP == kCfMaxPoints && k >= n) break;
+                    x[k] = rec[k];
+                }
+                sx = rec[n], sxx = rec[n + 1], det = rec[n + 2], rdet = rec[n + 3], rsxx = rec[n + 4];
+                fd = rec[n + 5] != 0.0f;
+            }
             float sxy = 0.0f;
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
                 if (NP == kCfMaxPoints && k >= n) break;
                 sxy = fadd(sxy, fmul(x[k], y[k]));
             }
-            const float sx = sxs[i], sxx = sxxs[i], det = dets[i];
             float al = 0.0f, b = 0.0f, e = 0.0f;
             bool done = false;
             if (det > 0.0f) {
-                const float a1 = fdiv(fsub(fmul(fn, sxy), fmul(sx, sy)), det);
-                const float b1 = fdiv(fsub(fmul(sxx, sy), fmul(sx, sxy)), det);
+                const float a1 = cf_div(fsub(fmul(fn, sxy), fmul(sx, sy)), det, rdet, fd);
+                const float b1 = cf_div(fsub(fmul(sxx, sy), fmul(sx, sxy)), det, rdet, fd);
                 if (a1 >= 0.0f && b1 >= 0.0f) {
                     al = a1;
                     b = b1;
-                    e = cf_sse<NP>(x, y, n, al, b);
+#pragma unroll
+                    for (int k = 0; k < NP; ++k) {
+                        if (NP == kCfMaxPoints && k >= n) break;
+                        const float d = fsub(fadd(fmul(al, x[k]), b), y[k]);
+                        e = fadd(e, fmul(d, d));
+                    }
                     done = true;
                 }
             }
             if (!done) {
-                const float m = fdiv(sy, fn);
-                const float b0 = m > 0.0f ? m : 0.0f;
-                const float e0 = cf_sse<NP>(x, y, n, 0.0f, b0);
-                const float q = sxx > 0.0f ? fdiv(sxy, sxx) : 0.0f;
+                const float q = sxx > 0.0f ? cf_div(sxy, sxx, rsxx, fd) : 0.0f;
                 const float a0 = q > 0.0f ? q : 0.0f;
-                const float e1 = cf_sse<NP>(x, y, n, a0, 0.0f);
+                // b = 0 boundary: fl(a0 x) + 0 = fl(a0 x) exactly (a0 x >= +0)
+                float e1 = 0.0f;
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                    if (NP == kCfMaxPoints && k >= n) break;
+                    const float d = fsub(fmul(a0, x[k]), y[k]);
+                    e1 = fadd(e1, fmul(d, d));
+                }
                 if (e1 < e0) {
                     al = a0;
                     b = 0.0f;
@@ -269,9 +316,10 @@ __global__ void __launch_bounds__(256) curve_fit_kernel(CurveParams p) {
                 best = e;
                 bal = al;
                 bb = b;
-                bc = fmul(__int2float_rn(i), 0.125f);
+                bi = i;
             }
         }
+        const float bc = fmul(__int2float_rn(bi), 0.125f);
         float pr = fsub(1.0f, fadd(fdiv(bal, fadd(__int2float_rn(K), bc)), bb));
         pr = pr < 0.0f ? 0.0f : (pr > 1.0f ? 1.0f : pr);
         if (!ok) flag_data_error(p.st);
@@ -290,7 +338,7 @@ int launch_curve_fit(ekya_handle* h, long long n_sets, int np, const float* acc,
                      float* out_pred, float* out_params, cudaStream_t s) {
     if (n_sets == 0) return EKYA_OK;
     CurveParams p{n_sets, np, acc, full_epochs, out_pred, out_params, h->dstate};
-    const size_t smem = (size_t)kCfGrid * (np + 3) * 4;
+    const size_t smem = (size_t)kCfGrid * cf_rec(np) * 4;
     auto k = np == 5 ? curve_fit_kernel<5> : curve_fit_kernel<kCfMaxPoints>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
