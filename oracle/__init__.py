@@ -101,6 +101,8 @@ def lib():
         L.orc_uniform.restype = ctypes.c_int64
         L.orc_pareto.argtypes = [ctypes.c_int64, ctypes.c_int32, P, P, P]
         L.orc_pareto.restype = ctypes.c_int64
+        L.orc_prune.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, P, P, ctypes.c_float, P]
+        L.orc_prune.restype = ctypes.c_int64
         L.orc_window.argtypes = [ctypes.POINTER(Dims), P, P, P, P, P, ctypes.c_int32, P, P, P]
         L.orc_window.restype = ctypes.c_int64
         L.orc_curve_fit.argtypes = [ctypes.c_int64, ctypes.c_int32, P, P, P, P]
@@ -385,6 +387,21 @@ def pareto(cost, post):
     if lib().orc_pareto(sets, n, _p(cost), _p(post), _p(m)) < 0:
         raise ValueError("oracle: invalid pareto shape")
     return m
+
+
+def prune(cost, hist_acc, margin):
+    """History-based pruning (readings PN1-PN3): cost [Q][n], hist_acc [Q][H][n] (NaN =
+    unmeasured) -> keep mask [Q] (bit k = config k kept), number of invalid queries."""
+    cost = _c(cost, np.float32)
+    hist_acc = _c(hist_acc, np.float32)
+    Q, n = cost.shape
+    H = hist_acc.shape[1]
+    assert hist_acc.shape == (Q, H, n)
+    keep = np.zeros(Q, np.uint32)
+    bad = lib().orc_prune(Q, H, n, _p(cost), _p(hist_acc), float(margin), _p(keep))
+    if bad < 0:
+        raise ValueError("oracle: invalid prune arguments")
+    return keep, int(bad)
 
 
 def curve_fit(acc, full_epochs):

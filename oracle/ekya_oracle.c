@@ -846,6 +846,60 @@ int64_t orc_pareto(int64_t n_sets, int32_t n, const float* cost, const float* po
     return 0;
 }
 
+/* PN1-PN3: pruning of configurations that have historically not been useful (P:1179-1180
+ * "configurations that are usually significantly distant from the configurations on the
+ * Pareto curve of the resource-accuracy profile").  Per stream (query q) and history window
+ * j, the Pareto boundary at config k's cost is the best accuracy of any real config measured
+ * in j whose cost is not above cost[k] (PN1; k itself counts, so the gap is >= 0 and 0 on
+ * the boundary); config k is "far" in j iff fl(boundary - acc_j(k)) > margin.  Config k is
+ * pruned iff it is far in strictly more than half of the windows that measured it (PN2);
+ * never-measured configs are kept, padding (cost +INF) is never kept.  Costs are the
+ * stream's current profile (PN3).  Invalid data (cost NaN or < 0, a real config's
+ * measured accuracy outside [0,1]): keep mask 0, counted in the return value.  Literal
+ * O(H n^2) loops. */
+int64_t orc_prune(int64_t n_query, int32_t H, int32_t n, const float* cost, const float* hist_acc, float margin,
+                  uint32_t* out_keep)
+{
+    if (n_query < 0 || H < 0 || n < 0 || n > 31 || isnan(margin)) return -1;
+    int64_t bad = 0;
+    for (int64_t q = 0; q < n_query; ++q) {
+        const float* c = cost + q * n;
+        const float* A = hist_acc + q * (int64_t)H * n;
+        int ok = 1;
+        for (int32_t k = 0; k < n; ++k) {
+            if (!(c[k] >= 0.0f)) ok = 0;
+            else if (!isinf(c[k]))
+                for (int32_t j = 0; j < H; ++j)
+                    if (!isnan(A[(int64_t)j * n + k]) && !orc_in01(A[(int64_t)j * n + k])) ok = 0;
+        }
+        if (!ok) {
+            out_keep[q] = 0;
+            ++bad;
+            continue;
+        }
+        uint32_t keep = 0;
+        for (int32_t k = 0; k < n; ++k) {
+            if (isinf(c[k])) continue;
+            int64_t measured = 0, far = 0;
+            for (int32_t j = 0; j < H; ++j) {
+                const float* a = A + (int64_t)j * n;
+                if (isnan(a[k])) continue;
+                ++measured;
+                float boundary = a[k];
+                for (int32_t k2 = 0; k2 < n; ++k2) {
+                    if (isinf(c[k2]) || isnan(a[k2])) continue;
+                    if (c[k2] <= c[k] && a[k2] > boundary) boundary = a[k2];
+                }
+                const float gap = boundary - a[k];
+                if (gap > margin) ++far;
+            }
+            if (!(2 * far > measured)) keep |= 1u << k;
+        }
+        out_keep[q] = keep;
+    }
+    return bad;
+}
+
 /* ========================================================================
  * NEXT-2: the micro-profiler's curve fit and extrapolation
  * ("fit the accuracy-epoch points to the a non-linear curve model ...

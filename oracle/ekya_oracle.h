@@ -86,6 +86,10 @@ int64_t orc_uniform(const orc_dims* d, const float* stale, const float* cost, co
                     const uint16_t* lmu, const float* lf, int32_t fixed_gamma, float inference_weight,
                     uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum, float* out_mean);
 int64_t orc_pareto(int64_t n_sets, int32_t n, const float* cost, const float* post, uint32_t* out_mask);
+/* history-based pruning of configurations far from the Pareto boundary (
+ * readings PN1-PN3) */
+int64_t orc_prune(int64_t n_query, int32_t H, int32_t n, const float* cost, const float* hist_acc, float margin,
+                  uint32_t* out_keep);
 
 /* ---- NEXT-2: micro-profiler curve fit + extrapolation (
  *      readings CF1-CF3) ---- */

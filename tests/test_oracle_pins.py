@@ -734,6 +734,78 @@ def test_pareto_spec_examples_and_properties():
                 assert any(c[j] <= c[k] and p[j] >= p[k] for j in on)
 
 
+def test_prune_worked_examples():
+    """PN1-PN3 on hand-worked cases: costs 1, 2, 3 and three windows.
+    w0 = (.5, .7, .6): config 2 sits .1 below the boundary (.7 at cost <= 3); w1 = (.6,
+    .62, .64): on the boundary everywhere; w2 = (.7, .6, .5): configs 1, 2 are .1 and .2
+    below.  Margin .05: config 1 far in 1/3 windows (kept), config 2 in 2/3 (pruned)."""
+    nan = float("nan")
+    c = np.array([[1.0, 2.0, 3.0]], np.float32)
+    A = np.array([[[.5, .7, .6], [.6, .62, .64], [.7, .6, .5]]], np.float32)
+    assert oracle.prune(c, A, 0.05) == (np.array([0b011], np.uint32), 0)
+    # exactly half of the measured windows far: kept ("usually" = strict majority)
+    assert int(oracle.prune(c, A[:, :2], 0.05)[0][0]) == 0b111
+    # unmeasured windows do not count: config 2 measured in w0 only, far there
+    A2 = A[:, :2].copy()
+    A2[0, 1, 2] = nan
+    assert int(oracle.prune(c, A2, 0.05)[0][0]) == 0b011
+    # never measured: kept; a margin above every gap keeps all, a negative one prunes
+    # every measured config
+    A3 = A.copy()
+    A3[0, :, 2] = nan
+    assert int(oracle.prune(c, A3, 0.05)[0][0]) == 0b111
+    assert int(oracle.prune(c, A, 1.0)[0][0]) == 0b111
+    assert int(oracle.prune(c, A, -1.0)[0][0]) == 0
+    assert int(oracle.prune(c, A3, -1.0)[0][0]) == 0b100
+    # padding (cost +INF) is never kept and does not raise the boundary
+    cp = np.array([[1.0, 2.0, np.inf]], np.float32)
+    Ap = np.array([[[.5, .6, 1.0]]], np.float32)
+    assert int(oracle.prune(cp, Ap, 0.0)[0][0]) == 0b011
+    # equal cost counts as "not above": the worse of two equal-cost configs is far
+    assert int(oracle.prune(np.array([[1.0, 1.0]], np.float32),
+                            np.array([[[.5, .6]]], np.float32), 0.05)[0][0]) == 0b10
+    # invalid data: mask 0 and counted; a padding config's accuracy is not data
+    bad_c = np.array([[1.0, nan, 3.0]], np.float32)
+    assert oracle.prune(bad_c, A, 0.05) == (np.array([0], np.uint32), 1)
+    Ab = A.copy()
+    Ab[0, 1, 0] = 1.5
+    assert oracle.prune(c, Ab, 0.05) == (np.array([0], np.uint32), 1)
+    Apb = Ap.copy()
+    Apb[0, 0, 2] = 7.0
+    assert oracle.prune(cp, Apb, 0.0)[1] == 0
+
+
+def test_prune_invariants_and_pareto_relation():
+    """Random tie-heavy sets: the mask permutes with the configs, ignores the window order,
+    grows with the margin; with one window, margin 0 and acc = post it keeps the Pareto
+    frontier (PR1, pinned above) plus exactly the configs whose accuracy some real config
+    at no higher cost matches."""
+    rng = np.random.default_rng(41)
+    for _ in range(200):
+        n = int(rng.integers(1, 32))
+        H = int(rng.integers(0, 7))
+        c = (rng.choice([1.0, 2.0, 3.0, 5.0], n) * rng.integers(1, 3, n)).astype(np.float32)
+        c[rng.uniform(size=n) < 0.1] = np.inf
+        A = np.round(rng.uniform(0, 1, (H, n)), 1).astype(np.float32)
+        A[rng.uniform(size=(H, n)) < 0.2] = np.nan
+        m = float(rng.choice([0.0, 0.1, 0.25]))
+        keep = int(oracle.prune(c[None], A[None], m)[0][0])
+        perm = rng.permutation(n)
+        kp = int(oracle.prune(c[perm][None], A[:, perm][None], m)[0][0])
+        assert kp == sum(1 << i for i in range(n) if keep >> int(perm[i]) & 1)
+        assert int(oracle.prune(c[None], A[rng.permutation(H)][None], m)[0][0]) == keep
+        assert keep & ~int(oracle.prune(c[None], A[None], m + 0.2)[0][0]) == 0
+        p = np.round(rng.uniform(0, 1, n), 1).astype(np.float32)
+        k1 = int(oracle.prune(c[None], p[None, None], 0.0)[0][0])
+        par = int(oracle.pareto(c[None], p[None])[0])
+        assert par & ~k1 == 0
+        for k in range(n):
+            if k1 >> k & 1 and not par >> k & 1:
+                assert any(j != k and np.isfinite(c[j]) and c[j] <= c[k] and p[j] == p[k] for j in range(n))
+            if np.isfinite(c[k]) and not k1 >> k & 1:
+                assert any(np.isfinite(c[j]) and c[j] <= c[k] and p[j] > p[k] for j in range(n))
+
+
 # ---------------------------------------------------------------------------
 # NEXT-2: micro-profiler curve fit (P:1177, S:106-108, S:147-163)
 # ---------------------------------------------------------------------------
