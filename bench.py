@@ -384,6 +384,7 @@ def run_ours(args, rank, world, local_rank):
         context.update(run_next1(ek, h, w, T, O, dev))
         context.update(run_next2(ek, h, w, dev))
         context.update(run_next3(ek, h, w, T, O, dev))
+        context.update(run_next3_prune(ek, h, w, T, P))
         context.update(run_next4(ek, h, w, O, dev))
     if rank != 0:
         return
@@ -507,6 +508,25 @@ def run_next3(ek, h, w, T, O, dev):
             "next3_pareto": {"sets": B * V, "configs": G, "ms": ms_p, "sets_per_s": B * V / (ms_p / 1000.0),
                              "hbm_frac": bytes_p / (ms_p / 1000.0) / 1e9 / peak,
                              "mean_frontier_size": frontier}}
+
+
+def run_next3_prune(ek, h, w, T, P):
+    """SURVEY 8(f) NEXT-3's pruning beside the step (readings PN1-PN3): the
+    step's 65,536 config-3 profiler histories (500 windows x 18 configs) against the config-4
+    tables' costs of the first 65,536 streams, margin 0.05."""
+    Q, H, G = P["hist_acc"].shape
+    cost = T["cost"].reshape(-1, T["cost"].shape[-1])[:Q, :G].contiguous()
+    keep = torch.empty((Q,), dtype=torch.uint32, device=cost.device)
+    ms = _time_ms(lambda: ek.ekya_prune_configs(h, cost, P["hist_acc"], 0.05, keep))
+    assert h.last_error() == 0
+    peak, _, _ = measured_peaks()
+    nbytes = Q * (H * G * 4 + G * 4 + 4)
+    k = keep.cpu().numpy().view(np.uint32)
+    kept = float(np.unpackbits(k.view(np.uint8)).sum()) / k.size
+    return {"next3_prune": {"streams": Q, "windows": H, "configs": G, "margin": 0.05, "ms": ms,
+                            "streams_per_s": Q / (ms / 1000.0),
+                            "hbm_frac": nbytes / (ms / 1000.0) / 1e9 / peak,
+                            "mean_configs_kept": kept}}
 
 
 def run_next1(ek, h, w, T, O, dev):

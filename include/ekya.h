@@ -255,12 +255,31 @@ int ekya_curve_fit(ekya_handle* h, int64_t n_sets, int32_t n_points, const float
  * B*V): bit k of out_mask[s] set iff config k is real (cost finite) and no other
  * real config has cost' <= cost and post' >= post with one strict (P:147 Figure
  * 3's "Pareto boundary"; reading PR1).
+ *
+ * ekya_prune_configs -- pruning of configurations "that have historically not been
+ * useful ... usually significantly distant from the configurations on the Pareto
+ * curve of the resource-accuracy profile".  Per stream q of n_query:
+ * cost [n_query][n] (the current profile; +INF = padding), hist_acc
+ * [n_query][n_hist][n] (the stream's history windows, NaN = not measured; the
+ * layout of ekya_profile_estimate's hist_acc).
+ *   PN1 in window j the Pareto boundary at config k's cost is the best accuracy of
+ *       any real config measured in j with cost <= cost[k] (k included); k is far
+ *       in j iff fl(boundary - acc_j(k)) > margin.
+ *   PN2 bit k of out_keep[q] is set iff k is real and far in at most half of the
+ *       windows that measured it (never-measured configs are kept).
+ *   PN3 costs do not depend on the window (epochs x per-epoch cost x data
+ *       fraction).
+ * Limits: n <= 31, n_hist <= 2^20 (EKYA_ERR_LIMIT); margin NaN: EKYA_ERR_ARG.
+ * Invalid stream (cost NaN or < 0, a real config's measured accuracy outside
+ * [0,1]): out_keep 0 + EKYA_ERR_DATA.
  * ------------------------------------------------------------------------- */
 int ekya_uniform_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int32_t fixed_gamma,
                           float inference_weight, uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum_q32,
                           float* out_mean, ekya_stream_t stream);
 int ekya_pareto(ekya_handle* h, int64_t n_sets, int32_t n, const float* cost, const float* post,
                 uint32_t* out_mask, ekya_stream_t stream);
+int ekya_prune_configs(ekya_handle* h, int64_t n_query, int32_t n_hist, int32_t n, const float* cost,
+                       const float* hist_acc, float margin, uint32_t* out_keep, ekya_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * ekya_place -- placement of scheduling decisions onto discrete GPUs (SURVEY 8(f)

@@ -186,6 +186,18 @@ int ekya_pareto(ekya_handle* h, int64_t n_sets, int32_t n, const float* cost, co
     return launch_pareto(h, (long long)n_sets, n, cost, post, out_mask, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int ekya_prune_configs(ekya_handle* h, int64_t n_query, int32_t n_hist, int32_t n, const float* cost,
+                       const float* hist_acc, float margin, uint32_t* out_keep, ekya_stream_t stream) {
+    if (!h) return EKYA_ERR_ARG;
+    if (n_query < 0 || n_hist < 0 || n < 0) return EKYA_ERR_SHAPE;
+    if (n > 31 || n_hist > (1 << 20)) return EKYA_ERR_LIMIT;
+    if (margin != margin) return EKYA_ERR_ARG;
+    if (n_query > 0 && (!out_keep || (n > 0 && !cost) || (n > 0 && n_hist > 0 && !hist_acc))) return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    return launch_prune(h, (long long)n_query, n_hist, n, cost, hist_acc, margin, out_keep,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
 size_t ekya_window_workspace_bytes(const ekya_dims* d) {
     if (!d || d->n_inst < 0 || d->n_streams < 1) return 0;
     return window_workspace_bytes(*d);

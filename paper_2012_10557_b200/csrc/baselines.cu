@@ -8,6 +8,7 @@
 // average of rule 2 -- then the exact Q32 objective by a warp reduction.
 // ekya_pareto: one thread per (instance, stream) set, its configs in registers,
 // the O(n^2) dominance test sequential.
+// ekya_prune_configs: history-based pruning, one warp per stream.
 #include <algorithm>
 
 #include "launch.h"
@@ -122,6 +123,245 @@ __global__ void __launch_bounds__(256) pareto_kernel(ParetoParams p) {
     }
 }
 
+struct PruneParams {
+    long long n_query;
+    int H, n;
+    const float* cost;
+    const float* acc;
+    float margin;
+    uint32_t* out_keep;
+    DevState* st;
+};
+
+// PN1-PN3: one warp per stream (query).  The stream's real configs are ranked by (cost, index)
+// once; per history window the Pareto boundary at every config's cost is then a prefix
+// maximum in that order (equal costs share the value at their group's end), so a window
+// costs one pass forward and one backward over n registers instead of n^2 comparisons.
+// Lanes own windows: each warp stages 32 consecutive windows (n floats each, contiguous)
+// with coalesced loads into shared memory and every lane reads its own row in cost order.
+// Counts per config: measured in the low, far in the high 16 bits of one register (a lane
+// sees at most ceil(H / 32) <= 32768 windows).
+template <int NM>
+__global__ void __launch_bounds__(kBaseWarps * 32) prune_kernel(PruneParams p) {
+    __shared__ float rows[kBaseWarps][32 * 31];
+    __shared__ uint8_t perm_s[kBaseWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int H = p.H, n = p.n;
+    float* sr = rows[warp];
+    for (long long q = (long long)blockIdx.x * kBaseWarps + warp; q < p.n_query;
+         q += (long long)gridDim.x * kBaseWarps) {
+        const float ck = lane < n ? __ldg(p.cost + q * n + lane) : INFINITY;
+        const bool cok = lane >= n || ck >= 0.0f;   // NaN or negative cost: R-ERR
+        const bool real = lane < n && cok && !isinf(ck);
+        // rank by (cost, index) among the real configs; group end = no later equal cost
+        int rank = 0;
+        bool later_tie = false;
+        for (int k2 = 0; k2 < n; ++k2) {
+            const float c2 = __shfl_sync(0xffffffffu, ck, k2);
+            const bool r2 = __shfl_sync(0xffffffffu, real, k2);
+            if (r2 && (c2 < ck || (c2 == ck && k2 < lane))) ++rank;
+            if (r2 && c2 == ck && k2 > lane) later_tie = true;
+        }
+        const int nr = __popc(__ballot_sync(0xffffffffu, real));
+        const unsigned ends = __reduce_or_sync(0xffffffffu, real && !later_tie ? 1u << rank : 0u);
+        if (real) perm_s[warp][rank] = (uint8_t)lane;
+        __syncwarp();
+        int pi[NM];
+#pragma unroll
+        for (int i = 0; i < NM; ++i) pi[i] = i < nr ? perm_s[warp][i] : 0;
+        unsigned cnt[NM];
+#pragma unroll
+        for (int i = 0; i < NM; ++i) cnt[i] = 0;
+        bool aok = true;
+        const float* A = p.acc + q * (long long)H * n;
+        for (int j0 = 0; j0 < H; j0 += 32) {
+            const int nw = min(32, H - j0);
+            const float* src = A + (long long)j0 * n;
+            __syncwarp();
+            for (int e = lane; e < nw * n; e += 32) sr[e] = __ldg(src + e);
+            __syncwarp();
+            if (lane < nw) {
+                const float* a = sr + lane * n;
+                float av[NM], pm[NM];
+                float m = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < NM; ++i) {
+                    if (i < nr) {
+                        av[i] = a[pi[i]];
+                        aok &= isnan(av[i]) || in01(av[i]);
+                        m = fmaxf(m, av[i]);   // NaN (unmeasured) never wins
+                        pm[i] = m;
+                    }
+                }
+                float cur = -INFINITY;
+#pragma unroll
+                for (int i = NM - 1; i >= 0; --i) {
+                    if (i < nr) {
+                        if (ends >> i & 1) cur = pm[i];
+                        if (!isnan(av[i])) cnt[i] += 1u + ((fsub(cur, av[i]) > p.margin) ? 0x10000u : 0u);
+                    }
+                }
+            }
+        }
+        const bool ok = __all_sync(0xffffffffu, cok && aok);
+        unsigned keep = 0;
+#pragma unroll
+        for (int i = 0; i < NM; ++i) {
+            if (i < nr) {
+                const unsigned meas = __reduce_add_sync(0xffffffffu, cnt[i] & 0xFFFFu);
+                const unsigned far = __reduce_add_sync(0xffffffffu, cnt[i] >> 16);
+                if (!(2ull * far > meas)) keep |= 1u << pi[i];
+            }
+        }
+        if (lane == 0) {
+            if (!ok) flag_data_error(p.st);
+            p.out_keep[q] = ok ? keep : 0u;
+        }
+        __syncwarp();   // perm_s / rows are rewritten by the next query
+    }
+}
+
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
+constexpr int kPruneWarps = 4, kPruneStages = 3;
+
+// The same for streams of exactly N configs (the paper's |Gamma| = 18).  Each warp copies its
+// next 32 windows with cp.async while it evaluates the current 32 (two buffers), storing
+// every row in cost order (column k to position rank(k); padding positions hold NaN, i.e.
+// unmeasured), so a lane reads its row with 8-byte loads at compile-time offsets.  The
+// accuracy range check folds into a NaN-ignoring minimum and the prefix maximum.  Without
+// equal costs the boundary is the prefix maximum itself; with them (rare) the prefix maxima
+// overwrite the row and the accuracies are re-read from global memory (L2).
+template <int N>
+__global__ void __launch_bounds__(kPruneWarps * 32, 8) prune_sorted_kernel(PruneParams p) {
+    static_assert(N % 2 == 0, "8-byte row loads");
+    __shared__ __align__(16) float rows[kPruneWarps][kPruneStages][32 * N];
+    __shared__ int dst_s[kPruneWarps][N];   // column k -> position rank(k), or -1 (padding)
+    __shared__ int col_s[kPruneWarps][N];   // position -> column, or -1 (padding)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int H = p.H;
+    for (long long q = (long long)blockIdx.x * kPruneWarps + warp; q < p.n_query;
+         q += (long long)gridDim.x * kPruneWarps) {
+        const float ck = lane < N ? __ldg(p.cost + q * N + lane) : INFINITY;
+        const bool cok = lane >= N || ck >= 0.0f;
+        const bool real = lane < N && cok && !isinf(ck);
+        int rank = 0;
+        bool later_tie = false;
+#pragma unroll
+        for (int k2 = 0; k2 < N; ++k2) {
+            const float c2 = __shfl_sync(0xffffffffu, ck, k2);
+            const bool r2 = __shfl_sync(0xffffffffu, real, k2);
+            if (r2 && (c2 < ck || (c2 == ck && k2 < lane))) ++rank;
+            if (r2 && c2 == ck && k2 > lane) later_tie = true;
+        }
+        const unsigned rm = __ballot_sync(0xffffffffu, real);
+        const int nr = __popc(rm);
+        const unsigned ends = __reduce_or_sync(0xffffffffu, real && !later_tie ? 1u << rank : 0u);
+        const bool ties = ends != (1u << nr) - 1u;
+        __syncwarp();
+        if (lane < N) {
+            const int pos = real ? rank : nr + lane - __popc(rm & ((1u << lane) - 1u));
+            dst_s[warp][lane] = real ? pos : -1;
+            col_s[warp][pos] = real ? lane : -1;
+        }
+        for (int e = lane; e < 32 * (N - nr); e += 32) {   // padding positions: NaN in both buffers
+            const int w = e / (N - nr), k = nr + (e - w * (N - nr));
+            rows[warp][0][w * N + k] = __int_as_float(0x7fc00000);
+            rows[warp][1][w * N + k] = __int_as_float(0x7fc00000);
+        }
+        __syncwarp();
+        const float* A = p.acc + q * (long long)H * N;
+        auto issue = [&](int buf, int j0) {
+            const int nw = min(32, H - j0);
+            const float* src = A + (long long)j0 * N;
+            float* dst = rows[warp][buf];
+            int w = lane / N, col = lane - (lane / N) * N;   // element lane + 32 t = w N + col
+#pragma unroll 6
+            for (int t = 0; t < N; ++t) {
+                if (w < nw) {
+                    const int d = dst_s[warp][col];
+                    if (d >= 0) cp_async4(dst + w * N + d, src + w * N + col);
+                }
+                col += 32 % N;
+                w += 32 / N;
+                if (col >= N) col -= N, ++w;
+            }
+            cp_async_commit();
+        };
+        unsigned cnt[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) cnt[i] = 0;
+        float lo = 0.0f, hi = 0.0f;   // NaN-ignoring range of the measured accuracies
+#pragma unroll
+        for (int sb = 0; sb < kPruneStages - 1; ++sb) {
+            if (32 * sb < H) issue(sb, 32 * sb);
+            else cp_async_commit();
+        }
+        for (int j0 = 0, it = 0; j0 < H; j0 += 32, ++it) {
+            const int jn = j0 + 32 * (kPruneStages - 1);
+            if (jn < H) issue((it + kPruneStages - 1) % kPruneStages, jn);
+            else cp_async_commit();
+            cp_async_wait<kPruneStages - 1>();
+            __syncwarp();
+            float* sr = rows[warp][it % kPruneStages] + lane * N;
+            if (lane < min(32, H - j0)) {
+                const float2* a2 = reinterpret_cast<const float2*>(sr);
+                float m = -INFINITY;
+                if (!ties) {   // the boundary at position i is the prefix maximum
+#pragma unroll
+                    for (int i2 = 0; i2 < N / 2; ++i2) {
+                        const float2 v2 = a2[i2];
+#pragma unroll
+                        for (int h2 = 0; h2 < 2; ++h2) {
+                            const int i = 2 * i2 + h2;
+                            const float v = h2 ? v2.y : v2.x;
+                            lo = fminf(lo, v);
+                            m = fmaxf(m, v);
+                            cnt[i] += (v == v ? 1u : 0u) + (fsub(m, v) > p.margin ? 0x10000u : 0u);
+                        }
+                    }
+                } else {       // equal costs: the prefix maximum at the group's end
+#pragma unroll
+                    for (int i = 0; i < N; ++i) {
+                        const float v = sr[i];
+                        lo = fminf(lo, v);
+                        m = fmaxf(m, v);
+                        sr[i] = m;
+                    }
+                    const float* arow = A + (long long)(j0 + lane) * N;
+                    float cur = -INFINITY;
+#pragma unroll
+                    for (int i = N - 1; i >= 0; --i) {
+                        if (ends >> i & 1) cur = sr[i];
+                        const int c = col_s[warp][i];
+                        const float v = c >= 0 ? __ldg(arow + c) : __int_as_float(0x7fc00000);
+                        cnt[i] += (v == v ? 1u : 0u) + (fsub(cur, v) > p.margin ? 0x10000u : 0u);
+                    }
+                }
+                hi = fmaxf(hi, m);
+            }
+            __syncwarp();   // this buffer is refilled by the next iteration's copy
+        }
+        const bool ok = __all_sync(0xffffffffu, cok && lo >= 0.0f && hi <= 1.0f);
+        unsigned keep = 0;   // bit = position
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const unsigned meas = __reduce_add_sync(0xffffffffu, cnt[i] & 0xFFFFu);
+            const unsigned far = __reduce_add_sync(0xffffffffu, cnt[i] >> 16);
+            if (i < nr && !(2ull * far > meas)) keep |= 1u << i;
+        }
+        const unsigned kept_cols = __ballot_sync(0xffffffffu, real && (keep >> rank & 1));
+        if (lane == 0) {
+            if (!ok) flag_data_error(p.st);
+            p.out_keep[q] = ok ? kept_cols : 0u;
+        }
+    }
+}
+
 }  // namespace
 
 int launch_uniform(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int fixed_gamma, float weight,
@@ -144,6 +384,24 @@ int launch_pareto(ekya_handle* h, long long n_sets, int n, const float* cost, co
     const int grid = (int)std::min<long long>(need, (long long)h->sm_count * 8);
     auto k = n <= 8 ? pareto_kernel<8> : n <= 18 ? pareto_kernel<18> : pareto_kernel<31>;
     k<<<grid, 256, 0, s>>>(p);
+    h->launches++;
+    return cuda_status(cudaGetLastError());
+}
+
+int launch_prune(ekya_handle* h, long long n_query, int H, int n, const float* cost, const float* acc, float margin,
+                 uint32_t* out_keep, cudaStream_t s) {
+    if (n_query == 0) return EKYA_OK;
+    PruneParams p{n_query, H, n, cost, acc, margin, out_keep, h->dstate};
+    const long long need = (n_query + kBaseWarps - 1) / kBaseWarps;
+    const int grid = (int)std::min<long long>(need, (long long)h->sm_count * 8);
+    if (n == 18) {
+        const long long need4 = (n_query + kPruneWarps - 1) / kPruneWarps;
+        prune_sorted_kernel<18><<<(int)std::min<long long>(need4, (long long)h->sm_count * 16), kPruneWarps * 32, 0, s>>>(p);
+        h->launches++;
+        return cuda_status(cudaGetLastError());
+    }
+    auto k = n <= 8 ? prune_kernel<8> : n <= 18 ? prune_kernel<18> : prune_kernel<31>;
+    k<<<grid, kBaseWarps * 32, 0, s>>>(p);
     h->launches++;
     return cuda_status(cudaGetLastError());
 }

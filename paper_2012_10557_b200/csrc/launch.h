@@ -44,6 +44,8 @@ int launch_uniform(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int
                    uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum, float* out_mean, cudaStream_t s);
 int launch_pareto(ekya_handle* h, long long n_sets, int n, const float* cost, const float* post,
                   uint32_t* out_mask, cudaStream_t s);
+int launch_prune(ekya_handle* h, long long n_query, int H, int n, const float* cost, const float* acc, float margin,
+                 uint32_t* out_keep, cudaStream_t s);
 
 int launch_curve_fit(ekya_handle* h, long long n_sets, int np, const float* acc, const int* full_epochs,
                      float* out_pred, float* out_params, cudaStream_t s);

@@ -26,7 +26,7 @@ LAMBDA_NONE = 7
 SYMBOLS = ["ekya_create", "ekya_destroy", "ekya_last_error", "ekya_launch_count", "ekya_version",
            "ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate",
            "ekya_comm_unique_id", "ekya_comm_init", "ekya_gather_decisions", "ekya_counters", "ekya_place",
-           "ekya_checkpoint_decide", "ekya_uniform_schedule", "ekya_pareto", "ekya_curve_fit",
+           "ekya_checkpoint_decide", "ekya_uniform_schedule", "ekya_pareto", "ekya_prune_configs", "ekya_curve_fit",
            "ekya_window_workspace_bytes", "ekya_window_schedule"]
 
 
@@ -94,6 +94,8 @@ def load_library(path: str = LIB_PATH):
     L.ekya_uniform_schedule.restype = ctypes.c_int
     L.ekya_pareto.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P, P, P, P]
     L.ekya_pareto.restype = ctypes.c_int
+    L.ekya_prune_configs.argtypes = [P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, P, P, ctypes.c_float, P, P]
+    L.ekya_prune_configs.restype = ctypes.c_int
     L.ekya_window_workspace_bytes.argtypes = [ctypes.POINTER(Dims)]
     L.ekya_window_workspace_bytes.restype = ctypes.c_size_t
     L.ekya_window_schedule.argtypes = [P, ctypes.POINTER(Dims), ctypes.POINTER(Tables), ctypes.c_int, P,
@@ -255,6 +257,18 @@ def ekya_pareto(h: Handle, cost, post, out_mask, stream=None):
                          _ptr(post, torch.float32, "post", True), _ptr(out_mask, torch.uint32, "out_mask"),
                          _stream(stream))
     _check(code, "ekya_pareto")
+
+
+def ekya_prune_configs(h: Handle, cost, hist_acc, margin: float, out_keep, stream=None):
+    L = load_library()
+    Q, n = cost.shape
+    H = hist_acc.shape[1]
+    if tuple(hist_acc.shape) != (Q, H, n) or tuple(out_keep.shape) != (Q,):
+        raise ValueError("ekya_prune_configs: cost [Q][n], hist_acc [Q][H][n], out_keep [Q]")
+    code = L.ekya_prune_configs(h.ptr, Q, H, n, _ptr(cost, torch.float32, "cost", True),
+                                _ptr(hist_acc, torch.float32, "hist_acc", True), float(margin),
+                                _ptr(out_keep, torch.uint32, "out_keep"), _stream(stream))
+    _check(code, "ekya_prune_configs")
 
 
 def ekya_window_workspace_bytes(dims: Dims) -> int:
@@ -423,6 +437,13 @@ def uniform_schedule(h, tables: dict, units, steal_units, unit_gpu_seconds, a_mi
 def pareto(h, cost, post, stream=None):
     out = torch.empty(cost.shape[:-1], dtype=torch.uint32, device=cost.device)
     ekya_pareto(h, cost, post, out, stream=stream)
+    return out
+
+
+def prune_configs(h, cost, hist_acc, margin, stream=None):
+    """History-based pruning (PN1-PN3): cost [Q][n], hist_acc [Q][H][n] -> keep mask [Q] u32."""
+    out = torch.empty(cost.shape[:1], dtype=torch.uint32, device=cost.device)
+    ekya_prune_configs(h, cost, hist_acc, margin, out, stream=stream)
     return out
 
 

@@ -515,6 +515,48 @@ def test_pareto_bitexact(h):
         assert_eq(m, oracle.pareto(c, p), f"pareto mask n={n}")
 
 
+@pytest.mark.parametrize("name,pc", [c for c in PROF_CASES if c[0] != "big-h"], ids=[c[0] for c in PROF_CASES
+                                                                                    if c[0] != "big-h"])
+def test_prune_profile_histories_bitexact(h, name, pc):
+    """History-based pruning (PN1-PN3) on the profiler's history accuracies (dense, sparse,
+    ragged, no history) with the schedulers' cost tables, at three margins."""
+    P = synth.profile_inputs(pc)
+    acc = P["hist_acc"].numpy()
+    Q, G = acc.shape[0], acc.shape[2]
+    cfg = variant(synth.CONFIG2, n_inst=(Q + 9) // 10, ragged=True)
+    _, inst = tables(cfg)
+    cost = np.ascontiguousarray(inst.cost.reshape(-1, inst.cost.shape[-1])[:Q, :G])
+    for m in (0.0, 0.02, 0.1):
+        keep = ek().prune_configs(h, torch.from_numpy(cost).cuda(), torch.from_numpy(acc).cuda(), m)
+        ok, bad = oracle.prune(cost, acc, m)
+        assert bad == 0 and h.last_error() == 0
+        assert_eq(keep, ok, f"keep mask margin={m}")
+
+
+def test_prune_random_edges_bitexact(h):
+    """Tie-heavy costs and accuracies, unmeasured and padding configs, every register-bound
+    instantiation (n <= 8, 18, 31), window counts around the 32-window staging, invalid
+    streams."""
+    rng = np.random.default_rng(43)
+    for n, H in [(1, 1), (5, 0), (8, 31), (9, 32), (18, 33), (18, 500), (31, 65), (31, 7)]:
+        Q = 300
+        c = (rng.choice([1.0, 2.0, 3.0, 5.0], (Q, n)) * rng.integers(1, 3, (Q, n))).astype(np.float32)
+        c[rng.uniform(size=c.shape) < 0.1] = np.inf
+        A = np.round(rng.uniform(0, 1, (Q, H, n)), 1).astype(np.float32)
+        A[rng.uniform(size=A.shape) < 0.2] = np.nan
+        A[Q // 2:] = rng.uniform(0, 1, A[Q // 2:].shape).astype(np.float32)   # no ties
+        if H:
+            A[7, :, :] = np.nan                                                  # nothing measured
+            A[9, 0, 0] = 1.5                                                     # invalid unless padding
+        c[11, 0] = np.nan                                                        # invalid
+        c[13, -1] = -1.0                                                         # invalid
+        for m in (0.0, 0.15):
+            keep = ek().prune_configs(h, torch.from_numpy(c).cuda(), torch.from_numpy(A).cuda(), m)
+            ok, bad = oracle.prune(c, A, m)
+            assert bad > 0 and h.last_error() == -6
+            assert_eq(keep, ok, f"keep mask n={n} H={H} margin={m}")
+
+
 # ---------------------------------------------------------------------------
 # NEXT-2: micro-profiler curve fit
 # ---------------------------------------------------------------------------

@@ -32,6 +32,8 @@ if a.next:
     ekya.curve_fit(h, acc, torch.full((S,), 30, dtype=torch.int32, device=dev))
     ekya.uniform_schedule(h, T, *w.args)
     ekya.pareto(h, T["cost"], T["post"])
+    Q, G2 = P["hist_acc"].shape[0], P["hist_acc"].shape[2]
+    ekya.prune_configs(h, T["cost"].reshape(-1, G)[:Q, :G2].contiguous(), P["hist_acc"], 0.05)
     ekya.place(h, O.dec[0]["alloc"], w.U, 8)
     n = B * V
     tau = torch.rand(n, device=dev) * 100

@@ -13,7 +13,7 @@ NAMES = [("cluster2_kernel", "profile_cluster"), ("cluster_kernel", "profile_clu
          ("radius_kernel", "profile_radius"), ("grid_kernel", "eval_grid"), ("list_kernel", "eval_list"),
          ("thief_kernel<0>", "thief_steepest"), ("thief_kernel<1>", "thief_literal"),
          ("curve_fit_kernel", "next2_curve_fit"), ("uniform_kernel", "next3_uniform"),
-         ("pareto_kernel", "next3_pareto"), ("place_kernel", "next4_placement"),
+         ("pareto_kernel", "next3_pareto"), ("prune_kernel", "next3_prune"), ("place_kernel", "next4_placement"),
          ("checkpoint_kernel", "next4_checkpoint")]
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_issued.avg.pct_of_peak_sustained_active",
@@ -89,7 +89,7 @@ def main(ev, tag):
     step_ms = bench["ms_per_step"]
     fd = {n: d for n, d in full}
     for n in ["profile_cluster", "profile_radius", "eval_grid", "eval_list", "thief_steepest", "thief_literal",
-              "next2_curve_fit", "next3_uniform", "next3_pareto", "next4_placement", "next4_checkpoint"]:
+              "next2_curve_fit", "next3_uniform", "next3_pareto", "next3_prune", "next4_placement", "next4_checkpoint"]:
         ms = per.get(n, [])
         nm = sum(ms) / len(ms) if ms else float("nan")
         share = sum(ms) / tot if ms else float("nan")
