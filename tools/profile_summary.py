@@ -13,7 +13,7 @@ NAMES = [("cluster2_kernel", "profile_cluster"), ("cluster_kernel", "profile_clu
          ("radius_kernel", "profile_radius"), ("grid_kernel", "eval_grid"), ("list_kernel", "eval_list"),
          ("thief_kernel<0>", "thief_steepest"), ("thief_kernel<1>", "thief_literal"),
          ("curve_fit_kernel", "next2_curve_fit"), ("uniform_kernel", "next3_uniform"),
-         ("pareto_kernel", "next3_pareto"), ("prune_kernel", "next3_prune"), ("place_kernel", "next4_placement"),
+         ("pareto_kernel", "next3_pareto"), ("prune_", "next3_prune"), ("place_kernel", "next4_placement"),
          ("checkpoint_kernel", "next4_checkpoint")]
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_issued.avg.pct_of_peak_sustained_active",
