@@ -268,10 +268,10 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 8) prune_sorted_kernel(Prune
             dst_s[warp][lane] = real ? pos : -1;
             col_s[warp][pos] = real ? lane : -1;
         }
-        for (int e = lane; e < 32 * (N - nr); e += 32) {   // padding positions: NaN in both buffers
+        for (int e = lane; e < 32 * (N - nr); e += 32) {   // padding positions: NaN in every buffer
             const int w = e / (N - nr), k = nr + (e - w * (N - nr));
-            rows[warp][0][w * N + k] = __int_as_float(0x7fc00000);
-            rows[warp][1][w * N + k] = __int_as_float(0x7fc00000);
+#pragma unroll
+            for (int sb = 0; sb < kPruneStages; ++sb) rows[warp][sb][w * N + k] = __int_as_float(0x7fc00000);
         }
         __syncwarp();
         const float* A = p.acc + q * (long long)H * N;

@@ -515,6 +515,20 @@ def test_pareto_bitexact(h):
         assert_eq(m, oracle.pareto(c, p), f"pareto mask n={n}")
 
 
+def dirty_shared_memory(h):
+    """Leave out-of-range bit patterns (7.0) in every SM's shared memory: the profiler kernels
+    stage a 54 KB history tile per query (the call is invalid data and flags; cleared here),
+    so a later kernel that reads shared memory it never wrote fails parity instead of
+    reading the zeros of a fresh context."""
+    pc = synth.ProfileConfig("p", 2048, 500, 27, 18)
+    P = {k: v.cuda() for k, v in synth.profile_inputs(pc).items()}
+    P["hist"].fill_(7.0)
+    for mode in (ek().PROFILE_CLUSTER, ek().PROFILE_RADIUS):
+        ek().profile_estimate(h, P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=mode)
+    torch.cuda.synchronize()
+    h.last_error()
+
+
 @pytest.mark.parametrize("name,pc", [c for c in PROF_CASES if c[0] != "big-h"], ids=[c[0] for c in PROF_CASES
                                                                                     if c[0] != "big-h"])
 def test_prune_profile_histories_bitexact(h, name, pc):
@@ -526,6 +540,7 @@ def test_prune_profile_histories_bitexact(h, name, pc):
     cfg = variant(synth.CONFIG2, n_inst=(Q + 9) // 10, ragged=True)
     _, inst = tables(cfg)
     cost = np.ascontiguousarray(inst.cost.reshape(-1, inst.cost.shape[-1])[:Q, :G])
+    dirty_shared_memory(h)
     for m in (0.0, 0.02, 0.1):
         keep = ek().prune_configs(h, torch.from_numpy(cost).cuda(), torch.from_numpy(acc).cuda(), m)
         ok, bad = oracle.prune(cost, acc, m)
@@ -538,6 +553,7 @@ def test_prune_random_edges_bitexact(h):
     instantiation (n <= 8, 18, 31), window counts around the 32-window staging, invalid
     streams."""
     rng = np.random.default_rng(43)
+    dirty_shared_memory(h)
     for n, H in [(1, 1), (5, 0), (8, 31), (9, 32), (18, 33), (18, 500), (31, 65), (31, 7)]:
         Q = 300
         c = (rng.choice([1.0, 2.0, 3.0, 5.0], (Q, n)) * rng.integers(1, 3, (Q, n))).astype(np.float32)
