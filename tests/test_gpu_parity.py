@@ -33,6 +33,27 @@ def ek():
     return ekya
 
 
+@pytest.fixture(scope="module")
+def _dirty_inputs(h):
+    pc = synth.ProfileConfig("p", 1184, 500, 27, 18)
+    P = {k: v.cuda() for k, v in synth.profile_inputs(pc).items()}
+    P["hist"].fill_(7.0)
+    return P
+
+
+@pytest.fixture(autouse=True)
+def dirty_shared_memory(h, _dirty_inputs):
+    """Before every test, leave out-of-range bit patterns (7.0) in every SM's shared memory:
+    the profiler kernels stage a 54 KB history tile per query (invalid data: flagged, and
+    cleared here), so a kernel that reads shared memory it never wrote fails parity instead
+    of reading the zeros of a fresh context."""
+    P = _dirty_inputs
+    for mode in (ek().PROFILE_CLUSTER, ek().PROFILE_RADIUS):
+        ek().profile_estimate(h, P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=mode)
+    torch.cuda.synchronize()
+    h.last_error()
+
+
 def tables(cfg, lo=0, hi=None):
     T = synth.sched_tables(cfg, lo, hi)
     inst = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
@@ -515,20 +536,6 @@ def test_pareto_bitexact(h):
         assert_eq(m, oracle.pareto(c, p), f"pareto mask n={n}")
 
 
-def dirty_shared_memory(h):
-    """Leave out-of-range bit patterns (7.0) in every SM's shared memory: the profiler kernels
-    stage a 54 KB history tile per query (the call is invalid data and flags; cleared here),
-    so a later kernel that reads shared memory it never wrote fails parity instead of
-    reading the zeros of a fresh context."""
-    pc = synth.ProfileConfig("p", 2048, 500, 27, 18)
-    P = {k: v.cuda() for k, v in synth.profile_inputs(pc).items()}
-    P["hist"].fill_(7.0)
-    for mode in (ek().PROFILE_CLUSTER, ek().PROFILE_RADIUS):
-        ek().profile_estimate(h, P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=mode)
-    torch.cuda.synchronize()
-    h.last_error()
-
-
 @pytest.mark.parametrize("name,pc", [c for c in PROF_CASES if c[0] != "big-h"], ids=[c[0] for c in PROF_CASES
                                                                                     if c[0] != "big-h"])
 def test_prune_profile_histories_bitexact(h, name, pc):
@@ -540,7 +547,6 @@ def test_prune_profile_histories_bitexact(h, name, pc):
     cfg = variant(synth.CONFIG2, n_inst=(Q + 9) // 10, ragged=True)
     _, inst = tables(cfg)
     cost = np.ascontiguousarray(inst.cost.reshape(-1, inst.cost.shape[-1])[:Q, :G])
-    dirty_shared_memory(h)
     for m in (0.0, 0.02, 0.1):
         keep = ek().prune_configs(h, torch.from_numpy(cost).cuda(), torch.from_numpy(acc).cuda(), m)
         ok, bad = oracle.prune(cost, acc, m)
@@ -553,7 +559,6 @@ def test_prune_random_edges_bitexact(h):
     instantiation (n <= 8, 18, 31), window counts around the 32-window staging, invalid
     streams."""
     rng = np.random.default_rng(43)
-    dirty_shared_memory(h)
     for n, H in [(1, 1), (5, 0), (8, 31), (9, 32), (18, 33), (18, 500), (31, 65), (31, 7)]:
         Q = 300
         c = (rng.choice([1.0, 2.0, 3.0, 5.0], (Q, n)) * rng.integers(1, 3, (Q, n))).astype(np.float32)
