@@ -21,6 +21,8 @@
 // by a correctly rounded reciprocal, 2-byte config stores.
 #include <algorithm>
 
+#include <type_traits>
+
 #include "launch.h"
 #include "stream_tables.cuh"
 
@@ -277,26 +279,31 @@ __global__ void __launch_bounds__(kGridWarps * 32, 1) grid_kernel(EvalParams p) 
                 const uint2* qp = qst + k;
                 float4* gp = reinterpret_cast<float4*>(p.out_grid + ((q0 + k) << 2));
                 unsigned* cp = p.out_grid_cfg ? reinterpret_cast<unsigned*>(p.out_grid_cfg + ((q0 + k) << 2)) : nullptr;
-                for (; k < k_hi; k += 32, qp += 32, gp += 32) {
-                    const uint2 s2 = *qp;
-                    float v4[4];
-                    unsigned cfg4 = 0;
+                // one loop per config-output case: no per-quad null test of the config pointer
+                auto interior = [&](auto with_cfg) {
+                    for (; k < k_hi; k += 32, qp += 32, gp += 32) {
+                        const uint2 s2 = *qp;
+                        float v4[4];
+                        unsigned cfg4 = 0;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const unsigned wj = j < 2 ? s2.x : s2.y;
-                        const unsigned ri = __byte_perm(wj, 0u, 0x4440u + 2u * (j & 1));
-                        const unsigned rt = __byte_perm(wj, 0u, 0x4441u + 2u * (j & 1));
-                        const unsigned lo = ld_shared_u8(lad_s + ri) * (unsigned)lblk;
-                        const uint2 vc = ld_shared_v2(tvc_s + lo + rt * 8);
-                        v4[j] = __uint_as_float(vc.x);
-                        cfg4 |= vc.y << (8 * j);
+                        for (int j = 0; j < 4; ++j) {
+                            const unsigned wj = j < 2 ? s2.x : s2.y;
+                            const unsigned ri = __byte_perm(wj, 0u, 0x4440u + 2u * (j & 1));
+                            const unsigned rt = __byte_perm(wj, 0u, 0x4441u + 2u * (j & 1));
+                            const unsigned lo = ld_shared_u8(lad_s + ri) * (unsigned)lblk;
+                            const uint2 vc = ld_shared_v2(tvc_s + lo + rt * 8);
+                            v4[j] = __uint_as_float(vc.x);
+                            if constexpr (decltype(with_cfg)::value) cfg4 |= vc.y << (8 * j);
+                        }
+                        *gp = make_float4(v4[0], v4[1], v4[2], v4[3]);
+                        if constexpr (decltype(with_cfg)::value) {
+                            *cp = cfg4;
+                            cp += 32;
+                        }
                     }
-                    *gp = make_float4(v4[0], v4[1], v4[2], v4[3]);
-                    if (cp) {
-                        *cp = cfg4;
-                        cp += 32;
-                    }
-                }
+                };
+                if (cp) interior(std::true_type{});
+                else interior(std::false_type{});
                 if (lane == 0 && k_lo > 0) quad_generic(0);
                 for (int kk = k_hi + lane; kk < nq; kk += 32) quad_generic(kk);
             } else {
