@@ -32,14 +32,37 @@ struct UniformParams {
     DevState* st;
 };
 
+constexpr int kUniStage = 512;   // staged (cost, post) floats per warp
+
+// The instance's cost and post tables are read once, coalesced, for the validity test and
+// kept in the warp's shared memory (V nG <= kUniStage) for the per-stream scans, so the
+// lanes' scans hit shared memory instead of issuing dependent global loads.
 __global__ void __launch_bounds__(kBaseWarps * 32) uniform_kernel(UniformParams p) {
+    __shared__ float s_cost[kBaseWarps][kUniStage], s_post[kBaseWarps][kUniStage];
     const ekya_dims& d = p.d;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int V = d.n_streams, J = 2 * V, nG = d.n_gamma, nL = d.n_lambda, U = d.units;
     const float keep = fsub(1.0f, p.weight);
+    const bool stage = V * nG <= kUniStage;
     for (long long b = (long long)blockIdx.x * kBaseWarps + warp; b < d.n_inst;
          b += (long long)gridDim.x * kBaseWarps) {
-        const bool ok = warp_instance_valid(p.t, b, V, nG, nL);
+        // R-ERR validity (as warp_instance_valid), staging cost and post on the way
+        bool vok = true;
+        const long long v0 = b * V;
+        for (int i = lane; i < V; i += 32) vok &= in01(__ldg(p.t.stale + v0 + i));
+        __syncwarp();   // the previous instance's scans are done with the staging buffers
+        for (int i = lane; i < V * nG; i += 32) {
+            const float c = __ldg(p.t.cost + v0 * nG + i), po = __ldg(p.t.post + v0 * nG + i);
+            if (!(c >= 0.0f)) vok = false;
+            else if (!isinf(c)) vok &= in01(po);
+            if (stage) {
+                s_cost[warp][i] = c;
+                s_post[warp][i] = po;
+            }
+        }
+        for (int i = lane; i < V * nL; i += 32)
+            if (__ldg(p.t.lam_min_units + v0 * nL + i) != kLmuPad) vok &= in01(__ldg(p.t.lam_factor + v0 * nL + i));
+        const bool ok = __all_sync(0xffffffffu, vok);
         if (!ok && lane == 0) flag_data_error(p.st);
         unsigned long long S = 0;
         for (int v = lane; v < V; v += 32) {
@@ -49,16 +72,16 @@ __global__ void __launch_bounds__(kBaseWarps * 32) uniform_kernel(UniformParams 
             const int ri = share - rt;
             const long long bv = b * V + v;
             const float stale = __ldg(p.t.stale + bv);
-            const float* cost = p.t.cost + bv * nG;
-            const float* post = p.t.post + bv * nG;
+            const float* cost = stage ? s_cost[warp] + v * nG : p.t.cost + bv * nG;
+            const float* post = stage ? s_post[warp] + v * nG : p.t.post + bv * nG;
             // U2: the fixed retraining config (1-based, 0 = none)
             int g = p.fixed_gamma;
             if (g < 0) {
                 g = 0;
                 float bp = 0.0f;
                 for (int k = 0; k < nG; ++k) {
-                    if (isinf(__ldg(cost + k))) continue;   // padding
-                    const float pk = __ldg(post + k);
+                    if (isinf(cost[k])) continue;   // padding
+                    const float pk = post[k];
                     if (g == 0 || pk > bp) {
                         g = k + 1;
                         bp = pk;
@@ -70,7 +93,7 @@ __global__ void __launch_bounds__(kBaseWarps * 32) uniform_kernel(UniformParams 
             uint8_t cfg = (uint8_t)(kLambdaNone << 5);
             if (l >= 0) {
                 float acc = stale, w;
-                if (g > 0 && window_acc(stale, __ldg(post + g - 1), __ldg(cost + g - 1), rt, d.unit_gpu_seconds, &w))
+                if (g > 0 && window_acc(stale, post[g - 1], cost[g - 1], rt, d.unit_gpu_seconds, &w))
                     acc = w;
                 val = fmul(__ldg(p.t.lam_factor + bv * nL + l), acc);
                 cfg = (uint8_t)(g | (l << 5));
