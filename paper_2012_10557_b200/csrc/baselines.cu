@@ -128,18 +128,26 @@ __global__ void __launch_bounds__(256) pareto_kernel(ParetoParams p) {
     for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < p.n_sets;
          s += (long long)gridDim.x * blockDim.x) {
         float c[NM], q[NM];
+        bool pad[NM];
 #pragma unroll
         for (int k = 0; k < NM; ++k) {
             c[k] = k < n ? __ldg(p.cost + s * n + k) : INFINITY;
             q[k] = k < n ? __ldg(p.post + s * n + k) : 0.0f;
+            pad[k] = isinf(c[k]);
+            // padding never dominates: its accuracy below every real one (>= any real q
+            // fails); identical points never dominate each other, so j = k needs no test
+            if (pad[k]) q[k] = -INFINITY;
         }
         unsigned m = 0;
 #pragma unroll
         for (int k = 0; k < NM; ++k) {
-            bool dom = isinf(c[k]);
+            bool dom = pad[k];
 #pragma unroll
-            for (int j = 0; j < NM; ++j)
-                if (j != k) dom |= !isinf(c[j]) && c[j] <= c[k] && q[j] >= q[k] && (c[j] < c[k] || q[j] > q[k]);
+            for (int j = 0; j < NM; ++j) {
+                if (j == k) continue;
+                // branch-free: cost' <= cost, post' >= post, and not the same point
+                dom |= (c[j] <= c[k]) & (q[j] >= q[k]) & ((c[j] != c[k]) | (q[j] != q[k]));
+            }
             m |= dom ? 0u : (1u << k);
         }
         p.out_mask[s] = m;
