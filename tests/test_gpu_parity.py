@@ -382,6 +382,50 @@ def test_config3_full_batch_sampled(h):
                 assert_eq(cl[q:q + 1], ocl, f"cluster q={q}")
 
 
+def test_next_rows_full_batch_sampled(h):
+    """The NEXT rows at the bench's full sizes and launch configuration, on sampled outputs:
+    the window timeline, uniform baseline, Pareto frontier and placement over config 4's
+    65,536 instances; pruning over config 3's 65,536 histories with config-4 costs."""
+    cfg = synth.CONFIG4
+    Td = synth.sched_tables(cfg, device="cuda")
+    e = ek()
+    avg, ev, done = e.window_schedule(h, Td, *args(cfg))
+    ua, uc, us, um = e.uniform_schedule(h, Td, *args(cfg))
+    par = e.pareto(h, Td["cost"], Td["post"])
+    a, *_ = e.thief_schedule(h, Td, *args(cfg))
+    pj, pq, pg, npc, load = e.place(h, a, cfg.units, 8)
+    assert h.last_error() == 0
+    sample = [0, 65535] + list(np.random.default_rng(9).integers(0, cfg.n_inst, 6))
+    Tc = {k: pick(v, sample).cpu() for k, v in Td.items()}
+    inst = oracle.Instances(*(Tc[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            *args(cfg))
+    oavg, oev, odone, _ = oracle.window(inst)
+    assert_eq(pick(ev, sample), oev, "window invocations")
+    assert_eq(pick(done, sample), odone, "window completion times")
+    assert_eq(pick(avg, sample), oavg, "window average")
+    oa, oc, osum, _, _ = oracle.uniform(inst)
+    assert_eq(pick(ua, sample), oa, "uniform alloc")
+    assert_eq(pick(us, sample), osum, "uniform sum")
+    assert_eq(pick(par, sample), oracle.pareto(inst.cost, inst.post), "pareto mask")
+    opj, opq, opg, onp, oload, _ = oracle.place(pick(a, sample).cpu().numpy(), cfg.units, 8)
+    assert_eq(pick(pj, sample), opj, "piece jobs")
+    assert_eq(pick(pg, sample), opg, "piece gpus")
+    assert_eq(pick(load, sample), oload, "gpu loads")
+    # pruning: config-3 histories (device generation in chunks), config-4 costs of the first
+    # 65,536 streams
+    pc = synth.CONFIG3
+    acc = torch.empty((pc.n_query, pc.n_hist, pc.n_gamma), device="cuda")
+    for q0 in range(0, pc.n_query, 4096):
+        acc[q0:q0 + 4096] = synth.profile_inputs(pc, q0, q0 + 4096, device="cuda")["hist_acc"]
+    cost = Td["cost"].reshape(-1, Td["cost"].shape[-1])[:pc.n_query, :pc.n_gamma].contiguous()
+    keep = e.prune_configs(h, cost, acc, 0.05)
+    assert h.last_error() == 0
+    qs = [0, 65535] + list(np.random.default_rng(10).integers(0, pc.n_query, 30))
+    ok, bad = oracle.prune(pick(cost, qs).cpu().numpy(), pick(acc, qs).cpu().numpy(), 0.05)
+    assert bad == 0
+    assert_eq(pick(keep, qs), ok, "prune keep mask")
+
+
 def adversarial_ties(n_inst=24):
     """Config-2 instances edited so the config choice hits every tie path: duplicated
     gamma (exact ties -> lowest index), 1-ulp neighbours (near ties inside 2^-21), a zero
