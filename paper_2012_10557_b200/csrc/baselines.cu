@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kBaseWarps * 32) uniform_kernel(UniformParams 
             if (__ldg(p.t.lam_min_units + v0 * nL + i) != kLmuPad) vok &= in01(__ldg(p.t.lam_factor + v0 * nL + i));
         const bool ok = __all_sync(0xffffffffu, vok);
         if (!ok && lane == 0) flag_data_error(p.st);
+        __syncwarp();   // the staged tables are visible to every lane (a vote is not a fence)
         unsigned long long S = 0;
         for (int v = lane; v < V; v += 32) {
             // U1: static split
