@@ -87,14 +87,20 @@ class Workload:
         return self.table_bytes() + self.B * (2 * self.J + self.V + 16)
 
 
-def gen_device(w: Workload, dev):
-    """Generate the batch on the device in chunks (bit-identical to CPU generation)."""
-    T = synth.sched_tables(w.cfg, w.i0, w.i0 + w.B, device=dev)
+def gen_list_rows(w: Workload, dev):
+    """LIST allocation rows of the step (device generation in 1,024-instance chunks)."""
     rows = torch.empty((w.B, w.N, w.J), dtype=torch.uint16, device=dev)
     ch = 1024
     for b0 in range(0, w.B, ch):
         b1 = min(w.B, b0 + ch)
         rows[b0:b1] = synth.list_allocs(w.cfg, w.N, w.i0 + b0, w.i0 + b1, device=dev)
+    return rows
+
+
+def gen_device(w: Workload, dev):
+    """Generate the batch on the device in chunks (bit-identical to CPU generation)."""
+    T = synth.sched_tables(w.cfg, w.i0, w.i0 + w.B, device=dev)
+    rows = gen_list_rows(w, dev)
     p = w.pcfg
     P = {"cur": torch.empty((w.Q, p.n_class), device=dev),
          "hist": torch.empty((w.Q, p.n_hist, p.n_class), device=dev),

@@ -281,6 +281,38 @@ def thief(inst: Instances, mode: int = STEEPEST):
     return alloc, cfg, s, mean, steps, int(bad)
 
 
+def host_threads() -> int:
+    """Host cores this process may use (the oracle's thread pool size)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def per_instance_parallel(fn, inst: Instances, *args, threads: int | None = None):
+    """Run fn(inst_subset, *args) over instance blocks on a thread pool of all host cores and
+    concatenate the array outputs (trailing int = bad count, summed).  Marshalling only: the
+    instances are independent and each block runs the unchanged single-threaded oracle code;
+    ctypes releases the GIL inside the C call."""
+    from concurrent.futures import ThreadPoolExecutor
+    threads = threads or host_threads()
+    B = inst.B
+    if B == 0 or threads <= 1:
+        return fn(inst, *args)
+    bounds = np.linspace(0, B, min(B, threads * 4) + 1).astype(np.int64)
+    blocks = [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1) if bounds[i + 1] > bounds[i]]
+    lib()   # load once before the threads start
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        parts = list(ex.map(lambda lh: fn(inst.subset(np.arange(lh[0], lh[1])), *args), blocks))
+    out = []
+    for i, first in enumerate(parts[0]):
+        if isinstance(first, np.ndarray):
+            out.append(np.concatenate([p[i] for p in parts]))
+        else:
+            out.append(sum(p[i] for p in parts))
+    return tuple(out)
+
+
 def bruteforce(inst: Instances):
     d = inst.dims()
     B, V = inst.B, inst.V

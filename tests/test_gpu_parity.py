@@ -354,12 +354,90 @@ def test_config4_full_batch_sampled(h):
     assert_eq(pick(a, sample), oa, "alloc")
     assert_eq(pick(s, sample), osum, "sum")
     assert_eq(pick(c, sample), oc, "cfg")
+    assert_eq(pick(m, sample), omean, "mean")
+    assert_eq(pick(st, sample), osteps, "steps")
+    # LITERAL over the same full batch
+    a, c, s, m, st = e.thief_schedule(h, Td, *args(cfg), mode=1)
+    assert h.last_error() == 0
+    oa, oc, osum, omean, osteps, _ = oracle.thief(inst, 1)
+    assert_eq(pick(a, sample), oa, "literal alloc")
+    assert_eq(pick(s, sample), osum, "literal sum")
+    assert_eq(pick(c, sample), oc, "literal cfg")
+    assert_eq(pick(m, sample), omean, "literal mean")
+    assert_eq(pick(st, sample), osteps, "literal steps")
     og, ocfg, _ = oracle.eval_grid(inst)
     assert_eq(pick(grid, sample), og, "grid")
     assert_eq(pick(gcfg, sample), ocfg, "grid cfg")
     os_, om, ocf, _ = oracle.eval_list(inst, pick(rows, sample).cpu().numpy())
     assert_eq(pick(ls, sample), os_, "list sum")
+    assert_eq(pick(lm, sample), om, "list mean")
     assert_eq(pick(lc, sample), ocf, "list cfg")
+
+
+def test_config4_list_bench_launch_sampled(h):
+    """LIST in exactly the launch configuration bench.py times: 65,536 config-4 instances x
+    4,096 rows, generated on the device by bench.gen_list_rows, evaluated by the same
+    ekya_eval_allocations call as bench.run_step with all three outputs (sum, mean, cfg).
+    At 4,096 rows the kernel builds stream tables as one task per stream, double-buffered
+    across the ~443 instances of each CTA, so builds of instance j+1 overlap rows of j.
+    24 sampled instances (all 4,096 rows each, incl. both ends of the batch) vs the oracle."""
+    import bench
+    e = ek()
+    dev = torch.device("cuda")
+    w = bench.Workload(synth.CONFIG4.n_inst, synth.CONFIG4.n_alloc, 0)
+    Td = synth.sched_tables(w.cfg, 0, w.B, device=dev)
+    rows = bench.gen_list_rows(w, dev)
+    ls = torch.empty((w.B, w.N), dtype=torch.uint64, device=dev)
+    lm = torch.empty((w.B, w.N), dtype=torch.float32, device=dev)
+    lc = torch.empty((w.B, w.N, w.V), dtype=torch.uint8, device=dev)
+    e.ekya_eval_allocations(h, e.dims_from(Td, *w.args), e.make_tables(**Td), e.EVAL_LIST, w.N, rows, ls, lm, lc)
+    torch.cuda.synchronize()
+    assert h.last_error() == 0
+    rng = np.random.default_rng(11)
+    sample = [0, 1, 442, 443, 444, 32767, 65534, 65535] + list(rng.integers(0, w.B, 16))
+    Tc = synth.sched_tables(w.cfg)            # CPU generation of the same instances
+    inst = oracle.Instances(*(pick(Tc[k], sample).numpy() for k in ("stale", "cost", "post", "lam_min_units",
+                                                              "lam_factor")), *w.args)
+    rc = pick(rows, sample).cpu()
+    for i, b in enumerate(sample):
+        assert torch.equal(rc[i], synth.list_allocs(w.cfg, w.N, b, b + 1)[0]), "device/host row generator mismatch"
+    os_, om, ocf, bad = oracle.per_instance_parallel(oracle.eval_list, inst, rc.numpy())
+    assert bad == 0
+    assert_eq(pick(ls, sample), os_, "list sum")
+    assert_eq(pick(lm, sample), om, "list mean")
+    assert_eq(pick(lc, sample), ocf, "list cfg")
+
+
+def config5_device_tables(B, dev):
+    """Config-5 tables (V = 100, U = 800) for instances [0, B) on the device, in chunks."""
+    cfg = variant(synth.CONFIG5, n_inst=B)
+    parts = [synth.sched_tables(cfg, b0, min(B, b0 + 16384), device=dev) for b0 in range(0, B, 16384)]
+    return cfg, {k: torch.cat([p[k] for p in parts]) for k in parts[0]}
+
+
+def test_config5_sample_both_modes(h):
+    """Config 5 (V = 100, U = 800) thief in both modes on a 131,072-instance batch (the
+    per-GPU shard size of the 1M-instance, 8-GPU run, rounded up), sampled at instances
+    0..63 ("parity-check a fixed sample (instances 0...63)") against the oracle
+    on a thread pool of all host cores (the oracle's STEEPEST costs ~1e2 core-s per
+    config-5 instance)."""
+    e = ek()
+    cfg, Td = config5_device_tables(131072, torch.device("cuda"))
+    sample = list(range(64))
+    Tc = synth.sched_tables(cfg, 0, 64)
+    inst = oracle.Instances(*(Tc[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            *args(cfg))
+    for mode in (1, 0):
+        a, c, s, m, st = e.thief_schedule(h, Td, *args(cfg), mode=mode)
+        assert h.last_error() == 0
+        oa, oc, osum, omean, osteps, bad = oracle.per_instance_parallel(oracle.thief, inst, mode)
+        assert bad == 0
+        assert_eq(a[:64], oa, f"alloc mode {mode}")
+        assert_eq(s[:64], osum, f"sum mode {mode}")
+        assert_eq(c[:64], oc, f"cfg mode {mode}")
+        assert_eq(m[:64], omean, f"mean mode {mode}")
+        assert_eq(st[:64], osteps, f"steps mode {mode}")
+        assert (a.to(torch.int64).sum(1) == cfg.units).all()
 
 
 def test_config3_full_batch_sampled(h):

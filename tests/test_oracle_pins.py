@@ -226,6 +226,37 @@ def test_pickconfigs_gamma_empty_special_case():
     assert vals[1] == 0.0 and (cfg[1] >> 5) == 7
 
 
+def test_pickconfigs_exact_ties_and_amin_boundary():
+    """C7 (Alg. 2's strict '>' from best_accuracy): on exact ties the lowest
+    index wins, for gamma (no retraining first) and for lambda; C3: a lambda whose accuracy
+    equals a_MIN exactly is admissible (">= a_MIN").  uT = 20, a_MIN = 0.4.
+      stream 0: stale 0.5, lambdas factor 0.875 twice (both need 1 unit) -> lambda 0;
+                configs 0 and 1 identical (cost 10, post 0.8): at r_train 1, f = 1/2,
+                value 0.875 (0.8 - 0.5 * 0.3) = 0.56875 for both -> gamma 1 (index 0 + 1).
+      stream 1: stale 0.6, one config with post = stale (cost 5): its window value equals
+                the stale model's -> no retraining (gamma 0); lambda 1 (factor 1.0) needs
+                3 units, so at r_infer 2 lambda 0 (factor 0.75, value 0.45).
+      stream 2: stale 0.5, lambda factor 0.8: accuracy 0.5 * 0.8 = 0.4 = a_MIN exactly
+                (both binary32 0.4f) -> admissible, value 0.4; no real config (padding)."""
+    inf = float("inf")
+    inst = oracle.Instances([[0.5, 0.6, 0.5]],
+                            [[[10.0, 10.0], [5.0, inf], [inf, inf]]],
+                            [[[0.8, 0.8], [0.6, 0.0], [0.0, 0.0]]],
+                            [[[1, 1], [1, 3], [1, 0xFFFF]]],
+                            [[[0.875, 0.875], [0.75, 1.0], [0.8, 1.0]]], 12, 1, 20.0, 0.4)
+    assert np.float32(0.5) * np.float32(0.8) == np.float32(0.4)
+    s, cfg, vals = oracle.pickconfigs(inst, 0, [2, 1, 2, 1, 1, 0])
+    assert cfg.tolist() == [1, 0, 0]
+    assert vals[0] == np.float32(0.875) * np.float32(np.float32(0.8) - np.float32(0.5) * (np.float32(0.8) -
+                                                                                         np.float32(0.5)))
+    assert vals[0] == pytest.approx(0.56875, abs=1e-7)
+    assert vals[1] == np.float32(0.75) * np.float32(0.6)
+    assert vals[2] == np.float32(0.4)
+    # the same choices through a LIST row and a GRID cell of stream 0
+    ls, lm, lc, bad = oracle.eval_list(inst, np.array([[[2, 1, 2, 1, 1, 0]]], np.uint16))
+    assert bad == 0 and lc[0, 0].tolist() == [1, 0, 0]
+
+
 def test_table1_uniform_inference_accuracy():
     """at 0.75 GPU each, inference accuracy drops 65% -> 49% and 50% -> 37.5%."""
     fx, inst = table1_inst()
@@ -449,6 +480,23 @@ def test_profile_spec_examples():
             assert est[0, 0] == pytest.approx(e["expect"], abs=1e-7), e["cite"]
 
 
+def test_profile_radius_inclusive_at_exact_boundary():
+    """C17: similar iff d <= tau, inclusive.  cur (0.5, 0.5) vs window (0.5, 0.25):
+    every operation of rule 5 is exact here (d^2 = 0 + 0.0625, sqrt = 0.25), so at
+    tau = 0.25 the window is similar and at the next binary32 below 0.25 it is not.  Also
+    in CLUSTER's join and every other profile path tau is the only threshold, so this is
+    the whole boundary behaviour."""
+    below = float(np.nextafter(np.float32(0.25), np.float32(0.0)))
+    for tau, hit in ((0.25, True), (below, False), (0.0, False)):
+        est, n, _, bad = oracle.profile([[0.5, 0.5]], [[[0.5, 0.25]]], [[[0.625]]], [[0.125]], tau=tau)
+        assert bad == 0
+        assert n[0, 0] == (1 if hit else 0)
+        assert est[0, 0] == (np.float32(0.625) if hit else np.float32(0.125))
+    # a window at distance exactly 0 is similar even at tau = 0
+    est, n, _, _ = oracle.profile([[0.5, 0.5]], [[[0.5, 0.5]]], [[[0.625]]], [[0.125]], tau=0.0)
+    assert n[0, 0] == 1 and est[0, 0] == np.float32(0.625)
+
+
 @pytest.mark.parametrize("sparse", [False, True])
 def test_profile_radius_vs_float64_bruteforce(sparse):
     cfg = synth.ProfileConfig("t", 24, 300, 27, 18, sparse=sparse)
@@ -510,6 +558,49 @@ def test_cluster_degenerate_identical_histograms():
     est, n, cl, _ = oracle.profile(hist[:, 0], hist, acc, [[0.0]], mode=oracle.CLUSTER, k=5)
     assert (cl[0] == 0).all() and n[0, 0] == H
     assert est[0, 0] == pytest.approx(acc.astype(np.float64).mean(), abs=1e-7)
+
+
+def _hist2(xs):
+    """Two-class histograms (x, 1 - x); every value below is a multiple of 1/16, so the
+    coordinates, their differences and squares are exact in binary32."""
+    return np.array([[[x, 1.0 - x] for x in xs]], np.float32)
+
+
+def test_cluster_init_and_ties_hand_worked():
+    """C19 initial centroids mu_i = h_floor(iH/k) and lowest index on distance ties.
+    H = 4 windows x = 1/16, 9/16, 3/4, 5/16 (histograms (x, 1-x)), k = 3:
+      init mu = (h_0, h_1, h_2) = (1/16, 9/16, 3/4)   [floor(4/3) = 1, floor(8/3) = 2];
+      assign: 5/16 is equidistant (1/4) from 1/16 and 9/16 -> lowest index 0:
+              (0, 1, 2, 0);
+      update: mu_0 = (1/16 + 5/16)/2 = 3/16, mu_1 = 9/16, mu_2 = 3/4;
+      reassign: unchanged -> stop.  Final (0, 1, 2, 0).
+    (A ceil(iH/k) init, mu = (1/16, 3/4, 5/16), converges to (0, 1, 1, 2) instead.)
+    The query (3/16, 13/16) joins cluster 0: estimate = mean of windows 0 and 3."""
+    hist = _hist2([1 / 16, 9 / 16, 3 / 4, 5 / 16])
+    acc = np.array([[[0.25], [0.5], [0.75], [0.5]]], np.float32)
+    est, n, cl, bad = oracle.profile(_hist2([3 / 16])[:, 0], hist, acc, [[0.0]], mode=oracle.CLUSTER, k=3)
+    assert bad == 0
+    assert cl[0].tolist() == [0, 1, 2, 0, 0]
+    assert n[0, 0] == 2 and est[0, 0] == np.float32(0.375)
+
+
+def test_cluster_empty_cluster_keeps_its_centroid():
+    """C19 "empty cluster keeps its centroid", hand-worked.  H = 7 windows
+    x = 11/16, 13/16, 11/16, 0, 5/8, 7/8, 0 (histograms (x, 1-x)), k = 3:
+      init mu = (h_0, h_2, h_4) = (11/16, 11/16, 5/8);
+      assign (ties to the lowest index, so cluster 1 -- a copy of centroid 0 -- gets
+              nobody): (0, 0, 0, 2, 2, 0, 2);
+      update: mu_0 = (11+13+11+14)/64 = 49/64, mu_1 = 11/16 KEPT (empty), mu_2 = 5/24;
+      assign: 11/16 -> mu_1 (distance 0), 13/16 -> mu_0, 5/8 -> mu_1 (1/16 vs 9/64),
+              7/8 -> mu_0, 0 -> mu_2: (1, 0, 1, 2, 1, 0, 2);
+      update: mu_0 = 27/32, mu_1 = 2/3, mu_2 = 0;  assign: unchanged -> stop.
+    The query (11/16, 5/16) joins cluster 1 = windows {0, 2, 4}."""
+    hist = _hist2([11 / 16, 13 / 16, 11 / 16, 0.0, 5 / 8, 7 / 8, 0.0])
+    acc = np.array([[[0.5], [0.1], [0.75], [0.2], [1.0], [0.3], [0.4]]], np.float32)
+    est, n, cl, bad = oracle.profile(_hist2([11 / 16])[:, 0], hist, acc, [[0.0]], mode=oracle.CLUSTER, k=3)
+    assert bad == 0
+    assert cl[0].tolist() == [1, 0, 1, 2, 1, 0, 2, 1]
+    assert n[0, 0] == 3 and est[0, 0] == np.float32(0.75)
 
 
 def test_cluster_on_synth_converges_to_fixed_point():
@@ -887,6 +978,68 @@ def test_window_single_stream_closed_form():
     assert bad == 0 and ev[0] == 2 and done[0, 0] == t1
     assert avg[0] == np.float32(np.float32(0.0) + seg1 + seg2) / np.float32(1.0)
     assert avg[0] == pytest.approx(23 / 30, abs=1e-6)
+
+
+def test_window_partial_progress_two_streams():
+    """W3 (retraining branch) and W6 on a hand-worked two-stream timeline.
+
+    U = 4, steal_units 8 > every share, so no steal is ever possible (C14) and every
+    invocation keeps the fair start (C9): r_infer = r_train = 1 per stream.  uT = 10, one
+    lambda (factor 1, needs 1 unit), a_MIN 0, stale 0.5.
+      A: cost 2.5, post 0.75 -> f = 1/4, window value 0.6875 > 0.5: retrains, done at 1/4.
+      B: cost 7.5, post 0.75 -> f = 3/4, value 0.5625 > 0.5: retrains, done at 3/4.
+    Invocation 1 (tau = 0) ends at tau* = 1/4 (W4).  B has done (1/4)/(3/4) = 1/3 of its
+    work, so R_B = 7.5 (1 - 1/3) = 5 (W6).  Invocation 2 (tau = 1/4): B's residual cost is
+    R_B / (1 - 1/4) = 20/3 (W3), f = 2/3, so B completes at 1/4 + (2/3)(3/4) = 3/4 -- the
+    progress carried over exactly.  Invocation 3 at 3/4: both done, run to 1.
+    Realized averages (W5): A = 1/4 * 0.5 + 3/4 * 0.75 = 0.6875,
+    B = 3/4 * 0.5 + 1/4 * 0.75 = 0.5625; window average 0.625; 3 invocations.
+    Dropping the residual rescale (B done at 5/8) or keeping the done fraction instead of
+    the remaining one (B done at 1/2) both move B's completion time."""
+    inst = oracle.Instances([[0.5, 0.5]], [[[2.5], [7.5]]], [[[0.75], [0.75]]], [[[1], [1]]],
+                            [[[1.0], [1.0]]], 4, 8, 10.0, 0.0)
+    a, c, _, _, steps, _ = oracle.thief(inst, oracle.STEEPEST)
+    assert a.tolist() == [[1, 1, 1, 1]] and steps[0] == 0 and (c & 31).tolist() == [[1, 1]]
+    for mode in (oracle.STEEPEST, oracle.LITERAL):
+        avg, ev, done, bad = oracle.window(inst, mode)
+        assert bad == 0 and ev[0] == 3
+        assert done[0, 0] == np.float32(0.25)
+        assert done[0, 1] == pytest.approx(0.75, abs=1e-6)
+        exact_A = Fr(1, 4) * Fr(1, 2) + Fr(3, 4) * Fr(3, 4)
+        exact_B = Fr(3, 4) * Fr(1, 2) + Fr(1, 4) * Fr(3, 4)
+        assert exact_A == Fr(11, 16) and exact_B == Fr(9, 16)
+        assert avg[0] == pytest.approx(float((exact_A + exact_B) / 2), abs=2e-6)
+
+
+def test_window_idle_stream_starts_after_a_completion():
+    """W3 (idle branch) on a hand-worked two-stream timeline: units freed by a finished
+    retraining let an idle stream start, with its cost scaled to the shorter residual window.
+
+    U = 4, steal_units 1, uT = 10, one lambda (factor 1, needs 1 unit), a_MIN 0, stale 0.5.
+      A: cost 5, post 0.75: f(1) = 1/2 (value 0.625), f(2) = 1/4 (value 0.6875).
+      B: cost 12, post 0.875: f(1) = 6/5 > 1 (infeasible), f(2) = 3/5 (value 0.65).
+    tau = 0, fair start (1, 1 | 1, 1): the only improving steal moves B's training unit to
+    A's (+1/16; giving A's to B is +0.025 - 0.125 < 0; any inference steal zeroes a
+    stream), after which nothing improves, in both modes: A (1, 2) done at 1/4, B (1, 0)
+    idle.  tau = 1/4: A's training unit is worthless to A (done), and B's residual cost
+    is 12 / (3/4) = 16 (W3), so with 2 units f = 16/20 = 4/5 (value 0.575 > 0.5): B
+    starts and completes at 1/4 + (4/5)(3/4) = 17/20.  Realized (W5):
+    A = 1/4 * 0.5 + 3/4 * 0.75 = 0.6875,
+    B = 1/4 * 0.5 + (3/5) * 0.5 + (3/20) * 0.875 = 0.55625, average 0.621875.
+    Without the rescale B would finish at 1/4 + (3/5)(3/4) = 7/10."""
+    inst = oracle.Instances([[0.5, 0.5]], [[[5.0], [12.0]]], [[[0.75], [0.875]]], [[[1], [1]]],
+                            [[[1.0], [1.0]]], 4, 1, 10.0, 0.0)
+    for mode in (oracle.STEEPEST, oracle.LITERAL):
+        a, c, _, _, steps, _ = oracle.thief(inst, mode)
+        assert a.tolist() == [[1, 2, 1, 0]] and (c & 31).tolist() == [[1, 0]]
+        avg, ev, done, bad = oracle.window(inst, mode)
+        assert bad == 0 and ev[0] == 3
+        assert done[0, 0] == np.float32(0.25)
+        assert done[0, 1] == pytest.approx(17 / 20, abs=1e-6)
+        exact_A = Fr(1, 4) * Fr(1, 2) + Fr(3, 4) * Fr(3, 4)
+        exact_B = Fr(1, 4) * Fr(1, 2) + Fr(3, 5) * Fr(1, 2) + Fr(3, 20) * Fr(7, 8)
+        assert avg[0] == pytest.approx(float((exact_A + exact_B) / 2), abs=2e-6)
+        assert float((exact_A + exact_B) / 2) == 0.621875
 
 
 def test_window_without_retraining_is_the_thief_estimate():

@@ -1,0 +1,68 @@
+"""Mutation check of the oracle's pins: each mutant is a one-line change to
+oracle/ekya_oracle.c (a plausible mistake); the -m "not gpu" oracle pins must fail on it.
+Runs in a scratch copy under /tmp; prints the first failing test per mutant.
+usage: python tools/mutants.py [name ...]"""
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+MUTANTS = {
+    # NEXT-1 window timeline (readings W3, W6)
+    "W3-idle-no-rescale": ("if (stt[v] == 0) cs = isinf(c) ? c : c * sc;", "if (stt[v] == 0) cs = c;"),
+    "W3-retraining-no-rescale": ("else if (stt[v] == 1 && k + 1 == g[v]) cs = R[v] * sc;",
+                                 "else if (stt[v] == 1 && k + 1 == g[v]) cs = R[v];"),
+    "W6-keep-done-fraction": ("const float keep = 1.0f - q;", "const float keep = q;"),
+    # A1 RADIUS threshold (C17)
+    "C17-strict": ("sim[h] = dist <= p->tau;", "sim[h] = dist < p->tau;"),
+    "rule5-d2-as-d": ("float dist = sqrtf(d2);", "float dist = d2;"),
+    "C18-nan-counted": ("if (!sim[h] || isnan(a)) continue;", "if (!sim[h]) continue;"),
+    "C19-init-ceil": ("hq + ((i * H) / K) * C", "hq + ((i * H + K - 1) / K) * C"),
+    "C19-nearest-ties": ("if (di < bd) {                     /* lowest index on ties (C19) */",
+                         "if (di <= bd) {                     /* lowest index on ties (C19) */"),
+    "C19-empty-cluster": ("if (cnt[i] == 0) continue;   /* empty", "if (0) continue;   /* empty"),
+    # rules 1-4 (Alg. 2)
+    "C5-strict-feasible": ("return f <= 1.0f;", "return f < 1.0f;"),
+    "rule2-sign": ("float g = post - prod;", "float g = post + prod;"),
+    "rule4-truncating-q32": ("return (uint64_t)llrintf(y);", "return (uint64_t)y;"),
+    "C7-last-index-wins": ("if (a > best) {                    /* strict", "if (a >= best) {                    /* strict"),
+    "C7-lambda-last-index": ("if (best < 0 || acc > best_acc) {", "if (best < 0 || acc >= best_acc) {"),
+    "C2-keepup-strict": ("if (ri < (int32_t)lmu[l]) continue;", "if (ri <= (int32_t)lmu[l]) continue;"),
+    "C3-amin-strict": ("if (!(acc >= a_min)) continue;", "if (!(acc > a_min)) continue;"),
+    # Alg. 1 (A4-A5)
+    "C9-fair-half-up": ("int32_t rt = share / 2;", "int32_t rt = (share + 1) / 2;"),
+    "C14-floor": ("if (temp[victim] < 0) break;", "if (temp[victim] <= 0) break;"),
+    "C13-accept-ties": ("if (acc > best_acc) {", "if (acc >= best_acc) {"),
+    "C12-steepest-victim-floor": ("if (t == w || alloc[w] < D) continue;", "if (t == w || alloc[w] <= D) continue;"),
+}
+
+
+def run(name, old, new):
+    tmp = f"/tmp/ekya_mut_{os.getpid()}"
+    shutil.rmtree(tmp, ignore_errors=True)
+    os.makedirs(tmp)
+    for d in ("oracle", "synth", "tests"):
+        shutil.copytree(os.path.join(ROOT, d), os.path.join(tmp, d),
+                        ignore=shutil.ignore_patterns("_build", "__pycache__"))
+    shutil.copy(os.path.join(ROOT, "pytest.ini"), tmp)
+    src_path = os.path.join(tmp, "oracle", "ekya_oracle.c")
+    src = open(src_path).read()
+    assert src.count(old) == 1, f"{name}: pattern not unique"
+    open(src_path, "w").write(src.replace(old, new))
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_oracle_pins.py", "-x", "-q", "-m", "not gpu",
+                        "-p", "no:cacheprovider"], cwd=tmp, capture_output=True, text=True)
+    shutil.rmtree(tmp, ignore_errors=True)
+    failed = [ln.split(" ")[1] for ln in r.stdout.splitlines() if ln.startswith("FAILED")]
+    return r.returncode != 0, failed
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(MUTANTS)
+    ok = True
+    for n in names:
+        killed, failed = run(n, *MUTANTS[n])
+        ok &= killed
+        print(f"{n:28s} {'killed by ' + (failed[0] if failed else '?') if killed else 'SURVIVED'}")
+    sys.exit(0 if ok else 1)

@@ -39,7 +39,8 @@ def main(rep, kern, units, top=30):
     ts = sum(smp.values()) or 1
     print(f"instructions per unit {tot / units:.0f}")
     cache = {}
-    for (f, l), v in sorted(res.items(), key=lambda x: -x[1])[:top]:
+    key = (lambda x: -smp[x[0]]) if os.environ.get("BY_SAMPLES") else (lambda x: -x[1])
+    for (f, l), v in sorted(res.items(), key=key)[:top]:
         if f not in cache:
             cache[f] = open(f).read().split("\n") if os.path.exists(f) else []
         t = cache[f][l - 1].strip()[:80] if l - 1 < len(cache[f]) else ""
