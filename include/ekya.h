@@ -254,7 +254,10 @@ int ekya_curve_fit(ekya_handle* h, int64_t n_sets, int32_t n_points, const float
  * (cost [n_sets][n], post [n_sets][n]; e.g. a table's cost/post with n_sets =
  * B*V): bit k of out_mask[s] set iff config k is real (cost finite) and no other
  * real config has cost' <= cost and post' >= post with one strict (P:147 Figure
- * 3's "Pareto boundary"; reading PR1).
+ * 3's "Pareto boundary"; reading PR1).  n = 0 with n_sets > 0 (sets
+ * without configurations, S:115's empty input): EKYA_ERR_SHAPE.  Invalid data
+ * (R-ERR: a cost NaN, negative or -INF -- only +INF is padding --, a real config's
+ * post outside [0,1] or NaN): that set's mask 0 + EKYA_ERR_DATA.
  *
  * ekya_prune_configs -- pruning of configurations "that have historically not been
  * useful ... usually significantly distant from the configurations on the Pareto

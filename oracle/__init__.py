@@ -291,9 +291,10 @@ def host_threads() -> int:
 
 def per_instance_parallel(fn, inst: Instances, *args, threads: int | None = None):
     """Run fn(inst_subset, *args) over instance blocks on a thread pool of all host cores and
-    concatenate the array outputs (trailing int = bad count, summed).  Marshalling only: the
-    instances are independent and each block runs the unchanged single-threaded oracle code;
-    ctypes releases the GIL inside the C call."""
+    concatenate the array outputs (trailing int = bad count, summed).  Array arguments whose
+    first dimension is the instance count (e.g. LIST rows [B][N][J]) are sliced with the
+    block.  Marshalling only: the instances are independent and each block runs the
+    unchanged single-threaded oracle code; ctypes releases the GIL inside the C call."""
     from concurrent.futures import ThreadPoolExecutor
     threads = threads or host_threads()
     B = inst.B
@@ -302,8 +303,14 @@ def per_instance_parallel(fn, inst: Instances, *args, threads: int | None = None
     bounds = np.linspace(0, B, min(B, threads * 4) + 1).astype(np.int64)
     blocks = [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1) if bounds[i + 1] > bounds[i]]
     lib()   # load once before the threads start
+
+    def block(lh):
+        idx = np.arange(lh[0], lh[1])
+        a = [x[lh[0]:lh[1]] if isinstance(x, np.ndarray) and x.ndim >= 1 and x.shape[0] == B else x
+             for x in args]
+        return fn(inst.subset(idx), *a)
     with ThreadPoolExecutor(max_workers=threads) as ex:
-        parts = list(ex.map(lambda lh: fn(inst.subset(np.arange(lh[0], lh[1])), *args), blocks))
+        parts = list(ex.map(block, blocks))
     out = []
     for i, first in enumerate(parts[0]):
         if isinstance(first, np.ndarray):
@@ -409,16 +416,18 @@ def uniform(inst: Instances, fixed_gamma: int = HIGHEST_POST, inference_weight: 
     return alloc, cfg, s, mean, int(bad)
 
 
-def pareto(cost, post):
-    """Pareto-frontier mask (bit k = config k) of each set of configs (reading PR1)."""
+def pareto(cost, post, with_bad=False):
+    """Pareto-frontier mask (bit k = config k) of each set of configs (reading PR1); with
+    with_bad, also the number of invalid sets (R-ERR, mask 0)."""
     cost = _c(cost, np.float32)
     post = _c(post, np.float32)
     n = cost.shape[-1]
     sets = cost.size // max(1, n)
     m = np.zeros(cost.shape[:-1], np.uint32)
-    if lib().orc_pareto(sets, n, _p(cost), _p(post), _p(m)) < 0:
+    bad = lib().orc_pareto(sets, n, _p(cost), _p(post), _p(m))
+    if bad < 0:
         raise ValueError("oracle: invalid pareto shape")
-    return m
+    return (m, int(bad)) if with_bad else m
 
 
 def prune(cost, hist_acc, margin):

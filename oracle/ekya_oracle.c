@@ -824,14 +824,28 @@ int64_t orc_uniform(const orc_dims* d, const float* stale, const float* cost, co
 /* PR1: the Pareto frontier of a stream's configurations in (cost, accuracy) (Figure 3,
  * P:147 "Pareto boundary"): config k is on it iff no other real config k'
  * has cost' <= cost and post' >= post with at least one strict.  Padding (cost +INF) is
- * never on it.  Bit k of out_mask[set] (k = 0..n-1) marks config k. */
+ * never on it.  Bit k of out_mask[set] (k = 0..n-1) marks config k.  Invalid data (R-ERR:
+ * a cost that is NaN, negative or -INF, a real config's accuracy outside [0,1] or NaN):
+ * that set's mask is 0 and it is counted in the return value.  n = 0 (no configurations
+ * at all, S:115's empty input) is an argument error. */
 int64_t orc_pareto(int64_t n_sets, int32_t n, const float* cost, const float* post, uint32_t* out_mask)
 {
-    if (n_sets < 0 || n < 0 || n > 32) return -1;
+    if (n_sets < 0 || n < 1 || n > 32) return -1;
+    int64_t bad = 0;
     for (int64_t s = 0; s < n_sets; ++s) {
         const float* c = cost + s * n;
         const float* p = post + s * n;
         uint32_t m = 0;
+        int valid = 1;
+        for (int32_t k = 0; k < n; ++k) {
+            if (!(c[k] >= 0.0f)) valid = 0;                       /* NaN, negative, -INF */
+            else if (!isinf(c[k]) && !(p[k] >= 0.0f && p[k] <= 1.0f)) valid = 0;
+        }
+        if (!valid) {
+            ++bad;
+            out_mask[s] = 0;
+            continue;
+        }
         for (int32_t k = 0; k < n; ++k) {
             if (isinf(c[k])) continue;
             int dominated = 0;
@@ -843,7 +857,7 @@ int64_t orc_pareto(int64_t n_sets, int32_t n, const float* cost, const float* po
         }
         out_mask[s] = m;
     }
-    return 0;
+    return bad;
 }
 
 /* PN1-PN3: pruning of configurations that have historically not been useful (P:1179-1180

@@ -175,13 +175,8 @@ int ekya_pareto(ekya_handle* h, int64_t n_sets, int32_t n, const float* cost, co
     if (!h) return EKYA_ERR_ARG;
     if (n_sets < 0 || n < 0) return EKYA_ERR_SHAPE;
     if (n > 31) return EKYA_ERR_LIMIT;
-    if (n_sets > 0 && n > 0 && (!cost || !post || !out_mask)) return EKYA_ERR_ARG;
-    if (n_sets > 0 && n == 0) {
-        if (!out_mask) return EKYA_ERR_ARG;
-        if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
-        return cudaMemsetAsync(out_mask, 0, (size_t)n_sets * 4, reinterpret_cast<cudaStream_t>(stream)) ==
-                       cudaSuccess ? EKYA_OK : EKYA_ERR_CUDA;
-    }
+    if (n_sets > 0 && n == 0) return EKYA_ERR_SHAPE;   // no configurations: S:115's empty input
+    if (n_sets > 0 && (!cost || !post || !out_mask)) return EKYA_ERR_ARG;
     if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
     return launch_pareto(h, (long long)n_sets, n, cost, post, out_mask, reinterpret_cast<cudaStream_t>(stream));
 }

@@ -119,6 +119,7 @@ struct ParetoParams {
     const float* cost;
     const float* post;
     uint32_t* out_mask;
+    DevState* st;
 };
 
 // one set per thread: the set's n <= 31 (cost, post) pairs in registers (NM = compile-time
@@ -130,11 +131,13 @@ __global__ void __launch_bounds__(256) pareto_kernel(ParetoParams p) {
          s += (long long)gridDim.x * blockDim.x) {
         float c[NM], q[NM];
         bool pad[NM];
+        bool ok = true;   // R-ERR: costs >= 0 (+INF = padding), real accuracies in [0, 1]
 #pragma unroll
         for (int k = 0; k < NM; ++k) {
             c[k] = k < n ? __ldg(p.cost + s * n + k) : INFINITY;
             q[k] = k < n ? __ldg(p.post + s * n + k) : 0.0f;
             pad[k] = isinf(c[k]);
+            ok &= c[k] >= 0.0f && (pad[k] || (q[k] >= 0.0f && q[k] <= 1.0f));
             // padding never dominates: its accuracy below every real one (>= any real q
             // fails); identical points never dominate each other, so j = k needs no test
             if (pad[k]) q[k] = -INFINITY;
@@ -151,7 +154,8 @@ __global__ void __launch_bounds__(256) pareto_kernel(ParetoParams p) {
             }
             m |= dom ? 0u : (1u << k);
         }
-        p.out_mask[s] = m;
+        if (!ok) flag_data_error(p.st);
+        p.out_mask[s] = ok ? m : 0u;
     }
 }
 
@@ -362,7 +366,10 @@ __global__ void __launch_bounds__(kPruneWarps * 32, 8) prune_sorted_kernel(Prune
                         const float v = sr[i];
                         lo = fminf(lo, v);
                         m = fmaxf(m, v);
-                        sr[i] = m;
+                        // only the real positions: the padding ones must stay NaN for the
+                        // buffer's next use (cp.async refills real positions only); an
+                        // all-unmeasured row would leave -inf there and fail the range check
+                        if (i < nr) sr[i] = m;
                     }
                     const float* arow = A + (long long)(j0 + lane) * N;
                     float cur = -INFINITY;
@@ -411,7 +418,7 @@ int launch_uniform(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int
 int launch_pareto(ekya_handle* h, long long n_sets, int n, const float* cost, const float* post,
                   uint32_t* out_mask, cudaStream_t s) {
     if (n_sets == 0) return EKYA_OK;
-    ParetoParams p{n_sets, n, cost, post, out_mask};
+    ParetoParams p{n_sets, n, cost, post, out_mask, h->dstate};
     const long long need = (n_sets + 255) / 256;
     const int grid = (int)std::min<long long>(need, (long long)h->sm_count * 8);
     auto k = n <= 8 ? pareto_kernel<8> : n <= 18 ? pareto_kernel<18> : pareto_kernel<31>;

@@ -122,7 +122,9 @@ def _check(code, what):
         raise EkyaError(code, what)
 
 
-def _ptr(t, dtype, name, optional=False):
+def _ptr(t, dtype, name, optional=False, numel=None):
+    """Device pointer of a contiguous CUDA tensor of `dtype`; with `numel`, the tensor must
+    hold exactly that many elements (the count the C call will read or write)."""
     if t is None:
         if optional:
             return None
@@ -133,11 +135,19 @@ def _ptr(t, dtype, name, optional=False):
         raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} must hold {numel} elements, got {t.numel()}")
     return ctypes.c_void_p(t.data_ptr()) if t.numel() else None
 
 
-def _stream(stream):
-    s = torch.cuda.current_stream() if stream is None else stream
+def _stream(stream, h=None):
+    """The stream to launch on: the given one, else the current stream of the handle's device.
+    A stream on another device than the handle's is rejected."""
+    dev = h.device if h is not None else None
+    s = (torch.cuda.current_stream(dev) if dev is not None else torch.cuda.current_stream()) \
+        if stream is None else stream
+    if dev is not None and s.device.index is not None and s.device.index != dev:
+        raise ValueError(f"stream is on cuda:{s.device.index}, the handle on cuda:{dev}")
     return ctypes.c_void_p(s.cuda_stream)
 
 
@@ -184,11 +194,23 @@ def make_dims(n_inst, n_streams, n_gamma, n_lambda, units, steal_units, unit_gpu
 
 
 def make_tables(stale, cost, post, lam_min_units, lam_factor):
-    """Device tables; keep the tensors alive while the returned struct is in use."""
-    return Tables(_ptr(stale, torch.float32, "stale"), _ptr(cost, torch.float32, "cost", True),
-                  _ptr(post, torch.float32, "post", True),
-                  _ptr(lam_min_units, torch.uint16, "lam_min_units"),
-                  _ptr(lam_factor, torch.float32, "lam_factor"))
+    """Device tables; keep the tensors alive while the returned struct is in use.  The
+    element counts are remembered and checked against the dims of every call."""
+    t = Tables(_ptr(stale, torch.float32, "stale"), _ptr(cost, torch.float32, "cost", True),
+               _ptr(post, torch.float32, "post", True),
+               _ptr(lam_min_units, torch.uint16, "lam_min_units"),
+               _ptr(lam_factor, torch.float32, "lam_factor"))
+    t.numels = (stale.numel(), cost.numel(), post.numel(), lam_min_units.numel(), lam_factor.numel())
+    return t
+
+
+def _check_tables(dims, tables):
+    BV = dims.n_inst * dims.n_streams
+    want = (BV, BV * dims.n_gamma, BV * dims.n_gamma, BV * dims.n_lambda, BV * dims.n_lambda)
+    got = getattr(tables, "numels", None)
+    if got is not None and tuple(got) != want:
+        raise ValueError(f"tables hold {got} elements, dims need {want} (stale, cost, post, lam_min_units, "
+                         "lam_factor)")
 
 
 def dims_from(tables: dict, units, steal_units, unit_gpu_seconds, a_min):
@@ -204,48 +226,59 @@ def ekya_eval_allocations(h: Handle, dims: Dims, tables: Tables, mode: int, n_al
                           out_sum_q32=None, out_mean=None, out_cfg=None, out_grid=None,
                           out_grid_cfg=None, stream=None):
     L = load_library()
+    _check_tables(dims, tables)
+    B, V = dims.n_inst, dims.n_streams
+    nl = B * n_alloc if mode == EVAL_LIST else None
+    ng = B * V * n_cells(dims.units) if mode == EVAL_GRID else None
     code = L.ekya_eval_allocations(
         h.ptr, ctypes.byref(dims), ctypes.byref(tables), mode, n_alloc,
-        _ptr(alloc, torch.uint16, "alloc", True), _ptr(out_sum_q32, torch.uint64, "out_sum_q32", True),
-        _ptr(out_mean, torch.float32, "out_mean", True), _ptr(out_cfg, torch.uint8, "out_cfg", True),
-        _ptr(out_grid, torch.float32, "out_grid", True),
-        _ptr(out_grid_cfg, torch.uint8, "out_grid_cfg", True), _stream(stream))
+        _ptr(alloc, torch.uint16, "alloc", True, nl and nl * 2 * V),
+        _ptr(out_sum_q32, torch.uint64, "out_sum_q32", True, nl),
+        _ptr(out_mean, torch.float32, "out_mean", True, nl), _ptr(out_cfg, torch.uint8, "out_cfg", True, nl and nl * V),
+        _ptr(out_grid, torch.float32, "out_grid", True, ng),
+        _ptr(out_grid_cfg, torch.uint8, "out_grid_cfg", True, ng), _stream(stream, h))
     _check(code, "ekya_eval_allocations")
 
 
 def ekya_thief_schedule(h: Handle, dims: Dims, tables: Tables, mode: int, out_alloc, out_cfg,
                         out_sum_q32, out_mean=None, out_steps=None, stream=None):
     L = load_library()
+    _check_tables(dims, tables)
+    B, V = dims.n_inst, dims.n_streams
     code = L.ekya_thief_schedule(h.ptr, ctypes.byref(dims), ctypes.byref(tables), mode,
-                                 _ptr(out_alloc, torch.uint16, "out_alloc"),
-                                 _ptr(out_cfg, torch.uint8, "out_cfg"),
-                                 _ptr(out_sum_q32, torch.uint64, "out_sum_q32"),
-                                 _ptr(out_mean, torch.float32, "out_mean", True),
-                                 _ptr(out_steps, torch.uint32, "out_steps", True), _stream(stream))
+                                 _ptr(out_alloc, torch.uint16, "out_alloc", numel=2 * B * V),
+                                 _ptr(out_cfg, torch.uint8, "out_cfg", numel=B * V),
+                                 _ptr(out_sum_q32, torch.uint64, "out_sum_q32", numel=B),
+                                 _ptr(out_mean, torch.float32, "out_mean", True, B),
+                                 _ptr(out_steps, torch.uint32, "out_steps", True, B), _stream(stream, h))
     _check(code, "ekya_thief_schedule")
 
 
 def ekya_profile_estimate(h: Handle, pdims: ProfileDims, cur, hist, hist_acc, fallback, out_est,
                           out_n, out_cluster=None, stream=None):
     L = load_library()
-    code = L.ekya_profile_estimate(h.ptr, ctypes.byref(pdims), _ptr(cur, torch.float32, "cur"),
-                                   _ptr(hist, torch.float32, "hist", True),
-                                   _ptr(hist_acc, torch.float32, "hist_acc", True),
-                                   _ptr(fallback, torch.float32, "fallback"),
-                                   _ptr(out_est, torch.float32, "out_est"),
-                                   _ptr(out_n, torch.int32, "out_n"),
-                                   _ptr(out_cluster, torch.int32, "out_cluster", True), _stream(stream))
+    Q, H, C, G = pdims.n_query, pdims.n_hist, pdims.n_class, pdims.n_gamma
+    code = L.ekya_profile_estimate(h.ptr, ctypes.byref(pdims), _ptr(cur, torch.float32, "cur", numel=Q * C),
+                                   _ptr(hist, torch.float32, "hist", True, Q * H * C),
+                                   _ptr(hist_acc, torch.float32, "hist_acc", True, Q * H * G),
+                                   _ptr(fallback, torch.float32, "fallback", numel=Q * G),
+                                   _ptr(out_est, torch.float32, "out_est", numel=Q * G),
+                                   _ptr(out_n, torch.int32, "out_n", numel=Q * G),
+                                   _ptr(out_cluster, torch.int32, "out_cluster", True, Q * (H + 1)),
+                                   _stream(stream, h))
     _check(code, "ekya_profile_estimate")
 
 
 def ekya_uniform_schedule(h: Handle, dims: Dims, tables: Tables, fixed_gamma: int, inference_weight: float,
                           out_alloc, out_cfg, out_sum_q32, out_mean=None, stream=None):
     L = load_library()
+    _check_tables(dims, tables)
+    B, V = dims.n_inst, dims.n_streams
     code = L.ekya_uniform_schedule(h.ptr, ctypes.byref(dims), ctypes.byref(tables), int(fixed_gamma),
-                                   float(inference_weight), _ptr(out_alloc, torch.uint16, "out_alloc"),
-                                   _ptr(out_cfg, torch.uint8, "out_cfg"),
-                                   _ptr(out_sum_q32, torch.uint64, "out_sum_q32"),
-                                   _ptr(out_mean, torch.float32, "out_mean", True), _stream(stream))
+                                   float(inference_weight), _ptr(out_alloc, torch.uint16, "out_alloc", numel=2 * B * V),
+                                   _ptr(out_cfg, torch.uint8, "out_cfg", numel=B * V),
+                                   _ptr(out_sum_q32, torch.uint64, "out_sum_q32", numel=B),
+                                   _ptr(out_mean, torch.float32, "out_mean", True, B), _stream(stream, h))
     _check(code, "ekya_uniform_schedule")
 
 
@@ -253,9 +286,11 @@ def ekya_pareto(h: Handle, cost, post, out_mask, stream=None):
     L = load_library()
     n = cost.shape[-1]
     n_sets = cost.numel() // max(1, n)
+    if tuple(post.shape) != tuple(cost.shape):
+        raise ValueError("ekya_pareto: post must have cost's shape")
     code = L.ekya_pareto(h.ptr, n_sets, n, _ptr(cost, torch.float32, "cost", True),
-                         _ptr(post, torch.float32, "post", True), _ptr(out_mask, torch.uint32, "out_mask"),
-                         _stream(stream))
+                         _ptr(post, torch.float32, "post", True),
+                         _ptr(out_mask, torch.uint32, "out_mask", numel=n_sets), _stream(stream, h))
     _check(code, "ekya_pareto")
 
 
@@ -267,7 +302,7 @@ def ekya_prune_configs(h: Handle, cost, hist_acc, margin: float, out_keep, strea
         raise ValueError("ekya_prune_configs: cost [Q][n], hist_acc [Q][H][n], out_keep [Q]")
     code = L.ekya_prune_configs(h.ptr, Q, H, n, _ptr(cost, torch.float32, "cost", True),
                                 _ptr(hist_acc, torch.float32, "hist_acc", True), float(margin),
-                                _ptr(out_keep, torch.uint32, "out_keep"), _stream(stream))
+                                _ptr(out_keep, torch.uint32, "out_keep"), _stream(stream, h))
     _check(code, "ekya_prune_configs")
 
 
@@ -278,19 +313,23 @@ def ekya_window_workspace_bytes(dims: Dims) -> int:
 def ekya_window_schedule(h: Handle, dims: Dims, tables: Tables, mode: int, workspace, out_avg, out_events, out_done,
                          stream=None):
     L = load_library()
+    _check_tables(dims, tables)
+    B, V = dims.n_inst, dims.n_streams
     code = L.ekya_window_schedule(h.ptr, ctypes.byref(dims), ctypes.byref(tables), mode,
                                   _ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
-                                  _ptr(out_avg, torch.float32, "out_avg"), _ptr(out_events, torch.uint32, "out_events"),
-                                  _ptr(out_done, torch.float32, "out_done"), _stream(stream))
+                                  _ptr(out_avg, torch.float32, "out_avg", numel=B),
+                                  _ptr(out_events, torch.uint32, "out_events", numel=B),
+                                  _ptr(out_done, torch.float32, "out_done", numel=B * V), _stream(stream, h))
     _check(code, "ekya_window_schedule")
 
 
 def ekya_curve_fit(h: Handle, acc, full_epochs, out_pred, out_params=None, stream=None):
     L = load_library()
     S, n = acc.shape
-    code = L.ekya_curve_fit(h.ptr, S, n, _ptr(acc, torch.float32, "acc"), _ptr(full_epochs, torch.int32, "full_epochs"),
-                            _ptr(out_pred, torch.float32, "out_pred"),
-                            _ptr(out_params, torch.float32, "out_params", True), _stream(stream))
+    code = L.ekya_curve_fit(h.ptr, S, n, _ptr(acc, torch.float32, "acc"),
+                            _ptr(full_epochs, torch.int32, "full_epochs", numel=S),
+                            _ptr(out_pred, torch.float32, "out_pred", numel=S),
+                            _ptr(out_params, torch.float32, "out_params", True, 3 * S), _stream(stream, h))
     _check(code, "ekya_curve_fit")
 
 
@@ -298,20 +337,22 @@ def ekya_place(h: Handle, units: int, gpus: int, alloc, out_piece_job, out_piece
                out_gpu_load=None, stream=None):
     L = load_library()
     B, J = alloc.shape
+    P = B * (J + gpus)
     code = L.ekya_place(h.ptr, B, J, units, gpus, _ptr(alloc, torch.uint16, "alloc"),
-                        _ptr(out_piece_job, torch.uint16, "out_piece_job"),
-                        _ptr(out_piece_q, torch.uint32, "out_piece_q"),
-                        _ptr(out_piece_gpu, torch.int16, "out_piece_gpu"),
-                        _ptr(out_n_pieces, torch.uint16, "out_n_pieces"),
-                        _ptr(out_gpu_load, torch.uint32, "out_gpu_load", True), _stream(stream))
+                        _ptr(out_piece_job, torch.uint16, "out_piece_job", numel=P),
+                        _ptr(out_piece_q, torch.uint32, "out_piece_q", numel=P),
+                        _ptr(out_piece_gpu, torch.int16, "out_piece_gpu", numel=P),
+                        _ptr(out_n_pieces, torch.uint16, "out_n_pieces", numel=B),
+                        _ptr(out_gpu_load, torch.uint32, "out_gpu_load", True, B * gpus), _stream(stream, h))
     _check(code, "ekya_place")
 
 
 def ekya_checkpoint_decide(h: Handle, tau, t, T, a, a_star, A, delta_ckpt, out, stream=None):
     L = load_library()
-    args = [_ptr(x, torch.float32, nm) for x, nm in ((tau, "tau"), (t, "t"), (T, "T"), (a, "a"),
-                                                   (a_star, "a_star"), (A, "A"), (delta_ckpt, "delta_ckpt"))]
-    code = L.ekya_checkpoint_decide(h.ptr, out.numel(), *args, _ptr(out, torch.uint8, "out"), _stream(stream))
+    n = out.numel()
+    args = [_ptr(x, torch.float32, nm, numel=n) for x, nm in ((tau, "tau"), (t, "t"), (T, "T"), (a, "a"),
+                                                              (a_star, "a_star"), (A, "A"), (delta_ckpt, "delta_ckpt"))]
+    code = L.ekya_checkpoint_decide(h.ptr, n, *args, _ptr(out, torch.uint8, "out"), _stream(stream, h))
     _check(code, "ekya_checkpoint_decide")
 
 
@@ -336,7 +377,7 @@ def ekya_gather_decisions(h: Handle, local, root_buf, root=0, stream=None):
         rb = ctypes.c_void_p(root_buf.data_ptr())
     nbytes = local.numel() * local.element_size()
     _check(load_library().ekya_gather_decisions(h.ptr, ctypes.c_void_p(local.data_ptr()), nbytes, rb,
-                                                root, _stream(stream)), "ekya_gather_decisions")
+                                                root, _stream(stream, h)), "ekya_gather_decisions")
 
 
 # ---------------------------------------------------------------------------

@@ -656,6 +656,22 @@ def test_pareto_bitexact(h):
         c[rng.uniform(size=c.shape) < 0.1] = np.inf
         m = ek().pareto(h, torch.from_numpy(c).cuda(), torch.from_numpy(p).cuda())
         assert_eq(m, oracle.pareto(c, p), f"pareto mask n={n}")
+    assert h.last_error() == 0
+    # invalid data (R-ERR): NaN / negative / -inf costs, real accuracies outside [0, 1]
+    c = (rng.choice([1.0, 2.0, 3.0], (3000, 18))).astype(np.float32)
+    p = rng.uniform(0, 1, (3000, 18)).astype(np.float32)
+    c[rng.uniform(size=c.shape) < 0.1] = np.inf
+    p[np.isinf(c)] = 9.0                                  # padding accuracies are ignored
+    c[5, 3], c[7, 0], c[9, 17] = np.nan, -1.0, -np.inf
+    p[11, 2], p[13, 4] = 1.5, np.nan
+    c[11, 2] = c[13, 4] = 1.0
+    m = ek().pareto(h, torch.from_numpy(c).cuda(), torch.from_numpy(p).cuda())
+    om, bad = oracle.pareto(c, p, with_bad=True)
+    assert bad == 5 and h.last_error() == -6
+    assert_eq(m, om, "pareto mask (invalid sets)")
+    with pytest.raises(ek().EkyaError) as ex:
+        ek().pareto(h, torch.zeros((4, 0), device="cuda"), torch.zeros((4, 0), device="cuda"))
+    assert ex.value.code == -3
 
 
 @pytest.mark.parametrize("name,pc", [c for c in PROF_CASES if c[0] != "big-h"], ids=[c[0] for c in PROF_CASES
@@ -698,6 +714,26 @@ def test_prune_random_edges_bitexact(h):
             ok, bad = oracle.prune(c, A, m)
             assert bad > 0 and h.last_error() == -6
             assert_eq(keep, ok, f"keep mask n={n} H={H} margin={m}")
+
+
+def test_prune_equal_costs_padding_and_unmeasured_rows(h):
+    """|Gamma| = 18 (the cost-sorted staging kernel) with padding configs, equal costs (the
+    prefix-maximum-at-group-end branch), H >= 128 so every staging buffer is reused several
+    times, and whole windows unmeasured (all NaN): padding positions must stay unmeasured
+    across buffer reuse, so these valid inputs keep the oracle's mask with no data error."""
+    rng = np.random.default_rng(44)
+    Q, n = 200, 18
+    for H in (128, 130, 500):
+        c = rng.choice([1.0, 2.0, 4.0], (Q, n)).astype(np.float32)   # many equal costs
+        c[:, 15:] = np.inf                                            # padding positions
+        A = rng.uniform(0, 1, (Q, H, n)).astype(np.float32)
+        A[:, ::3, :] = np.nan                                         # unmeasured windows
+        A[rng.uniform(size=A.shape) < 0.1] = np.nan
+        for m in (0.0, 0.1):
+            keep = ek().prune_configs(h, torch.from_numpy(c).cuda(), torch.from_numpy(A).cuda(), m)
+            ok, bad = oracle.prune(c, A, m)
+            assert bad == 0 and h.last_error() == 0, f"H={H}"
+            assert_eq(keep, ok, f"keep mask H={H} margin={m}")
 
 
 # ---------------------------------------------------------------------------

@@ -825,6 +825,22 @@ def test_pareto_spec_examples_and_properties():
                 assert any(c[j] <= c[k] and p[j] >= p[k] for j in on)
 
 
+def test_pareto_invalid_data_and_empty_input():
+    """R-ERR for the frontier: a NaN, negative or -INF cost, or a real config's accuracy
+    outside [0, 1] (or NaN) invalidates the set (mask 0, counted); +INF is padding and its
+    accuracy is ignored; S:115's empty input (no configurations) is an argument error."""
+    inf, nan = float("inf"), float("nan")
+    c = np.array([[1.0, 2.0], [nan, 2.0], [-1.0, 2.0], [-inf, 2.0], [1.0, 2.0], [1.0, 2.0], [1.0, inf]],
+                 np.float32)
+    p = np.array([[0.5, 0.6], [0.5, 0.6], [0.5, 0.6], [0.5, 0.6], [1.5, 0.6], [nan, 0.6], [0.5, 7.0]],
+                 np.float32)
+    m, bad = oracle.pareto(c, p, with_bad=True)
+    assert bad == 5
+    assert m.tolist() == [0b11, 0, 0, 0, 0, 0, 0b01]
+    with pytest.raises(ValueError):
+        oracle.pareto(np.zeros((3, 0), np.float32), np.zeros((3, 0), np.float32))
+
+
 def test_prune_worked_examples():
     """PN1-PN3 on hand-worked cases: costs 1, 2, 3 and three windows.
     w0 = (.5, .7, .6): config 2 sits .1 below the boundary (.7 at cost <= 3); w1 = (.6,
