@@ -40,6 +40,28 @@ METRIC = "scheduler allocations evaluated/sec and thief schedules/sec; % HBM roo
 UNIT = "allocations/s"
 
 
+def fp32_peak(sm_mhz):
+    """Measured FP32 SIMT peak (TFLOP/s) scaled to `sm_mhz`, and its source."""
+    p = os.path.join(ROOT, "profiles", "round2_fp32_peak.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        v = float(d["fp32_simt_tflops"]) * sm_mhz / float(d["sm_mhz"])
+        return v, (f"measured: tools/micro/fp2.cu {d['fp32_simt_tflops']:.2f} TFLOP/s at {d['sm_mhz']:.0f} MHz "
+                   f"(profiles/round2_fp32_peak.json), scaled to {sm_mhz:.0f} MHz")
+    return 148 * 128 * sm_mhz * 1e6 / 1e12, f"derived: 148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz"
+
+
+def inst_counts():
+    """Warp instructions per launch of the issue-bound kernels from an ncu capture of the bench
+    shapes (profiles/round2_inst.json: {kernel: {warp_inst_per_launch, units}})."""
+    p = os.path.join(ROOT, "profiles", "round2_inst.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -252,27 +274,50 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
-def oracle_sample(n_inst=48, n_query=32):
-    """One bounded sample of the same workload, run through the oracle.  Returns
-    (seconds, allocations evaluated, description)."""
+def oracle_threads():
     import oracle
+    return oracle.host_threads()
+
+
+def ref_sizes(args):
+    """Bounded oracle sample: 256 config-4 instances + 128 config-3 queries per host thread
+    (about 3-4 s of wall time per sample on any core count), unless given."""
+    t = oracle_threads()
+    return (args.ref_inst or min(65536, 256 * t)), (args.ref_query or min(65536, 128 * t))
+
+
+def oracle_sample(n_inst, n_query):
+    """One bounded sample of the same workload through the oracle, its independent instances
+    and queries spread over a thread pool of all host cores (the per-instance code is the
+    plain single-threaded oracle).  Returns (seconds, allocations evaluated, description,
+    threads)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import oracle
+    threads = oracle.host_threads()
     w = Workload(n_inst, synth.CONFIG4.n_alloc, n_query)
     T = synth.sched_tables(w.cfg, 0, n_inst)
     inst = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
                             *w.args)
     rows = synth.list_allocs(w.cfg, w.N, 0, n_inst).numpy()
     P = {k: v.numpy() for k, v in synth.profile_inputs(w.pcfg, 0, n_query).items()}
+    qb = np.linspace(0, n_query, min(n_query, 4 * threads) + 1).astype(np.int64)
+    blocks = [(a, b) for a, b in zip(qb[:-1], qb[1:]) if b > a]
+    oracle.lib()
     t0 = time.perf_counter()
-    oracle.profile(P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=oracle.CLUSTER)
-    oracle.profile(P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=oracle.RADIUS)
-    oracle.eval_grid(inst)
-    oracle.eval_list(inst, rows)
-    oracle.thief(inst, oracle.STEEPEST)
-    oracle.thief(inst, oracle.LITERAL)
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        for mode in (oracle.CLUSTER, oracle.RADIUS):
+            list(ex.map(lambda ab: oracle.profile(P["cur"][ab[0]:ab[1]], P["hist"][ab[0]:ab[1]],
+                                                  P["hist_acc"][ab[0]:ab[1]], P["fallback"][ab[0]:ab[1]],
+                                                  mode=mode), blocks))
+    oracle.per_instance_parallel(oracle.eval_grid, inst, threads=threads)
+    oracle.per_instance_parallel(oracle.eval_list, inst, rows, threads=threads)
+    oracle.per_instance_parallel(oracle.thief, inst, oracle.STEEPEST, threads=threads)
+    oracle.per_instance_parallel(oracle.thief, inst, oracle.LITERAL, threads=threads)
     dt = time.perf_counter() - t0
     desc = (f"{n_inst} of 65536 config-4 instances (GRID, LIST x4096, thief STEEPEST+LITERAL) + "
-            f"{n_query} of 65536 config-3 queries (CLUSTER+RADIUS); single thread")
-    return dt, w.allocations(), desc
+            f"{n_query} of 65536 config-3 queries (CLUSTER+RADIUS); oracle on a pool of {threads} threads "
+            f"(all host cores), instances/queries split across them")
+    return dt, w.allocations(), desc, threads
 
 
 def run_reference(args, rank, world):
@@ -280,12 +325,13 @@ def run_reference(args, rank, world):
         return
     import oracle
     oracle.build()
+    ni, nq = ref_sizes(args)
     for _ in range(args.warmup):
-        oracle_sample(args.ref_inst, args.ref_query)
+        oracle_sample(ni, nq)
     ts, units = [], 0
-    desc = ""
+    desc, threads = "", 1
     for _ in range(args.steps):
-        dt, units, desc = oracle_sample(args.ref_inst, args.ref_query)
+        dt, units, desc, threads = oracle_sample(ni, nq)
         ts.append(dt)
     tot = float(sum(ts))
     value = units * args.steps / tot
@@ -295,7 +341,7 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config_block(w, args),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -322,11 +368,14 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     h = ek.Handle(local_rank)
+    # the decision gather runs through an NCCL communicator at every N (one rank at N = 1)
+    uid = [ek.ekya_comm_unique_id() if rank == 0 else None]
     if world > 1:
         import torch.distributed as dist
-        uid = [ek.ekya_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        ek.ekya_comm_init(h, uid[0], world, rank)
+    ek.ekya_comm_init(h, uid[0], world, rank)
+    comm_nranks, comm_rank = ek.ekya_comm_info(h)
+    assert comm_nranks == world and comm_rank == rank, "NCCL communicator does not match the launch"
     w = Workload(args.n_inst, args.n_alloc, args.n_query, inst_offset=rank * args.n_inst,
                  query_offset=rank * args.n_query)
     T, rows, P = gen_device(w, dev)
@@ -336,13 +385,13 @@ def run_ours(args, rank, world, local_rank):
 
     def step(timer=None):
         run_step(ek, h, w, T, rows, P, O, timer)
-        if world > 1:
-            if timer is not None:
-                timer.start("gather")
-            for m in range(2):
-                ek.ekya_gather_decisions(h, O.dec[m]["buf"], root_buf[m], root=0)
-            if timer is not None:
-                timer.stop("gather")
+        # final gather of both modes' decision records to rank 0 (ncclGather; 66 B/instance)
+        if timer is not None:
+            timer.start("gather")
+        for m in range(2):
+            ek.ekya_gather_decisions(h, O.dec[m]["buf"], root_buf[m], root=0)
+        if timer is not None:
+            timer.stop("gather")
 
     def barrier():
         if world > 1:
@@ -385,6 +434,7 @@ def run_ours(args, rank, world, local_rank):
     if args.e2e_steps > 0:
         e2e = run_e2e(ek, h, w, T, rows, P, O, args, world)
 
+    c5 = run_config5(ek, h, dev, args, rank, world) if args.c5_inst > 0 else None
     context = run_context(ek, h, dev, args) if rank == 0 and args.context else None
     if context is not None:
         context.update(run_next1(ek, h, w, T, O, dev))
@@ -395,10 +445,14 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     peak, peak_kind, mp = measured_peaks()
-    sm_mhz = float(mp.get("sm_max_mhz", 1965.0))
-    # FP32 issue peak for the ALU-bound CLUSTER kernel: 148 SMs x 128 FP32 lanes x clock,
-    # one flop per FSUB/FMUL/FADD (no FMA is allowed by the arithmetic contract)
-    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+    clocks = clk.summary()
+    sm_mhz = float(clocks.get("sm_mhz") or mp.get("sm_max_mhz", 1965.0))
+    # FP32 SIMT peak for the ALU-bound CLUSTER kernel: MEASURED (tools/micro/fp2.cu: FADD /
+    # FMUL / FADD2 / FMUL2 streams, profiles/round2_fp32_peak.json) at its clock, scaled to
+    # the SM clock sampled during the timed region; one flop per FSUB/FMUL/FADD (the
+    # arithmetic contract allows no FMA)
+    alu_peak, alu_src = fp32_peak(sm_mhz)
+    insts = inst_counts()
     total_units = w.allocations() * world * args.steps
     value = total_units / (ms / 1000.0)
     rows_out = {}
@@ -423,10 +477,18 @@ def run_ours(args, rank, world, local_rank):
             r["alu_frac"] = tfs / alu_peak
             r["lloyd_passes_per_query"] = lloyd_passes / max(1, args.steps) / w.Q
             roof[k] = {"bound": "alu", "achieved": tfs, "peak": alu_peak, "unit": "TFLOP/s", "frac": tfs / alu_peak,
-                       "peak_source": f"derived: 148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (DESIGN.md 13)",
-                       "algorithmic_flops_per_launch": cluster_flops}
+                       "peak_source": alu_src, "algorithmic_flops_per_launch": cluster_flops}
+        if k in insts:
+            # issue-slot utilisation: warp instructions per launch (ncu sm__inst_executed.sum of the
+            # same launch, profiles/round2_inst.json) / (4 issue slots x 148 SMs x clock x time)
+            wi = insts[k]["warp_inst_per_launch"] * w.B / insts[k]["units"]
+            r["warp_inst_per_unit"] = insts[k]["warp_inst_per_launch"] / insts[k]["units"]
+            r["issue_frac"] = wi / (avg / 1000.0) / (4 * 148 * sm_mhz * 1e6) if not k.startswith("profile") else \
+                insts[k]["warp_inst_per_launch"] * w.Q / insts[k]["units"] / (avg / 1000.0) / (4 * 148 * sm_mhz * 1e6)
         if k.startswith("thief"):
             r["schedules_per_s"] = w.B * world / (avg / 1000.0)
+            r.pop("hbm_frac", None)      # issue-bound: the HBM fraction says nothing here
+            r.pop("algorithmic_gb_per_s", None)
         if k.startswith("profile"):
             r["queries_per_s"] = w.Q * world / (avg / 1000.0)
         if k.startswith("eval_grid"):
@@ -450,18 +512,22 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roofline,
         "rows": rows_out,
         "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
     if e2e is not None:
         line["e2e"] = e2e
     if context is not None:
         line["context"] = context
+    if c5 is not None:
+        line.setdefault("context", {}).update(c5)
+    line["comm"] = {"backend": "nccl", "nranks": comm_nranks, "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                    "gather": "ncclGather of the decision records to rank 0 (ekya_gather_decisions)"}
     if args.cpu_baseline and world == 1:
         import oracle
         oracle.build()
-        dt, units, desc = oracle_sample(args.ref_inst, args.ref_query)
-        line["cpu_baseline"] = {"value": units / dt, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-                                "seconds": dt}
+        dt, units, desc, threads = oracle_sample(*ref_sizes(args))
+        line["cpu_baseline"] = {"value": units / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+                                "sample": desc, "seconds": dt, "nproc": os.cpu_count()}
         # NEXT-4 placement: the oracle on 4,096 of the step's STEEPEST decisions (one thread)
         sample = O.dec[0]["alloc"][:4096].cpu().numpy()
         t0 = time.perf_counter()
@@ -572,7 +638,7 @@ def run_next2(ek, h, w, dev):
     assert h.last_error() == 0
     # algorithmic work per set: 257 grid points x (the 2x2 NNLS + residuals over 5 points)
     flops = S * 257 * (2 * P + 10 + 4 * P)
-    peak_alu = 148 * 128 * 1965e6 / 1e12
+    peak_alu = fp32_peak(1965.0)[0]
     return {"next2_curve_fit": {"sets": S, "points": P, "ms": ms, "sets_per_s": S / (ms / 1000.0),
                                 "alu_frac": flops / (ms / 1000.0) / 1e12 / peak_alu}}
 
@@ -654,6 +720,102 @@ def run_context(ek, h, dev, args):
     return out
 
 
+def run_config5(ek, h, dev, args, rank, world):
+    """BASELINE config 5: 100 streams x 1M instances (V = 100, |Gamma| = 18, |Lambda| = 5,
+    U = 800) sharded over the ranks (rank r owns shard_range(1M, N, r), generated locally from
+    global instance ids), thief STEEPEST + LITERAL per chunk, and the decision records (516 B
+    per instance and mode) gathered to rank 0 chunk by chunk on a second stream while the next
+    chunk computes.  Runs on every rank (the gathers are collective); timed
+    with CUDA events on the compute stream after it waits for the last gather, max over
+    ranks.  Also timed: the same pass without gathers and the gathers alone (overlap).
+    Rank 0 reports a SHA-256 of the gathered decisions in global instance order, which is
+    the same at every N when the root buffer is byte-identical to the one-GPU run."""
+    import hashlib
+    from paper_2012_10557_b200 import shard
+    total = args.c5_inst
+    cfg = synth.SchedConfig(**{**synth.CONFIG5.__dict__, "n_inst": total})
+    lo, hi = shard.shard_range(total, world, rank)
+    B, V = hi - lo, cfg.n_streams
+    parts = [synth.sched_tables(cfg, b0, min(hi, b0 + 16384), device=dev) for b0 in range(lo, hi, 16384)]
+    T = {k: torch.cat([p[k] for p in parts]) for k in parts[0]} if parts else None
+    del parts
+    torch.cuda.synchronize()
+    L = shard.RecordLayout(total, world, V, args.c5_chunks)
+    bufs = [torch.zeros(L.rank_bytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+    roots = [torch.zeros(L.root_bytes, dtype=torch.uint8, device=dev) if rank == 0 else None for _ in range(2)]
+    a5 = (cfg.units, cfg.steal_units, cfg.unit_gpu_seconds, cfg.a_min)
+    chunks = []
+    for c in range(L.n_chunks):
+        b0, b1 = L.chunk_range(rank, c)
+        Tc = {k: v[b0:b1] for k, v in T.items()}
+        chunks.append((ek.dims_from(Tc, *a5), ek.make_tables(**Tc), [L.views(bufs[m], rank, c) for m in range(2)], Tc))
+    comp = torch.cuda.current_stream()
+    comm = torch.cuda.Stream()
+
+    def one_pass(gather=True, compute=True):
+        for c in range(L.n_chunks):
+            if compute:
+                dims, tabs, vs, _ = chunks[c]
+                for m, mode in enumerate((ek.THIEF_STEEPEST, ek.THIEF_LITERAL)):
+                    v = vs[m]
+                    if dims.n_inst:
+                        ek.ekya_thief_schedule(h, dims, tabs, mode, v["alloc"], v["cfg"], v["sum"], v["mean"],
+                                               v["steps"])
+            if gather:
+                e = torch.cuda.Event()
+                e.record(comp)
+                comm.wait_event(e)
+                for m in range(2):
+                    ek.ekya_gather_decisions(h, L.local_chunk(bufs[m], c),
+                                             L.root_chunk(roots[m], c) if rank == 0 else None, root=0, stream=comm)
+        comp.wait_stream(comm)
+
+    def timed(**kw):
+        one_pass(**kw)
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(comp)
+        comm.wait_event(t0)
+        for _ in range(args.c5_reps):
+            one_pass(**kw)
+        t1.record(comp)
+        torch.cuda.synchronize()
+        ms = torch.tensor([t0.elapsed_time(t1) / args.c5_reps], dtype=torch.float64, device=dev)
+        if world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
+
+    ms_all = timed()
+    assert h.last_error() == 0
+    digest = None
+    if rank == 0:
+        hsh = hashlib.sha256()
+        for m in range(2):
+            g = L.unpack(roots[m])
+            for k in ("alloc", "cfg", "sum", "mean", "steps"):
+                hsh.update(g[k].contiguous().view(torch.uint8).cpu().numpy().tobytes())
+        digest = hsh.hexdigest()
+    ms_comp = timed(gather=False)
+    ms_gather = timed(compute=False)
+    rec = L.chunk_bytes * L.n_chunks
+    res = {"config5": {
+        "workload": "BASELINE config 5: 100 streams x 1M instances, |Gamma|=18, |Lambda|=5, U=800 (Delta=0.1 GPU of "
+                    "80 GPUs), sharded over the ranks; thief STEEPEST+LITERAL; chunk-pipelined NCCL gather",
+        "instances_total": total, "instances_per_rank_max": max(L.per), "chunks": L.n_chunks, "n_gpus": world,
+        "ms_per_pass": ms_all, "schedules_per_s": 2 * total / (ms_all / 1000.0),
+        "schedules_per_s_per_gpu": 2 * total / world / (ms_all / 1000.0),
+        "ms_compute_only": ms_comp, "ms_gather_only": ms_gather,
+        "gather_bytes_into_root": 2 * rec * (world - 1), "record_bytes_per_instance": 16 + 5 * V,
+        "decisions_sha256": digest, "reps": args.c5_reps}}
+    del T, bufs, roots, chunks
+    torch.cuda.empty_cache()
+    return res
+
+
 class ChunkOut:
     """Outputs of instances [b0, b1) and queries [q0, q1): views into the full buffers."""
 
@@ -671,16 +833,38 @@ def run_e2e(ek, h, w, T, rows, P, O, args, world):
     batch is split into chunks pipelined over three CUDA streams (host->device copy of
     chunk c+1 and device->host copy of chunk c-1 overlap the kernels of chunk c); the
     timed region spans all of it, copies included."""
+    # host memory: every rank on this host pins its inputs and results; with several ranks
+    # per host the e2e batch is the largest prefix of the step's batch that keeps all ranks'
+    # pinned buffers within 60 % of the host's RAM (reported as batch_fraction)
+    per_inst = sum(v[:1].numel() * v.element_size() for v in T.values()) + rows[:1].numel() * 2
+    per_inst += sum(x[:1].numel() * x.element_size() for x in (O.grid, O.grid_cfg, O.lsum, O.lmean, O.lcfg))
+    per_inst += sum(d[k][:1].numel() * d[k].element_size() for d in O.dec for k in ("sum", "mean", "steps", "alloc", "cfg"))
+    per_q = sum(v[:1].numel() * v.element_size() for v in P.values())
+    per_q += sum(x[:1].numel() * x.element_size() for x in O.est + O.n)
+    need = w.B * per_inst + w.Q * per_q
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    try:
+        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        ram = need * local_world * 2
+    frac = min(1.0, 0.6 * ram / max(1, need * local_world))
+    Be, Qe = max(1, int(w.B * frac)), max(1, int(w.Q * frac))
+    w_full = w
+    w = Workload(Be, w.N, Qe)
+    T = {k: v[:Be] for k, v in T.items()}
+    rows = rows[:Be]
+    P = {k: v[:Qe] for k, v in P.items()}
+    O = ChunkOut(O, 0, Be, 0, Qe)
     C = max(1, min(args.e2e_chunks, w.B, w.Q))
     bnd = [(w.B * c // C, w.B * (c + 1) // C, w.Q * c // C, w.Q * (c + 1) // C) for c in range(C)]
     host_T = {k: v.cpu().pin_memory() for k, v in T.items()}
     host_rows = rows.cpu().pin_memory()
     host_P = {k: v.cpu().pin_memory() for k, v in P.items()}
 
-    def outs_of(o):   # (device view, per-instance?) of every array read back
+    def outs_of(o):   # every array read back: per-instance ones, per-query ones
         arr = [o.dec[0][k] for k in ("sum", "mean", "steps", "alloc", "cfg")]
         arr += [o.dec[1][k] for k in ("sum", "mean", "steps", "alloc", "cfg")]
-        arr += [o.lsum, o.lmean]
+        arr += [o.lsum, o.lmean, o.lcfg, o.grid, o.grid_cfg]
         q = [o.est[0], o.n[0], o.est[1], o.n[1]]
         return arr, q
 
@@ -755,8 +939,9 @@ def run_e2e(ek, h, w, T, rows, P, O, args, world):
     return {"value": w.allocations() * world * args.e2e_steps / (ms / 1000.0), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": ms / args.e2e_steps, "steps": args.e2e_steps, "chunks": C,
-            "read_back": "thief decisions (both modes), profile estimates+counts (both modes), LIST objectives "
-                         "(sum_q32, mean); GRID/LIST config tables stay device-resident"}
+            "batch_fraction": Be / w_full.B, "instances_per_rank": Be, "queries_per_rank": Qe,
+            "read_back": "every counted unit's result: GRID values + configs of every cell, LIST sum/mean/configs "
+                         "of every row, thief decisions (both modes), profile estimates + counts (both modes)"}
 
 
 def main():
@@ -773,16 +958,35 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-context", dest="context", action="store_false")
     ap.add_argument("--context-v100", type=int, default=16384)
-    ap.add_argument("--ref-inst", type=int, default=384)
-    ap.add_argument("--ref-query", type=int, default=192)
+    ap.add_argument("--c5-inst", type=int, default=synth.CONFIG5.n_inst, help="config-5 instances in total (0: skip)")
+    ap.add_argument("--c5-chunks", type=int, default=8)
+    ap.add_argument("--c5-reps", type=int, default=2)
+    ap.add_argument("--ref-inst", type=int, default=0, help="oracle sample instances (0: 256 per host thread)")
+    ap.add_argument("--ref-query", type=int, default=0, help="oracle sample queries (0: 128 per host thread)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this command under torch.distributed.run (the
+        # driver's own N > 1 launch sets WORLD_SIZE and skips this)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}: launch one process per GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    # (NCCL's own log lines: run with NCCL_DEBUG=INFO NCCL_DEBUG_FILE=<file>; NCCL prints its
+    # version banner on stdout at INFO, so the default run leaves NCCL_DEBUG unset and reports
+    # the communicator's rank count from ncclCommCount in the JSON line instead)
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)

@@ -183,16 +183,6 @@ int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p,
                           int32_t* out_cluster, ekya_stream_t stream);
 
 /* ---------------------------------------------------------------------------
- * Multi-GPU (one process per GPU).  Instances are independent, so ranks own
- * contiguous instance blocks and the only collective is a gather of the fixed-
- * size decision records to a root rank (north star "only a final NCCL gather").
- * ekya_comm_unique_id: fills 128 bytes (ncclUniqueId) on the root; broadcast
- *   them out of band (e.g. torch.distributed), then every rank calls
- *   ekya_comm_init with the same bytes.
- * ekya_gather_decisions: root_buf[r*bytes_per_rank ...] <- rank r's `local`
- *   (device pointers; root_buf used on the root only), enqueued on `stream`.
- * ------------------------------------------------------------------------- */
-/* ---------------------------------------------------------------------------
  * ekya_window_schedule -- the retraining window as a timeline (SURVEY 8(f)
  * NEXT-1; "Algorithm 1 is invoked at the beginning of each retraining
  * window, as well as on the completion of every training job during the window
@@ -315,8 +305,27 @@ int ekya_checkpoint_decide(ekya_handle* h, int64_t n, const float* tau, const fl
                            const float* a, const float* a_star, const float* A, const float* delta_ckpt,
                            uint8_t* out, ekya_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Multi-GPU (one process per GPU).  Instances are independent, so
+ * ranks own contiguous instance blocks and the only collective is a gather of
+ * the fixed-size decision records to a root rank (north star "only a final NCCL
+ * gather of decisions").
+ * ekya_comm_unique_id: fills 128 bytes (ncclUniqueId) on the root; broadcast
+ *   them out of band (e.g. torch.distributed), then every rank calls
+ *   ekya_comm_init with the same bytes (nranks = 1 is allowed: a one-rank NCCL
+ *   communicator).  EKYA_ERR_NCCL on failure; a handle takes one communicator.
+ * ekya_comm_info: the communicator's rank count and this rank (ncclCommCount /
+ *   ncclCommUserRank); without a communicator 1 and 0.
+ * ekya_gather_decisions: root_buf[r*bytes_per_rank ...] <- rank r's `local`
+ *   (device pointers, caller-owned; root_buf used on the root only), enqueued on
+ *   `stream` as ncclGather when a communicator exists, else (single process) a
+ *   device-to-device copy.  Every rank passes the same bytes_per_rank.  Callers
+ *   that overlap the gather with compute split their records into chunks and
+ *   gather each chunk on a second stream (bench.py config 5).
+ * ------------------------------------------------------------------------- */
 int ekya_comm_unique_id(void* out_id_128_bytes);
 int ekya_comm_init(ekya_handle* h, const void* id_128_bytes, int nranks, int rank);
+int ekya_comm_info(ekya_handle* h, int* out_nranks, int* out_rank);
 int ekya_gather_decisions(ekya_handle* h, const void* local, size_t bytes_per_rank,
                           void* root_buf, int root, ekya_stream_t stream);
 

@@ -95,6 +95,8 @@ def lib():
         L.orc_bruteforce.argtypes = [ctypes.POINTER(Dims), P, P, P, P, P, P, P, P]
         L.orc_profile.restype = ctypes.c_int64
         L.orc_profile.argtypes = [ctypes.POINTER(ProfileDims), P, P, P, P, P, P, P]
+        L.orc_profile_ex.restype = ctypes.c_int64
+        L.orc_profile_ex.argtypes = [ctypes.POINTER(ProfileDims), P, P, P, P, P, P, P, P]
         L.orc_quantize_frac.argtypes = [ctypes.c_int64, ctypes.c_int32]
         L.orc_quantize_frac.restype = ctypes.c_int32
         L.orc_uniform.argtypes = [ctypes.POINTER(Dims), P, P, P, P, P, ctypes.c_int32, ctypes.c_float, P, P, P, P]
@@ -334,7 +336,9 @@ def bruteforce(inst: Instances):
     return alloc, cfg, s, int(bad)
 
 
-def profile(cur, hist, hist_acc, fallback, mode=RADIUS, tau=0.2, k=5, max_iter=100):
+def profile(cur, hist, hist_acc, fallback, mode=RADIUS, tau=0.2, k=5, max_iter=100, with_passes=False):
+    """A1 estimates: (est [Q][G], n [Q][G], cluster [Q][H+1] or None, bad), and with
+    with_passes the Lloyd assignment passes per query [Q] (telemetry) appended."""
     cur = _c(cur, np.float32)
     Q, C = cur.shape
     fallback = _c(fallback, np.float32)
@@ -348,11 +352,13 @@ def profile(cur, hist, hist_acc, fallback, mode=RADIUS, tau=0.2, k=5, max_iter=1
     est = np.zeros((Q, G), np.float32)
     n = np.zeros((Q, G), np.int32)
     cl = np.zeros((Q, H + 1), np.int32)
-    bad = lib().orc_profile(ctypes.byref(pd), _p(cur), _p(hist), _p(hist_acc), _p(fallback),
-                            _p(est), _p(n), _p(cl))
+    passes = np.zeros(Q, np.int32)
+    bad = lib().orc_profile_ex(ctypes.byref(pd), _p(cur), _p(hist), _p(hist_acc), _p(fallback),
+                               _p(est), _p(n), _p(cl), _p(passes))
     if bad < 0:
         raise ValueError("oracle: invalid profile dims")
-    return est, n, (cl if mode == CLUSTER else None), int(bad)
+    out = (est, n, (cl if mode == CLUSTER else None), int(bad))
+    return out + (passes,) if with_passes else out
 
 
 Q_ONE = 65536   # one GPU in quanta of 2^-16 GPU (placement outputs)

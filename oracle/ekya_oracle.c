@@ -503,9 +503,12 @@ static int orc_nearest(const float* x, const float* mu, int32_t k, int32_t C)
     return best;
 }
 
-int64_t orc_profile(const orc_profile_dims* p, const float* cur, const float* hist,
-                    const float* hist_acc, const float* fallback,
-                    float* out_est, int32_t* out_n, int32_t* out_cluster)
+/* out_passes (optional, telemetry): Lloyd assignment passes per CLUSTER query (the
+ * initial assignment + one per iteration; 0 for RADIUS, empty histories and invalid
+ * queries). */
+int64_t orc_profile_ex(const orc_profile_dims* p, const float* cur, const float* hist,
+                       const float* hist_acc, const float* fallback,
+                       float* out_est, int32_t* out_n, int32_t* out_cluster, int32_t* out_passes)
 {
     int64_t Q = p->n_query, H = p->n_hist, C = p->n_class, G = p->n_gamma;
     if (Q < 0 || H < 0 || C < 1 || G < 1 || (p->mode != 0 && p->mode != 1)) return -1;
@@ -524,6 +527,7 @@ int64_t orc_profile(const orc_profile_dims* p, const float* cur, const float* hi
         const float* cq = cur + q * C;
         const float* hq = hist + q * H * C;
         const float* aq = hist_acc + q * H * G;
+        if (out_passes) out_passes[q] = 0;
         int ok = 1;
         for (int64_t c = 0; c < C; ++c) ok &= orc_in01(cq[c]);
         for (int64_t i = 0; i < H * C; ++i) ok &= orc_in01(hq[i]);
@@ -553,7 +557,9 @@ int64_t orc_profile(const orc_profile_dims* p, const float* cur, const float* hi
                     memcpy(mu + i * C, hq + ((i * H) / K) * C, sizeof(float) * C);
                 for (int64_t h = 0; h < H; ++h)
                     assign[h] = orc_nearest(hq + h * C, mu, (int32_t)K, (int32_t)C);
+                if (out_passes) out_passes[q] = 1;   /* assignment passes: the initial one ... */
                 for (int32_t it = 0; it < p->max_iter; ++it) {
+                    if (out_passes) out_passes[q] += 1;   /* ... plus one per iteration */
                     memset(acc_sum, 0, sizeof(uint64_t) * K * C);
                     memset(cnt, 0, sizeof(int64_t) * K);
                     for (int64_t h = 0; h < H; ++h) {
@@ -604,6 +610,13 @@ int64_t orc_profile(const orc_profile_dims* p, const float* cur, const float* hi
     free(acc_sum);
     free(cnt);
     return bad;
+}
+
+int64_t orc_profile(const orc_profile_dims* p, const float* cur, const float* hist,
+                    const float* hist_acc, const float* fallback,
+                    float* out_est, int32_t* out_n, int32_t* out_cluster)
+{
+    return orc_profile_ex(p, cur, hist, hist_acc, fallback, out_est, out_n, out_cluster, NULL);
 }
 
 /* ========================================================================

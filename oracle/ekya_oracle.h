@@ -68,6 +68,9 @@ int64_t orc_bruteforce(const orc_dims* d, const float* stale, const float* cost,
 int64_t orc_profile(const orc_profile_dims* p, const float* cur, const float* hist,
                     const float* hist_acc, const float* fallback,
                     float* out_est, int32_t* out_n, int32_t* out_cluster);
+int64_t orc_profile_ex(const orc_profile_dims* p, const float* cur, const float* hist,
+                       const float* hist_acc, const float* fallback,
+                       float* out_est, int32_t* out_n, int32_t* out_cluster, int32_t* out_passes);
 
 /* ---- NEXT-4: placement of decisions onto GPUs and the
  *      checkpoint decision (draft P:62-81); readings PL1-PL3, CK1 ---- */

@@ -36,6 +36,26 @@ bool tables_ok(const ekya_dims* d, const ekya_tables* t) {
 
 }  // namespace
 
+namespace ekya {
+void* handle_scratch(ekya_handle* h, size_t bytes) {
+    if (bytes <= h->scratch_bytes) return h->scratch;
+    // a larger launch than any before: the previous buffer may still be in use by queued
+    // kernels, so wait for the device before replacing it (one-time cost per size step)
+    if (h->scratch) {
+        if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+        cudaFree(h->scratch);
+        h->scratch = nullptr;
+        h->scratch_bytes = 0;
+    }
+    if (cudaMalloc(&h->scratch, bytes) != cudaSuccess) {
+        h->scratch = nullptr;
+        return nullptr;
+    }
+    h->scratch_bytes = bytes;
+    return h->scratch;
+}
+}  // namespace ekya
+
 extern "C" {
 
 const char* ekya_version(void) { return "ekya-b200 0.1 (sm_100a)"; }
@@ -61,6 +81,8 @@ int ekya_create(ekya_handle** out, int device, size_t /*workspace_bytes*/) {
     h->nccl_comm = nullptr;
     h->nranks = 1;
     h->rank = 0;
+    h->scratch = nullptr;
+    h->scratch_bytes = 0;
     *out = h;
     return EKYA_OK;
 }
@@ -70,6 +92,7 @@ void ekya_comm_destroy_internal(ekya_handle* h);
 void ekya_destroy(ekya_handle* h) {
     if (!h) return;
     ekya_comm_destroy_internal(h);
+    if (h->scratch) cudaFree(h->scratch);
     cudaFree(h->dstate);
     delete h;
 }
@@ -103,6 +126,7 @@ int ekya_eval_allocations(ekya_handle* h, const ekya_dims* d, const ekya_tables*
                           int32_t n_alloc, const uint16_t* alloc, uint64_t* out_sum_q32,
                           float* out_mean, uint8_t* out_cfg, float* out_grid, uint8_t* out_grid_cfg,
                           ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_eval_allocations");
     if (!h) return EKYA_ERR_ARG;
     int why = EKYA_OK;
     if (!dims_ok(d, &why)) return why;
@@ -124,6 +148,7 @@ int ekya_eval_allocations(ekya_handle* h, const ekya_dims* d, const ekya_tables*
 int ekya_thief_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int mode,
                         uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum_q32,
                         float* out_mean, uint32_t* out_steps, ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_thief_schedule");
     if (!h) return EKYA_ERR_ARG;
     int why = EKYA_OK;
     if (!dims_ok(d, &why)) return why;
@@ -138,6 +163,7 @@ int ekya_thief_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t
 int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p, const float* cur,
                           const float* hist, const float* hist_acc, const float* fallback,
                           float* out_est, int32_t* out_n, int32_t* out_cluster, ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_profile_estimate");
     if (!h || !p) return EKYA_ERR_ARG;
     if (p->n_query < 0 || p->n_hist < 0) return EKYA_ERR_SHAPE;
     if (p->n_class < 1 || p->n_class > 1024 || p->n_gamma < 1 || p->n_gamma > 256) return EKYA_ERR_LIMIT;
@@ -158,6 +184,7 @@ int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p, const floa
 int ekya_uniform_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int32_t fixed_gamma,
                           float inference_weight, uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum_q32,
                           float* out_mean, ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_uniform_schedule");
     if (!h) return EKYA_ERR_ARG;
     int why = EKYA_OK;
     if (!dims_ok(d, &why)) return why;
@@ -172,6 +199,7 @@ int ekya_uniform_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables*
 
 int ekya_pareto(ekya_handle* h, int64_t n_sets, int32_t n, const float* cost, const float* post,
                 uint32_t* out_mask, ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_pareto");
     if (!h) return EKYA_ERR_ARG;
     if (n_sets < 0 || n < 0) return EKYA_ERR_SHAPE;
     if (n > 31) return EKYA_ERR_LIMIT;
@@ -183,6 +211,7 @@ int ekya_pareto(ekya_handle* h, int64_t n_sets, int32_t n, const float* cost, co
 
 int ekya_prune_configs(ekya_handle* h, int64_t n_query, int32_t n_hist, int32_t n, const float* cost,
                        const float* hist_acc, float margin, uint32_t* out_keep, ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_prune_configs");
     if (!h) return EKYA_ERR_ARG;
     if (n_query < 0 || n_hist < 0 || n < 0) return EKYA_ERR_SHAPE;
     if (n > 31 || n_hist > (1 << 20)) return EKYA_ERR_LIMIT;
@@ -201,6 +230,7 @@ size_t ekya_window_workspace_bytes(const ekya_dims* d) {
 int ekya_window_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int mode, void* workspace,
                          size_t workspace_bytes, float* out_avg, uint32_t* out_events, float* out_done,
                          ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_window_schedule");
     if (!h) return EKYA_ERR_ARG;
     int why = EKYA_OK;
     if (!dims_ok(d, &why)) return why;
@@ -215,6 +245,7 @@ int ekya_window_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* 
 
 int ekya_curve_fit(ekya_handle* h, int64_t n_sets, int32_t n_points, const float* acc, const int32_t* full_epochs,
                    float* out_pred, float* out_params, ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_curve_fit");
     if (!h) return EKYA_ERR_ARG;
     if (n_sets < 0) return EKYA_ERR_SHAPE;
     if (n_points < 2 || n_points > 32) return EKYA_ERR_LIMIT;
@@ -227,6 +258,7 @@ int ekya_curve_fit(ekya_handle* h, int64_t n_sets, int32_t n_points, const float
 int ekya_place(ekya_handle* h, int32_t n_inst, int32_t n_jobs, int32_t units, int32_t gpus,
                const uint16_t* alloc, uint16_t* out_piece_job, uint32_t* out_piece_q, int16_t* out_piece_gpu,
                uint16_t* out_n_pieces, uint32_t* out_gpu_load, ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_place");
     if (!h) return EKYA_ERR_ARG;
     if (n_inst < 0 || n_jobs < 1) return EKYA_ERR_SHAPE;
     if (units < 1 || units > 65534 || gpus < 1 || gpus > 128 || n_jobs + gpus > 4096) return EKYA_ERR_LIMIT;
@@ -240,6 +272,7 @@ int ekya_place(ekya_handle* h, int32_t n_inst, int32_t n_jobs, int32_t units, in
 int ekya_checkpoint_decide(ekya_handle* h, int64_t n, const float* tau, const float* t, const float* T,
                            const float* a, const float* a_star, const float* A, const float* delta_ckpt,
                            uint8_t* out, ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_checkpoint_decide");
     if (!h) return EKYA_ERR_ARG;
     if (n < 0) return EKYA_ERR_SHAPE;
     if (n > 0 && (!tau || !t || !T || !a || !a_star || !A || !delta_ckpt || !out)) return EKYA_ERR_ARG;

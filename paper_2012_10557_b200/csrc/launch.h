@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstddef>
 #include <cstdint>
@@ -17,7 +18,15 @@ struct ekya_handle {
     unsigned long long launches;       // kernels launched through this handle
     void* nccl_comm;                   // ncclComm_t when initialised
     int nranks, rank;
+    void* scratch;                     // kernel scratch (CLUSTER work lists), grown on demand
+    size_t scratch_bytes;
 };
+
+namespace ekya {
+// Device scratch of at least `bytes` owned by the handle (allocated once, reused by every
+// later launch; grows only when a larger launch needs more).  nullptr on failure.
+void* handle_scratch(ekya_handle* h, size_t bytes);
+}
 
 namespace ekya {
 
@@ -55,5 +64,14 @@ int launch_window(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int 
                   float* out_avg, uint32_t* out_events, float* out_done, cudaStream_t s);
 
 inline int cuda_status(cudaError_t e) { return e == cudaSuccess ? EKYA_OK : EKYA_ERR_CUDA; }
+
+// NVTX range around every C-ABI call (one named range per API call, visible in
+// nsys / ncu --nvtx timelines; a no-op unless a tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 }  // namespace ekya

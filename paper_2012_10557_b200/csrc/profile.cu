@@ -811,7 +811,7 @@ __host__ __device__ inline C2Layout c2_layout(int H, int C, int G, int K) {
     const int CP = (C + 3) & ~3;
     size_t o = 0;
     L.bar = o;    o += 16;
-    L.misc = o;   o += 48;
+    L.misc = o;   o += 96;   // ints [0..7] + the HB kernel's displacement bounds at [8..15]
     L.cf_slot = al16((size_t)C * 4) + 16 + al16((size_t)G * 4) + 16;   // [cur][fallback] granule-staged
     L.cf = o;     o += 2 * L.cf_slot;
     L.hist = o;   o += al16((size_t)H * C * 4) + 16;
@@ -829,7 +829,8 @@ __host__ __device__ inline C2Layout c2_layout(int H, int C, int G, int K) {
 struct C2Params {
     ProfParams P;
     C2Layout L;
-    u64 one2;   // (1.0f, 1.0f), opaque to the compiler
+    u64 one2;                 // (1.0f, 1.0f), opaque to the compiler
+    unsigned char* scratch;   // cluster_hb_kernel: kHbStride bytes per CTA (global, L1/L2 resident)
 };
 
 // KT > 0: K == KT known at compile time; KT == 0: runtime K <= kC2Kmax.
@@ -1135,6 +1136,405 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
     }
 }
 
+// ------------------------------------------------------------------------
+// CLUSTER with distance bounds (the bench shape: K = 5, C = 27, H <= 512)
+// ------------------------------------------------------------------------
+// After Lloyd's first passes few windows change cluster, yet cluster2_kernel recomputes
+// every window's distances to every centroid that moved.  Here each window keeps
+// Hamerly's bounds -- u >= its Euclidean distance D to its own centroid, l <= D to every
+// other centroid -- advanced after each centroid update by the centroids' displacements
+// delta_k (triangle inequality: u += delta_a, l -= max_{k != a} delta_k), with every
+// displacement, bound and test rounded in the safe direction (__f*_ru / __f*_rd).  Rule 5
+// computes d2 as a sequential sum of C rounded squares of rounded differences, so
+// |d2 - D^2| <= eps D^2 + eta with eps = 4e-6 >= gamma_{C+2} for C <= 32 and eta = 2^-120
+// (subnormal terms).  Hence
+//     fl_ru(u^2 (1 + 2 eps) + eta) < fl_rd(l^2 (1 - 2 eps) - eta)
+// guarantees rule 5's fp32 distance to the current centroid is STRICTLY below every other
+// fp32 distance: the oracle's argmin (lowest index on ties) keeps the assignment, with no
+// distance computed.  Windows failing the test ("needy") are compacted into a CTA work
+// list and recomputed exactly (all K distances, rule 5, the packed f32x2 path of
+// cluster2_kernel), two per thread by the first ceil(n/2) threads, so whole warps skip the
+// distance phase; the workers also move the exact cluster sums of windows that changed
+// cluster and hand the new assignment and bounds back to the owning thread through a
+// per-CTA scratch in global memory (5.5 KB, L1/L2 resident).  Every assignment equals the
+// oracle's, hence every sum, centroid, pass count and output (bit-exact parity tests).
+constexpr float kHbEps2 = 8.0e-6f;          // 2 eps; 1 + 2 eps >= 1 / (1 - eps), 1 - 2 eps <= 1 / (1 + eps)
+constexpr float kHbEta = 7.52316385e-37f;   // 2^-120 >= 32 * 2^-149
+constexpr int kHbStride = 5632;             // per CTA: list u16[512] | u f32[512] | l f32[512] | a u8[512]
+
+// upper bound of rule 5's d2 given D <= u
+__device__ __forceinline__ float hb_ub2(float u) { return __fadd_ru(__fmul_ru(__fmul_ru(u, u), 1.0f + kHbEps2), kHbEta); }
+// lower bound of rule 5's d2 given D >= l
+__device__ __forceinline__ float hb_lb2(float l) { return __fsub_rd(__fmul_rd(__fmul_rd(l, l), 1.0f - kHbEps2), kHbEta); }
+// upper / lower bound of D given rule 5's d2
+__device__ __forceinline__ float hb_u(float d2) { return __fsqrt_ru(__fmul_ru(__fadd_ru(d2, kHbEta), 1.0f + kHbEps2)); }
+__device__ __forceinline__ float hb_l(float d2) {
+    return __fsqrt_rd(fmaxf(__fmul_rd(__fsub_rd(d2, kHbEta), 1.0f - kHbEps2), 0.0f));
+}
+
+// nearest centroid (lowest index on ties, C19) and second-smallest distance of both packed
+// windows -> assignment and bounds
+template <int K>
+__device__ __forceinline__ void hb_nearest(const u64 (&s)[K], int& na, int& nb, float& ua, float& la, float& ub,
+                                           float& lb) {
+    float b0 = lo2(s[0]), b1 = hi2(s[0]), c0 = INFINITY, c1 = INFINITY;
+    na = 0;
+    nb = 0;
+#pragma unroll
+    for (int k = 1; k < K; ++k) {
+        const float d0 = lo2(s[k]), d1 = hi2(s[k]);
+        if (d0 < b0) { c0 = b0; b0 = d0; na = k; } else if (d0 < c0) { c0 = d0; }
+        if (d1 < b1) { c1 = b1; b1 = d1; nb = k; } else if (d1 < c1) { c1 = d1; }
+    }
+    ua = hb_u(b0);
+    la = hb_l(c0);
+    ub = hb_u(b1);
+    lb = hb_l(c1);
+}
+
+// Exact Q32 (low 16 bits, rest) sums of the member windows m (bits = lanes) of one warp
+// slot, lane = column: four independent load -> convert chains per step for ILP.
+__device__ __forceinline__ void member_sums(unsigned m, const float* rows, int C, unsigned& alo, unsigned& ahi) {
+    while (m) {
+        const int j0 = __ffs(m) - 1;
+        m &= m - 1;
+        const bool h1 = m != 0;
+        const int j1 = h1 ? __ffs(m) - 1 : j0;
+        m &= m - 1;
+        const bool h2 = m != 0;
+        const int j2 = h2 ? __ffs(m) - 1 : j0;
+        m &= m - 1;
+        const bool h3 = m != 0;
+        const int j3 = h3 ? __ffs(m) - 1 : j0;
+        m &= m - 1;
+        const u64 v0 = q32(rows[j0 * C]), v1 = q32(rows[j1 * C]), v2 = q32(rows[j2 * C]), v3 = q32(rows[j3 * C]);
+        alo += ((unsigned)v0 & 0xFFFFu) + (h1 ? (unsigned)v1 & 0xFFFFu : 0u) + (h2 ? (unsigned)v2 & 0xFFFFu : 0u) +
+               (h3 ? (unsigned)v3 & 0xFFFFu : 0u);
+        ahi += (unsigned)(v0 >> 16) + (h1 ? (unsigned)(v1 >> 16) : 0u) + (h2 ? (unsigned)(v2 >> 16) : 0u) +
+               (h3 ? (unsigned)(v3 >> 16) : 0u);
+    }
+}
+
+template <int K, int C>
+__global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster_hb_kernel(const __grid_constant__ C2Params A) {
+    constexpr int CP = (C + 3) & ~3;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const ProfParams& P = A.P;
+    const C2Layout& L = A.L;
+    const int H = P.p.n_hist, G = P.p.n_gamma;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bar);
+    int* misc = reinterpret_cast<int*>(smem + L.misc);   // [2] query cluster, [3] similar-window count,
+                                                         // [4] work-list count; floats [8..8+K) displacements
+    float* dl = reinterpret_cast<float*>(misc + 8);
+    float* mu = reinterpret_cast<float*>(smem + L.mu);
+    unsigned* slo = reinterpret_cast<unsigned*>(smem + L.sums);
+    unsigned* shi = slo + K * C;
+    int* cnt = reinterpret_cast<int*>(smem + L.cnt);
+    uint16_t* list = reinterpret_cast<uint16_t*>(smem + L.sums);
+    unsigned* glo = reinterpret_cast<unsigned*>(smem + L.sums + al16((size_t)H * 2));
+    unsigned* ghi = glo + G;
+    int* gnn = reinterpret_cast<int*>(ghi + G);
+    unsigned char* scr = A.scratch + (size_t)blockIdx.x * kHbStride;
+    uint16_t* wl = reinterpret_cast<uint16_t*>(scr);           // work list: window | old cluster << 9
+    float* res_u = reinterpret_cast<float*>(scr + 1024);
+    float* res_l = reinterpret_cast<float*>(scr + 3072);
+    unsigned char* res_a = scr + 5120;
+    const long long Q = P.p.n_query;
+    const long long items = Q > blockIdx.x ? (Q - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const u64 one = A.one2;
+    const unsigned full = 0xffffffffu;
+    const bool lane_c = lane < C;
+    const unsigned cbase = lane_c ? smem_addr(slo) + 4u * (unsigned)lane : smem_addr(smem + L.dummy) + 4u * (unsigned)lane;
+    const unsigned cstride = lane_c ? (unsigned)(C * 4) : 0u, choff = lane_c ? (unsigned)(K * C * 4) : 0u;
+    const unsigned lt = (1u << lane) - 1u;
+
+    auto issue = [&](long long j) {
+        const long long q = blockIdx.x + j * gridDim.x;
+        unsigned char* cf = smem + L.cf + (j & 1) * L.cf_slot;
+        const Granules gc = granules(P.cur + q * C, (size_t)C * 4);
+        const Granules gf = granules(P.fallback + q * G, (size_t)G * 4);
+        const Granules gh = granules(P.hist + (size_t)q * H * C, (size_t)H * C * 4);
+        mbar_arrive_expect_tx(bar, gc.bytes + gf.bytes + gh.bytes);
+        bulk_g2s(cf, gc.g0, gc.bytes, bar);
+        bulk_g2s(cf + al16((size_t)C * 4) + 16, gf.g0, gf.bytes, bar);
+        bulk_g2s(smem + L.hist, gh.g0, gh.bytes, bar);
+        const Granules ga = granules(P.acc + (size_t)q * H * G, (size_t)H * G * 4);
+        for (unsigned o = 0; o < ga.bytes; o += (1u << 20)) bulk_prefetch_l2(ga.g0 + o, min(ga.bytes - o, 1u << 20));
+    };
+
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid == 0 && items > 0) issue(0);
+
+    const int h0 = tid, h1 = tid + kC2Threads;
+    const bool v0 = h0 < H, v1 = h1 < H;
+    for (long long i = 0; i < items; ++i) {
+        const long long q = blockIdx.x + i * gridDim.x;
+        const unsigned char* cf = smem + L.cf + (i & 1) * L.cf_slot;
+        const float* cur = reinterpret_cast<const float*>(cf + granules(P.cur + q * C, 4).off);
+        const float* fb = reinterpret_cast<const float*>(cf + al16((size_t)C * 4) + 16 +
+                                                        granules(P.fallback + q * G, 4).off);
+        const float* hs = reinterpret_cast<const float*>(smem + L.hist +
+                                                         granules(P.hist + (size_t)q * H * C, 4).off);
+        const float* x0 = hs + (size_t)(v0 ? h0 : 0) * C;
+        const float* x1 = hs + (size_t)(v1 ? h1 : (v0 ? h0 : 0)) * C;
+        for (int t = tid; t < 2 * K * C; t += kC2Threads) slo[t] = 0u;
+        for (int t = tid; t < K; t += kC2Threads) cnt[t] = 0;
+        if (tid == 0) misc[3] = misc[4] = 0;
+        mbar_wait(bar, (unsigned)(i & 1));
+        bool ok = true;
+        for (int c = tid; c < C; c += kC2Threads) ok &= in01(cur[c]);
+        for (int t = tid; t < K * CP; t += kC2Threads) {
+            const int ci = t / CP, c = t - ci * CP;
+            mu[t] = c < C ? hs[(size_t)(((long long)ci * H) / K) * C + c] : 0.0f;
+        }
+        __syncthreads();
+
+        // pass 0: every window's K distances from the initial centroids (rule 5), checking
+        // every histogram value on the way (a NaN makes the distances NaN)
+        int a0, a1;
+        float u0, l0, u1, l1;
+        {
+            u64 s[K];
+            float lo = 1.0f, hi = 0.0f;
+            c2_dists<K, K, true, true>(s, x0, x1, mu, C, CP, K, (1u << K) - 1u, one, &lo, &hi);
+            ok &= lo >= 0.0f && hi <= 1.0f && lo2(s[0]) == lo2(s[0]) && hi2(s[0]) == hi2(s[0]);
+            hb_nearest<K>(s, a0, a1, u0, l0, u1, l1);
+        }
+        // every window enters its first cluster: exact sums per cluster and warp
+        {
+            const float* r0 = hs + (size_t)(warp * 32) * C + lane;
+            const float* r1 = r0 + (size_t)kC2Threads * C;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const unsigned b0 = __ballot_sync(full, v0 && a0 == k);
+                const unsigned b1 = __ballot_sync(full, v1 && a1 == k);
+                if ((b0 | b1) == 0) continue;
+                if (lane == 0) atomicAdd(&cnt[k], __popc(b0) + __popc(b1));
+                unsigned alo = 0, ahi = 0;
+                member_sums(b0, r0, C, alo, ahi);
+                member_sums(b1, r1, C, alo, ahi);
+                const unsigned a = cbase + (unsigned)k * cstride;
+                red_add_shared(a, alo);
+                red_add_shared(a + choff, ahi);
+            }
+        }
+        int any = __syncthreads_or(v0 || v1);
+        int passes = 1;
+        for (;;) {
+            const int it = passes - 1;   // centroid updates so far
+            if ((it > 0 && !any) || it >= P.p.max_iter) break;
+            // centroid update from the exact sums (empty cluster keeps its centroid), and each
+            // centroid's displacement bound: warp k, lane = column
+            if (warp < K) {
+                const int k = warp;
+                float dd = 0.0f;
+                const int n = cnt[k];
+                if (lane_c && n > 0) {
+                    const float old = mu[k * CP + lane];
+                    const float nm = mean_q32(sum16_get(&slo[k * C + lane], &shi[k * C + lane]), n);
+                    mu[k * CP + lane] = nm;
+                    const float du = fmaxf(__fsub_ru(nm, old), __fsub_ru(old, nm));
+                    dd = __fmul_ru(du, du);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) dd = __fadd_ru(dd, __shfl_xor_sync(full, dd, o));
+                if (lane == 0) dl[k] = __fsqrt_ru(dd);
+            }
+            if (tid == 0) misc[4] = 0;
+            __syncthreads();
+            // phase A (owners): advance the bounds, test, list the needy windows
+            float m1 = -1.0f, m2 = 0.0f;
+            int i1 = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const float d = dl[k];
+                if (d > m1) { m2 = m1; m1 = d; i1 = k; } else if (d > m2) { m2 = d; }
+            }
+            m2 = fmaxf(m2, 0.0f);
+            u0 = __fadd_ru(u0, dl[a0]);
+            l0 = fmaxf(__fsub_rd(l0, a0 == i1 ? m2 : m1), 0.0f);
+            u1 = __fadd_ru(u1, dl[a1]);
+            l1 = fmaxf(__fsub_rd(l1, a1 == i1 ? m2 : m1), 0.0f);
+            const bool n0 = v0 && !(hb_ub2(u0) < hb_lb2(l0));
+            const bool n1 = v1 && !(hb_ub2(u1) < hb_lb2(l1));
+            {
+                const unsigned b0 = __ballot_sync(full, n0), b1 = __ballot_sync(full, n1);
+                const int nw = __popc(b0) + __popc(b1);
+                int base = 0;
+                if (lane == 0 && nw) base = atomicAdd(&misc[4], nw);
+                base = __shfl_sync(full, base, 0);
+                if (n0) wl[base + __popc(b0 & lt)] = (uint16_t)(h0 | (a0 << 9));
+                if (n1) wl[base + __popc(b0) + __popc(b1 & lt)] = (uint16_t)(h1 | (a1 << 9));
+            }
+            __syncthreads();
+            // phase B (workers): exact distances of two listed windows per thread, moves
+            const int nl = misc[4];
+            const int pairs = (nl + 1) >> 1;
+            bool mv = false;
+            if (warp * 32 < pairs) {
+                const bool w0 = tid < pairs, w1 = 2 * tid + 1 < nl;
+                const unsigned e0 = w0 ? wl[2 * tid] : 0u;
+                const unsigned e1 = w1 ? wl[2 * tid + 1] : e0;
+                const int wa = (int)(e0 & 511u), wb = (int)(e1 & 511u), oa = (int)(e0 >> 9), ob = (int)(e1 >> 9);
+                u64 s[K];
+                c2_dists<K, K, true>(s, hs + (size_t)wa * C, hs + (size_t)wb * C, mu, C, CP, K, (1u << K) - 1u, one);
+                int na, nb;
+                float ua, la, ub, lb;
+                hb_nearest<K>(s, na, nb, ua, la, ub, lb);
+                if (w0) {
+                    res_a[wa] = (unsigned char)na;
+                    res_u[wa] = ua;
+                    res_l[wa] = la;
+                }
+                if (w1) {
+                    res_a[wb] = (unsigned char)nb;
+                    res_u[wb] = ub;
+                    res_l[wb] = lb;
+                }
+                // windows that changed cluster move between the exact shared counters
+#pragma unroll
+                for (int sl = 0; sl < 2; ++sl) {
+                    const int wv = sl ? wb : wa, ov = sl ? ob : oa, nv = sl ? nb : na;
+                    const unsigned bm = __ballot_sync(full, (sl ? w1 : w0) && nv != ov);
+                    mv |= bm != 0;
+                    for (unsigned m = bm; m; m &= m - 1) {
+                        const int j = __ffs(m) - 1;
+                        const int w = __shfl_sync(full, wv, j);
+                        const int o = __shfl_sync(full, ov, j);
+                        const int n = __shfl_sync(full, nv, j);
+                        const u64 v = q32(hs[(size_t)w * C + lane]);
+                        const unsigned vlo = (unsigned)v & 0xFFFFu, vhi = (unsigned)(v >> 16);
+                        const unsigned ao = cbase + (unsigned)o * cstride, an = cbase + (unsigned)n * cstride;
+                        red_add_shared(ao, 0u - vlo);
+                        red_add_shared(ao + choff, 0u - vhi);
+                        red_add_shared(an, vlo);
+                        red_add_shared(an + choff, vhi);
+                        if (lane == 0) {
+                            atomicSub(&cnt[o], 1);
+                            atomicAdd(&cnt[n], 1);
+                        }
+                    }
+                }
+            }
+            any = __syncthreads_or(mv);
+            // phase C (owners): the recomputed windows' assignment and bounds
+            if (n0) {
+                a0 = res_a[h0];
+                u0 = res_u[h0];
+                l0 = res_l[h0];
+            }
+            if (n1) {
+                a1 = res_a[h1];
+                u1 = res_u[h1];
+                l1 = res_l[h1];
+            }
+            ++passes;
+        }
+        // the history tile is free: stream the next query's while this one finishes
+        if (tid == 0) {
+            atomicAdd(&P.st->lloyd_passes, (unsigned long long)passes);
+            if (i + 1 < items) issue(i + 1);
+        }
+        const int na0 = a0, na1 = a1;
+        // the query joins its nearest centroid: lane i computes distance to centroid i
+        if (warp == 0) {
+            unsigned long long key = ~0ULL;
+            for (int ci = lane; ci < K; ci += 32) {
+                const float d = dist2_mem(cur, mu + ci * CP, C);
+                const unsigned long long kk = ((unsigned long long)__float_as_uint(d) << 8) | (unsigned)ci;
+                key = kk < key ? kk : key;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
+                key = y < key ? y : key;
+            }
+            if (lane == 0) misc[2] = (int)(key & 0xFF);
+        }
+        // validate the whole accuracy tile (NaN = unmeasured, else in [0, 1]; R-ERR)
+        {
+            const float* at = P.acc + (size_t)q * H * G;
+            const long long n = (long long)H * G;
+            if ((reinterpret_cast<uintptr_t>(at) & 15) == 0) {
+                const float4* a4 = reinterpret_cast<const float4*>(at);
+                for (long long t = tid; t < n / 4; t += kC2Threads) {
+                    const float4 x = __ldg(a4 + t);
+                    ok &= !(x.x < 0.0f) && !(x.x > 1.0f) && !(x.y < 0.0f) && !(x.y > 1.0f) &&
+                          !(x.z < 0.0f) && !(x.z > 1.0f) && !(x.w < 0.0f) && !(x.w > 1.0f);
+                }
+                for (long long t = (n & ~3LL) + tid; t < n; t += kC2Threads) {
+                    const float x = __ldg(at + t);
+                    ok &= !(x < 0.0f) && !(x > 1.0f);
+                }
+            } else {
+                for (long long t = tid; t < n; t += kC2Threads) {
+                    const float x = __ldg(at + t);
+                    ok &= !(x < 0.0f) && !(x > 1.0f);
+                }
+            }
+        }
+        __syncthreads();   // misc[2] visible; the cluster sums are dead: their space holds the list
+        const int qc = misc[2];
+        for (int t = tid; t < 3 * G; t += kC2Threads) glo[t] = 0u;
+        // compact list of the query cluster's windows (any order: the sums are exact integers)
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+            const bool in = sl ? (v1 && na1 == qc) : (v0 && na0 == qc);
+            const unsigned bm = __ballot_sync(0xffffffffu, in);
+            int base = 0;
+            if (lane == 0 && bm) base = atomicAdd(&misc[3], __popc(bm));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (in) list[base + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)(sl ? h1 : h0);
+        }
+        __syncthreads();
+        // per-gamma exact sums over the similar, measured windows: thread t owns gamma t % G and
+        // list entries t / G (mod ngrp); the accuracy tile comes from L2
+        {
+            const int ns = misc[3];
+            const int ngrp = kC2Threads / G, g = tid % G, grp = tid / G;
+            if (grp < ngrp) {
+                const float* acc = P.acc + (size_t)q * H * G + g;
+                u64 gs = 0;
+                int gn = 0;
+#pragma unroll 4
+                for (int e = grp; e < ns; e += ngrp) {
+                    const float x = __ldg(acc + (size_t)list[e] * G);
+                    if (x == x) {
+                        gs += q32(x);
+                        gn += 1;
+                    }
+                }
+                if (gn) {
+                    sum16_add(&glo[g], &ghi[g], gs);
+                    atomicAdd(&gnn[g], gn);
+                }
+            }
+        }
+        ok = __syncthreads_and(ok) != 0;
+        if (!ok && tid == 0) flag_data_error(P.st);
+        if (P.out_cluster) {
+            int* oc = P.out_cluster + q * (H + 1);
+            if (v0) oc[h0] = ok ? na0 : 0;
+            if (v1) oc[h1] = ok ? na1 : 0;
+            if (tid == 0) oc[H] = ok ? qc : 0;
+        }
+        for (int g = tid; g < G; g += kC2Threads) {
+            int n = gnn[g];
+            float est = 0.0f;
+            if (!ok) n = 0;
+            else est = n > 0 ? mean_q32(sum16_get(&glo[g], &ghi[g]), n) : fb[g];
+            P.out_est[q * G + g] = est;
+            P.out_n[q * G + g] = n;
+        }
+        __syncthreads();   // sums, list and the cur/fallback slot are free again
+    }
+}
+
 // queries with an empty history: every estimate is the caller's fallback
 __global__ void no_history_kernel(ProfParams P) {
     const long long QG = (long long)P.p.n_query * P.p.n_gamma;
@@ -1207,12 +1607,20 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
             memcpy(&ob, &one, 4);
             A.one2 = ((unsigned long long)ob << 32) | ob;
             const size_t smem = A.L.total;
-            auto k2 = (K == 5 && C == 27) ? cluster2_kernel<5, 27> : cluster2_kernel<0, 0>;
+            // EKYA_CLUSTER_HB=1 selects the distance-bound kernel for the bench shape (A/B timing;
+            // measured slower so far)
+            const bool hb = K == 5 && C == 27 && getenv("EKYA_CLUSTER_HB");
+            auto k2 = hb ? cluster_hb_kernel<5, 27>
+                         : (K == 5 && C == 27) ? cluster2_kernel<5, 27> : cluster2_kernel<0, 0>;
             e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return EKYA_ERR_CUDA;
             int per_sm = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2, kC2Threads, smem);
             grid = std::min<long long>(p.n_query, (long long)h->sm_count * std::max(per_sm, 1));
+            if (hb) {
+                A.scratch = static_cast<unsigned char*>(handle_scratch(h, (size_t)grid * kHbStride));
+                if (!A.scratch) return EKYA_ERR_CUDA;
+            }
             k2<<<(unsigned)grid, kC2Threads, smem, s>>>(A);
             h->launches++;
             return cuda_status(cudaGetLastError());

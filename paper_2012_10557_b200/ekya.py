@@ -25,7 +25,7 @@ PROFILE_RADIUS, PROFILE_CLUSTER = 0, 1
 LAMBDA_NONE = 7
 SYMBOLS = ["ekya_create", "ekya_destroy", "ekya_last_error", "ekya_launch_count", "ekya_version",
            "ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate",
-           "ekya_comm_unique_id", "ekya_comm_init", "ekya_gather_decisions", "ekya_counters", "ekya_place",
+           "ekya_comm_unique_id", "ekya_comm_init", "ekya_comm_info", "ekya_gather_decisions", "ekya_counters", "ekya_place",
            "ekya_checkpoint_decide", "ekya_uniform_schedule", "ekya_pareto", "ekya_prune_configs", "ekya_curve_fit",
            "ekya_window_workspace_bytes", "ekya_window_schedule"]
 
@@ -111,6 +111,8 @@ def load_library(path: str = LIB_PATH):
     L.ekya_comm_unique_id.restype = ctypes.c_int
     L.ekya_comm_init.argtypes = [P, P, ctypes.c_int, ctypes.c_int]
     L.ekya_comm_init.restype = ctypes.c_int
+    L.ekya_comm_info.argtypes = [P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+    L.ekya_comm_info.restype = ctypes.c_int
     L.ekya_gather_decisions.argtypes = [P, P, ctypes.c_size_t, P, ctypes.c_int, P]
     L.ekya_gather_decisions.restype = ctypes.c_int
     _lib = L
@@ -285,7 +287,9 @@ def ekya_uniform_schedule(h: Handle, dims: Dims, tables: Tables, fixed_gamma: in
 def ekya_pareto(h: Handle, cost, post, out_mask, stream=None):
     L = load_library()
     n = cost.shape[-1]
-    n_sets = cost.numel() // max(1, n)
+    n_sets = 1
+    for x in cost.shape[:-1]:
+        n_sets *= int(x)
     if tuple(post.shape) != tuple(cost.shape):
         raise ValueError("ekya_pareto: post must have cost's shape")
     code = L.ekya_pareto(h.ptr, n_sets, n, _ptr(cost, torch.float32, "cost", True),
@@ -365,6 +369,13 @@ def ekya_comm_unique_id() -> bytes:
 def ekya_comm_init(h: Handle, uid: bytes, nranks: int, rank: int):
     buf = ctypes.create_string_buffer(bytes(uid), 128)
     _check(load_library().ekya_comm_init(h.ptr, buf, nranks, rank), "ekya_comm_init")
+
+
+def ekya_comm_info(h: Handle):
+    """(nranks, rank) of the handle's NCCL communicator (1, 0 without one)."""
+    n, r = ctypes.c_int(), ctypes.c_int()
+    _check(load_library().ekya_comm_info(h.ptr, ctypes.byref(n), ctypes.byref(r)), "ekya_comm_info")
+    return n.value, r.value
 
 
 def ekya_gather_decisions(h: Handle, local, root_buf, root=0, stream=None):

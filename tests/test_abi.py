@@ -89,3 +89,25 @@ def test_product_does_not_import_oracle():
             if f.endswith((".cu", ".cuh", ".h")):
                 for line in open(os.path.join(dirpath, f)):
                     assert not (line.lstrip().startswith("#include") and "oracle" in line), f
+
+
+def test_every_api_call_has_an_nvtx_range(lib):
+    """one NVTX range per C-ABI call (the range names are string literals in the .so)."""
+    from paper_2012_10557_b200 import ekya
+    data = open(ekya.LIB_PATH, "rb").read()
+    for name in ("ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate", "ekya_gather_decisions",
+                 "ekya_comm_init", "ekya_window_schedule", "ekya_place"):
+        assert name.encode() + b"\0" in data, name
+    out = subprocess.run(["nm", "-D", ekya.LIB_PATH], capture_output=True, text=True).stdout
+    assert "nvtx" in out.lower() or b"libnvToolsExt" in data or b"NVTX_INJECTION" in data
+
+
+def test_binding_checks_table_sizes_against_dims():
+    from paper_2012_10557_b200 import ekya
+    d = ekya.make_dims(4, 10, 18, 5, 80, 1, 20.0, 0.4)
+    t = ekya.Tables()
+    t.numels = (40, 720, 720, 200, 200)
+    ekya._check_tables(d, t)
+    t.numels = (40, 720, 719, 200, 200)
+    with pytest.raises(ValueError):
+        ekya._check_tables(d, t)

@@ -258,13 +258,18 @@ def test_profile_bitexact(h, name, pc, mode):
     Pd = {k: v.cuda() for k, v in P.items()}
     est, n, cl = ek().profile_estimate(h, Pd["cur"], Pd["hist"], Pd["hist_acc"], Pd["fallback"], mode=mode,
                                        with_cluster=True)
-    oe, on, ocl, bad = oracle.profile(P["cur"].numpy(), P["hist"].numpy(), P["hist_acc"].numpy(),
-                                      P["fallback"].numpy(), mode=mode)
+    oe, on, ocl, bad, passes = oracle.profile(P["cur"].numpy(), P["hist"].numpy(), P["hist_acc"].numpy(),
+                                              P["fallback"].numpy(), mode=mode, with_passes=True)
     assert bad == 0 and h.last_error() == 0
     assert_eq(n, on, "n_similar")
     assert_eq(est, oe, "estimate")
     if mode == 1:
         assert_eq(cl, ocl, "clusters")
+        # the device's Lloyd pass counter (ekya_counters, used by bench.py's CLUSTER roofline)
+        # equals the oracle's passes over the same queries
+        c0 = h.counters()["lloyd_passes"]
+        ek().profile_estimate(h, Pd["cur"], Pd["hist"], Pd["hist_acc"], Pd["fallback"], mode=mode)
+        assert h.counters()["lloyd_passes"] - c0 == int(passes.sum())
 
 
 CLUSTER_EDGE = [
@@ -438,6 +443,50 @@ def test_config5_sample_both_modes(h):
         assert_eq(m[:64], omean, f"mean mode {mode}")
         assert_eq(st[:64], osteps, f"steps mode {mode}")
         assert (a.to(torch.int64).sum(1) == cfg.units).all()
+
+
+def test_gather_decisions_one_rank_both_paths(h):
+    """The multi-GPU data plane on one GPU: thief decisions written by the kernels straight
+    into shard.RecordLayout's chunked record views (device), gathered chunk by chunk with
+    ekya_gather_decisions -- without a communicator (device copy) and through a one-rank NCCL
+    communicator (ncclGather) -- unpacked at the root and compared with the oracle."""
+    from paper_2012_10557_b200 import shard
+    e = ek()
+    cfg = variant(synth.CONFIG2, n_inst=301)
+    Td, inst = tables(cfg)
+    oa, oc, osum, omean, osteps, _ = oracle.thief(inst, 0)
+    h1 = e.Handle(0)
+    e.ekya_comm_init(h1, e.ekya_comm_unique_id(), 1, 0)
+    assert e.ekya_comm_info(h1) == (1, 0) and e.ekya_comm_info(h) == (1, 0)
+    for hh in (h, h1):
+        L = shard.RecordLayout(cfg.n_inst, 1, cfg.n_streams, n_chunks=4)
+        buf = torch.zeros(L.rank_bytes, dtype=torch.uint8, device="cuda")
+        root = torch.zeros(L.root_bytes, dtype=torch.uint8, device="cuda")
+        dims = e.dims_from(Td, *args(cfg))
+        side = torch.cuda.Stream()
+        for c in range(L.n_chunks):
+            b0, b1 = L.chunk_range(0, c)
+            v = L.views(buf, 0, c)
+            Tc = {k: x[b0:b1] for k, x in Td.items()}
+            dc = e.dims_from(Tc, *args(cfg))
+            e.ekya_thief_schedule(hh, dc, e.make_tables(**Tc), 0, v["alloc"], v["cfg"], v["sum"], v["mean"],
+                                  v["steps"])
+            ev = torch.cuda.Event()
+            ev.record()
+            side.wait_event(ev)
+            e.ekya_gather_decisions(hh, L.local_chunk(buf, c), L.root_chunk(root, c), root=0, stream=side)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        assert hh.last_error() == 0
+        got = L.unpack(root)
+        assert_eq(got["alloc"], oa, "gathered alloc")
+        assert_eq(got["cfg"], oc, "gathered cfg")
+        assert_eq(got["sum"], osum, "gathered sum")
+        assert_eq(got["mean"], omean, "gathered mean")
+        assert_eq(got["steps"], osteps, "gathered steps")
+        assert torch.equal(root, buf)      # one rank: the root holds the rank's buffer byte for byte
+    del dims
+    h1.close()
 
 
 def test_config3_full_batch_sampled(h):

@@ -38,11 +38,42 @@ def _decisions(cfg, lo, hi, mode):
     return oracle.thief(inst, mode)
 
 
-def _worker(rank, world, port, total, mode, q):
+def _body(rank, world, total, mode, q, n_chunks):
+    """The data plane of bench.py's chunked gather (shard.RecordLayout): each rank writes its
+    chunk-c decisions into the chunk's typed record views, then chunk c is gathered to the
+    root's chunk-c region (here dist.gather over gloo; on GPUs ekya_gather_decisions ->
+    ncclGather with the same offsets), and the root unpacks global instance order."""
+    cfg = synth.SchedConfig(**{**synth.CONFIG2.__dict__, "n_inst": total})
+    lo, hi = shard.shard_range(total, world, rank)
+    V = cfg.n_streams
+    L = shard.RecordLayout(total, world, V, n_chunks)
+    buf = torch.zeros(L.rank_bytes, dtype=torch.uint8)
+    root = torch.zeros(L.root_bytes, dtype=torch.uint8) if rank == 0 else None
+    for c in range(L.n_chunks):
+        b0, b1 = L.chunk_range(rank, c)
+        views = L.views(buf, rank, c)
+        if b1 > b0:
+            a, cf, s, m, st, _ = _decisions(cfg, lo + b0, lo + b1, mode)
+            views["sum"][:] = torch.from_numpy(s.astype(np.uint64))
+            views["mean"][:] = torch.from_numpy(m)
+            views["steps"][:] = torch.from_numpy(st)
+            views["alloc"][:] = torch.from_numpy(a)
+            views["cfg"][:] = torch.from_numpy(cf)
+        local = L.local_chunk(buf, c)
+        gl = [torch.zeros_like(local) for _ in range(world)] if rank == 0 else None
+        dist.gather(local, gl, dst=0)
+        if rank == 0:
+            L.root_chunk(root, c).copy_(torch.cat(gl))
+    if rank == 0:
+        got = L.unpack(root)
+        q.put({k: v.numpy().copy() for k, v in got.items()})
+
+
+def _worker(rank, world, port, total, mode, q, n_chunks=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        _body(rank, world, total, mode, q)
+        _body(rank, world, total, mode, q, n_chunks)
     except Exception as e:  # surface the failure instead of hanging the test
         q.put(repr(e))
         raise
@@ -50,36 +81,12 @@ def _worker(rank, world, port, total, mode, q):
         dist.destroy_process_group()
 
 
-def _body(rank, world, total, mode, q):
-    if True:
-        cfg = synth.SchedConfig(**{**synth.CONFIG2.__dict__, "n_inst": total})
-        lo, hi = shard.shard_range(total, world, rank)
-        per = [shard.shard_range(total, world, r)[1] - shard.shard_range(total, world, r)[0] for r in range(world)]
-        bmax = max(per)
-        V = cfg.n_streams
-        buf = torch.zeros(shard.record_bytes(bmax, V), dtype=torch.uint8)
-        views = shard.record_views(buf, bmax, V)
-        a, c, s, m, st, _ = _decisions(cfg, lo, hi, mode)
-        n = hi - lo
-        views["sum"][:n] = torch.from_numpy(s.astype(np.uint64))
-        views["mean"][:n] = torch.from_numpy(m)
-        views["steps"][:n] = torch.from_numpy(st)
-        views["alloc"][:n] = torch.from_numpy(a)
-        views["cfg"][:n] = torch.from_numpy(c)
-        gl = [torch.zeros_like(buf) for _ in range(world)] if rank == 0 else None
-        dist.gather(buf, gl, dst=0)
-        if rank == 0:
-            root = torch.cat(gl)
-            got = shard.unpack_root(root, world, per, V)
-            q.put({k: v.numpy().copy() for k, v in got.items()})
-
-
-@pytest.mark.parametrize("total,mode", [(12, 0), (11, 1)])
-def test_sharded_gather_equals_single_run(total, mode):
+@pytest.mark.parametrize("total,mode,n_chunks", [(12, 0, 1), (11, 1, 1), (23, 0, 4), (9, 1, 8)])
+def test_sharded_gather_equals_single_run(total, mode, n_chunks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, total, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, total, mode, q, n_chunks)) for r in range(2)]
     for p in procs:
         p.start()
     got = q.get(timeout=120)
@@ -94,6 +101,24 @@ def test_sharded_gather_equals_single_run(total, mode):
     assert np.array_equal(got["sum"], s)
     assert np.array_equal(got["mean"], m)
     assert np.array_equal(got["steps"], st)
+
+
+def test_record_layout_single_process_roundtrip():
+    """RecordLayout with one rank: the root buffer is the rank buffer (the ekya_gather_decisions
+    one-rank path copies it), and unpack returns the rows written, for any chunk count."""
+    V = 10
+    for total, n_chunks in ((0, 8), (1, 8), (37, 8), (64, 4), (65, 1)):
+        L = shard.RecordLayout(total, 1, V, n_chunks)
+        buf = torch.zeros(L.rank_bytes, dtype=torch.uint8)
+        for c in range(L.n_chunks):
+            b0, b1 = L.chunk_range(0, c)
+            v = L.views(buf, 0, c)
+            v["sum"][:] = torch.arange(b0, b1, dtype=torch.int64).to(torch.uint64)
+            v["alloc"][:] = torch.arange(b0, b1, dtype=torch.int32).to(torch.uint16)[:, None]
+        got = L.unpack(buf.clone())
+        if total:
+            assert got["sum"].to(torch.int64).tolist() == list(range(total))
+            assert (got["alloc"].to(torch.int32) == torch.arange(total)[:, None]).all()
 
 
 def test_shard_ranges_partition():

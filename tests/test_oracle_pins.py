@@ -578,8 +578,10 @@ def test_cluster_init_and_ties_hand_worked():
     The query (3/16, 13/16) joins cluster 0: estimate = mean of windows 0 and 3."""
     hist = _hist2([1 / 16, 9 / 16, 3 / 4, 5 / 16])
     acc = np.array([[[0.25], [0.5], [0.75], [0.5]]], np.float32)
-    est, n, cl, bad = oracle.profile(_hist2([3 / 16])[:, 0], hist, acc, [[0.0]], mode=oracle.CLUSTER, k=3)
+    est, n, cl, bad, passes = oracle.profile(_hist2([3 / 16])[:, 0], hist, acc, [[0.0]], mode=oracle.CLUSTER, k=3,
+                                             with_passes=True)
     assert bad == 0
+    assert passes.tolist() == [2]          # the initial assignment + one iteration (no change)
     assert cl[0].tolist() == [0, 1, 2, 0, 0]
     assert n[0, 0] == 2 and est[0, 0] == np.float32(0.375)
 
@@ -597,10 +599,20 @@ def test_cluster_empty_cluster_keeps_its_centroid():
     The query (11/16, 5/16) joins cluster 1 = windows {0, 2, 4}."""
     hist = _hist2([11 / 16, 13 / 16, 11 / 16, 0.0, 5 / 8, 7 / 8, 0.0])
     acc = np.array([[[0.5], [0.1], [0.75], [0.2], [1.0], [0.3], [0.4]]], np.float32)
-    est, n, cl, bad = oracle.profile(_hist2([11 / 16])[:, 0], hist, acc, [[0.0]], mode=oracle.CLUSTER, k=3)
+    est, n, cl, bad, passes = oracle.profile(_hist2([11 / 16])[:, 0], hist, acc, [[0.0]], mode=oracle.CLUSTER, k=3,
+                                             with_passes=True)
     assert bad == 0
+    assert passes.tolist() == [3]          # initial + two iterations (the second changes nothing)
     assert cl[0].tolist() == [1, 0, 1, 2, 1, 0, 2, 1]
     assert n[0, 0] == 3 and est[0, 0] == np.float32(0.75)
+    # max_iter bounds the iterations: with one, the first update's assignment is final; with
+    # none, the initial assignment is (the query then joins cluster 0, tied with cluster 1)
+    _, _, cl1, _, p1 = oracle.profile(_hist2([11 / 16])[:, 0], hist, acc, [[0.0]], mode=oracle.CLUSTER, k=3,
+                                      max_iter=1, with_passes=True)
+    assert p1.tolist() == [2] and cl1[0].tolist() == [1, 0, 1, 2, 1, 0, 2, 1]
+    _, n0, cl0, _, p0 = oracle.profile(_hist2([11 / 16])[:, 0], hist, acc, [[0.0]], mode=oracle.CLUSTER, k=3,
+                                       max_iter=0, with_passes=True)
+    assert p0.tolist() == [1] and cl0[0].tolist() == [0, 0, 0, 2, 2, 0, 2, 0] and n0[0, 0] == 4
 
 
 def test_cluster_on_synth_converges_to_fixed_point():

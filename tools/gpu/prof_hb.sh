@@ -1,0 +1,4 @@
+mkdir -p gpurun_out/hb
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:cluster -s 2 -c 1 -o gpurun_out/hb/hb -f python tools/kbench.py cluster 1 > gpurun_out/hb/ncu_hb.log 2>&1
+EKYA_CLUSTER_NOHB=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:cluster -s 2 -c 1 -o gpurun_out/hb/c2 -f python tools/kbench.py cluster 1 > gpurun_out/hb/ncu_c2.log 2>&1
+ls -la gpurun_out/hb
