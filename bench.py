@@ -39,6 +39,26 @@ import synth  # noqa: E402
 METRIC = "scheduler allocations evaluated/sec and thief schedules/sec; % HBM roofline"
 UNIT = "allocations/s"
 
+# The driver reads ONE JSON line from stdout.  Libraries write banners to fd 1 (NCCL prints
+# its version line when NCCL_DEBUG is set in the environment), so fd 1 is pointed at stderr
+# for the whole run and the JSON line goes to a private duplicate of the original stdout.
+_JSON_OUT = None
+
+
+def emit(line):
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        _JSON_OUT = sys.stdout
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
+
+
+def _stdout_to_stderr():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
 
 def fp32_peak(sm_mhz):
     """Measured FP32 SIMT peak (TFLOP/s) scaled to `sm_mhz`, and its source."""
@@ -344,7 +364,7 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def config_block(w, args):
@@ -533,7 +553,7 @@ def run_ours(args, rank, world, local_rank):
         t0 = time.perf_counter()
         oracle.place(sample, w.U, 8)
         line["cpu_baseline"]["next4_placement_instances_per_s"] = sample.shape[0] / (time.perf_counter() - t0)
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def _time_ms(fn, reps=10):
@@ -976,6 +996,7 @@ def main():
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
         sys.exit(subprocess.call(cmd))
+    _stdout_to_stderr()   # after the re-launch: the ranks inherit the real stdout
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -54,7 +54,7 @@ def main(ev, tag):
                          capture_output=True, text=True).stdout
     fr = list(csv.reader(txt.splitlines()))
     h, units = fr[0], fr[1]
-    full, traffic = [], {}
+    full, traffic, insts = [], {}, {}
     thief = 0
     for r in fr[2:]:
         d = dict(zip(h, r))
@@ -66,15 +66,26 @@ def main(ev, tag):
         wr = float(d["dram__bytes_write.sum"]) * SCALE.get(u["dram__bytes_write.sum"], 1)
         if name:
             traffic[name] = rd + wr
+            ie = d.get("smsp__inst_executed.sum", "")
+            if ie:
+                ie = float(ie) * {"inst": 1, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9}.get(
+                    u.get("smsp__inst_executed.sum", "inst"), 1)
+                # prof_driver.py launches every row at the bench sizes: 65,536 instances / queries
+                insts[name] = {"warp_inst_per_launch": ie, "units": 65536,
+                               "source": f"ncu --set full, smsp__inst_executed.sum ({tag})"}
         full.append((name or d["Kernel Name"][:40], {k: (d.get(k, ""), u.get(k, "")) for k in KEYS}))
     with open(os.path.join(out_dir, "traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
+    with open(os.path.join(out_dir, "round2_inst.json"), "w") as f:
+        json.dump(insts, f, indent=1)
     with open(os.path.join(out_dir, f"{tag}_ncu_full_summary.csv"), "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["row"] + KEYS)
         for n, d in full:
             w.writerow([n] + [f"{v} {u}".strip() for v, u in d.values()])
-    bench = json.load(open(os.path.join(ev, "bench.json")))
+    # the JSON line (a library banner may precede it in older captures)
+    with open(os.path.join(ev, "bench.json")) as f:
+        bench = json.loads([ln for ln in f if ln.startswith("{")][-1])
     with open(os.path.join(out_dir, f"{tag}_bench.json"), "w") as f:
         json.dump(bench, f, indent=1)
     md = [f"# {tag}: launch list, ncu counters, bench line\n",
