@@ -56,6 +56,7 @@ struct ThiefParams {
     size_t warp_bytes;   // shared bytes per warp (state + staged tables)
     size_t state_bytes;  // shared bytes of the per-warp state
     int stage;           // stage stale/cost/post of the instance in shared memory
+    int nsm;             // G* cache slots per stream - 1 (a power of two minus one)
 };
 
 // Per-stream record rec[v][8] (Q32 units): [0] current value, [1] up (inference
@@ -63,36 +64,45 @@ struct ThiefParams {
 // [5] move with thief = training (training +D, inference -D), [6] move with
 // thief = inference (inference +D, training -D); kInvalid where the victim has
 // fewer than D units.
+//
+// Every record entry is value(rt', ri') = fl(F(ri') G*(rt')) at one of seven
+// splits, so an entry costs two shared lookups once both functions are at hand:
+//   F(ri)  = factor of lambda*(ri): a per-stream ladder of at most 8 keep-up
+//            thresholds (ascending, u16) -- lambda* changes only there -- read as one
+//            16-byte row and counted with four SIMD compares;
+//   G*(rt) = max over {none} + feasible Gamma of rule 2: memoised per stream in a
+//            direct-mapped cache of NS (rt, value) slots, filled on a miss.
+// A step re-evaluates the two touched streams with one lane per record entry
+// (lanes 8k + e, e < 7), i.e. 14 lanes in one pass.
 struct WarpState {
     long long* rec;              // [V][8]
     int* alloc;                  // [J]
-    int* lthr;                   // [V][8] lambda* breakpoints, ascending (INT_MAX = unused)
-    float* lfac;                 // [V][8] factor of lambda* at the breakpoint
-    int* lidx;                   // [V][8] index of lambda* at the breakpoint
-    float* gc;                   // [V][4] G*(rt-D), G*(rt), G*(rt+D) cached for rt = grt[v]
-    int* grt;                    // [V]    (-1 = empty)
+    uint4* lthr;                 // [V] eight u16 lambda* thresholds, ascending (0xFFFF = unused)
+    float* lfac;                 // [V][8] factor of lambda* at the threshold
+    signed char* lidx;           // [V][8] index of lambda* at the threshold
+    uint2* gc;                   // [V][NS] G* cache: (rt, value bits), rt = 0xFFFFFFFF empty
     __device__ __forceinline__ long long cur(int v) const { return rec[v * 8]; }
     __device__ __forceinline__ long long up(int j) const { return rec[(j >> 1) * 8 + 1 + (j & 1)]; }
     __device__ __forceinline__ long long dn(int j) const { return rec[(j >> 1) * 8 + 3 + (j & 1)]; }
     __device__ __forceinline__ long long mv(int j) const { return rec[(j >> 1) * 8 + 6 - (j & 1)]; }
 };
 
-__host__ __device__ inline size_t thief_warp_bytes(int V) {
+__host__ __device__ inline size_t thief_warp_bytes(int V, int NS) {
     const size_t J = 2 * (size_t)V;
-    size_t b = 8 * 8 * (size_t)V + 4 * J + 3 * 4 * 8 * (size_t)V + 4 * 4 * (size_t)V + 4 * (size_t)V;
+    size_t b = 8 * 8 * (size_t)V + 4 * J + 16 * (size_t)V + 4 * 8 * (size_t)V + 8 * (size_t)V +
+               8 * (size_t)NS * (size_t)V;
     return (b + 15) & ~size_t(15);
 }
 
-__device__ inline WarpState carve(unsigned char* base, int V) {
+__device__ inline WarpState carve(unsigned char* base, int V, int NS) {
     const int J = 2 * V;
     WarpState w;
-    w.rec = reinterpret_cast<long long*>(base);
-    w.alloc = reinterpret_cast<int*>(w.rec + 8 * V);
-    w.lthr = w.alloc + J;
-    w.lfac = reinterpret_cast<float*>(w.lthr + 8 * V);
-    w.lidx = reinterpret_cast<int*>(w.lfac + 8 * V);
-    w.gc = reinterpret_cast<float*>(w.lidx + 8 * V);
-    w.grt = reinterpret_cast<int*>(w.gc + 4 * V);
+    w.rec = reinterpret_cast<long long*>(base);                        // 8-byte aligned
+    w.gc = reinterpret_cast<uint2*>(w.rec + 8 * V);                    // 8-byte aligned
+    w.lthr = reinterpret_cast<uint4*>(w.gc + (size_t)NS * V);          // 16-byte aligned (NS even)
+    w.lfac = reinterpret_cast<float*>(w.lthr + V);
+    w.alloc = reinterpret_cast<int*>(w.lfac + 8 * V);
+    w.lidx = reinterpret_cast<signed char*>(w.alloc + J);
     return w;
 }
 
@@ -131,15 +141,17 @@ struct InstView {
     }
 };
 
+// IEEE division off the hot path (the exact shared-reciprocal path covers the paper's shapes)
+__device__ __noinline__ float fdiv_cold(float a, float b) { return __fdiv_rn(a, b); }
+
 // Warp-collective, once per stream: lambda* ladder (Alg. 2 lines 3-4, rule 3).
 // lambda*(ri) depends only on the admissible set {l : t_l <= ri} (t_l = lmu_l if
 // fl(stale f_l) >= a_MIN, else never), which equals the set at the largest
 // t_l <= ri; so the thresholds are stored ascending (ties: lambda order) with
-// lambda*(t) and its factor, and a lookup is one ballot over lanes 0..7: the
-// lanes with t <= ri form a prefix and its last lane holds lambda*(ri).
+// lambda*(t) and its factor, and F(ri) is the entry of the last threshold <= ri.
 __device__ void init_ladder(const InstView& in, const WarpState& S, int v, const ekya_dims& d) {
     const int lane = threadIdx.x & 31, nL = d.n_lambda;
-    int t = INT_MAX;
+    unsigned t = 0xFFFFu;
     float acc = 0.0f, f = 0.0f;
     if (lane < nL) {
         const uint16_t m = in.lmu[(size_t)v * nL + lane];
@@ -150,8 +162,9 @@ __device__ void init_ladder(const InstView& in, const WarpState& S, int v, const
     // lambda*(t) over {l : t_l <= t}: highest accuracy, lowest index on ties
     int best = -1, rank = 0;
     float bacc = 0.0f;
+#pragma unroll 1
     for (int l = 0; l < nL; ++l) {
-        const int tl = __shfl_sync(FULL, t, l);
+        const unsigned tl = __shfl_sync(FULL, t, l);
         const float al = __shfl_sync(FULL, acc, l);
         if (tl <= t && (best < 0 || al > bacc)) {
             best = l;
@@ -160,112 +173,149 @@ __device__ void init_ladder(const InstView& in, const WarpState& S, int v, const
         rank += (tl < t || (tl == t && l < lane)) ? 1 : 0;
     }
     const float fb = __shfl_sync(FULL, f, best < 0 ? 0 : best);
+    // unused / inadmissible lambdas sort last (t = 0xFFFF) and are never reached
+    const int pos = lane < nL ? rank : lane;
     if (lane < 8) {
-        // unused / inadmissible lambdas sort last (t = INT_MAX) and are never reached
-        const int pos = lane < nL ? rank : lane;
-        S.lthr[v * 8 + pos] = t;
+        unsigned short* th = reinterpret_cast<unsigned short*>(S.lthr + v);
+        th[pos] = (unsigned short)t;
         S.lfac[v * 8 + pos] = fb;
-        S.lidx[v * 8 + pos] = best;
+        S.lidx[v * 8 + pos] = (signed char)best;
     }
 }
 
-// lambda* ladder lookup of stream v at ri: slot of lambda*(ri) in the ladder, -1 if none
-__device__ __forceinline__ int ladder_slot(int tk, int ri) {
-    const unsigned m = __ballot_sync(FULL, (threadIdx.x & 31) < 8 && tk <= ri);
-    return 31 - __clz(m);   // -1 when m == 0
+// number of ladder thresholds <= ri (0 .. 8): the ladder slot of lambda*(ri) is count - 1
+__device__ __forceinline__ int ladder_count(const uint4& th, int ri) {
+    const unsigned r = (unsigned)min(ri, 0xFFFE);
+    const unsigned rr = r | (r << 16);
+    return (__popc(__vcmpleu2(th.x, rr)) + __popc(__vcmpleu2(th.y, rr)) + __popc(__vcmpleu2(th.z, rr)) +
+            __popc(__vcmpleu2(th.w, rr))) >> 4;
 }
 
-// Warp-collective update of stream v's entries in the state arrays.
-__device__ __forceinline__ void update_stream(const InstView& in, const WarpState& S, int v, const ekya_dims& d,
-                                              bool fast) {
-    const int lane = threadIdx.x & 31;
-    const int D = d.steal_units, nG = d.n_gamma;
-    const int ri = S.alloc[2 * v], rt = S.alloc[2 * v + 1];
-    const float stale = in.stale[v];
-    float cost = 0.0f, post = 0.0f, diff = 0.0f;
-    if (lane >= 1 && lane <= nG) {
-        const float4 c = in.get(v, lane - 1, nG);
-        cost = c.x;
-        post = c.y;
-        diff = c.z;
-    }
-    const int tk = lane < 8 ? S.lthr[v * 8 + lane] : INT_MAX;
-    const float fk = lane < 8 ? S.lfac[v * 8 + lane] : -1.0f;
-    const bool mine = lane >= 1 && lane <= nG;
-    // G*(r): lane g evaluates rule 2 for config g, REDUX max; values are >= 0 or
-    // the -1 sentinel, so signed-int order of the bits = float order.  The divisor
-    // fl(r uT) is shared by the warp: with `fast` the division is the exact
-    // shared-reciprocal fast path (stream_tables.cuh), branch-free.
-    auto gstar = [&](int r) -> float {
-        const float den = fmul(__int2float_rn(r), d.unit_gpu_seconds);
-        float f;
-        if (fast) {
-            const SharedDiv dv(den);
-            f = dv.div(cost);
-        } else {
-            f = mine && r >= 1 ? fdiv(cost, den) : 2.0f;
-        }
-        const float w = fsub(post, fmul(f, diff));
-        const float g = lane == 0 ? stale : (mine && r >= 1 && f <= 1.0f ? w : -1.0f);
-        const int m = __reduce_max_sync(FULL, __float_as_int(g));
-        return r < 0 ? -1.0f : __int_as_float(m);
-    };
-    // G* at rt-D, rt, rt+D, reusing the stream's cached values when rt moved by D
-    const int crt = S.grt[v];
-    float G[3];
-    if (crt == rt) {
-        G[0] = S.gc[v * 4]; G[1] = S.gc[v * 4 + 1]; G[2] = S.gc[v * 4 + 2];
-    } else if (crt >= 0 && crt == rt - D) {
-        G[0] = S.gc[v * 4 + 1]; G[1] = S.gc[v * 4 + 2]; G[2] = gstar(rt + D);
-    } else if (crt >= 0 && crt == rt + D) {
-        G[2] = S.gc[v * 4 + 1]; G[1] = S.gc[v * 4]; G[0] = gstar(rt - D);
-    } else {
-        G[0] = gstar(rt - D); G[1] = gstar(rt); G[2] = gstar(rt + D);
-    }
-    float fac[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const int ri2 = ri + D * (k - 1);
-        const int sl = ladder_slot(tk, ri2);   // ri2 < 0 never reaches a threshold (t >= 0)
-        const float f = __shfl_sync(FULL, fk, sl < 0 ? 0 : sl);
-        fac[k] = sl >= 0 ? f : -1.0f;
-    }
-    __syncwarp();
-    if (lane == 0) {
-        S.gc[v * 4] = G[0]; S.gc[v * 4 + 1] = G[1]; S.gc[v * 4 + 2] = G[2];
-        S.grt[v] = rt;
-    }
-    // lanes 0..6 each produce one of the seven record entries, no divergence:
-    // lane: 0 cur (rt,ri) 1 (rt,ri+D) 2 (rt+D,ri) 3 (rt,ri-D) 4 (rt-D,ri) 5 (rt+D,ri-D) 6 (rt-D,ri+D)
-    const float Ga = (lane == 2 || lane == 5) ? G[2] : (lane == 4 || lane == 6) ? G[0] : G[1];
-    const float fb = (lane == 1 || lane == 6) ? fac[2] : (lane == 3 || lane == 5) ? fac[0] : fac[1];
-    const long long val = fb < 0.0f ? 0LL : (long long)q32(fmul(fb, Ga));
-    const long long c = fac[1] < 0.0f ? 0LL : (long long)q32(fmul(fac[1], G[1]));
-    const bool valid = (lane == 3 || lane == 5) ? ri >= D : (lane == 4 || lane == 6) ? rt >= D : true;
-    const long long out = lane == 0 ? c : (valid ? val - c : kInvalid);
-    if (lane < 7) S.rec[v * 8 + lane] = out;
-    __syncwarp();
-}
-
-// Warp-collective: exact argmax config byte of stream v at its final split.
-__device__ uint8_t stream_cfg(const InstView& in, const WarpState& S, int v, int ri, int rt, const ekya_dims& d) {
+// G*(r) of stream v (r >= 0), warp-collective: lane g evaluates rule 2 for retraining
+// config g (lane 0 = no retraining), one REDUX max; values are >= 0 or the -1 sentinel,
+// so signed-int order of the bits = float order.  The divisor fl(r uT) is shared by the
+// warp: with `fast` the division is the exact shared-reciprocal fast path
+// (stream_tables.cuh), branch-free.
+__device__ __forceinline__ float gstar_warp(const InstView& in, int v, int r, const ekya_dims& d, bool fast) {
     const int lane = threadIdx.x & 31, nG = d.n_gamma;
-    const int tk = lane < 8 ? S.lthr[v * 8 + lane] : INT_MAX;
-    const int sl = ladder_slot(tk, ri);
-    if (sl < 0) return (uint8_t)(kLambdaNone << 5);
-    const int l = S.lidx[v * 8 + sl];
-    const float fac = S.lfac[v * 8 + sl];
-    const float stale = in.stale[v];
-    float a = -1.0f;
-    if (lane == 0) a = fmul(fac, stale);
-    else if (lane <= nG) {
-        const float4 c = in.get(v, lane - 1, nG);
-        float w;
-        if (window_acc(stale, c.y, c.x, rt, d.unit_gpu_seconds, &w)) a = fmul(fac, w);
+    const bool mine = lane >= 1 && lane <= nG;
+    float4 c = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (mine) c = in.get(v, lane - 1, nG);
+    const float den = fmul(__int2float_rn(r), d.unit_gpu_seconds);
+    float f;
+    if (fast) {
+        const SharedDiv dv(den);
+        f = dv.div(c.x);
+    } else {
+        f = mine && r >= 1 ? fdiv_cold(c.x, den) : 2.0f;
     }
-    const int m = __reduce_max_sync(FULL, __float_as_int(a));
-    const unsigned hits = __ballot_sync(FULL, __float_as_int(a) == m);
-    return (uint8_t)((__ffs(hits) - 1) | (l << 5));
+    const float w = fsub(c.y, fmul(f, c.z));
+    const float g = lane == 0 ? in.stale[v] : (mine && r >= 1 && f <= 1.0f ? w : -1.0f);
+    return __int_as_float(__reduce_max_sync(FULL, __float_as_int(g)));
+}
+
+// G*(r) of stream v (r >= 0) by one lane: the same maximum over the same rule-2 values
+// (fmaxf of values >= 0 and -1 sentinels equals the integer-bit maximum above)
+__device__ __forceinline__ float gstar_lane(const InstView& in, int v, int r, const ekya_dims& d, bool fast) {
+    const int nG = d.n_gamma;
+    float G = in.stale[v];
+    if (r < 1) return G;
+    const float den = fmul(__int2float_rn(r), d.unit_gpu_seconds);
+    if (fast) {
+        const SharedDiv dv(den);
+#pragma unroll 1
+        for (int g = 0; g < nG; ++g) {
+            const float4 c = in.get(v, g, nG);
+            const float f = dv.div(c.x);
+            const float w = fsub(c.y, fmul(f, c.z));
+            G = f <= 1.0f ? fmaxf(G, w) : G;
+        }
+    } else {
+#pragma unroll 1
+        for (int g = 0; g < nG; ++g) {
+            const float4 c = in.get(v, g, nG);
+            const float f = fdiv_cold(c.x, den);
+            if (f <= 1.0f) G = fmaxf(G, fsub(c.y, fmul(f, c.z)));
+        }
+    }
+    return G;
+}
+
+// Warp-collective: record entries of up to four streams s0..s3 (-1 = none), lane 8k + e
+// computing entry e of stream s_k at its split: e = 0 cur (rt,ri), 1 (rt,ri+D),
+// 2 (rt+D,ri), 3 (rt,ri-D), 4 (rt-D,ri), 5 (rt+D,ri-D), 6 (rt-D,ri+D).
+__device__ __forceinline__ void update_streams(const InstView& in, const WarpState& S, int s0, int s1, int s2,
+                                               int s3, const ekya_dims& d, bool fast, int nsm) {
+    const int lane = threadIdx.x & 31, D = d.steal_units;
+    const int k = lane >> 3, e = lane & 7;
+    const int s = k == 0 ? s0 : k == 1 ? s1 : k == 2 ? s2 : s3;
+    const bool act = e < 7 && s >= 0;
+    int ri = 0, rt = 0;
+    if (act) {
+        ri = S.alloc[2 * s];
+        rt = S.alloc[2 * s + 1];
+    }
+    const int drt = (e == 2 || e == 5) ? D : (e == 4 || e == 6) ? -D : 0;
+    const int dri = (e == 1 || e == 6) ? D : (e == 3 || e == 5) ? -D : 0;
+    const int rt2 = rt + drt, ri2 = ri + dri;
+    const bool valid = act && rt2 >= 0 && ri2 >= 0;
+    float G = 0.0f;
+    bool need = false;
+    if (valid) {
+        const uint2 c = S.gc[s * (nsm + 1) + (rt2 & nsm)];
+        need = c.x != (unsigned)rt2;
+        G = __uint_as_float(c.y);
+    }
+    for (unsigned m = __ballot_sync(FULL, need); m; m = __ballot_sync(FULL, need)) {
+        const int src = __ffs(m) - 1;
+        const int ms = __shfl_sync(FULL, s, src), mr = __shfl_sync(FULL, rt2, src);
+        const float gv = gstar_warp(in, ms, mr, d, fast);
+        if (lane == 0) S.gc[ms * (nsm + 1) + (mr & nsm)] = make_uint2((unsigned)mr, __float_as_uint(gv));
+        if (need && s == ms && rt2 == mr) {
+            G = gv;
+            need = false;
+        }
+    }
+    float F = -1.0f;
+    if (valid) {
+        const int cnt = ladder_count(S.lthr[s], ri2);
+        if (cnt > 0) F = S.lfac[s * 8 + cnt - 1];
+    }
+    const long long val = F < 0.0f ? 0LL : (long long)q32(fmul(F, G));
+    const long long c = __shfl_sync(FULL, val, lane & ~7);
+    if (act) S.rec[s * 8 + e] = e == 0 ? c : (valid ? val - c : kInvalid);
+    __syncwarp();
+}
+
+// Exact argmax config byte of stream v at its final split, one lane per stream: rule 3's
+// (lambda*, gamma*) with gamma* the lowest index maximising fl(f_lambda* g_gamma) (strict '>'
+// in index order keeps the lowest; gamma = none is index 0).
+__device__ uint8_t stream_cfg_lane(const InstView& in, const WarpState& S, int v, int ri, int rt,
+                                   const ekya_dims& d, bool fast) {
+    const int nG = d.n_gamma;
+    const int cnt = ladder_count(S.lthr[v], ri);
+    if (cnt == 0) return (uint8_t)(kLambdaNone << 5);
+    const int l = S.lidx[v * 8 + cnt - 1];
+    const float fac = S.lfac[v * 8 + cnt - 1];
+    float best = fmul(fac, in.stale[v]);
+    int gb = 0;
+    if (rt >= 1) {
+        const float den = fmul(__int2float_rn(rt), d.unit_gpu_seconds);
+        const SharedDiv dv(den);
+#pragma unroll 1
+        for (int g = 0; g < nG; ++g) {
+            const float4 c = in.get(v, g, nG);
+            const float f = fast ? dv.div(c.x) : fdiv_cold(c.x, den);
+            if (f <= 1.0f) {
+                const float a = fmul(fac, fsub(c.y, fmul(f, c.z)));
+                if (a > best) {
+                    best = a;
+                    gb = g + 1;
+                }
+            }
+        }
+    }
+    return (uint8_t)(gb | (l << 5));
 }
 
 __device__ __forceinline__ bool uT_fast(const ekya_dims& d) {
@@ -303,7 +353,8 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
     const ekya_dims& d = p.d;
     const int V = d.n_streams, J = 2 * V, D = d.steal_units, U = d.units, nG = d.n_gamma, nL = d.n_lambda;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const WarpState S = carve(smem + warp * p.warp_bytes, V);
+    const int nsm = p.nsm;
+    const WarpState S = carve(smem + warp * p.warp_bytes, V, nsm + 1);
     float* staged = reinterpret_cast<float*>(smem + warp * p.warp_bytes + p.state_bytes);
     const long long b = (long long)blockIdx.x * p.warps + warp;
     if (b >= d.n_inst) return;
@@ -311,30 +362,33 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
     InstView in{p.t.stale + b * V, p.t.cost + b * V * nG, p.t.post + b * V * nG,
                 p.t.lam_min_units + b * V * nL, p.t.lam_factor + b * V * nL, nullptr};
 
-    // ---- validity (R-ERR) ----
+    // ---- validity (R-ERR), the exact-division test and the staging, in one pass ----
+    // (lanes over a stream's configs: |Gamma| <= 31)
     bool ok = true;
-    for (int i = lane; i < V; i += 32) ok &= in01(__ldg(in.stale + i));
-    for (int i = lane; i < V * nG; i += 32) {
-        const float c = __ldg(in.cost + i);
-        if (!(c >= 0.0f)) ok = false;
-        else if (!isinf(c)) ok &= in01(__ldg(in.post + i));
+    // exact shared-reciprocal division applies to every cost and every fl(r uT), r <= U + D
+    bool fast = uT_fast(d);
+    float4* cpd = reinterpret_cast<float4*>(staged);
+    float* st = reinterpret_cast<float*>(cpd + V * nG);
+    for (int i = lane; i < V; i += 32) {
+        const float x = __ldg(in.stale + i);
+        ok &= in01(x);
+        if (p.stage) st[i] = x;
+    }
+    for (int v = 0; v < V; ++v) {
+        if (lane < nG) {
+            const float c = __ldg(in.cost + v * nG + lane), po = __ldg(in.post + v * nG + lane);
+            if (!(c >= 0.0f)) ok = false;
+            else if (!isinf(c)) ok &= in01(po);
+            fast &= fast_dividend(c);
+            if (p.stage) cpd[v * nG + lane] = make_float4(c, po, fsub(po, __ldg(in.stale + v)), 0.0f);
+        }
     }
     for (int i = lane; i < V * nL; i += 32)
         if (__ldg(in.lmu + i) != kLmuPad) ok &= in01(__ldg(in.lf + i));
+    __syncwarp();
     ok = __all_sync(FULL, ok);
-    // exact shared-reciprocal division applies to every cost and every fl(r uT), r <= U + D
-    bool fast = uT_fast(d);
-    for (int i = lane; i < V * nG; i += 32) fast &= fast_dividend(__ldg(in.cost + i));
     fast = __all_sync(FULL, fast);
-    if (p.stage && ok) {   // stale and (cost, post, post - stale) into this warp's shared memory
-        float4* cpd = reinterpret_cast<float4*>(staged);
-        float* st = reinterpret_cast<float*>(cpd + V * nG);
-        for (int i = lane; i < V; i += 32) st[i] = __ldg(in.stale + i);
-        for (int i = lane; i < V * nG; i += 32) {
-            const float c = __ldg(in.cost + i), po = __ldg(in.post + i);
-            cpd[i] = make_float4(c, po, fsub(po, __ldg(in.stale + i / nG)), 0.0f);
-        }
-        __syncwarp();
+    if (p.stage) {   // stale and (cost, post, post - stale) in this warp's shared memory
         in.stale = st;
         in.cpd = cpd;
     }
@@ -357,10 +411,20 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
         S.alloc[2 * v + 1] = rt;
         S.alloc[2 * v] = share - rt;
     }
+#pragma unroll 1
     for (int v = 0; v < V; ++v) init_ladder(in, S, v, d);
-    for (int v = lane; v < V; v += 32) S.grt[v] = -1;
+#pragma unroll 1
+    for (int i = lane; i < V * (nsm + 1); i += 32) S.gc[i] = make_uint2(0xFFFFFFFFu, 0u);
     __syncwarp();
-    for (int v = 0; v < V; ++v) update_stream(in, S, v, d, fast);
+    // G* at rt - D, rt, rt + D of every stream, one lane each (two slots may collide when
+    // 2D = 0 mod NS: either complete (rt, value) pair is a valid cache entry)
+    for (int i = lane; i < 3 * V; i += 32) {
+        const int v = i / 3, r = S.alloc[2 * v + 1] + D * (i - 3 * v - 1);
+        if (r >= 0) S.gc[v * (nsm + 1) + (r & nsm)] = make_uint2((unsigned)r, __float_as_uint(gstar_lane(in, v, r, d, fast)));
+    }
+    __syncwarp();
+    for (int v = 0; v < V; v += 4)
+        update_streams(in, S, v, v + 1 < V ? v + 1 : -1, v + 2 < V ? v + 2 : -1, v + 3 < V ? v + 3 : -1, d, fast, nsm);
 
     unsigned steps = 0;
     if (MODE == EKYA_THIEF_STEEPEST) {
@@ -421,8 +485,7 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
                 S.alloc[t] += D;
             }
             __syncwarp();
-            update_stream(in, S, t >> 1, d, fast);
-            if ((w >> 1) != (t >> 1)) update_stream(in, S, w >> 1, d, fast);
+            update_streams(in, S, t >> 1, (w >> 1) != (t >> 1) ? (w >> 1) : -1, -1, -1, d, fast, nsm);
             if (++steps >= max_steps) {
                 if (lane == 0) flag_data_error(p.st);
                 break;
@@ -444,8 +507,7 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
                         S.alloc[t] += D;
                     }
                     __syncwarp();
-                    update_stream(in, S, t >> 1, d, fast);
-                    if ((w >> 1) != (t >> 1)) update_stream(in, S, w >> 1, d, fast);
+                    update_streams(in, S, t >> 1, (w >> 1) != (t >> 1) ? (w >> 1) : -1, -1, -1, d, fast, nsm);
                     ++steps;
                 } while (lit_cond(S, t, w, J));
                 pos = w + 1;
@@ -458,10 +520,8 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
     for (int v = lane; v < V; v += 32) part += (unsigned long long)S.cur(v);
     const unsigned long long sum = shfl_sum_u64(part);
     for (int j = lane; j < J; j += 32) p.out_alloc[b * J + j] = (uint16_t)S.alloc[j];
-    for (int v = 0; v < V; ++v) {
-        const uint8_t c = stream_cfg(in, S, v, S.alloc[2 * v], S.alloc[2 * v + 1], d);
-        if (lane == 0) p.out_cfg[b * V + v] = c;
-    }
+    for (int v = lane; v < V; v += 32)
+        p.out_cfg[b * V + v] = stream_cfg_lane(in, S, v, S.alloc[2 * v], S.alloc[2 * v + 1], d, fast);
     if (lane == 0) {
         p.out_sum[b] = sum;
         if (p.out_mean) p.out_mean[b] = mean_q32(sum, V);
@@ -485,20 +545,23 @@ int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int m
     p.out_sum = reinterpret_cast<unsigned long long*>(out_sum);
     p.out_mean = out_mean;
     p.out_steps = out_steps;
-    p.warps = kThiefThreads / 32;
-    p.state_bytes = thief_warp_bytes(d.n_streams);
+    // G* cache: 32 slots per stream for the paper's stream counts, fewer for wide instances
+    const int ns = d.n_streams <= 16 ? 32 : 8;
+    p.nsm = ns - 1;
+    p.state_bytes = thief_warp_bytes(d.n_streams, ns);
     const size_t tbytes = ((size_t)d.n_streams * (4 * d.n_gamma + 1) * 4 + 15) & ~size_t(15);
     p.stage = tbytes <= 8192;
     p.warp_bytes = p.state_bytes + (p.stage ? tbytes : 0);
+    p.warps = (int)std::min<size_t>(kThiefThreads / 32, h->smem_optin / p.warp_bytes);
+    if (p.warps < 1) return EKYA_ERR_SHAPE;
     size_t smem = p.warp_bytes * p.warps;
-    if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0) return EKYA_OK;
     auto kern = mode == EKYA_THIEF_STEEPEST ? thief_kernel<EKYA_THIEF_STEEPEST> : thief_kernel<EKYA_THIEF_LITERAL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
     long long grid = (d.n_inst + p.warps - 1) / p.warps;
     if (grid > 0x7fffffffLL) return EKYA_ERR_SHAPE;
-    kern<<<(unsigned)grid, kThiefThreads, smem, s>>>(p);
+    kern<<<(unsigned)grid, p.warps * 32, smem, s>>>(p);
     h->launches++;
     return cuda_status(cudaGetLastError());
 }

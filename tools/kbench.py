@@ -33,6 +33,10 @@ if which in ("cluster", "radius"):
     mode = ekya.PROFILE_CLUSTER if which == "cluster" else ekya.PROFILE_RADIUS
     fn = lambda: ekya.profile_estimate(h, P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=mode)
 else:
+    if os.environ.get("KB_C5"):   # config-5 shape (V = 100, U = 800)
+        w.cfg = synth.SchedConfig(**{**synth.CONFIG5.__dict__, "n_inst": w.B})
+        c = w.cfg
+        w.args = (c.units, c.steal_units, c.unit_gpu_seconds, c.a_min)
     T = synth.sched_tables(w.cfg, 0, w.B, device=dev)
     args = w.args
     if which == "grid":
