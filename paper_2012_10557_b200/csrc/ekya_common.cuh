@@ -149,6 +149,28 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
                  : "memory");
 }
 
+// plain arrival (release at CTA scope: this thread's prior shared writes are visible to
+// every thread whose wait observes the phase completion)
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// shared-memory counters with release / acquire semantics at CTA scope (monotonic
+// dependency counters that never alias, unlike a parity-tracked mbarrier phase)
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+// warp-uniform wait until *p >= target
+__device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
+    while (ld_acquire(p) < target) {
+    }
+}
+
 __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
     unsigned ok;
     asm volatile(
@@ -159,6 +181,24 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned 
         : "r"(smem_addr(bar)), "r"(parity)
         : "memory");
     return ok != 0;
+}
+
+// try_wait with a suspend-time hint: the waiting warp is parked (no issue slots spent
+// spinning) until the phase completes or about `ns` nanoseconds pass
+__device__ __forceinline__ bool mbar_try_wait_hint(unsigned long long* bar, unsigned parity, unsigned ns) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity), "r"(ns)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, unsigned parity, unsigned ns = 20000) {
+    while (!mbar_try_wait_hint(bar, parity, ns)) {
+    }
 }
 
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {

@@ -20,6 +20,7 @@
 // marks the row bad), V table lookups, an add-with-carry exact sum, the mean
 // by a correctly rounded reciprocal, 2-byte config stores.
 #include <algorithm>
+#include <cstdlib>
 
 #include <type_traits>
 
@@ -118,7 +119,8 @@ __host__ __device__ inline ListLayout list_layout(int U, int V, int nG, int nL, 
     L.tabs = o;   o += L.tabset * ntabs;
     L.inst_bytes = inst_layout(V, nG, nL).total;
     L.inst = o;   o += 2 * L.inst_bytes;
-    L.bars = o;   o += 32;   // 2 mbarriers + 2 task counters
+    L.bars = o;   o += 416;  // list_kernel: 2 mbarriers + 2 task counters; list2_kernel: 18 mbarriers, counter,
+                             // bad[2], 32 per-warp row-copy mbarriers
     L.total = o;
     return L;
 }
@@ -613,6 +615,292 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
     }
 }
 
+// ------------------------------------------------------------------------
+// LIST for the paper's shape (V = 10, |Gamma| = 18, |Lambda| = 5, U <= 80), barrier-free
+// ------------------------------------------------------------------------
+// The same work as list_kernel -- per instance V stream-table builds and N rows -- but the
+// CTA never synchronises as a whole.  Tasks come from ONE monotonic shared counter: phase p
+// holds the row tasks of instance p-1 (64 rows each) and the build tasks of instance p (one
+// stream, all r_train rows, each), interleaved.  Dependencies are mbarriers in rings of 8
+// (instance i uses slot i & 7, phase parity (i >> 3) & 1):
+//   full[s]  (32 V arrivals: every lane of each build)  the tables of instance i (table set
+//            k = i & 1) are built -- each lane's arrive releases its own table writes;
+//   empty[s] (32 C arrivals: every lane of each row task)  the rows of instance i are done
+//            (set k may be rebuilt);
+//   inbar[k] (TMA bytes)   the inputs of instance i are staged in input buffer k.
+// A row task of instance i waits on full[i & 7]; a build task of instance i on empty of
+// instance i-2 and then inbar[k] (unambiguous: the next copy into buffer k is issued only
+// after the builds of i).  Every task waits only on tasks of earlier phases and tasks are
+// taken in phase order, so the pipeline cannot deadlock.  Warps may run ahead of the oldest
+// unfinished task, but not by 8 phases: every phase after a stalled build holds at least
+// min(C, V) tasks blocked behind it, and 4 (C + V) > 32 warps, so a ring slot is never
+// re-armed while a waiter of its previous use is pending.  The first row task of instance i (its
+// tables are complete, so input buffer k is free) issues the TMA of instance i+2's inputs
+// into buffer k and the L2 prefetch of instance i+1's rows.  A build task checks its stream
+// (R-ERR) and marks the instance bad by writing i + 1 into bad[k] before it arrives.
+constexpr int kL2V = 10, kL2G = 18, kL2L = 5;   // tables laid out for U = 80
+constexpr int kL2Rows = 64;                       // rows per row task (two per thread; 32 / 128 / 256 measured slower)
+
+struct List2Params {
+    ekya_dims d;
+    ekya_tables t;
+    DevState* st;
+    int n_alloc;
+    const uint16_t* alloc;
+    unsigned long long* out_sum;
+    float* out_mean;
+    uint8_t* out_cfg;
+    ListLayout L;
+    InstLayout IL;
+    double rcp_v;
+    int chunks;   // row tasks per instance (kL2Rows rows each)
+    size_t rowbuf;     // per-warp row staging buffers (shared offset), kL2RowBuf bytes each
+};
+constexpr int kL2RowBuf = kL2Rows * 2 * kL2V * 2 + 32;   // one task's rows + granule slack
+
+// One allocation row (one thread): V = 10 streams, rows 8-byte aligned, config bytes written
+// in pairs; bit-identical to list_kernel's row evaluation.
+__device__ __forceinline__ void list2_row(const List2Params& p, const unsigned char* tabs, bool ok, long long o,
+                                          const uint2* row2) {
+    constexpr int V = kL2V, V2 = kL2V / 2;
+    constexpr int tb = 5936;                           // tab_bytes(kL2U, kListRow)
+    constexpr int off_tvc = 96;                        // a16(kL2U + 1): lad[] precedes the entries
+    constexpr int kRowBytes = kListRow * 8;
+    const int U = p.d.units;
+    const unsigned UU = (unsigned)U | ((unsigned)U << 16);
+    uint2 pr[V2];
+#pragma unroll
+    for (int v2 = 0; v2 < V2; ++v2) pr[v2] = row2[v2];
+    unsigned mx = 0;
+#pragma unroll
+    for (int v2 = 0; v2 < V2; ++v2) mx = __vmaxu2(mx, __vmaxu2(pr[v2].x, pr[v2].y));
+    Q32Sum S;
+    int tot;
+    unsigned dev = 0;   // any bit set: some r_train / r_infer > U (clamped)
+    uint16_t* cr2 = p.out_cfg ? reinterpret_cast<uint16_t*>(p.out_cfg) + o * V2 : nullptr;
+    if ((mx & 0xFFFFu) <= (unsigned)U && (mx >> 16) <= (unsigned)U) {
+        // every entry <= U: no clamping; the unit total is one packed 16x2 sum (<= V U < 2^16)
+        unsigned acc = 0;
+#pragma unroll
+        for (int v2 = 0; v2 < V2; ++v2) {
+            uint2 e[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const unsigned w = hh ? pr[v2].y : pr[v2].x;
+                const unsigned char* t = tabs + (2 * v2 + hh) * tb;
+                acc += w;
+                e[hh] = *reinterpret_cast<const uint2*>(t + off_tvc + (w >> 16) * kRowBytes + t[w & 0xFFFFu]);
+                S.add(e[hh]);
+            }
+            if (cr2) cr2[v2] = (uint16_t)__byte_perm(e[0].y, e[1].y, 0x0073);
+        }
+        tot = (int)((acc & 0xFFFFu) + (acc >> 16));
+    } else {
+        // some entry > U: clamp to U, evaluate, and flag the row below (R-ERR)
+        tot = 0;
+#pragma unroll
+        for (int v2 = 0; v2 < V2; ++v2) {
+            uint2 e[2];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const unsigned w = hh ? pr[v2].y : pr[v2].x;
+                const unsigned pc = __vminu2(w, UU);
+                dev |= w ^ pc;
+                const int ri = (int)(pc & 0xFFFFu), rt = (int)(pc >> 16);
+                tot += ri + rt;
+                const unsigned char* t = tabs + (2 * v2 + hh) * tb;
+                e[hh] = *reinterpret_cast<const uint2*>(t + off_tvc + rt * kRowBytes + t[ri]);
+                S.add(e[hh]);
+            }
+            if (cr2) cr2[v2] = (uint16_t)__byte_perm(e[0].y, e[1].y, 0x0073);
+        }
+    }
+    const bool rok = ok && dev == 0 && tot <= U;   // Eq. 1 constraint 2
+    unsigned long long s = S.value();
+    if (!rok) {                                     // R-ERR: zero the row
+        s = 0;
+        if (p.out_cfg)
+            for (int v = 0; v < V; ++v) p.out_cfg[o * V + v] = 0;
+        if (ok) flag_data_error(p.st);
+    }
+    p.out_sum[o] = s;
+    if (p.out_mean) {
+        // mean = (float)((double)s / (V 2^32)) by the correctly rounded reciprocal and one
+        // exact-residual correction (as list_kernel)
+        const double a = __ull2double_rn(s);
+        const double q0 = __dmul_rn(a, p.rcp_v);
+        const double q = __fma_rn(__fma_rn(-(double)V, q0, a), p.rcp_v, q0);
+        p.out_mean[o] = rok ? __double2float_rn(__dmul_rn(q, 2.3283064365386963e-10)) : 0.0f;
+    }
+}
+
+__global__ void __launch_bounds__(kListThreads, 1) list2_kernel(const __grid_constant__ List2Params p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int V = kL2V, nG = kL2G, nL = kL2L;
+    constexpr int tb = 5936;
+    const ekya_dims& d = p.d;
+    constexpr int RT = kL2Rows;
+    const int U = d.units, N = p.n_alloc, C = p.chunks, T = C + V;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const ListLayout& L = p.L;
+    const InstLayout& IL = p.IL;
+    unsigned long long* inbar = reinterpret_cast<unsigned long long*>(smem + L.bars);
+    unsigned long long* full = inbar + 2;    // [8]
+    unsigned long long* empty = inbar + 10;  // [8]
+    unsigned* ctr = reinterpret_cast<unsigned*>(inbar + 18);
+    int* bad = reinterpret_cast<int*>(ctr + 1);   // bad[k] = i + 1: instance i (set k) is invalid
+    const long long B = d.n_inst, g = gridDim.x, b0 = blockIdx.x;
+    const long long n = B > b0 ? (B - 1 - b0) / g + 1 : 0;   // instances of this CTA
+    if (n == 0) return;
+
+    auto issue_inputs = [&](long long b, int k) {
+        unsigned char* dst = smem + L.inst + k * L.inst_bytes;
+        const Granules gs[5] = {granules(p.t.stale + b * V, (size_t)V * 4),
+                                granules(p.t.cost + b * V * nG, (size_t)V * nG * 4),
+                                granules(p.t.post + b * V * nG, (size_t)V * nG * 4),
+                                granules(p.t.lam_min_units + b * V * nL, (size_t)V * nL * 2),
+                                granules(p.t.lam_factor + b * V * nL, (size_t)V * nL * 4)};
+        const size_t off[5] = {IL.stale, IL.cost, IL.post, IL.lmu, IL.lf};
+        unsigned tot = 0;
+        for (int i = 0; i < 5; ++i) tot += gs[i].bytes;
+        mbar_arrive_expect_tx(&inbar[k], tot);
+        for (int i = 0; i < 5; ++i)
+            if (gs[i].bytes) bulk_g2s(dst + off[i], gs[i].g0, gs[i].bytes, &inbar[k]);
+    };
+
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(&inbar[k], 1);
+            bad[k] = 0;
+        }
+        for (int s = 0; s < 8; ++s) {
+            mbar_init(&full[s], 32 * V);
+            mbar_init(&empty[s], 32 * C);
+        }
+        for (int w = 0; w < kListThreads / 32; ++w) mbar_init(&inbar[20 + w], 1);
+        *ctr = 0;
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        issue_inputs(b0, 0);
+        if (n > 1) issue_inputs(b0 + g, 1);
+    }
+
+    StreamIn* si = reinterpret_cast<StreamIn*>(smem + L.sin + (size_t)warp * a16(sizeof(StreamIn)));
+    // this warp's row staging buffer and its TMA barrier (phase = number of row tasks so far)
+    unsigned char* rbuf = smem + p.rowbuf + (size_t)warp * kL2RowBuf;
+    unsigned long long* rbar = inbar + 20 + warp;
+    unsigned rphase = 0;
+    const unsigned total = (unsigned)((n + 1) * T);
+    // phase layout: R0 rows, then builds and rows alternating, then what is left -- the builds
+    // of instance ph start once the rows of ph - 2 (previous phase) have had time to drain, and
+    // end well before the rows of ph (next phase) need them
+    const int R0 = C / 4, m = min(V, C - R0);
+    long long ph = 0;        // this warp's phase (tasks are taken in increasing order)
+    unsigned pstart = 0;     // first task of phase ph
+    for (;;) {
+        unsigned tau = 0;
+        if (lane == 0) tau = atomicAdd(ctr, 1u);
+        tau = __shfl_sync(0xffffffffu, tau, 0);
+        if (tau >= total) break;
+        while (tau >= pstart + (unsigned)T) {
+            ++ph;
+            pstart += (unsigned)T;
+        }
+        const int t = (int)(tau - pstart);
+        bool is_build;
+        int idx;
+        if (t < R0) {
+            is_build = false;
+            idx = t;
+        } else if (t < R0 + 2 * m) {
+            is_build = ((t - R0) & 1) == 0;
+            idx = is_build ? (t - R0) >> 1 : R0 + ((t - R0) >> 1);
+        } else {
+            is_build = V > C - R0;
+            idx = is_build ? t - R0 - m : t - m;
+        }
+        if (is_build) {
+            const long long i = ph;
+            if (i >= n) continue;
+            const int k = (int)(i & 1);
+            const unsigned par = (unsigned)((i >> 1) & 1);
+            if (i >= 2) mbar_wait_sleep(&empty[(i - 2) & 7], (unsigned)(((i - 2) >> 3) & 1));   // rows of i - 2 done
+            mbar_wait_sleep(&inbar[k], par);
+            const long long b = b0 + i * g;
+            const unsigned char* ib = smem + L.inst + k * L.inst_bytes;
+            const float* stale = reinterpret_cast<const float*>(ib + IL.stale + granules(p.t.stale + b * V, 4).off);
+            const float* cost = reinterpret_cast<const float*>(ib + IL.cost + granules(p.t.cost + b * V * nG, 4).off);
+            const float* post = reinterpret_cast<const float*>(ib + IL.post + granules(p.t.post + b * V * nG, 4).off);
+            const uint16_t* lmu =
+                reinterpret_cast<const uint16_t*>(ib + IL.lmu + granules(p.t.lam_min_units + b * V * nL, 2).off);
+            const float* lf = reinterpret_cast<const float*>(ib + IL.lf + granules(p.t.lam_factor + b * V * nL, 4).off);
+            const int v = idx;
+            // stream v's profile into the warp's StreamIn, with its R-ERR checks
+            const float st = stale[v];
+            bool vok = in01(st);
+            float c = 0.0f;
+            if (lane < nG) {
+                c = cost[v * nG + lane];
+                const float po = post[v * nG + lane];
+                if (!(c >= 0.0f)) vok = false;
+                else if (!isinf(c)) vok &= in01(po);
+                si->cpd[lane] = make_float4(c, po, fsub(po, st), 0.0f);
+            }
+            if (lane < nL) {
+                const float f = lf[v * nL + lane];
+                const uint16_t mu = lmu[v * nL + lane];
+                if (mu != kLmuPad) vok &= in01(f);
+                si->lf[lane] = f;
+                si->lmu[lane] = mu;
+            }
+            const bool allok = __all_sync(0xffffffffu, vok);
+            const unsigned fastm = __ballot_sync(0xffffffffu, lane >= nG || fast_dividend(c));
+            if (lane == 0) {
+                si->stale = st;
+                si->fast = fastm == 0xffffffffu;
+                if (!allok) {
+                    bad[k] = (int)(i + 1);
+                    flag_data_error(p.st);
+                }
+            }
+            __syncwarp();
+            unsigned char* tv = smem + L.tabs + k * L.tabset + v * tb;
+            warp_build_tables<19, kL2G, kL2L, kListRow, 8>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
+                                                          reinterpret_cast<unsigned long long*>(tv + 96), 0, U + 1,
+                                                          true);
+            mbar_arrive(&full[i & 7]);
+        } else {
+            const long long i = ph - 1;
+            if (i < 0) continue;
+            const int k = (int)(i & 1);
+            mbar_wait_sleep(&full[i & 7], (unsigned)((i >> 3) & 1));
+            if (idx == 0 && lane == 0 && i + 2 < n)   // instance i's tables are complete: buffer k is free
+                issue_inputs(b0 + (i + 2) * g, k);
+            const bool ok = bad[k] != (int)(i + 1);
+            const long long b = b0 + i * g;
+            const unsigned char* tabs = smem + L.tabs + k * L.tabset;
+            // the task's rows (contiguous) into the warp's buffer by one bulk copy
+            const int rb = idx * RT, nr = min(RT, N - rb);
+            const long long o0 = b * N + rb;   // first row of the task
+            const uintptr_t ga = reinterpret_cast<uintptr_t>(p.alloc) + (uintptr_t)o0 * (2 * V * 2);
+            const unsigned off = (unsigned)(ga & 15u), bytes = (off + (unsigned)nr * (2 * V * 2) + 15u) & ~15u;
+            if (lane == 0) {
+                mbar_arrive_expect_tx(rbar, bytes);
+                bulk_g2s(rbuf, reinterpret_cast<const void*>(ga - off), bytes, rbar);
+            }
+            mbar_wait_sleep(rbar, rphase & 1u);
+            ++rphase;
+            const uint2* rows = reinterpret_cast<const uint2*>(rbuf + off);
+            if (lane < nr) list2_row(p, tabs, ok, o0 + lane, rows + lane * (V / 2));
+            if (lane + 32 < nr) list2_row(p, tabs, ok, o0 + lane + 32, rows + (lane + 32) * (V / 2));
+            __syncwarp();   // every lane's reads of the buffer precede the next task's copy
+            mbar_arrive(&empty[i & 7]);
+        }
+    }
+}
+
 int resident_grid(ekya_handle* h, const void* fn, int threads, size_t smem, long long work) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
@@ -695,6 +983,36 @@ int launch_eval_list(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, i
     size_t smem = p.L.total;
     if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
     if (d.n_inst == 0 || n_alloc == 0) return EKYA_OK;
+    // the paper's shape with 8-byte aligned rows and 2-byte aligned config output: the
+    // barrier-free pipeline (list2_kernel), its task counter bounded by 2^32
+    const long long per_cta = (d.n_inst + h->sm_count - 1) / h->sm_count;
+    const int chunks = (n_alloc + kL2Rows - 1) / kL2Rows;
+    if (fast && p.L.ntabs == 2 && !(reinterpret_cast<uintptr_t>(alloc) & 7) &&
+        !(reinterpret_cast<uintptr_t>(out_cfg) & 1) && (per_cta + 1) * (long long)(chunks + 10) < (1LL << 32) &&
+        !getenv("EKYA_LIST_V1")) {
+        List2Params q{};
+        q.d = d;
+        q.t = t;
+        q.st = h->dstate;
+        q.n_alloc = n_alloc;
+        q.alloc = alloc;
+        q.out_sum = p.out_sum;
+        q.out_mean = out_mean;
+        q.out_cfg = out_cfg;
+        q.L = p.L;
+        q.IL = p.IL;
+        q.rcp_v = p.rcp_v;
+        q.chunks = chunks;
+        q.rowbuf = a16(smem);
+        smem = q.rowbuf + (size_t)kL2RowBuf * (kListThreads / 32);
+        if (smem > h->smem_optin) return EKYA_ERR_SHAPE;
+        cudaError_t e2 = cudaFuncSetAttribute(list2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e2 != cudaSuccess) return EKYA_ERR_CUDA;
+        const int grid = (int)std::min<long long>(h->sm_count, d.n_inst);
+        list2_kernel<<<grid, kListThreads, smem, s>>>(q);
+        h->launches++;
+        return cuda_status(cudaGetLastError());
+    }
     auto kern = fast ? list_kernel<19, 10, 18, 5, kFastU>
                      : pick_gm(d.n_gamma, list_kernel<8, 0, 0, 0, 0>, list_kernel<16, 0, 0, 0, 0>,
                                list_kernel<19, 0, 0, 0, 0>, list_kernel<24, 0, 0, 0, 0>, list_kernel<32, 0, 0, 0, 0>);

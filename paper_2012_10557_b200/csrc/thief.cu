@@ -144,42 +144,52 @@ struct InstView {
 // IEEE division off the hot path (the exact shared-reciprocal path covers the paper's shapes)
 __device__ __noinline__ float fdiv_cold(float a, float b) { return __fdiv_rn(a, b); }
 
-// Warp-collective, once per stream: lambda* ladder (Alg. 2 lines 3-4, rule 3).
+// lambda* ladder of stream v (Alg. 2 lines 3-4, rule 3), one lane per stream.
 // lambda*(ri) depends only on the admissible set {l : t_l <= ri} (t_l = lmu_l if
 // fl(stale f_l) >= a_MIN, else never), which equals the set at the largest
 // t_l <= ri; so the thresholds are stored ascending (ties: lambda order) with
 // lambda*(t) and its factor, and F(ri) is the entry of the last threshold <= ri.
-__device__ void init_ladder(const InstView& in, const WarpState& S, int v, const ekya_dims& d) {
-    const int lane = threadIdx.x & 31, nL = d.n_lambda;
-    unsigned t = 0xFFFFu;
-    float acc = 0.0f, f = 0.0f;
-    if (lane < nL) {
-        const uint16_t m = in.lmu[(size_t)v * nL + lane];
-        f = in.lf[(size_t)v * nL + lane];
-        acc = fmul(in.stale[v], f);
-        if (m != kLmuPad && acc >= d.a_min) t = m;
-    }
-    // lambda*(t) over {l : t_l <= t}: highest accuracy, lowest index on ties
-    int best = -1, rank = 0;
-    float bacc = 0.0f;
-#pragma unroll 1
-    for (int l = 0; l < nL; ++l) {
-        const unsigned tl = __shfl_sync(FULL, t, l);
-        const float al = __shfl_sync(FULL, acc, l);
-        if (tl <= t && (best < 0 || al > bacc)) {
-            best = l;
-            bacc = al;
+// Slot rank(l) = #{l' : (t_l', l') < (t_l, l)}; slots nL..7 stay unused (0xFFFF).
+__device__ __forceinline__ void init_ladder_lane(const InstView& in, const WarpState& S, int v, const ekya_dims& d) {
+    const int nL = d.n_lambda;
+    unsigned t[kMaxLambda];
+    float acc[kMaxLambda], f[kMaxLambda];
+    const float st = in.stale[v];
+#pragma unroll
+    for (int l = 0; l < kMaxLambda; ++l) {
+        t[l] = 0xFFFFu;
+        acc[l] = 0.0f;
+        f[l] = 0.0f;
+        if (l < nL) {
+            const uint16_t m = in.lmu[(size_t)v * nL + l];
+            f[l] = in.lf[(size_t)v * nL + l];
+            acc[l] = fmul(st, f[l]);
+            if (m != kLmuPad && acc[l] >= d.a_min) t[l] = m;
         }
-        rank += (tl < t || (tl == t && l < lane)) ? 1 : 0;
     }
-    const float fb = __shfl_sync(FULL, f, best < 0 ? 0 : best);
-    // unused / inadmissible lambdas sort last (t = 0xFFFF) and are never reached
-    const int pos = lane < nL ? rank : lane;
-    if (lane < 8) {
-        unsigned short* th = reinterpret_cast<unsigned short*>(S.lthr + v);
-        th[pos] = (unsigned short)t;
-        S.lfac[v * 8 + pos] = fb;
-        S.lidx[v * 8 + pos] = (signed char)best;
+    unsigned short* th = reinterpret_cast<unsigned short*>(S.lthr + v);
+#pragma unroll
+    for (int p = 0; p < 8; ++p) th[p] = 0xFFFFu;
+#pragma unroll
+    for (int l = 0; l < kMaxLambda; ++l) {
+        if (l < nL) {
+            // lambda*(t_l) over {l' : t_l' <= t_l}: highest accuracy, lowest index on ties
+            int best = 0, rank = 0;
+            float bacc = -1.0f, fb = 0.0f;
+#pragma unroll
+            for (int l2 = 0; l2 < kMaxLambda; ++l2) {
+                if (l2 < nL) {
+                    const bool take = t[l2] <= t[l] && acc[l2] > bacc;
+                    best = take ? l2 : best;
+                    fb = take ? f[l2] : fb;
+                    bacc = take ? acc[l2] : bacc;
+                    rank += (t[l2] < t[l] || (t[l2] == t[l] && l2 < l)) ? 1 : 0;
+                }
+            }
+            th[rank] = (unsigned short)t[l];
+            S.lfac[v * 8 + rank] = fb;
+            S.lidx[v * 8 + rank] = (signed char)best;
+        }
     }
 }
 
@@ -412,7 +422,7 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
         S.alloc[2 * v] = share - rt;
     }
 #pragma unroll 1
-    for (int v = 0; v < V; ++v) init_ladder(in, S, v, d);
+    for (int v = lane; v < V; v += 32) init_ladder_lane(in, S, v, d);
 #pragma unroll 1
     for (int i = lane; i < V * (nsm + 1); i += 32) S.gc[i] = make_uint2(0xFFFFFFFFu, 0u);
     __syncwarp();
@@ -431,20 +441,27 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
         const unsigned max_steps = 1u << 26;
         for (;;) {
             // per-stream best down, top-2 by stream
-            unsigned long long k1 = 0;
-            for (int v = lane; v < V; v += 32) {
-                const unsigned long long k = stream_down_key(S, v);
-                k1 = k > k1 ? k : k1;
+            unsigned long long k1 = 0, k2 = 0;
+            int s1;
+            if (V <= 32) {   // one stream per lane: its key serves both reductions
+                const unsigned long long k = lane < V ? stream_down_key(S, lane) : 0ULL;
+                k1 = warp_max_u64(k);
+                s1 = k1 ? (key_job(k1) >> 1) : -1;
+                k2 = warp_max_u64(lane == s1 ? 0ULL : k);
+            } else {
+                for (int v = lane; v < V; v += 32) {
+                    const unsigned long long k = stream_down_key(S, v);
+                    k1 = k > k1 ? k : k1;
+                }
+                k1 = warp_max_u64(k1);
+                s1 = k1 ? (key_job(k1) >> 1) : -1;
+                for (int v = lane; v < V; v += 32) {
+                    if (v == s1) continue;
+                    const unsigned long long k = stream_down_key(S, v);
+                    k2 = k > k2 ? k : k2;
+                }
+                k2 = warp_max_u64(k2);
             }
-            k1 = warp_max_u64(k1);
-            const int s1 = k1 ? (key_job(k1) >> 1) : -1;
-            unsigned long long k2 = 0;
-            for (int v = lane; v < V; v += 32) {
-                if (v == s1) continue;
-                const unsigned long long k = stream_down_key(S, v);
-                k2 = k > k2 ? k : k2;
-            }
-            k2 = warp_max_u64(k2);
             // per thief: best victim, then argmax over thieves
             unsigned long long bestkey = 0;
             int bestw = -1;
