@@ -28,6 +28,7 @@
 // unchanged, exactly as the sequential loop -- then the steal chain on that
 // victim, then the scan resumes after it.
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 
 #include "launch.h"
@@ -74,6 +75,10 @@ struct ThiefParams {
 //            direct-mapped cache of NS (rt, value) slots, filled on a miss.
 // A step re-evaluates the two touched streams with one lane per record entry
 // (lanes 8k + e, e < 7), i.e. 14 lanes in one pass.
+// STEEPEST selects from per-stream keys (skey) above this stream count; at or below it one
+// lane per thief job evaluates every candidate directly (J <= 32: one pass, cheaper)
+constexpr int kKeyPathV = 16;
+
 struct WarpState {
     long long* rec;              // [V][8]
     int* alloc;                  // [J]
@@ -81,28 +86,32 @@ struct WarpState {
     float* lfac;                 // [V][8] factor of lambda* at the threshold
     signed char* lidx;           // [V][8] index of lambda* at the threshold
     uint2* gc;                   // [V][NS] G* cache: (rt, value bits), rt = 0xFFFFFFFF empty
+    unsigned long long* skey;    // [V][4] the stream's best down / up / move key (0 = none)
     __device__ __forceinline__ long long cur(int v) const { return rec[v * 8]; }
     __device__ __forceinline__ long long up(int j) const { return rec[(j >> 1) * 8 + 1 + (j & 1)]; }
     __device__ __forceinline__ long long dn(int j) const { return rec[(j >> 1) * 8 + 3 + (j & 1)]; }
     __device__ __forceinline__ long long mv(int j) const { return rec[(j >> 1) * 8 + 6 - (j & 1)]; }
 };
 
-__host__ __device__ inline size_t thief_warp_bytes(int V, int NS) {
+__host__ __device__ inline size_t thief_warp_bytes(int V, int NS, bool keys) {
     const size_t J = 2 * (size_t)V;
     size_t b = 8 * 8 * (size_t)V + 4 * J + 16 * (size_t)V + 4 * 8 * (size_t)V + 8 * (size_t)V +
                8 * (size_t)NS * (size_t)V;
+    if (keys) b = ((b + 7) & ~size_t(7)) + 32 * (size_t)V;   // skey (STEEPEST, V > kKeyPathV)
     return (b + 15) & ~size_t(15);
 }
 
 __device__ inline WarpState carve(unsigned char* base, int V, int NS) {
     const int J = 2 * V;
     WarpState w;
-    w.rec = reinterpret_cast<long long*>(base);                        // 8-byte aligned
-    w.gc = reinterpret_cast<uint2*>(w.rec + 8 * V);                    // 8-byte aligned
+    w.rec = reinterpret_cast<long long*>(base);                        // 16-byte aligned
+    w.gc = reinterpret_cast<uint2*>(w.rec + 8 * V);                    // 16-byte aligned
     w.lthr = reinterpret_cast<uint4*>(w.gc + (size_t)NS * V);          // 16-byte aligned (NS even)
     w.lfac = reinterpret_cast<float*>(w.lthr + V);
     w.alloc = reinterpret_cast<int*>(w.lfac + 8 * V);
     w.lidx = reinterpret_cast<signed char*>(w.alloc + J);
+    w.skey = reinterpret_cast<unsigned long long*>(
+        (reinterpret_cast<uintptr_t>(w.lidx + 8 * V) + 7) & ~uintptr_t(7));   // V > kKeyPathV only
     return w;
 }
 
@@ -254,6 +263,7 @@ __device__ __forceinline__ float gstar_lane(const InstView& in, int v, int r, co
 // Warp-collective: record entries of up to four streams s0..s3 (-1 = none), lane 8k + e
 // computing entry e of stream s_k at its split: e = 0 cur (rt,ri), 1 (rt,ri+D),
 // 2 (rt+D,ri), 3 (rt,ri-D), 4 (rt-D,ri), 5 (rt+D,ri-D), 6 (rt-D,ri+D).
+template <int MODE>
 __device__ __forceinline__ void update_streams(const InstView& in, const WarpState& S, int s0, int s1, int s2,
                                                int s3, const ekya_dims& d, bool fast, int nsm) {
     const int lane = threadIdx.x & 31, D = d.steal_units;
@@ -294,6 +304,24 @@ __device__ __forceinline__ void update_streams(const InstView& in, const WarpSta
     const long long val = F < 0.0f ? 0LL : (long long)q32(fmul(F, G));
     const long long c = __shfl_sync(FULL, val, lane & ~7);
     if (act) S.rec[s * 8 + e] = e == 0 ? c : (valid ? val - c : kInvalid);
+    __syncwarp();
+    // the stream's best steal keys (STEEPEST's selection reads only these), lane k for s_k
+    if (MODE == EKYA_THIEF_STEEPEST && d.n_streams > kKeyPathV && lane < 4) {
+        const int sk = lane == 0 ? s0 : lane == 1 ? s1 : lane == 2 ? s2 : s3;
+        if (sk >= 0) {
+            const long long* r = S.rec + sk * 8;
+            const int j0 = 2 * sk, j1 = j0 + 1;
+            unsigned long long dk = 0, uk, mk = 0;
+            if (r[3] != kInvalid) dk = dkey(r[3], j0);
+            if (r[4] != kInvalid) dk = max(dk, dkey(r[4], j1));
+            uk = max(dkey(r[1], j0), dkey(r[2], j1));
+            if (r[6] != kInvalid) mk = dkey(r[6], j0);   // thief = inference job j0
+            if (r[5] != kInvalid) mk = max(mk, dkey(r[5], j1));
+            S.skey[sk * 4] = dk;
+            S.skey[sk * 4 + 1] = uk;
+            S.skey[sk * 4 + 2] = mk;
+        }
+    }
     __syncwarp();
 }
 
@@ -343,6 +371,7 @@ __device__ __forceinline__ bool lit_cond(const WarpState& S, int t, int w, int J
     const long long dn = S.dn(w);
     return dn != kInvalid && S.up(t) + dn > 0;
 }
+
 
 __device__ __forceinline__ unsigned long long stream_down_key(const WarpState& S, int v) {
     unsigned long long k = 0;
@@ -434,75 +463,136 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
     }
     __syncwarp();
     for (int v = 0; v < V; v += 4)
-        update_streams(in, S, v, v + 1 < V ? v + 1 : -1, v + 2 < V ? v + 2 : -1, v + 3 < V ? v + 3 : -1, d, fast, nsm);
+        update_streams<MODE>(in, S, v, v + 1 < V ? v + 1 : -1, v + 2 < V ? v + 2 : -1, v + 3 < V ? v + 3 : -1, d, fast, nsm);
 
     unsigned steps = 0;
     if (MODE == EKYA_THIEF_STEEPEST) {
+        // Best single steal (C12) from per-stream keys.  For thief t the candidates are the
+        // cross-stream steal from the best victim outside its stream (the top-2 down keys by
+        // stream, K1 / K2) and the move with its sibling; its value is the larger of the two.
+        // Maximising dkey(value, t) over t splits into: thieves outside K1's stream s1, whose
+        // best is the best up key outside s1 (top-2 up keys by stream, U1 / U2) shifted by
+        // K1's delta; s1's two jobs with K2; and the best move key M.  Ties resolve as the
+        // per-thief scan does (dkey order: larger delta, then lower job index; the victim of
+        // the chosen thief by the same rule as before).
         const unsigned max_steps = 1u << 26;
-        for (;;) {
-            // per-stream best down, top-2 by stream
-            unsigned long long k1 = 0, k2 = 0;
-            int s1;
-            if (V <= 32) {   // one stream per lane: its key serves both reductions
-                const unsigned long long k = lane < V ? stream_down_key(S, lane) : 0ULL;
-                k1 = warp_max_u64(k);
-                s1 = k1 ? (key_job(k1) >> 1) : -1;
-                k2 = warp_max_u64(lane == s1 ? 0ULL : k);
-            } else {
-                for (int v = lane; v < V; v += 32) {
-                    const unsigned long long k = stream_down_key(S, v);
-                    k1 = k > k1 ? k : k1;
+        if (V <= kKeyPathV) {
+            for (;;) {
+                // per-stream best down, top-2 by stream
+                unsigned long long k1 = 0, k2 = 0;
+                int s1;
+                if (V <= 32) {   // one stream per lane: its key serves both reductions
+                    const unsigned long long k = lane < V ? stream_down_key(S, lane) : 0ULL;
+                    k1 = warp_max_u64(k);
+                    s1 = k1 ? (key_job(k1) >> 1) : -1;
+                    k2 = warp_max_u64(lane == s1 ? 0ULL : k);
+                } else {
+                    for (int v = lane; v < V; v += 32) {
+                        const unsigned long long k = stream_down_key(S, v);
+                        k1 = k > k1 ? k : k1;
+                    }
+                    k1 = warp_max_u64(k1);
+                    s1 = k1 ? (key_job(k1) >> 1) : -1;
+                    for (int v = lane; v < V; v += 32) {
+                        if (v == s1) continue;
+                        const unsigned long long k = stream_down_key(S, v);
+                        k2 = k > k2 ? k : k2;
+                    }
+                    k2 = warp_max_u64(k2);
                 }
-                k1 = warp_max_u64(k1);
-                s1 = k1 ? (key_job(k1) >> 1) : -1;
-                for (int v = lane; v < V; v += 32) {
-                    if (v == s1) continue;
-                    const unsigned long long k = stream_down_key(S, v);
-                    k2 = k > k2 ? k : k2;
-                }
-                k2 = warp_max_u64(k2);
-            }
-            // per thief: best victim, then argmax over thieves
-            unsigned long long bestkey = 0;
-            int bestw = -1;
-            for (int t = lane; t < J; t += 32) {
-                const unsigned long long ck = ((t >> 1) != s1) ? k1 : k2;
-                bool have = false;
-                long long tot = 0;
-                int w = -1;
-                if (ck) {
-                    tot = S.up(t) + key_delta(ck);
-                    w = key_job(ck);
-                    have = true;
-                }
-                const long long m = S.mv(t);
-                if (m != kInvalid) {
-                    const int ws = t ^ 1;
-                    if (!have || m > tot || (m == tot && ws < w)) {
-                        tot = m;
-                        w = ws;
+                // per thief: best victim, then argmax over thieves
+                unsigned long long bestkey = 0;
+                int bestw = -1;
+                for (int t = lane; t < J; t += 32) {
+                    const unsigned long long ck = ((t >> 1) != s1) ? k1 : k2;
+                    bool have = false;
+                    long long tot = 0;
+                    int w = -1;
+                    if (ck) {
+                        tot = S.up(t) + key_delta(ck);
+                        w = key_job(ck);
                         have = true;
                     }
-                }
-                if (have) {
-                    const unsigned long long tk = dkey(tot, t);
-                    if (tk > bestkey) {
-                        bestkey = tk;
-                        bestw = w;
+                    const long long m = S.mv(t);
+                    if (m != kInvalid) {
+                        const int ws = t ^ 1;
+                        if (!have || m > tot || (m == tot && ws < w)) {
+                            tot = m;
+                            w = ws;
+                            have = true;
+                        }
+                    }
+                    if (have) {
+                        const unsigned long long tk = dkey(tot, t);
+                        if (tk > bestkey) {
+                            bestkey = tk;
+                            bestw = w;
+                        }
                     }
                 }
+                const unsigned long long gk = warp_max_u64(bestkey);
+                if (gk == 0 || key_delta(gk) <= 0) break;
+                const int t = key_job(gk);
+                const unsigned owner = __ballot_sync(FULL, bestkey == gk);
+                const int w = __shfl_sync(FULL, bestw, __ffs(owner) - 1);
+                if (lane == 0) {
+                    S.alloc[w] -= D;
+                    S.alloc[t] += D;
+                }
+                __syncwarp();
+                update_streams<MODE>(in, S, t >> 1, (w >> 1) != (t >> 1) ? (w >> 1) : -1, -1, -1, d, fast, nsm);
+                if (++steps >= max_steps) {
+                    if (lane == 0) flag_data_error(p.st);
+                    break;
+                }
             }
-            const unsigned long long gk = warp_max_u64(bestkey);
+        } else
+        for (;;) {
+            unsigned long long d1 = 0, d2 = 0, u1 = 0, u2 = 0, mb = 0;
+            int ds1 = -1, us1 = -1;
+            for (int v = lane; v < V; v += 32) {   // this lane's streams: partial top-2 by stream
+                const unsigned long long dk = S.skey[v * 4], uk = S.skey[v * 4 + 1], mk = S.skey[v * 4 + 2];
+                if (dk > d1) { d2 = d1; d1 = dk; ds1 = v; } else if (dk > d2) { d2 = dk; }
+                if (uk > u1) { u2 = u1; u1 = uk; us1 = v; } else if (uk > u2) { u2 = uk; }
+                mb = mk > mb ? mk : mb;
+            }
+            const unsigned long long K1 = warp_max_u64(d1);
+            const int s1 = K1 ? (key_job(K1) >> 1) : -1;
+            const unsigned long long K2 = warp_max_u64(ds1 == s1 ? d2 : d1);
+            const unsigned long long U1 = warp_max_u64(u1);
+            const int su = U1 ? (key_job(U1) >> 1) : -1;
+            const unsigned long long U2 = warp_max_u64(us1 == su ? u2 : u1);
+            unsigned long long gk = warp_max_u64(mb);
+            if (K1) {
+                const unsigned long long UK = su != s1 ? U1 : U2;
+                if (UK) {
+                    const unsigned long long c = dkey(key_delta(UK) + key_delta(K1), key_job(UK));
+                    gk = c > gk ? c : gk;
+                }
+            }
+            if (K2) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int t = 2 * s1 + h;
+                    const unsigned long long c = dkey(S.up(t) + key_delta(K2), t);
+                    gk = c > gk ? c : gk;
+                }
+            }
             if (gk == 0 || key_delta(gk) <= 0) break;
             const int t = key_job(gk);
-            const unsigned owner = __ballot_sync(FULL, bestkey == gk);
-            const int w = __shfl_sync(FULL, bestw, __ffs(owner) - 1);
+            // the victim of thief t: its best cross-stream victim, or its sibling (move) when
+            // that is strictly better or equal with the lower job index
+            const unsigned long long ck = (t >> 1) != s1 ? K1 : K2;
+            int w = ck ? key_job(ck) : -1;
+            const long long tot = ck ? S.up(t) + key_delta(ck) : 0;
+            const long long m = S.mv(t);
+            if (m != kInvalid && (!ck || m > tot || (m == tot && (t ^ 1) < w))) w = t ^ 1;
             if (lane == 0) {
                 S.alloc[w] -= D;
                 S.alloc[t] += D;
             }
             __syncwarp();
-            update_streams(in, S, t >> 1, (w >> 1) != (t >> 1) ? (w >> 1) : -1, -1, -1, d, fast, nsm);
+            update_streams<MODE>(in, S, t >> 1, (w >> 1) != (t >> 1) ? (w >> 1) : -1, -1, -1, d, fast, nsm);
             if (++steps >= max_steps) {
                 if (lane == 0) flag_data_error(p.st);
                 break;
@@ -524,7 +614,7 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
                         S.alloc[t] += D;
                     }
                     __syncwarp();
-                    update_streams(in, S, t >> 1, (w >> 1) != (t >> 1) ? (w >> 1) : -1, -1, -1, d, fast, nsm);
+                    update_streams<MODE>(in, S, t >> 1, (w >> 1) != (t >> 1) ? (w >> 1) : -1, -1, -1, d, fast, nsm);
                     ++steps;
                 } while (lit_cond(S, t, w, J));
                 pos = w + 1;
@@ -562,10 +652,13 @@ int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int m
     p.out_sum = reinterpret_cast<unsigned long long*>(out_sum);
     p.out_mean = out_mean;
     p.out_steps = out_steps;
-    // G* cache: 32 slots per stream for the paper's stream counts, fewer for wide instances
-    const int ns = d.n_streams <= 16 ? 32 : 8;
+    // G* cache: 32 slots per stream for the paper's stream counts; wide instances keep fewer
+    // so that the shared-memory carve-out leaves L1 room for the unstaged profile tables
+    // (config-5 shape, 16,384 instances: STEEPEST 5.53 ms at 8 slots, 4.17 at 4, 4.99 at 2;
+    // LITERAL 10.44 at 8, 10.57 at 4, 13.9 at 16)
+    const int ns = d.n_streams <= 16 ? 32 : (mode == EKYA_THIEF_STEEPEST ? 4 : 8);
     p.nsm = ns - 1;
-    p.state_bytes = thief_warp_bytes(d.n_streams, ns);
+    p.state_bytes = thief_warp_bytes(d.n_streams, ns, mode == EKYA_THIEF_STEEPEST && d.n_streams > kKeyPathV);
     const size_t tbytes = ((size_t)d.n_streams * (4 * d.n_gamma + 1) * 4 + 15) & ~size_t(15);
     p.stage = tbytes <= 8192;
     p.warp_bytes = p.state_bytes + (p.stage ? tbytes : 0);
