@@ -853,6 +853,25 @@ def test_pareto_invalid_data_and_empty_input():
         oracle.pareto(np.zeros((3, 0), np.float32), np.zeros((3, 0), np.float32))
 
 
+def test_prune_reading_vs_spec_example():
+    """PN1 measures distance from the Pareto boundary VERTICALLY (accuracy gap at the config's
+    cost), not as SPEC.md's relative cost distance.  P:1179-1180 fixes neither
+    ("significantly distant from the configurations on the Pareto curve").  Consequence,
+    pinned: SPEC's example (a config matched in accuracy by one 10x cheaper in every
+    window, margin 0.5) is KEPT here -- its accuracy gap is 0 -- while a config whose accuracy
+    falls below the boundary by more than the margin in most windows is dropped whatever its
+    cost ratio."""
+    c = np.array([[1.0, 10.0]], np.float32)
+    A = np.array([[[.6, .6], [.7, .7], [.5, .5]]], np.float32)
+    assert int(oracle.prune(c, A, 0.5)[0][0]) == 0b11     # S:132's drop is not this reading's
+    A2 = np.array([[[.6, .4], [.7, .5], [.5, .3]]], np.float32)
+    assert int(oracle.prune(c, A2, 0.15)[0][0]) == 0b01   # gap .2 > .15 in 3/3 windows
+    assert int(oracle.prune(c, A2, 0.25)[0][0]) == 0b11   # gap .2 <= .25: kept
+    # a costlier config ABOVE the cheaper one's accuracy is on the boundary: gap 0
+    A3 = np.array([[[.5, .9], [.5, .9], [.5, .9]]], np.float32)
+    assert int(oracle.prune(c, A3, 0.0)[0][0]) == 0b11
+
+
 def test_prune_worked_examples():
     """PN1-PN3 on hand-worked cases: costs 1, 2, 3 and three windows.
     w0 = (.5, .7, .6): config 2 sits .1 below the boundary (.7 at cost <= 3); w1 = (.6,

@@ -9,8 +9,10 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-NAMES = [("cluster2_kernel", "profile_cluster"), ("cluster_kernel", "profile_cluster"),
-         ("radius_kernel", "profile_radius"), ("grid_kernel", "eval_grid"), ("list_kernel", "eval_list"),
+# the bench's A1 launch: cluster2_kernel computes both estimates (fused); older captures ran
+# CLUSTER alone (PROFILE_ROW=profile_cluster)
+NAMES = [("cluster2_kernel", os.environ.get("PROFILE_ROW", "profile")), ("cluster_kernel", "profile_cluster"),
+         ("radius_kernel", "profile_radius"), ("grid_kernel", "eval_grid"), ("list_kernel", "eval_list"), ("list2_kernel", "eval_list"),
          ("thief_kernel<0>", "thief_steepest"), ("thief_kernel<1>", "thief_literal"),
          ("curve_fit_kernel", "next2_curve_fit"), ("uniform_kernel", "next3_uniform"),
          ("pareto_kernel", "next3_pareto"), ("prune_", "next3_prune"), ("place_kernel", "next4_placement"),
@@ -99,7 +101,7 @@ def main(ev, tag):
           "|---|---|---|---|---|---|---|---|"]
     step_ms = bench["ms_per_step"]
     fd = {n: d for n, d in full}
-    for n in ["profile_cluster", "profile_radius", "eval_grid", "eval_list", "thief_steepest", "thief_literal",
+    for n in ["profile", "profile_cluster", "profile_radius", "eval_grid", "eval_list", "thief_steepest", "thief_literal",
               "next2_curve_fit", "next3_uniform", "next3_pareto", "next3_prune", "next4_placement", "next4_checkpoint"]:
         ms = per.get(n, [])
         nm = sum(ms) / len(ms) if ms else float("nan")
