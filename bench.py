@@ -2,7 +2,7 @@
 """bench.py -- Ekya thief-scheduler hot path on B200 (driver contract: one JSON line).
 
 A step = one pass of the whole hot path over one batch:
-  A1  ekya_profile_estimate on config 3 (65,536 Waymo-shaped queries, C=27,
+  A1  ekya_profile_estimate_both on config 3 (65,536 Waymo-shaped queries, C=27,
       H=500, |Gamma|=18) in CLUSTER mode (BASELINE config 3: "5-cluster
       similarity estimate") and RADIUS mode (north star: distance threshold);
   A3  ekya_eval_allocations GRID and LIST (4,096 allocations per instance) on
@@ -183,13 +183,22 @@ def run_step(ek, h, w, T, rows, P, O, timer=None):
     dims = ek.dims_from(T, *w.args)
     tabs = ek.make_tables(**T)
     p = w.pcfg
-    steps = [
-        ("profile_cluster", lambda: ek.ekya_profile_estimate(
+    steps = []
+    if os.environ.get("EKYA_BENCH_PROFILE_UNFUSED"):   # A/B: the two modes as separate launches
+        steps += [
+            ("profile_cluster", lambda: ek.ekya_profile_estimate(
+                h, ek.ProfileDims(w.Q, p.n_hist, p.n_class, p.n_gamma, ek.PROFILE_CLUSTER, p.tau, p.k, p.max_iter),
+                P["cur"], P["hist"], P["hist_acc"], P["fallback"], O.est[1], O.n[1])),
+            ("profile_radius", lambda: ek.ekya_profile_estimate(
+                h, ek.ProfileDims(w.Q, p.n_hist, p.n_class, p.n_gamma, ek.PROFILE_RADIUS, p.tau, p.k, p.max_iter),
+                P["cur"], P["hist"], P["hist_acc"], P["fallback"], O.est[0], O.n[0]))]
+    else:
+        # A1: both estimates (RADIUS tau = 0.2 and CLUSTER k = 5) from ONE pass over each query's
+        # history tile (ekya_profile_estimate_both)
+        steps += [("profile", lambda: ek.ekya_profile_estimate_both(
             h, ek.ProfileDims(w.Q, p.n_hist, p.n_class, p.n_gamma, ek.PROFILE_CLUSTER, p.tau, p.k, p.max_iter),
-            P["cur"], P["hist"], P["hist_acc"], P["fallback"], O.est[1], O.n[1])),
-        ("profile_radius", lambda: ek.ekya_profile_estimate(
-            h, ek.ProfileDims(w.Q, p.n_hist, p.n_class, p.n_gamma, ek.PROFILE_RADIUS, p.tau, p.k, p.max_iter),
-            P["cur"], P["hist"], P["hist_acc"], P["fallback"], O.est[0], O.n[0])),
+            P["cur"], P["hist"], P["hist_acc"], P["fallback"], O.est[0], O.n[0], O.est[1], O.n[1]))]
+    steps += [
         ("eval_grid", lambda: ek.ekya_eval_allocations(h, dims, tabs, ek.EVAL_GRID, out_grid=O.grid,
                                                        out_grid_cfg=O.grid_cfg)),
         ("eval_list", lambda: ek.ekya_eval_allocations(h, dims, tabs, ek.EVAL_LIST, w.N, rows, O.lsum,
@@ -477,7 +486,7 @@ def run_ours(args, rank, world, local_rank):
     value = total_units / (ms / 1000.0)
     rows_out = {}
     bytes_of = {"eval_grid": w.grid_bytes(), "eval_list": w.list_bytes(), "profile_radius": w.profile_bytes(),
-                "profile_cluster": w.profile_bytes(), "thief_steepest": w.thief_bytes(),
+                "profile_cluster": w.profile_bytes(), "profile": w.profile_bytes(), "thief_steepest": w.thief_bytes(),
                 "thief_literal": w.thief_bytes()}
     pc = w.pcfg
     cluster_flops = lloyd_passes / max(1, args.steps) * pc.n_hist * pc.k * pc.n_class * 3
@@ -491,13 +500,15 @@ def run_ours(args, rank, world, local_rank):
             r["hbm_frac"] = gbs / peak
             roof[k] = {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                        "peak_source": peak_kind, "algorithmic_bytes_per_launch": bytes_of[k]}
-        if k == "profile_cluster":
-            tfs = cluster_flops / (avg / 1000.0) / 1e12
+        if k in ("profile_cluster", "profile"):
+            # CLUSTER's Lloyd distances (+ the fused RADIUS distances: one per window, H C 3 flop)
+            fl = cluster_flops + (w.Q * pc.n_hist * pc.n_class * 3 if k == "profile" else 0)
+            tfs = fl / (avg / 1000.0) / 1e12
             r["algorithmic_tflop_per_s"] = tfs
             r["alu_frac"] = tfs / alu_peak
             r["lloyd_passes_per_query"] = lloyd_passes / max(1, args.steps) / w.Q
             roof[k] = {"bound": "alu", "achieved": tfs, "peak": alu_peak, "unit": "TFLOP/s", "frac": tfs / alu_peak,
-                       "peak_source": alu_src, "algorithmic_flops_per_launch": cluster_flops}
+                       "peak_source": alu_src, "algorithmic_flops_per_launch": fl}
         if k in insts:
             # issue-slot utilisation: warp instructions per launch (ncu sm__inst_executed.sum of the
             # same launch, profiles/round2_inst.json) / (4 issue slots x 148 SMs x clock x time)

@@ -181,6 +181,17 @@ int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p,
                           const float* cur, const float* hist, const float* hist_acc,
                           const float* fallback, float* out_est, int32_t* out_n,
                           int32_t* out_cluster, ekya_stream_t stream);
+/* Both estimates of the same queries (p->mode is ignored; tau, k and max_iter are all
+ * used): out_est_radius / out_n_radius exactly as mode 0, out_est_cluster /
+ * out_n_cluster / out_cluster exactly as mode 1.  For k = 5, C = 27, H <= 512 (the
+ * paper's Waymo shape) one kernel computes both from a single read of each query's
+ * history tile; other shapes run the two modes back to back.  Same limits and errors as
+ * ekya_profile_estimate; every output array is [Q][G] (out_cluster as in mode 1). */
+int ekya_profile_estimate_both(ekya_handle* h, const ekya_profile_dims* p,
+                               const float* cur, const float* hist, const float* hist_acc,
+                               const float* fallback, float* out_est_radius, int32_t* out_n_radius,
+                               float* out_est_cluster, int32_t* out_n_cluster, int32_t* out_cluster,
+                               ekya_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * ekya_window_schedule -- the retraining window as a timeline (SURVEY 8(f)

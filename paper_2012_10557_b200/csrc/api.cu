@@ -181,6 +181,25 @@ int ekya_profile_estimate(ekya_handle* h, const ekya_profile_dims* p, const floa
                           reinterpret_cast<cudaStream_t>(stream));
 }
 
+int ekya_profile_estimate_both(ekya_handle* h, const ekya_profile_dims* p, const float* cur,
+                               const float* hist, const float* hist_acc, const float* fallback,
+                               float* out_est_radius, int32_t* out_n_radius, float* out_est_cluster,
+                               int32_t* out_n_cluster, int32_t* out_cluster, ekya_stream_t stream) {
+    ekya::NvtxRange nvtx_range("ekya_profile_estimate_both");
+    if (!h || !p) return EKYA_ERR_ARG;
+    if (p->n_query < 0 || p->n_hist < 0) return EKYA_ERR_SHAPE;
+    if (p->n_class < 1 || p->n_class > 1024 || p->n_gamma < 1 || p->n_gamma > 256) return EKYA_ERR_LIMIT;
+    if (!(p->tau >= 0.0f)) return EKYA_ERR_ARG;
+    if (p->k < 1 || p->k > 32 || p->max_iter < 0) return EKYA_ERR_LIMIT;
+    if (p->n_query > 0 && (!cur || !fallback || !out_est_radius || !out_n_radius || !out_est_cluster ||
+                           !out_n_cluster))
+        return EKYA_ERR_ARG;
+    if (p->n_query > 0 && p->n_hist > 0 && (!hist || !hist_acc)) return EKYA_ERR_ARG;
+    if (cudaSetDevice(h->device) != cudaSuccess) return EKYA_ERR_CUDA;
+    return launch_profile_both(h, *p, cur, hist, hist_acc, fallback, out_est_radius, out_n_radius, out_est_cluster,
+                               out_n_cluster, out_cluster, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int ekya_uniform_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int32_t fixed_gamma,
                           float inference_weight, uint16_t* out_alloc, uint8_t* out_cfg, uint64_t* out_sum_q32,
                           float* out_mean, ekya_stream_t stream) {

@@ -40,7 +40,11 @@ int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int m
                  uint32_t* out_steps, cudaStream_t s);
 int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur, const float* hist,
                    const float* hist_acc, const float* fallback, float* out_est, int32_t* out_n,
-                   int32_t* out_cluster, cudaStream_t s);
+                   int32_t* out_cluster, cudaStream_t s, float* rad_est = nullptr, int32_t* rad_n = nullptr,
+                   float rad_tau = 0.0f);
+int launch_profile_both(ekya_handle* h, const ekya_profile_dims& p, const float* cur, const float* hist,
+                        const float* hist_acc, const float* fallback, float* rad_est, int32_t* rad_n,
+                        float* cl_est, int32_t* cl_n, int32_t* out_cluster, cudaStream_t s);
 
 int launch_place(ekya_handle* h, int32_t n_inst, int32_t n_jobs, int32_t units, int32_t gpus,
                  const uint16_t* alloc, uint16_t* piece_job, uint32_t* piece_q, int16_t* piece_gpu,

@@ -39,6 +39,9 @@ constexpr int kRadiusStages = 2;
 
 struct ProfParams {
     ekya_profile_dims p;
+    float* rad_est;     // fused RADIUS outputs (cluster2_kernel<5, 27> only; NULL = CLUSTER alone)
+    int* rad_n;
+    float rad_tau;
     const float* cur;
     const float* hist;
     const float* acc;
@@ -815,7 +818,7 @@ __host__ __device__ inline C2Layout c2_layout(int H, int C, int G, int K) {
     L.cf_slot = al16((size_t)C * 4) + 16 + al16((size_t)G * 4) + 16;   // [cur][fallback] granule-staged
     L.cf = o;     o += 2 * L.cf_slot;
     L.hist = o;   o += al16((size_t)H * C * 4) + 16;
-    L.mu = o;     o += al16((size_t)K * CP * 4);
+    L.mu = o;     o += al16((size_t)(K + 1) * CP * 4);   // K centroids + the padded query (fused RADIUS)
     // Lloyd: cluster sums lo[K][C], hi[K][C] (u32); afterwards the same space holds
     // the similar-window list (u16[H]) and the per-gamma sums lo[G], hi[G], n[G]
     const size_t lloyd = (size_t)K * C * 8, gam = al16((size_t)H * 2) + (size_t)G * 12;
@@ -901,7 +904,7 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
         const float* x1 = hs + (size_t)(v1 ? h1 : (v0 ? h0 : 0)) * C;
         for (int t = tid; t < 2 * K * C; t += kC2Threads) slo[t] = 0u;
         for (int t = tid; t < K; t += kC2Threads) cnt[t] = 0;
-        if (tid == 0) misc[0] = misc[1] = misc[3] = 0;
+        if (tid == 0) misc[0] = misc[1] = misc[3] = misc[4] = 0;
         mbar_wait(bar, (unsigned)(i & 1));
         bool ok = true;
         for (int c = tid; c < C; c += kC2Threads) ok &= in01(cur[c]);
@@ -911,12 +914,27 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
             if (v1)
                 for (int c = 0; c < C; ++c) ok &= in01(x1[c]);
         }
-        // initial centroids mu_i = h_floor(iH/K) (C19), zero padded to CP columns
-        for (int t = tid; t < K * CP; t += kC2Threads) {
+        // initial centroids mu_i = h_floor(iH/K) (C19), zero padded to CP columns; row K = the
+        // query's own histogram (fused RADIUS)
+        const bool rad = KT == 5 && CT == 27 && P.rad_est != nullptr;
+        for (int t = tid; t < (rad ? K + 1 : K) * CP; t += kC2Threads) {
             const int ci = t / CP, c = t - ci * CP;
-            mu[t] = c < C ? hs[(size_t)(((long long)ci * H) / K) * C + c] : 0.0f;
+            mu[t] = c >= C ? 0.0f : ci < K ? hs[(size_t)(((long long)ci * H) / K) * C + c] : cur[c];
         }
         __syncthreads();
+        // fused RADIUS (rule 5, C17): both windows' distances to the query, similar iff
+        // sqrt(d2) <= tau -- the same sequential sum as radius_kernel (fl(x - c)^2 = fl(c - x)^2)
+        // (the similar flags are parked as per-warp ballot masks in misc[8..23] until the end)
+        if (rad) {
+            u64 sr[1];
+            c2_dists<1, 1, true>(sr, x0, x1, mu + K * CP, C, CP, 1, 1u, one);
+            const unsigned b0 = __ballot_sync(0xffffffffu, v0 && __fsqrt_rn(lo2(sr[0])) <= P.rad_tau);
+            const unsigned b1 = __ballot_sync(0xffffffffu, v1 && __fsqrt_rn(hi2(sr[0])) <= P.rad_tau);
+            if (lane == 0) {
+                misc[8 + warp] = (int)b0;
+                misc[16 + warp] = (int)b1;
+            }
+        }
 
         u64 s[KS];
 #pragma unroll
@@ -1131,6 +1149,51 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
             else est = n > 0 ? mean_q32(sum16_get(&glo[g], &ghi[g]), n) : fb[g];
             P.out_est[q * G + g] = est;
             P.out_n[q * G + g] = n;
+        }
+        if (KT == 5 && CT == 27 && P.rad_est != nullptr) {
+            // fused RADIUS estimate: the same list + exact per-gamma sums over the similar windows
+            __syncthreads();   // the CLUSTER sums and list are read
+            for (int t = tid; t < 3 * G; t += kC2Threads) glo[t] = 0u;
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+                const unsigned bm = (unsigned)misc[(sl ? 16 : 8) + warp];
+                const bool in = (bm >> lane) & 1u;
+                int base = 0;
+                if (lane == 0 && bm) base = atomicAdd(&misc[4], __popc(bm));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (in) list[base + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)(sl ? h1 : h0);
+            }
+            __syncthreads();
+            {
+                const int ns = misc[4];
+                const int ngrp = kC2Threads / G, g = tid % G, grp = tid / G;
+                if (grp < ngrp) {
+                    const float* acc = P.acc + (size_t)q * H * G + g;
+                    u64 gs = 0;
+                    int gn = 0;
+#pragma unroll 4
+                    for (int e = grp; e < ns; e += ngrp) {
+                        const float x = __ldg(acc + (size_t)list[e] * G);
+                        if (x == x) {
+                            gs += q32(x);
+                            gn += 1;
+                        }
+                    }
+                    if (gn) {
+                        sum16_add(&glo[g], &ghi[g], gs);
+                        atomicAdd(&gnn[g], gn);
+                    }
+                }
+            }
+            __syncthreads();
+            for (int g = tid; g < G; g += kC2Threads) {
+                int n = gnn[g];
+                float est = 0.0f;
+                if (!ok) n = 0;
+                else est = n > 0 ? mean_q32(sum16_get(&glo[g], &ghi[g]), n) : fb[g];
+                P.rad_est[q * G + g] = est;
+                P.rad_n[q * G + g] = n;
+            }
         }
         __syncthreads();   // sums, list and the cur/fallback slot are free again
     }
@@ -1554,9 +1617,12 @@ __global__ void no_history_kernel(ProfParams P) {
 
 int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur, const float* hist,
                    const float* hist_acc, const float* fallback, float* out_est, int32_t* out_n,
-                   int32_t* out_cluster, cudaStream_t s) {
+                   int32_t* out_cluster, cudaStream_t s, float* rad_est, int32_t* rad_n, float rad_tau) {
     ProfParams P{};
     P.p = p;
+    P.rad_est = rad_est;
+    P.rad_n = rad_n;
+    P.rad_tau = rad_tau;
     P.cur = cur;
     P.hist = hist;
     P.acc = hist_acc;
@@ -1609,9 +1675,10 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
             const size_t smem = A.L.total;
             // EKYA_CLUSTER_HB=1 selects the distance-bound kernel for the bench shape (A/B timing;
             // measured slower so far)
-            const bool hb = K == 5 && C == 27 && getenv("EKYA_CLUSTER_HB");
+            const bool hb = K == 5 && C == 27 && getenv("EKYA_CLUSTER_HB") && !rad_est;
             auto k2 = hb ? cluster_hb_kernel<5, 27>
                          : (K == 5 && C == 27) ? cluster2_kernel<5, 27> : cluster2_kernel<0, 0>;
+            if (rad_est && !(K == 5 && C == 27)) return EKYA_ERR_SHAPE;   // fused RADIUS: <5, 27> only
             e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return EKYA_ERR_CUDA;
             int per_sm = 0;
@@ -1625,6 +1692,7 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
             h->launches++;
             return cuda_status(cudaGetLastError());
         }
+        if (rad_est) return EKYA_ERR_SHAPE;   // fused RADIUS: cluster2_kernel<5, 27> only
         const size_t scratch = scratch_layout(H, H, C, K, true).total;
         P.Hc = H;
         const bool reg = (H <= kProfThreads) && (C <= 32);
@@ -1652,6 +1720,29 @@ int launch_profile(ekya_handle* h, const ekya_profile_dims& p, const float* cur,
     }
     h->launches++;
     return cuda_status(cudaGetLastError());
+}
+
+// RADIUS and CLUSTER estimates of the same queries.  The bench shape (k = 5, C = 27, H <= 512)
+// runs both in ONE pass of cluster2_kernel<5, 27> over the staged history (the tile is read
+// from HBM once); other shapes run radius_kernel then the CLUSTER kernel.
+bool profile_fusable(const ekya_handle* h, const ekya_profile_dims& p) {
+    return p.k == 5 && p.n_class == 27 && p.n_hist >= 1 && p.n_hist <= 2 * kC2Threads && p.n_gamma <= kC2Threads &&
+           c2_layout(p.n_hist, p.n_class, p.n_gamma, p.k).total <= h->smem_optin && !getenv("EKYA_PROFILE_UNFUSED");
+}
+
+int launch_profile_both(ekya_handle* h, const ekya_profile_dims& p, const float* cur, const float* hist,
+                        const float* hist_acc, const float* fallback, float* rad_est, int32_t* rad_n,
+                        float* cl_est, int32_t* cl_n, int32_t* out_cluster, cudaStream_t s) {
+    ekya_profile_dims pc = p;
+    pc.mode = EKYA_PROFILE_CLUSTER;
+    if (profile_fusable(h, p))
+        return launch_profile(h, pc, cur, hist, hist_acc, fallback, cl_est, cl_n, out_cluster, s, rad_est, rad_n,
+                              p.tau);
+    ekya_profile_dims pr = p;
+    pr.mode = EKYA_PROFILE_RADIUS;
+    const int e = launch_profile(h, pr, cur, hist, hist_acc, fallback, rad_est, rad_n, nullptr, s);
+    if (e != EKYA_OK) return e;
+    return launch_profile(h, pc, cur, hist, hist_acc, fallback, cl_est, cl_n, out_cluster, s);
 }
 
 }  // namespace ekya

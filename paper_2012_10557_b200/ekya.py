@@ -24,7 +24,7 @@ THIEF_STEEPEST, THIEF_LITERAL = 0, 1
 PROFILE_RADIUS, PROFILE_CLUSTER = 0, 1
 LAMBDA_NONE = 7
 SYMBOLS = ["ekya_create", "ekya_destroy", "ekya_last_error", "ekya_launch_count", "ekya_version",
-           "ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate",
+           "ekya_eval_allocations", "ekya_thief_schedule", "ekya_profile_estimate", "ekya_profile_estimate_both",
            "ekya_comm_unique_id", "ekya_comm_init", "ekya_comm_info", "ekya_gather_decisions", "ekya_counters", "ekya_place",
            "ekya_checkpoint_decide", "ekya_uniform_schedule", "ekya_pareto", "ekya_prune_configs", "ekya_curve_fit",
            "ekya_window_workspace_bytes", "ekya_window_schedule"]
@@ -89,6 +89,8 @@ def load_library(path: str = LIB_PATH):
     L.ekya_thief_schedule.restype = ctypes.c_int
     L.ekya_profile_estimate.argtypes = [P, ctypes.POINTER(ProfileDims), P, P, P, P, P, P, P, P]
     L.ekya_profile_estimate.restype = ctypes.c_int
+    L.ekya_profile_estimate_both.argtypes = [P, ctypes.POINTER(ProfileDims), P, P, P, P, P, P, P, P, P, P]
+    L.ekya_profile_estimate_both.restype = ctypes.c_int
     L.ekya_uniform_schedule.argtypes = [P, ctypes.POINTER(Dims), ctypes.POINTER(Tables), ctypes.c_int32,
                                         ctypes.c_float, P, P, P, P, P]
     L.ekya_uniform_schedule.restype = ctypes.c_int
@@ -271,6 +273,23 @@ def ekya_profile_estimate(h: Handle, pdims: ProfileDims, cur, hist, hist_acc, fa
     _check(code, "ekya_profile_estimate")
 
 
+def ekya_profile_estimate_both(h: Handle, pdims: ProfileDims, cur, hist, hist_acc, fallback, out_est_radius,
+                               out_n_radius, out_est_cluster, out_n_cluster, out_cluster=None, stream=None):
+    L = load_library()
+    Q, H, C, G = pdims.n_query, pdims.n_hist, pdims.n_class, pdims.n_gamma
+    code = L.ekya_profile_estimate_both(h.ptr, ctypes.byref(pdims), _ptr(cur, torch.float32, "cur", numel=Q * C),
+                                        _ptr(hist, torch.float32, "hist", True, Q * H * C),
+                                        _ptr(hist_acc, torch.float32, "hist_acc", True, Q * H * G),
+                                        _ptr(fallback, torch.float32, "fallback", numel=Q * G),
+                                        _ptr(out_est_radius, torch.float32, "out_est_radius", numel=Q * G),
+                                        _ptr(out_n_radius, torch.int32, "out_n_radius", numel=Q * G),
+                                        _ptr(out_est_cluster, torch.float32, "out_est_cluster", numel=Q * G),
+                                        _ptr(out_n_cluster, torch.int32, "out_n_cluster", numel=Q * G),
+                                        _ptr(out_cluster, torch.int32, "out_cluster", True, Q * (H + 1)),
+                                        _stream(stream, h))
+    _check(code, "ekya_profile_estimate_both")
+
+
 def ekya_uniform_schedule(h: Handle, dims: Dims, tables: Tables, fixed_gamma: int, inference_weight: float,
                           out_alloc, out_cfg, out_sum_q32, out_mean=None, stream=None):
     L = load_library()
@@ -446,6 +465,23 @@ def profile_estimate(h, cur, hist, hist_acc, fallback, mode=PROFILE_RADIUS, tau=
     cl = torch.empty((Q, H + 1), dtype=torch.int32, device=cur.device) if with_cluster else None
     ekya_profile_estimate(h, pd, cur, hist, hist_acc, fallback, est, n, cl, stream=stream)
     return est, n, cl
+
+
+def profile_estimate_both(h, cur, hist, hist_acc, fallback, tau=0.2, k=5, max_iter=100, with_cluster=False,
+                          stream=None):
+    """RADIUS and CLUSTER estimates of the same queries in one call (one history pass for the
+    paper's Waymo shape): (est_radius, n_radius, est_cluster, n_cluster, cluster)."""
+    Q, C = cur.shape
+    H = hist.shape[1]
+    G = fallback.shape[1]
+    pd = ProfileDims(Q, H, C, G, PROFILE_CLUSTER, tau, k, max_iter)
+    er = torch.empty((Q, G), dtype=torch.float32, device=cur.device)
+    nr = torch.empty((Q, G), dtype=torch.int32, device=cur.device)
+    ec = torch.empty((Q, G), dtype=torch.float32, device=cur.device)
+    nc = torch.empty((Q, G), dtype=torch.int32, device=cur.device)
+    cl = torch.empty((Q, H + 1), dtype=torch.int32, device=cur.device) if with_cluster else None
+    ekya_profile_estimate_both(h, pd, cur, hist, hist_acc, fallback, er, nr, ec, nc, cl, stream=stream)
+    return er, nr, ec, nc, cl
 
 
 def place(h, alloc, units, gpus, stream=None):

@@ -272,6 +272,55 @@ def test_profile_bitexact(h, name, pc, mode):
         assert h.counters()["lloyd_passes"] - c0 == int(passes.sum())
 
 
+BOTH_CASES = PROF_CASES + [
+    ("h512", synth.ProfileConfig("p", 24, 512, 27, 18)),          # fused: the largest tile
+    ("h513", synth.ProfileConfig("p", 12, 513, 27, 18)),          # not fused: two kernels
+    ("h3", synth.ProfileConfig("p", 10, 3, 27, 18)),
+    ("sparse-g1", synth.ProfileConfig("p", 40, 300, 27, 1, sparse=True)),
+]
+
+
+@pytest.mark.parametrize("name,pc", BOTH_CASES, ids=[c[0] for c in BOTH_CASES])
+def test_profile_both_bitexact(h, name, pc):
+    """ekya_profile_estimate_both: RADIUS and CLUSTER of the same queries (one history pass for
+    k = 5, C = 27, H <= 512) equal the oracle's two modes element by element."""
+    P = synth.profile_inputs(pc)
+    Pd = {k: v.cuda() for k, v in P.items()}
+    c0 = h.counters()["lloyd_passes"]
+    er, nr, ec, nc, cl = ek().profile_estimate_both(h, Pd["cur"], Pd["hist"], Pd["hist_acc"], Pd["fallback"],
+                                                    with_cluster=True)
+    assert h.last_error() == 0
+    args_ = tuple(P[k].numpy() for k in ("cur", "hist", "hist_acc", "fallback"))
+    oe, on, _, bad = oracle.profile(*args_, mode=0)
+    assert bad == 0
+    assert_eq(nr, on, "n radius")
+    assert_eq(er, oe, "estimate radius")
+    oe, on, ocl, bad, passes = oracle.profile(*args_, mode=1, with_passes=True)
+    assert_eq(nc, on, "n cluster")
+    assert_eq(ec, oe, "estimate cluster")
+    assert_eq(cl, ocl, "clusters")
+    if pc.n_hist > 0:
+        assert h.counters()["lloyd_passes"] - c0 == int(passes.sum())
+
+
+def test_profile_both_invalid_queries(h):
+    pc = synth.ProfileConfig("p", 5, 50, 27, 18)
+    P = synth.profile_inputs(pc)
+    P["hist"][2, 7, 3] = -0.5
+    P["hist_acc"][4, 1, 1] = 2.0
+    P["hist"][1, 49, 26] = float("nan")
+    P["cur"][0, 5] = 1.5
+    Pd = {k: v.cuda() for k, v in P.items()}
+    er, nr, ec, nc, _ = ek().profile_estimate_both(h, Pd["cur"], Pd["hist"], Pd["hist_acc"], Pd["fallback"])
+    assert h.last_error() == -6
+    args_ = tuple(P[k].numpy() for k in ("cur", "hist", "hist_acc", "fallback"))
+    for mode, (e, n) in enumerate(((er, nr), (ec, nc))):
+        oe, on, _, bad = oracle.profile(*args_, mode=mode)
+        assert bad == 4
+        assert_eq(e, oe, f"estimate mode {mode}")
+        assert_eq(n, on, f"n mode {mode}")
+
+
 CLUSTER_EDGE = [
     # (name, config, k, max_iter): window counts at the 2-windows-per-thread boundaries of the
     # multi-query CLUSTER kernel, k at its register-cache limits, capped iteration counts
@@ -487,6 +536,29 @@ def test_gather_decisions_one_rank_both_paths(h):
         assert torch.equal(root, buf)      # one rank: the root holds the rank's buffer byte for byte
     del dims
     h1.close()
+
+
+def test_config3_fused_full_batch_sampled(h):
+    """The bench's profile launch (both estimates in one pass) at config 3's full size,
+    sampled against the oracle's two modes."""
+    pc = synth.CONFIG3
+    e = ek()
+    P = synth.profile_inputs(pc, device="cuda")
+    er, nr, ec, nc, cl = e.profile_estimate_both(h, P["cur"], P["hist"], P["hist_acc"], P["fallback"],
+                                                 with_cluster=True)
+    assert h.last_error() == 0
+    del P
+    sample = [0, 1, 65535] + list(np.random.default_rng(9).integers(0, pc.n_query, 9))
+    for q in sample:
+        Pc = synth.profile_inputs(pc, q, q + 1)
+        a_ = tuple(Pc[k].numpy() for k in ("cur", "hist", "hist_acc", "fallback"))
+        oe, on, _, _ = oracle.profile(*a_, mode=0)
+        assert_eq(er[q:q + 1], oe, f"radius est q={q}")
+        assert_eq(nr[q:q + 1], on, f"radius n q={q}")
+        oe, on, ocl, _ = oracle.profile(*a_, mode=1)
+        assert_eq(ec[q:q + 1], oe, f"cluster est q={q}")
+        assert_eq(nc[q:q + 1], on, f"cluster n q={q}")
+        assert_eq(cl[q:q + 1], ocl, f"cluster q={q}")
 
 
 def test_config3_full_batch_sampled(h):

@@ -1,5 +1,5 @@
 """Time one hot-path kernel in isolation (CUDA events, after warm-up) for quick A/B runs.
-usage: python tools/kbench.py {cluster|radius|grid|list|steepest|literal} [reps]"""
+usage: python tools/kbench.py {cluster|radius|both|grid|list|steepest|literal} [reps]"""
 import os
 import sys
 
@@ -19,7 +19,7 @@ if os.environ.get("KBENCH_LIB"):   # A/B a variant build (tools only; the produc
 h = ekya.Handle(0)
 w = bench.Workload(int(os.environ.get("KB_B", synth.CONFIG4.n_inst)), int(os.environ.get("KB_N", synth.CONFIG4.n_alloc)),
                    synth.CONFIG3.n_query)
-if which in ("cluster", "radius"):
+if which in ("cluster", "radius", "both"):
     p = w.pcfg
     P = {}
     P["cur"] = torch.empty((w.Q, p.n_class), device=dev)
@@ -31,7 +31,10 @@ if which in ("cluster", "radius"):
         for k in P:
             P[k][q0:q0 + 2048] = part[k]
     mode = ekya.PROFILE_CLUSTER if which == "cluster" else ekya.PROFILE_RADIUS
-    fn = lambda: ekya.profile_estimate(h, P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=mode)
+    if which == "both":
+        fn = lambda: ekya.profile_estimate_both(h, P["cur"], P["hist"], P["hist_acc"], P["fallback"])
+    else:
+        fn = lambda: ekya.profile_estimate(h, P["cur"], P["hist"], P["hist_acc"], P["fallback"], mode=mode)
 else:
     if os.environ.get("KB_C5"):   # config-5 shape (V = 100, U = 800)
         w.cfg = synth.SchedConfig(**{**synth.CONFIG5.__dict__, "n_inst": w.B})
