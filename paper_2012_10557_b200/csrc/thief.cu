@@ -286,6 +286,7 @@ __device__ __forceinline__ void update_streams(const InstView& in, const WarpSta
         need = c.x != (unsigned)rt2;
         G = __uint_as_float(c.y);
     }
+    __syncwarp();   // every lane's cache read precedes a miss fill's write (lane 0, below)
     for (unsigned m = __ballot_sync(FULL, need); m; m = __ballot_sync(FULL, need)) {
         const int src = __ffs(m) - 1;
         const int ms = __shfl_sync(FULL, s, src), mr = __shfl_sync(FULL, rt2, src);
