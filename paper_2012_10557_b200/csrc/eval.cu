@@ -875,13 +875,9 @@ __global__ void __launch_bounds__(kListThreads, 1) list2_kernel(const __grid_con
             const long long i = ph - 1;
             if (i < 0) continue;
             const int k = (int)(i & 1);
-            mbar_wait_sleep(&full[i & 7], (unsigned)((i >> 3) & 1));
-            if (idx == 0 && lane == 0 && i + 2 < n)   // instance i's tables are complete: buffer k is free
-                issue_inputs(b0 + (i + 2) * g, k);
-            const bool ok = bad[k] != (int)(i + 1);
             const long long b = b0 + i * g;
-            const unsigned char* tabs = smem + L.tabs + k * L.tabset;
-            // the task's rows (contiguous) into the warp's buffer by one bulk copy
+            // the task's rows (contiguous) into the warp's buffer by one bulk copy, issued before
+            // the wait for the instance's tables so that the two latencies overlap
             const int rb = idx * RT, nr = min(RT, N - rb);
             const long long o0 = b * N + rb;   // first row of the task
             const uintptr_t ga = reinterpret_cast<uintptr_t>(p.alloc) + (uintptr_t)o0 * (2 * V * 2);
@@ -890,6 +886,11 @@ __global__ void __launch_bounds__(kListThreads, 1) list2_kernel(const __grid_con
                 mbar_arrive_expect_tx(rbar, bytes);
                 bulk_g2s(rbuf, reinterpret_cast<const void*>(ga - off), bytes, rbar);
             }
+            mbar_wait_sleep(&full[i & 7], (unsigned)((i >> 3) & 1));
+            if (idx == 0 && lane == 0 && i + 2 < n)   // instance i's tables are complete: buffer k is free
+                issue_inputs(b0 + (i + 2) * g, k);
+            const bool ok = bad[k] != (int)(i + 1);
+            const unsigned char* tabs = smem + L.tabs + k * L.tabset;
             mbar_wait_sleep(rbar, rphase & 1u);
             ++rphase;
             const uint2* rows = reinterpret_cast<const uint2*>(rbuf + off);
