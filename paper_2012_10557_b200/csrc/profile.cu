@@ -820,8 +820,8 @@ __host__ __device__ inline C2Layout c2_layout(int H, int C, int G, int K) {
     L.hist = o;   o += al16((size_t)H * C * 4) + 16;
     L.mu = o;     o += al16((size_t)(K + 1) * CP * 4);   // K centroids + the padded query (fused RADIUS)
     // Lloyd: cluster sums lo[K][C], hi[K][C] (u32); afterwards the same space holds
-    // the similar-window list (u16[H]) and the per-gamma sums lo[G], hi[G], n[G]
-    const size_t lloyd = (size_t)K * C * 8, gam = al16((size_t)H * 2) + (size_t)G * 12;
+    // the window list (u16[H]) and two sets of per-gamma sums lo[G], hi[G], n[G]
+    const size_t lloyd = (size_t)K * C * 8, gam = al16((size_t)H * 2) + (size_t)G * 24;
     L.sums = o;   o += al16(lloyd > gam ? lloyd : gam);
     L.cnt = o;    o += al16((size_t)K * 4);
     L.dummy = o;  o += 128;   // sink of the lanes beyond column C
@@ -849,7 +849,7 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
     const int CP = (C + 3) & ~3;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bar);
-    int* misc = reinterpret_cast<int*>(smem + L.misc);   // [0..1] changed-centroid masks, [2] query cluster,
+    int* misc = reinterpret_cast<int*>(smem + L.misc);   // [0..1] changed-centroid masks,
                                                          // [3] similar-window count
     float* mu = reinterpret_cast<float*>(smem + L.mu);
     unsigned* slo = reinterpret_cast<unsigned*>(smem + L.sums);
@@ -1060,77 +1060,99 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
             atomicAdd(&P.st->lloyd_passes, (unsigned long long)passes);
             if (i + 1 < items) issue(i + 1);
         }
-        // the query joins its nearest centroid: lane i computes distance to centroid i
-        if (warp == 0) {
+        // the query joins its nearest centroid (lowest index on ties, C19): every warp computes it
+        // (lane ci < K: distance to centroid ci; K <= 8), so no barrier publishes it
+        int qc;
+        {
             unsigned long long key = ~0ULL;
-            for (int ci = lane; ci < K; ci += 32) {
-                const float d = dist2_mem(cur, mu + ci * CP, C);
-                const unsigned long long kk = ((unsigned long long)__float_as_uint(d) << 8) | (unsigned)ci;
-                key = kk < key ? kk : key;
+            if (lane < K) {
+                const float d = dist2_mem(cur, mu + lane * CP, C);
+                key = ((unsigned long long)__float_as_uint(d) << 8) | (unsigned)lane;
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
+            for (int o = 4; o > 0; o >>= 1) {
                 const unsigned long long y = __shfl_xor_sync(0xffffffffu, key, o);
                 key = y < key ? y : key;
             }
-            if (lane == 0) misc[2] = (int)(key & 0xFF);
+            qc = (int)(__shfl_sync(0xffffffffu, key, 0) & 0xFF);
         }
-        // validate the whole accuracy tile (NaN = unmeasured, else in [0, 1]; R-ERR)
+        // the cluster sums are dead (the last pass's barrier): their space holds one list of the
+        // windows in the query's cluster (bit 14) and/or RADIUS-similar (bit 15), and both sets of
+        // per-gamma sums
+        for (int t = tid; t < 6 * G; t += kC2Threads) glo[t] = 0u;
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+            const bool inc = sl ? (v1 && na1 == qc) : (v0 && na0 == qc);
+            const bool inr = rad && ((((unsigned)misc[(sl ? 16 : 8) + warp]) >> lane) & 1u);
+            const unsigned bm = __ballot_sync(0xffffffffu, inc || inr);
+            int base = 0;
+            if (lane == 0 && bm) base = atomicAdd(&misc[3], __popc(bm));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (inc || inr)
+                list[base + __popc(bm & ((1u << lane) - 1u))] =
+                    (uint16_t)((sl ? h1 : h0) | (inc ? 0x4000 : 0) | (inr ? 0x8000 : 0));
+        }
+        __syncthreads();
+        // validate the whole accuracy tile (NaN = unmeasured, else in [0, 1]; R-ERR): NaN-ignoring
+        // running min / max from 0
         {
             const float* at = P.acc + (size_t)q * H * G;
             const long long n = (long long)H * G;
+            float lo = 0.0f, hi = 0.0f;
             if ((reinterpret_cast<uintptr_t>(at) & 15) == 0) {
                 const float4* a4 = reinterpret_cast<const float4*>(at);
                 for (long long t = tid; t < n / 4; t += kC2Threads) {
                     const float4 x = __ldg(a4 + t);
-                    ok &= !(x.x < 0.0f) && !(x.x > 1.0f) && !(x.y < 0.0f) && !(x.y > 1.0f) &&
-                          !(x.z < 0.0f) && !(x.z > 1.0f) && !(x.w < 0.0f) && !(x.w > 1.0f);
+                    lo = fminf(fminf(lo, x.x), fminf(x.y, fminf(x.z, x.w)));
+                    hi = fmaxf(fmaxf(hi, x.x), fmaxf(x.y, fmaxf(x.z, x.w)));
                 }
                 for (long long t = (n & ~3LL) + tid; t < n; t += kC2Threads) {
                     const float x = __ldg(at + t);
-                    ok &= !(x < 0.0f) && !(x > 1.0f);
+                    lo = fminf(lo, x);
+                    hi = fmaxf(hi, x);
                 }
             } else {
                 for (long long t = tid; t < n; t += kC2Threads) {
                     const float x = __ldg(at + t);
-                    ok &= !(x < 0.0f) && !(x > 1.0f);
+                    lo = fminf(lo, x);
+                    hi = fmaxf(hi, x);
                 }
             }
+            ok &= !(lo < 0.0f) && !(hi > 1.0f);
         }
-        __syncthreads();   // misc[2] visible; the cluster sums are dead: their space holds the list
-        const int qc = misc[2];
-        for (int t = tid; t < 3 * G; t += kC2Threads) glo[t] = 0u;
-        // compact list of the query cluster's windows (any order: the sums are exact integers)
-#pragma unroll
-        for (int sl = 0; sl < 2; ++sl) {
-            const bool in = sl ? (v1 && na1 == qc) : (v0 && na0 == qc);
-            const unsigned bm = __ballot_sync(0xffffffffu, in);
-            int base = 0;
-            if (lane == 0 && bm) base = atomicAdd(&misc[3], __popc(bm));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (in) list[base + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)(sl ? h1 : h0);
-        }
-        __syncthreads();
-        // per-gamma exact sums over the similar, measured windows: thread t owns gamma t % G and
-        // list entries t / G (mod ngrp); the accuracy tile comes from L2
+        // per-gamma exact sums over the listed windows' measured accuracies, both estimates from
+        // one load of each element: thread t owns gamma t % G and list entries t / G (mod ngrp);
+        // the accuracy tile comes from L2
         {
             const int ns = misc[3];
             const int ngrp = kC2Threads / G, g = tid % G, grp = tid / G;
             if (grp < ngrp) {
                 const float* acc = P.acc + (size_t)q * H * G + g;
-                u64 gs = 0;
-                int gn = 0;
+                u64 sc = 0, sr = 0;
+                int nc = 0, nr = 0;
 #pragma unroll 4
                 for (int e = grp; e < ns; e += ngrp) {
-                    const float x = __ldg(acc + (size_t)list[e] * G);
+                    const unsigned ent = list[e];
+                    const float x = __ldg(acc + (size_t)(ent & 0x3FFFu) * G);
                     if (x == x) {
-                        gs += q32(x);
-                        gn += 1;
+                        const u64 v = q32(x);
+                        if (ent & 0x4000u) {
+                            sc += v;
+                            nc += 1;
+                        }
+                        if (ent & 0x8000u) {
+                            sr += v;
+                            nr += 1;
+                        }
                     }
                 }
-                if (gn) {
-                    sum16_add(&glo[g], &ghi[g], gs);
-                    atomicAdd(&gnn[g], gn);
+                if (nc) {
+                    sum16_add(&glo[g], &ghi[g], sc);
+                    atomicAdd(&gnn[g], nc);
+                }
+                if (nr) {
+                    sum16_add(&glo[3 * G + g], &ghi[3 * G + g], sr);
+                    atomicAdd(&gnn[3 * G + g], nr);
                 }
             }
         }
@@ -1142,58 +1164,16 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
             if (v1) oc[h1] = ok ? na1 : 0;
             if (tid == 0) oc[H] = ok ? qc : 0;
         }
-        for (int g = tid; g < G; g += kC2Threads) {
-            int n = gnn[g];
+        // outputs: threads [0, G) the CLUSTER estimate, [G, 2G) the fused RADIUS estimate
+        for (int t = tid; t < (rad ? 2 * G : G); t += kC2Threads) {
+            const int set = t >= G, g = t - set * G;
+            const int o = set * 3 * G + g;
+            int n = gnn[o];
             float est = 0.0f;
             if (!ok) n = 0;
-            else est = n > 0 ? mean_q32(sum16_get(&glo[g], &ghi[g]), n) : fb[g];
-            P.out_est[q * G + g] = est;
-            P.out_n[q * G + g] = n;
-        }
-        if (KT == 5 && CT == 27 && P.rad_est != nullptr) {
-            // fused RADIUS estimate: the same list + exact per-gamma sums over the similar windows
-            __syncthreads();   // the CLUSTER sums and list are read
-            for (int t = tid; t < 3 * G; t += kC2Threads) glo[t] = 0u;
-#pragma unroll
-            for (int sl = 0; sl < 2; ++sl) {
-                const unsigned bm = (unsigned)misc[(sl ? 16 : 8) + warp];
-                const bool in = (bm >> lane) & 1u;
-                int base = 0;
-                if (lane == 0 && bm) base = atomicAdd(&misc[4], __popc(bm));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (in) list[base + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)(sl ? h1 : h0);
-            }
-            __syncthreads();
-            {
-                const int ns = misc[4];
-                const int ngrp = kC2Threads / G, g = tid % G, grp = tid / G;
-                if (grp < ngrp) {
-                    const float* acc = P.acc + (size_t)q * H * G + g;
-                    u64 gs = 0;
-                    int gn = 0;
-#pragma unroll 4
-                    for (int e = grp; e < ns; e += ngrp) {
-                        const float x = __ldg(acc + (size_t)list[e] * G);
-                        if (x == x) {
-                            gs += q32(x);
-                            gn += 1;
-                        }
-                    }
-                    if (gn) {
-                        sum16_add(&glo[g], &ghi[g], gs);
-                        atomicAdd(&gnn[g], gn);
-                    }
-                }
-            }
-            __syncthreads();
-            for (int g = tid; g < G; g += kC2Threads) {
-                int n = gnn[g];
-                float est = 0.0f;
-                if (!ok) n = 0;
-                else est = n > 0 ? mean_q32(sum16_get(&glo[g], &ghi[g]), n) : fb[g];
-                P.rad_est[q * G + g] = est;
-                P.rad_n[q * G + g] = n;
-            }
+            else est = n > 0 ? mean_q32(sum16_get(&glo[o], &ghi[o]), n) : fb[g];
+            (set ? P.rad_est : P.out_est)[q * G + g] = est;
+            (set ? P.rad_n : P.out_n)[q * G + g] = n;
         }
         __syncthreads();   // sums, list and the cur/fallback slot are free again
     }

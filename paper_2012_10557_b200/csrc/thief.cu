@@ -414,14 +414,14 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
         ok &= in01(x);
         if (p.stage) st[i] = x;
     }
-    for (int v = 0; v < V; ++v) {
-        if (lane < nG) {
-            const float c = __ldg(in.cost + v * nG + lane), po = __ldg(in.post + v * nG + lane);
-            if (!(c >= 0.0f)) ok = false;
-            else if (!isinf(c)) ok &= in01(po);
-            fast &= fast_dividend(c);
-            if (p.stage) cpd[v * nG + lane] = make_float4(c, po, fsub(po, __ldg(in.stale + v)), 0.0f);
-        }
+    // flat over (stream, config): every lane's loads are independent (one latency round trip)
+#pragma unroll 2
+    for (int i = lane; i < V * nG; i += 32) {
+        const int v = i / nG;
+        const float c = __ldg(in.cost + i), po = __ldg(in.post + i);
+        ok &= c >= 0.0f && (isinf(c) || in01(po));
+        fast &= fast_dividend(c);
+        if (p.stage) cpd[i] = make_float4(c, po, fsub(po, __ldg(in.stale + v)), 0.0f);
     }
     for (int i = lane; i < V * nL; i += 32)
         if (__ldg(in.lmu + i) != kLmuPad) ok &= in01(__ldg(in.lf + i));

@@ -1,5 +1,5 @@
 """Build an A/B variant of libekya.so with extra nvcc flags (tools only; the product loads
-paper_2012_10557_b200/libekya.so).  usage: python tools/build_variant.py OUT.so -DFLAG=..."""
+paper_2012_10557_b200/libekya.so).  usage: [EKYA_VARIANT_CSRC=DIR] python tools/build_variant.py OUT.so -DFLAG=..."""
 import os
 import subprocess
 import sys
@@ -16,7 +16,8 @@ common = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fm
 objs = []
 for src in B.SOURCES:
     obj = os.path.join(objdir, src.replace(".cu", ".o"))
-    subprocess.run(["nvcc", *common, "-c", os.path.join(B.CSRC, src), "-o", obj], check=True)
+    csrc = os.environ.get("EKYA_VARIANT_CSRC", B.CSRC)   # another source tree (A/B of a code change)
+    subprocess.run(["nvcc", *common, "-I", B.CSRC, "-c", os.path.join(csrc, src), "-o", obj], check=True)
     objs.append(obj)
 rt = B._nvidia_lib("cuda_runtime")
 subprocess.run(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out, *objs, "-L", lib,
