@@ -145,7 +145,10 @@ int ekya_eval_allocations(ekya_handle* h, const ekya_dims* d, const ekya_tables*
  *     steal repeatedly while strictly improving).
  * Outputs: out_alloc[b][2V] (u16 units, sum = U), out_cfg[b][V],
  * out_sum_q32[b] (exact objective), optional out_mean[b], out_steps[b]
- * (accepted steals).  Any V, U within the limits.
+ * (accepted steals).  Any V, U within the limits; n_inst < 2^32 - 2^24
+ * (EKYA_ERR_LIMIT).  LITERAL and wide instances (V > 16) run persistent warps
+ * that claim instances from a counter in the handle's device state, so one
+ * handle's thief launches must be stream-ordered (as for its error word).
  * ------------------------------------------------------------------------- */
 enum { EKYA_THIEF_STEEPEST = 0, EKYA_THIEF_LITERAL = 1 };
 int ekya_thief_schedule(ekya_handle* h, const ekya_dims* d, const ekya_tables* t, int mode,

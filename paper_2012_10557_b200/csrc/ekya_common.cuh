@@ -25,7 +25,9 @@ struct DevState {
     unsigned int err;                   // OR of kErr* bits
     unsigned int pad0;
     unsigned long long lloyd_passes;    // CLUSTER assignment passes (telemetry)
-    unsigned int pad[12];
+    unsigned int thief_next;            // thief: next instance to claim (0 between launches)
+    unsigned int thief_done;            // thief: warps past their last claim (0 between launches)
+    unsigned int pad[10];
 };
 
 __device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }

@@ -58,6 +58,7 @@ struct ThiefParams {
     size_t state_bytes;  // shared bytes of the per-warp state
     int stage;           // stage stale/cost/post of the instance in shared memory
     int nsm;             // G* cache slots per stream - 1 (a power of two minus one)
+    unsigned total_warps;   // warps launched (the claim counters' reset)
 };
 
 // Per-stream record rec[v][8] (Q32 units): [0] current value, [1] up (inference
@@ -387,8 +388,27 @@ __device__ __forceinline__ unsigned long long stream_down_key(const WarpState& S
 
 // MODE: EKYA_THIEF_STEEPEST or EKYA_THIEF_LITERAL (one kernel per mode keeps the hot loop's
 // code small)
-template <int MODE>
-__global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) {
+// lanes 0..4: bulk-prefetch instance bn's five input arrays into L2
+__device__ __forceinline__ void prefetch_instance(const ThiefParams& p, unsigned bn) {
+    const int lane = threadIdx.x & 31;
+    const ekya_dims& d = p.d;
+    const int V = d.n_streams, nG = d.n_gamma, nL = d.n_lambda;
+    if (lane < 5 && bn < (unsigned)d.n_inst) {
+        const Granules gi = lane == 0   ? granules(p.t.stale + (size_t)bn * V, (size_t)V * 4)
+                            : lane == 1 ? granules(p.t.cost + (size_t)bn * V * nG, (size_t)V * nG * 4)
+                            : lane == 2 ? granules(p.t.post + (size_t)bn * V * nG, (size_t)V * nG * 4)
+                            : lane == 3 ? granules(p.t.lam_min_units + (size_t)bn * V * nL, (size_t)V * nL * 2)
+                                        : granules(p.t.lam_factor + (size_t)bn * V * nL, (size_t)V * nL * 4);
+        if (gi.bytes) bulk_prefetch_l2(gi.g0, gi.bytes);
+    }
+}
+
+// One instance b by the calling warp (warp-collective; leaves with every lane's shared-memory
+// accesses done after the caller's __syncwarp).  `claim` is lane 0's pending claim of the
+// warp's next instance: consumed only after this instance's validity pass (the atomic's
+// latency overlaps those loads), broadcast into *next and prefetched into L2.
+template <int MODE, bool PERSIST>
+__device__ __forceinline__ void thief_one(const ThiefParams& p, long long b, unsigned claim, unsigned* next) {
     extern __shared__ __align__(16) unsigned char smem[];
     const ekya_dims& d = p.d;
     const int V = d.n_streams, J = 2 * V, D = d.steal_units, U = d.units, nG = d.n_gamma, nL = d.n_lambda;
@@ -396,8 +416,6 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
     const int nsm = p.nsm;
     const WarpState S = carve(smem + warp * p.warp_bytes, V, nsm + 1);
     float* staged = reinterpret_cast<float*>(smem + warp * p.warp_bytes + p.state_bytes);
-    const long long b = (long long)blockIdx.x * p.warps + warp;
-    if (b >= d.n_inst) return;
 
     InstView in{p.t.stale + b * V, p.t.cost + b * V * nG, p.t.post + b * V * nG,
                 p.t.lam_min_units + b * V * nL, p.t.lam_factor + b * V * nL, nullptr};
@@ -428,6 +446,10 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
     __syncwarp();
     ok = __all_sync(FULL, ok);
     fast = __all_sync(FULL, fast);
+    if (PERSIST) {
+        *next = __shfl_sync(FULL, claim, 0);
+        prefetch_instance(p, *next);
+    }
     if (p.stage) {   // stale and (cost, post, post - stale) in this warp's shared memory
         in.stale = st;
         in.cpd = cpd;
@@ -637,6 +659,40 @@ __global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) 
     }
 }
 
+// PERSIST: persistent warps claiming instances from a device counter (dynamic balance:
+// per-instance step counts vary): a warp claims its next instance while running the current
+// one and lanes 0..4 bulk-prefetch the next one's five input arrays into L2, so its validity /
+// staging pass does not wait on HBM.  Every warp makes exactly one failing claim; the last
+// warp past it (thief_done) returns both counters to 0 for the handle's next launch (launches
+// on one handle are stream-ordered, as for its error word).  Otherwise one instance per warp
+// (measured faster for STEEPEST at the paper's V = 10: 0.663 vs 0.674 ms; persistent LITERAL
+// 1.04 -> 0.99 ms, config-5 shape STEEPEST 4.17 -> 3.77, LITERAL 10.4 -> 9.5).
+template <int MODE, bool PERSIST>
+__global__ void __launch_bounds__(kThiefThreads, 8) thief_kernel(ThiefParams p) {
+    const int lane = threadIdx.x & 31;
+    if (!PERSIST) {
+        const long long b = (long long)blockIdx.x * p.warps + (threadIdx.x >> 5);
+        unsigned unused;
+        if (b < p.d.n_inst) thief_one<MODE, false>(p, b, 0u, &unused);
+        return;
+    }
+    const unsigned n = (unsigned)p.d.n_inst;
+    unsigned b = 0;
+    if (lane == 0) b = atomicAdd(&p.st->thief_next, 1u);
+    b = __shfl_sync(FULL, b, 0);
+    while (b < n) {
+        unsigned claim = 0, bn;
+        if (lane == 0) claim = atomicAdd(&p.st->thief_next, 1u);
+        thief_one<MODE, true>(p, (long long)b, claim, &bn);
+        __syncwarp();   // the next instance's state writes follow every lane's reads of this one's
+        b = bn;
+    }
+    if (lane == 0 && atomicAdd(&p.st->thief_done, 1u) == p.total_warps - 1) {
+        p.st->thief_next = 0;
+        p.st->thief_done = 0;
+    }
+}
+
 }  // namespace
 
 int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int mode,
@@ -667,11 +723,23 @@ int launch_thief(ekya_handle* h, const ekya_dims& d, const ekya_tables& t, int m
     if (p.warps < 1) return EKYA_ERR_SHAPE;
     size_t smem = p.warp_bytes * p.warps;
     if (d.n_inst == 0) return EKYA_OK;
-    auto kern = mode == EKYA_THIEF_STEEPEST ? thief_kernel<EKYA_THIEF_STEEPEST> : thief_kernel<EKYA_THIEF_LITERAL>;
+    // persistent claiming warps except for STEEPEST at the paper's stream counts (V <= 16),
+    // where one instance per warp measured faster (thief_kernel)
+    const bool persist = !(mode == EKYA_THIEF_STEEPEST && d.n_streams <= 16);
+    auto kern = mode == EKYA_THIEF_STEEPEST
+                    ? (persist ? thief_kernel<EKYA_THIEF_STEEPEST, true> : thief_kernel<EKYA_THIEF_STEEPEST, false>)
+                    : thief_kernel<EKYA_THIEF_LITERAL, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return EKYA_ERR_CUDA;
+    if (d.n_inst >= 0xFFFFFFFFLL - (1LL << 24)) return EKYA_ERR_LIMIT;
     long long grid = (d.n_inst + p.warps - 1) / p.warps;
+    if (persist) {   // as many CTAs as are resident at once
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, p.warps * 32, smem);
+        grid = std::min<long long>(grid, (long long)h->sm_count * std::max(per_sm, 1));
+    }
     if (grid > 0x7fffffffLL) return EKYA_ERR_SHAPE;
+    p.total_warps = (unsigned)(grid * p.warps);
     kern<<<(unsigned)grid, p.warps * 32, smem, s>>>(p);
     h->launches++;
     return cuda_status(cudaGetLastError());
