@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # CLUSTER alone (PROFILE_ROW=profile_cluster)
 NAMES = [("cluster2_kernel", os.environ.get("PROFILE_ROW", "profile")), ("cluster_kernel", "profile_cluster"),
          ("radius_kernel", "profile_radius"), ("grid_kernel", "eval_grid"), ("list_kernel", "eval_list"), ("list2_kernel", "eval_list"),
-         ("thief_kernel<0>", "thief_steepest"), ("thief_kernel<1>", "thief_literal"),
+         ("thief_kernel<0", "thief_steepest"), ("thief_kernel<1", "thief_literal"),
          ("curve_fit_kernel", "next2_curve_fit"), ("uniform_kernel", "next3_uniform"),
          ("pareto_kernel", "next3_pareto"), ("prune_", "next3_prune"), ("place_kernel", "next4_placement"),
          ("checkpoint_kernel", "next4_checkpoint")]
@@ -120,7 +120,8 @@ def main(ev, tag):
               f"{bench['roofline']['peak']:.1f} {bench['roofline']['unit']} = {bench['roofline']['frac']:.3f}.")
     md.append("")
     md.append("Per-row roofline fractions (bench, CUDA events): " + ", ".join(
-        (f"{k} {v['alu_frac']:.3f} (alu)" if "alu_frac" in v else f"{k} {v.get('hbm_frac', 0):.3f} (hbm)")
+        (f"{k} {v['alu_frac']:.3f} (alu)" if "alu_frac" in v else f"{k} {v['hbm_frac']:.3f} (hbm)"
+         if "hbm_frac" in v else f"{k} {v['issue_frac']:.3f} (issue)" if "issue_frac" in v else f"{k} -")
         for k, v in bench["rows"].items()))
     with open(os.path.join(out_dir, f"{tag}_summary.md"), "w") as f:
         f.write("\n".join(md) + "\n")
