@@ -202,6 +202,37 @@ def test_thief_invalid_instance_zeroed(h):
     assert_eq(s, osum, "sum")
 
 
+def test_thief_persistent_claims_back_to_back(h):
+    """LITERAL (and V > 16) run persistent warps claiming instances from a counter in the
+    handle's device state that the last warp resets: launches of different sizes back to back,
+    one with invalid instances (early exit inside the claim loop) and one empty, must each
+    match the oracle -- a counter left non-zero would skip instances of the next launch."""
+    base = variant(synth.CONFIG2, n_inst=5000, seed=77)
+    T = synth.sched_tables(base)
+    T["stale"][3, 0] = 1.5
+    T["cost"][4998, 2, 1] = -1.0
+    Td = {k: v.cuda() for k, v in T.items()}
+    full = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            *args(base))
+    # instances are independent: one oracle run per mode serves every prefix (STEEPEST, one
+    # instance per warp at V = 10, on the short prefixes only: its oracle is the slow one)
+    ref = {1: oracle.thief(full, 1), 0: oracle.thief(full.subset(list(range(37))), 0)}
+    for n in (5000, 1, 0, 37, 4737, 5000):   # > 4,736 resident warps: some claim twice
+        Tn = {k: v[:n].contiguous() for k, v in Td.items()}
+        for mode in ((1, 0) if n <= 37 else (1,)):
+            a, c, s, m, st = ek().thief_schedule(h, Tn, *args(base), mode=mode)
+            if n == 0:
+                assert a.numel() == 0
+                continue
+            oa, oc, osum, omean, osteps, _ = ref[mode]
+            bad = (n > 3) + (n > 4998)
+            assert h.last_error() == (-6 if bad else 0)
+            assert_eq(a, oa[:n], f"alloc n={n} mode={mode}")
+            assert_eq(s, osum[:n], f"sum n={n} mode={mode}")
+            assert_eq(c, oc[:n], f"cfg n={n} mode={mode}")
+            assert_eq(st, osteps[:n], f"steps n={n} mode={mode}")
+
+
 def test_thief_scaleout_shape(h):
     """Config 5 shape (V=100, U=800): LITERAL on 3 instances, STEEPEST on 1."""
     cfg = variant(synth.CONFIG5, n_inst=3)
