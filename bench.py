@@ -237,6 +237,9 @@ class KernelTimer:
     def totals_ms(self):
         return {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.ev.items()}
 
+    def launches_ms(self):
+        return {k: [a.elapsed_time(b) for a, b in v] for k, v in self.ev.items()}
+
 
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -452,6 +455,7 @@ def run_ours(args, rank, world, local_rank):
     lloyd_passes = c1["lloyd_passes"] - c0["lloyd_passes"]
     ms = t0.elapsed_time(t1)
     per = timer.totals_ms()
+    per_launch = timer.launches_ms()
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
@@ -494,6 +498,9 @@ def run_ours(args, rank, world, local_rank):
     for k, t in per.items():
         avg = t / args.steps
         r = {"ms_per_launch": avg, "share": t / ms}
+        if per_launch.get(k):   # median and best of the timed launches as well
+            r["ms_median"] = float(np.median(per_launch[k]))
+            r["ms_best"] = float(min(per_launch[k]))
         if k in bytes_of:
             gbs = bytes_of[k] / (avg / 1000.0) / 1e9
             r["algorithmic_gb_per_s"] = gbs
@@ -524,6 +531,9 @@ def run_ours(args, rank, world, local_rank):
             r["queries_per_s"] = w.Q * world / (avg / 1000.0)
         if k.startswith("eval_grid"):
             r["cells_per_s"] = w.B * w.V * w.nc * world / (avg / 1000.0)
+            # the north star's tuple count, cells x (|Gamma| + 1) x |Lambda| --
+            # DERIVED (the (gamma, lambda) enumeration the per-stream tables avoid), not work done
+            r["tuple_equiv_per_s_derived"] = r["cells_per_s"] * (T["cost"].shape[2] + 1) * T["lam_factor"].shape[2]
         if k.endswith("list"):
             r["allocation_vectors_per_s"] = w.B * w.N * world / (avg / 1000.0)
         rows_out[k] = r
