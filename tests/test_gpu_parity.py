@@ -760,6 +760,41 @@ def test_checkpoint_bitexact(h):
     assert_eq(out, oo, "checkpoint")
 
 
+def test_next_rows_exact_ties_and_clamp(h):
+    """The oracle pins' boundary cases on the GPU: CK1's exact tie (no checkpoint) and its
+    nextafter neighbour; U2's tied highest post (lowest index); CF2's all-zero-SSE grid
+    (c = 0) and CF3's clamp at 0."""
+    f = lambda *xs: [torch.tensor(x, dtype=torch.float32).cuda() for x in xs]
+    up = float(np.nextafter(np.float32(0.625), np.float32(1)))
+    args_ck = ([30, 30], [20, 20], [100, 100], [0.5, 0.5], [0.625, up], [0.5, 0.5], [2.5, 2.5])
+    out = ek().checkpoint_decide(h, *f(*args_ck))
+    oo, bad = oracle.checkpoint(*args_ck)
+    assert bad == 0 and oo.tolist() == [0, 1]
+    assert_eq(out, oo, "checkpoint tie")
+    c = variant(synth.CONFIG2, n_inst=40)
+    T = synth.sched_tables(c)
+    T["post"] = T["post"] * 0.5
+    for b in range(40):
+        for v in range(T["post"].shape[1]):
+            T["post"][b, v, (3 + b + v) % 18] = 1.0
+            T["post"][b, v, (11 + 2 * b + v) % 18] = 1.0
+    inst = oracle.Instances(*(T[k].numpy() for k in ("stale", "cost", "post", "lam_min_units", "lam_factor")),
+                            *args(c))
+    a, cf, sm, m = ek().uniform_schedule(h, {k: v.cuda() for k, v in T.items()}, *args(c))
+    oa, oc, osum, omean, bad = oracle.uniform(inst)
+    assert bad == 0
+    assert_eq(cf, oc, "uniform tied cfg")
+    assert_eq(sm, osum, "uniform tied sum")
+    acc = np.array([[0.5] * 5, [0.0, 1 / 64, 6 / 64, 6 / 64, 6 / 64], [0.0, 0.0, 3 / 64, 6 / 64, 6 / 64]],
+                   np.float32)
+    K = np.array([7, 1, 1], np.int32)
+    pred, prm = ek().curve_fit(h, torch.from_numpy(acc).cuda(), torch.from_numpy(K).cuda())
+    op, oprm, bad = oracle.curve_fit(acc, K)
+    assert bad == 0
+    assert_eq(pred, op, "curve fit pred")
+    assert_eq(prm, oprm, "curve fit params")
+
+
 # ---------------------------------------------------------------------------
 # NEXT-3: uniform baseline and Pareto frontier
 # ---------------------------------------------------------------------------

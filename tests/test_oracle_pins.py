@@ -721,6 +721,17 @@ def test_checkpoint_spec_examples():
     assert out[0] == 0                                 # a* = a, positive cost
 
 
+def test_checkpoint_exact_tie_keeps_training():
+    """CK1 is strict (checkpoint iff acc > base_acc): with (tau - t)(a* - a) equal to
+    delta A exactly (10 x 0.125 = 2.5 x 0.5 = 1.25, all exact in binary32) the two averaged
+    accuracies are equal as rationals, so there is no checkpoint; a hair more gain tips it."""
+    out, bad = oracle.checkpoint([30], [20], [100], [0.5], [0.625], [0.5], [2.5])
+    assert bad == 0 and out[0] == 0
+    out, bad = oracle.checkpoint([30], [20], [100], [0.5], [np.nextafter(np.float32(0.625), np.float32(1))],
+                                 [0.5], [2.5])
+    assert out[0] == 1
+
+
 def test_checkpoint_matches_the_averaged_accuracy_form():
     """acc > base_acc in exact rationals agrees with the oracle's simplified form
     wherever the two sides differ by more than 1e-5 (rounding can only flip near ties)."""
@@ -790,6 +801,35 @@ def test_uniform_half_weight_is_dominated_by_pickconfigs_and_thief():
                 assert list(a[b]) == list(fair[b] if fair.ndim == 2 else fair)
                 pc = oracle.pickconfigs(inst, b, fair)[0]
                 assert int(s[b]) <= pc <= int(ts[b]) and pc <= int(tl[b])
+
+
+def test_uniform_highest_post_ties_take_the_lowest_index():
+    """U2 ("the configuration ... that results in the highest accuracy"): on a tie of the
+    highest post-retraining accuracy the lowest-index config is the fixed one (C7's tie rule).
+    Two configs of every stream are forced to share the maximum; the reported gamma (cfg bits
+    0-4, 1-based) must be the lower of the two wherever a lambda is admissible."""
+    c = synth.SchedConfig(**{**synth.CONFIG2.__dict__, "n_inst": 40})
+    T = synth.sched_tables(c)
+    post = (T["post"].numpy() * np.float32(0.5)).astype(np.float32)   # every real post < 1 ...
+    cost = T["cost"].numpy()
+    for b in range(40):
+        for v in range(post.shape[1]):
+            i, j = (3 + b + v) % 18, (11 + 2 * b + v) % 18
+            lo_, hi_ = min(i, j), max(i, j)
+            post[b, v, lo_] = post[b, v, hi_] = np.float32(1.0)   # ... but these two
+    inst = oracle.Instances(T["stale"].numpy(), cost, post, T["lam_min_units"].numpy(),
+                            T["lam_factor"].numpy(), c.units, c.steal_units, c.unit_gpu_seconds, c.a_min)
+    a, cfg, s, mean, bad = oracle.uniform(inst)
+    assert bad == 0
+    checked = 0
+    for b in range(40):
+        for v in range(post.shape[1]):
+            if (cfg[b, v] >> 5) == oracle.LAMBDA_NONE:
+                continue
+            i, j = (3 + b + v) % 18, (11 + 2 * b + v) % 18
+            assert (cfg[b, v] & 31) == min(i, j) + 1
+            checked += 1
+    assert checked > 200
 
 
 def test_uniform_weight_and_no_retraining():
@@ -997,6 +1037,24 @@ def test_curve_fit_nnls_and_grid_optimal():
         assert chosen <= best + 1e-6
         p2, _, _ = oracle.curve_fit(a[s:s + 1], np.array([60]))
         assert p2[0] >= pred[s] - 1e-7
+
+
+def test_curve_fit_grid_ties_and_clamp():
+    """CF2: constant accuracy is fitted exactly (alpha = 0, beta2 = 1 - acc) at EVERY grid c --
+    the SSE is 0 throughout -- so the lowest grid index, c = 0, is the one reported.  CF3: the
+    extrapolation is clamped to [0, 1]; accuracies that start at 0 and barely rise give fits
+    whose value at epoch 1 lies below 0 (found by search; checked here from the returned
+    parameters), and the prediction is 0, never negative."""
+    for n in (2, 5):
+        pred, prm, bad = oracle.curve_fit(np.full((1, n), 0.5, np.float32), np.array([7]))
+        assert bad == 0 and prm[0].tolist() == [0.0, 0.0, 0.5] and pred[0] == 0.5
+    cases = np.array([[0.0, 1 / 64, 6 / 64, 6 / 64], [0.0, 0.0, 3 / 64, 6 / 64]], np.float32)
+    pred, prm, bad = oracle.curve_fit(cases, np.array([1, 1]))
+    assert bad == 0
+    for i in range(2):
+        al, c, b2 = (float(x) for x in prm[i])
+        assert 1.0 - (al / (1.0 + c) + b2) < -1e-3      # the unclamped model value
+        assert pred[i] == 0.0
 
 
 def test_curve_fit_invalid():

@@ -34,6 +34,37 @@ MUTANTS = {
     # Alg. 1 (A4-A5)
     "C9-fair-half-up": ("int32_t rt = share / 2;", "int32_t rt = (share + 1) / 2;"),
     "C14-floor": ("if (temp[victim] < 0) break;", "if (temp[victim] <= 0) break;"),
+    # Eq. 1 constraint 2 (LIST)
+    "EQ1-strict-total": ("if (tot > d->units) row_ok = 0;   /* Eq. 1 constraint 2 */",
+                         "if (tot >= d->units) row_ok = 0;   /* Eq. 1 constraint 2 */"),
+    "rule4-mean-over-V+1": ("double m = (double)s / ((double)n * 4294967296.0);",
+                            "double m = (double)s / ((double)(n + 1) * 4294967296.0);"),
+    # NEXT-4 placement (PL1, PL2) and checkpoint (CK1)
+    "PL1-quantize-up": ("while ((r << k) < (int64_t)U) ++k;", "while ((r << k) <= (int64_t)U) ++k;"),
+    "PL2-strict-fit": ("if (load[g] + pc[i].q <= ORC_Q_ONE)", "if (load[g] + pc[i].q < ORC_Q_ONE)"),
+    "PL2-ties-job-desc": ("if (a->job != b->job) return a->job < b->job ? -1 : 1;",
+                          "if (a->job != b->job) return a->job > b->job ? -1 : 1;"),
+    "CK1-ge": ("out[i] = lhs > rhs;", "out[i] = lhs >= rhs;"),
+    "CK1-gain-sign": ("const float gain = a_star[i] - a[i];", "const float gain = a[i] - a_star[i];"),
+    # NEXT-3 uniform (U1, U2), Pareto (PR1), pruning (PN1, PN2)
+    "U1-ceil": ("const int32_t rt = (int32_t)floorf(x);", "const int32_t rt = (int32_t)ceilf(x);"),
+    "U2-best-last-index": ("if (g == 0 || pv[k] > bp) { g = k + 1; bp = pv[k]; }",
+                           "if (g == 0 || pv[k] >= bp) { g = k + 1; bp = pv[k]; }"),
+    "U2-infeasible-zero": ("                float acc = st;\n", "                float acc = 0.0f;\n"),
+    "PR1-weak-dominance": ("if (c[j] <= c[k] && p[j] >= p[k] && (c[j] < c[k] || p[j] > p[k])) dominated = 1;",
+                           "if (c[j] <= c[k] && p[j] >= p[k]) dominated = 1;"),
+    "PN1-strict-cost": ("if (c[k2] <= c[k] && a[k2] > boundary) boundary = a[k2];",
+                        "if (c[k2] < c[k] && a[k2] > boundary) boundary = a[k2];"),
+    "PN2-half-inclusive": ("if (!(2 * far > measured)) keep |= 1u << k;",
+                           "if (!(2 * far >= measured)) keep |= 1u << k;"),
+    "PN1-gap-ge": ("if (gap > margin) ++far;", "if (gap >= margin) ++far;"),
+    # NEXT-2 curve fit (CF1-CF3)
+    "CF2-grid-ties-last": ("if (i == 0 || e < best) {", "if (i == 0 || e <= best) {"),
+    # (CF1's tie between the two boundary fits, `e1 < e0` -> `<=`, is left out: it changes the
+    # output only on an exact SSE tie of two distinct fits, none in 800 K random 64ths sets)
+    "CF3-no-clamp": ("p = p < 0.0f ? 0.0f : (p > 1.0f ? 1.0f : p);", "p = p;"),
+    "CF1-x-offset": ("const float den = (float)(k + 1) + c;", "const float den = (float)k + c;"),
+
     "C13-accept-ties": ("if (acc > best_acc) {", "if (acc >= best_acc) {"),
     "C12-steepest-victim-floor": ("if (t == w || alloc[w] < D) continue;", "if (t == w || alloc[w] <= D) continue;"),
 }
