@@ -34,6 +34,23 @@ MUTANTS = {
     # Alg. 1 (A4-A5)
     "C9-fair-half-up": ("int32_t rt = share / 2;", "int32_t rt = (share + 1) / 2;"),
     "C14-floor": ("if (temp[victim] < 0) break;", "if (temp[victim] <= 0) break;"),
+    # rules 1-2 (Alg. 2)
+    "rule1-denominator-rt+1": ("float denom = (float)rt * uT;          /* fl(float(rt) * uT) */",
+                               "float denom = (float)(rt + 1) * uT;          /* fl(float(rt) * uT) */"),
+    # (rule 1's explicit rt < 1 test is redundant in IEEE arithmetic -- cost / (0 uT) is +INF or
+    # NaN, never <= 1 -- so dropping it is an equivalent mutant, not listed)
+    "rule2-post-as-base": ("float g = post - prod;", "float g = stale + prod;"),
+    # Alg. 1: LITERAL order and acceptance, STEEPEST ties and victim floor
+    "C10-literal-victim-first": ("for (int32_t thief = 0; thief < J; ++thief) {          /* line 5 */",
+                                 "for (int32_t thief = J - 1; thief >= 0; --thief) {          /* line 5 */"),
+    "C12-steepest-ties-last": ("                if (s > best) {\n                    best = s;\n                    bt = t;",
+                               "                if (s >= best && s > cur) {\n                    best = s;\n                    bt = t;"),
+    # A1 CLUSTER (C19): Lloyd iteration count and the query's cluster
+    "C19-max-iter-off-by-one": ("for (int32_t it = 0; it < p->max_iter; ++it) {",
+                                "for (int32_t it = 0; it + 1 < p->max_iter; ++it) {"),
+    "C19-no-convergence-stop": ("if (!changed) break;", "if (0 && !changed) break;"),
+    "C20-fallback-zero": ("out_est[q * G + g] = n > 0 ? orc_mean_from_q32(s, n) : fallback[q * G + g];",
+                          "out_est[q * G + g] = n > 0 ? orc_mean_from_q32(s, n) : 0.0f;"),
     # Eq. 1 constraint 2 (LIST)
     "EQ1-strict-total": ("if (tot > d->units) row_ok = 0;   /* Eq. 1 constraint 2 */",
                          "if (tot >= d->units) row_ok = 0;   /* Eq. 1 constraint 2 */"),
