@@ -862,10 +862,16 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
     const long long Q = P.p.n_query;
     const long long items = Q > blockIdx.x ? (Q - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const u64 one = A.one2;
-    // this lane's counter address = cbase + cluster * cstride (+ choff for the high half)
-    const bool lane_c = lane < C;
-    const unsigned cbase = lane_c ? smem_addr(slo) + 4u * (unsigned)lane : smem_addr(smem + L.dummy) + 4u * (unsigned)lane;
-    const unsigned cstride = lane_c ? (unsigned)(C * 4) : 0u, choff = lane_c ? (unsigned)(K * C * 4) : 0u;
+    // this lane's counter address = cbase + cluster * cstride (+ choff for the high half).  Lane C
+    // (C < 32) carries the cluster counts in the same reds: its address is cnt[cluster] for both
+    // halves, its low value the count change and its high value 0; lanes past C add into a
+    // private dummy word.
+    const bool lane_c = lane < C, lane_n = lane == C;
+    const unsigned cbase = lane_c ? smem_addr(slo) + 4u * (unsigned)lane
+                           : lane_n ? smem_addr(cnt) : smem_addr(smem + L.dummy) + 4u * (unsigned)lane;
+    const unsigned cstride = lane_c ? (unsigned)(C * 4) : lane_n ? 4u : 0u;
+    const unsigned choff = lane_c ? (unsigned)(K * C * 4) : 0u;
+    const bool cnt_by_lane0 = C >= 32;   // no spare lane: lane 0 updates the counts itself
 
     // leader: TMA the history tile (+ cur, fallback into slot j & 1) of this CTA's j-th query and
     // bulk-prefetch its accuracy tile into L2
@@ -995,7 +1001,7 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                     const unsigned b0 = __ballot_sync(0xffffffffu, v0 && na0 == k);
                     const unsigned b1 = __ballot_sync(0xffffffffu, v1 && na1 == k);
                     if ((b0 | b1) == 0) continue;
-                    if (lane == 0) atomicAdd(&cnt[k], __popc(b0) + __popc(b1));
+                    if (cnt_by_lane0 && lane == 0) atomicAdd(&cnt[k], __popc(b0) + __popc(b1));
                     unsigned alo = 0, ahi = 0;
                     for (unsigned m = b0; m; m &= m - 1) {
                         const u64 v = q32(r0[(__ffs(m) - 1) * C]);
@@ -1006,6 +1012,10 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                         const u64 v = q32(r1[(__ffs(m) - 1) * C]);
                         alo += (unsigned)v & 0xFFFFu;
                         ahi += (unsigned)(v >> 16);
+                    }
+                    if (lane_n) {   // lane C: the members' count into cnt[k]
+                        alo = (unsigned)(__popc(b0) + __popc(b1));
+                        ahi = 0u;
                     }
                     const unsigned a = cbase + (unsigned)k * cstride;
                     red_add_shared(a, alo);
@@ -1021,13 +1031,15 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                         const int o = __shfl_sync(0xffffffffu, oav, j);
                         const int n = __shfl_sync(0xffffffffu, nav, j);
                         const u64 v = q32(rows[j * C]);
-                        const unsigned lo = (unsigned)v & 0xFFFFu, hi = (unsigned)(v >> 16);
+                        // lane C: one window leaves cnt[o] and enters cnt[n]
+                        const unsigned lo = lane_n ? 1u : (unsigned)v & 0xFFFFu;
+                        const unsigned hi = lane_n ? 0u : (unsigned)(v >> 16);
                         const unsigned ao = cbase + (unsigned)o * cstride, an = cbase + (unsigned)n * cstride;
                         red_add_shared(ao, 0u - lo);
                         red_add_shared(ao + choff, 0u - hi);
                         red_add_shared(an, lo);
                         red_add_shared(an + choff, hi);
-                        if (lane == 0) {
+                        if (cnt_by_lane0 && lane == 0) {
                             atomicSub(&cnt[o], 1);
                             atomicAdd(&cnt[n], 1);
                         }
