@@ -759,8 +759,13 @@ __device__ __forceinline__ void sum16_add(unsigned* lo, unsigned* hi, u64 v) {
 __device__ __forceinline__ void red_add_shared(unsigned addr, unsigned v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+// Both counters are read as signed 32-bit.  Pass 0 adds each warp's member sum S as (S mod 2^16,
+// S / 2^16) while moves add / subtract single windows' splits (v mod 2^16, v / 2^16), so the low
+// counter holds sum over the cluster's current members of (v mod 2^16) -- in [0, 512 (2^16 - 1)]
+// -- plus a fixed pass-0 offset in (-512 * 2^16, 0]: always within +-2^31, whatever the number of
+// passes; hi * 2^16 + lo is the exact cluster sum.
 __device__ __forceinline__ u64 sum16_get(const unsigned* lo, const unsigned* hi) {
-    return ((u64)*hi << 16) + *lo;
+    return (u64)((long long)(int)*hi * 65536LL + (long long)(int)*lo);
 }
 
 // The changed centroids' distances for N = popcount(chg) < K: the N centroid
@@ -1002,17 +1007,11 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                     const unsigned b1 = __ballot_sync(0xffffffffu, v1 && na1 == k);
                     if ((b0 | b1) == 0) continue;
                     if (cnt_by_lane0 && lane == 0) atomicAdd(&cnt[k], __popc(b0) + __popc(b1));
-                    unsigned alo = 0, ahi = 0;
-                    for (unsigned m = b0; m; m &= m - 1) {
-                        const u64 v = q32(r0[(__ffs(m) - 1) * C]);
-                        alo += (unsigned)v & 0xFFFFu;
-                        ahi += (unsigned)(v >> 16);
-                    }
-                    for (unsigned m = b1; m; m &= m - 1) {
-                        const u64 v = q32(r1[(__ffs(m) - 1) * C]);
-                        alo += (unsigned)v & 0xFFFFu;
-                        ahi += (unsigned)(v >> 16);
-                    }
+                    // the members' exact sum as one u64 (split into the counter pair once, below)
+                    u64 acc = 0;
+                    for (unsigned m = b0; m; m &= m - 1) acc += q32(r0[(__ffs(m) - 1) * C]);
+                    for (unsigned m = b1; m; m &= m - 1) acc += q32(r1[(__ffs(m) - 1) * C]);
+                    unsigned alo = (unsigned)acc & 0xFFFFu, ahi = (unsigned)(acc >> 16);
                     if (lane_n) {   // lane C: the members' count into cnt[k]
                         alo = (unsigned)(__popc(b0) + __popc(b1));
                         ahi = 0u;
