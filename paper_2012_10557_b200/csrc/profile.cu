@@ -903,6 +903,7 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
 
     const int h0 = tid, h1 = tid + kC2Threads;
     const bool v0 = h0 < H, v1 = h1 < H;
+    const int qslot = H < 2 * kC2Threads ? H : -1;   // the query's slot, if a window slot is free
     for (long long i = 0; i < items; ++i) {
         const long long q = blockIdx.x + i * gridDim.x;
         const unsigned char* cf = smem + L.cf + (i & 1) * L.cf_slot;
@@ -911,8 +912,12 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                                                         granules(P.fallback + q * G, 4).off);
         const float* hs = reinterpret_cast<const float*>(smem + L.hist +
                                                          granules(P.hist + (size_t)q * H * C, 4).off);
-        const float* x0 = hs + (size_t)(v0 ? h0 : 0) * C;
-        const float* x1 = hs + (size_t)(v1 ? h1 : (v0 ? h0 : 0)) * C;
+        // the query's own histogram rides in the first unused window slot (H < 512): its
+        // distances to the centroids come out of every Lloyd pass with the same packed code and
+        // nearest rule (C19), so the query's cluster needs no separate computation; the slot is
+        // invalid (v false) for every sum, move, list and output
+        const float* x0 = h0 == qslot ? cur : hs + (size_t)(v0 ? h0 : 0) * C;
+        const float* x1 = h1 == qslot ? cur : hs + (size_t)(v1 ? h1 : (v0 ? h0 : 0)) * C;
         for (int t = tid; t < 2 * K * C; t += kC2Threads) slo[t] = 0u;
         for (int t = tid; t < K; t += kC2Threads) cnt[t] = 0;
         if (tid == 0) misc[0] = misc[1] = misc[3] = misc[4] = 0;
@@ -1047,6 +1052,8 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
             }
             oa0 = na0;
             oa1 = na1;
+            if (h0 == qslot) misc[2] = na0;   // the query's nearest centroid at this pass's means
+            if (h1 == qslot) misc[2] = na1;
             const int any = __syncthreads_or((bm0 | bm1) != 0);
             const int it = passes++;
             if ((it > 0 && !any) || it >= P.p.max_iter) break;
@@ -1073,8 +1080,8 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
         }
         // the query joins its nearest centroid (lowest index on ties, C19): every warp computes it
         // (lane ci < K: distance to centroid ci; K <= 8), so no barrier publishes it
-        int qc;
-        {
+        int qc = misc[2];   // from the query's window slot (the last pass's barrier published it)
+        if (qslot < 0) {
             unsigned long long key = ~0ULL;
             if (lane < K) {
                 const float d = dist2_mem(cur, mu + lane * CP, C);
