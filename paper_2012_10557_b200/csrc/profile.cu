@@ -746,6 +746,13 @@ __device__ __forceinline__ void c2_dists(u64 (&s)[KS], const float* x0, const fl
     }
 }
 
+// position of the highest set bit of m != 0 (one FLO: bfind.u32)
+__device__ __forceinline__ int msb(unsigned m) {
+    int j;
+    asm("bfind.u32 %0, %1;" : "=r"(j) : "r"(m));
+    return j;
+}
+
 // Exact Q32 sums as two 32-bit shared counters: v = hi * 2^16 + lo with
 // lo < 2^16 and hi <= 2^16, so each half of a sum over <= 65,535 windows fits 32
 // bits; adds and subtracts are native 32-bit shared atomics (the 64-bit shared
@@ -1014,8 +1021,20 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                     if (cnt_by_lane0 && lane == 0) atomicAdd(&cnt[k], __popc(b0) + __popc(b1));
                     // the members' exact sum as one u64 (split into the counter pair once, below)
                     u64 acc = 0;
-                    for (unsigned m = b0; m; m &= m - 1) acc += q32(r0[(__ffs(m) - 1) * C]);
-                    for (unsigned m = b1; m; m &= m - 1) acc += q32(r1[(__ffs(m) - 1) * C]);
+                    // members from the highest lane down (any order: exact integers): the bit
+                    // index is one FLO, the row a byte offset from the warp's base
+                    const unsigned char* rb0 = reinterpret_cast<const unsigned char*>(r0);
+                    const unsigned char* rb1 = reinterpret_cast<const unsigned char*>(r1);
+                    for (unsigned m = b0; m;) {
+                        const int j = msb(m);
+                        m ^= 1u << j;
+                        acc += q32(*reinterpret_cast<const float*>(rb0 + j * (C * 4)));
+                    }
+                    for (unsigned m = b1; m;) {
+                        const int j = msb(m);
+                        m ^= 1u << j;
+                        acc += q32(*reinterpret_cast<const float*>(rb1 + j * (C * 4)));
+                    }
                     unsigned alo = (unsigned)acc & 0xFFFFu, ahi = (unsigned)(acc >> 16);
                     if (lane_n) {   // lane C: the members' count into cnt[k]
                         alo = (unsigned)(__popc(b0) + __popc(b1));
@@ -1030,8 +1049,9 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                 for (int sl = 0; sl < 2; ++sl) {
                     const float* rows = hs + (size_t)(warp * 32 + sl * kC2Threads) * C + lane;
                     const int oav = sl ? oa1 : oa0, nav = sl ? na1 : na0;
-                    for (unsigned m = sl ? bm1 : bm0; m; m &= m - 1) {
-                        const int j = __ffs(m) - 1;
+                    for (unsigned m = sl ? bm1 : bm0; m;) {
+                        const int j = msb(m);   // highest moved lane first (any order)
+                        m ^= 1u << j;
                         const int o = __shfl_sync(0xffffffffu, oav, j);
                         const int n = __shfl_sync(0xffffffffu, nav, j);
                         const u64 v = q32(rows[j * C]);
