@@ -821,22 +821,36 @@ __device__ __forceinline__ void c2_dists_n(u64 (&s)[KS], const float* x0, const 
 struct C2Layout {
     size_t bar, misc, cf, hist, mu, sums, cnt, dummy, total, cf_slot;
 };
+struct C2Fixed {
+    size_t bar, misc, mu, cnt, dummy, sums;
+};
+__host__ __device__ constexpr size_t c2_al16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ constexpr C2Fixed c2_fixed(int C, int K) {
+    const size_t CP = (size_t)((C + 3) & ~3);
+    const size_t mu = 16 + 96;
+    const size_t cnt = mu + c2_al16((size_t)(K + 1) * CP * 4);
+    const size_t dummy = cnt + c2_al16((size_t)K * 4);
+    return C2Fixed{0, 16, mu, cnt, dummy, dummy + 128};
+}
 __host__ __device__ inline C2Layout c2_layout(int H, int C, int G, int K) {
     C2Layout L;
-    const int CP = (C + 3) & ~3;
-    size_t o = 0;
-    L.bar = o;    o += 16;
-    L.misc = o;   o += 96;   // ints [0..7] + the HB kernel's displacement bounds at [8..15]
-    L.cf_slot = al16((size_t)C * 4) + 16 + al16((size_t)G * 4) + 16;   // [cur][fallback] granule-staged
-    L.cf = o;     o += 2 * L.cf_slot;
-    L.hist = o;   o += al16((size_t)H * C * 4) + 16;
-    L.mu = o;     o += al16((size_t)(K + 1) * CP * 4);   // K centroids + the padded query (fused RADIUS)
+    // regions whose offsets depend only on (C, K) first, so that a compile-time (K, C)
+    // instantiation addresses them with constants (c2_fixed); H- and G-sized regions after
+    const C2Fixed F = c2_fixed(C, K);
+    L.bar = F.bar;
+    L.misc = F.misc;     // ints [0..7] + the HB kernel's displacement bounds at [8..15]
+    L.mu = F.mu;         // K centroids + the padded query (fused RADIUS)
+    L.cnt = F.cnt;
+    L.dummy = F.dummy;   // sink of the lanes beyond column C
+    L.sums = F.sums;
     // Lloyd: cluster sums lo[K][C], hi[K][C] (u32); afterwards the same space holds
     // the window list (u16[H]) and two sets of per-gamma sums lo[G], hi[G], n[G]
     const size_t lloyd = (size_t)K * C * 8, gam = al16((size_t)H * 2) + (size_t)G * 24;
-    L.sums = o;   o += al16(lloyd > gam ? lloyd : gam);
-    L.cnt = o;    o += al16((size_t)K * 4);
-    L.dummy = o;  o += 128;   // sink of the lanes beyond column C
+    size_t o = F.sums + al16(lloyd > gam ? lloyd : gam);
+    L.cf_slot = al16((size_t)C * 4) + 16 + al16((size_t)G * 4) + 16;   // [cur][fallback] granule-staged
+    L.cf = o;     o += 2 * L.cf_slot;
+    // + 128: lanes past column C read (and ignore) up to 31 floats beyond the last row
+    L.hist = o;   o += al16((size_t)H * C * 4) + 16 + 128;
     L.total = o;
     return L;
 }
@@ -860,15 +874,21 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
     const int C = CT > 0 ? CT : P.p.n_class;
     const int CP = (C + 3) & ~3;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // (K, C) fixed at compile time: the (C, K)-only regions at constant offsets
+    constexpr C2Fixed FX = c2_fixed(CT > 0 ? CT : 1, KT > 0 ? KT : 1);
+    constexpr bool kFixed = KT > 0 && CT > 0;
+    const size_t o_misc = kFixed ? FX.misc : L.misc, o_mu = kFixed ? FX.mu : L.mu;
+    const size_t o_cnt = kFixed ? FX.cnt : L.cnt, o_dummy = kFixed ? FX.dummy : L.dummy;
+    const size_t o_sums = kFixed ? FX.sums : L.sums;
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + L.bar);
-    int* misc = reinterpret_cast<int*>(smem + L.misc);   // [0..1] changed-centroid masks,
-                                                         // [3] similar-window count
-    float* mu = reinterpret_cast<float*>(smem + L.mu);
-    unsigned* slo = reinterpret_cast<unsigned*>(smem + L.sums);
+    int* misc = reinterpret_cast<int*>(smem + o_misc);   // [0..1] changed-centroid masks,
+                                                         // [2] query cluster, [3] list count
+    float* mu = reinterpret_cast<float*>(smem + o_mu);
+    unsigned* slo = reinterpret_cast<unsigned*>(smem + o_sums);
     unsigned* shi = slo + K * C;
-    int* cnt = reinterpret_cast<int*>(smem + L.cnt);
-    uint16_t* list = reinterpret_cast<uint16_t*>(smem + L.sums);
-    unsigned* glo = reinterpret_cast<unsigned*>(smem + L.sums + al16((size_t)H * 2));
+    int* cnt = reinterpret_cast<int*>(smem + o_cnt);
+    uint16_t* list = reinterpret_cast<uint16_t*>(smem + o_sums);
+    unsigned* glo = reinterpret_cast<unsigned*>(smem + o_sums + al16((size_t)H * 2));
     unsigned* ghi = glo + G;
     int* gnn = reinterpret_cast<int*>(ghi + G);
     const long long Q = P.p.n_query;
@@ -880,7 +900,7 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
     // private dummy word.
     const bool lane_c = lane < C, lane_n = lane == C;
     const unsigned cbase = lane_c ? smem_addr(slo) + 4u * (unsigned)lane
-                           : lane_n ? smem_addr(cnt) : smem_addr(smem + L.dummy) + 4u * (unsigned)lane;
+                           : lane_n ? smem_addr(cnt) : smem_addr(smem + o_dummy) + 4u * (unsigned)lane;
     const unsigned cstride = lane_c ? (unsigned)(C * 4) : lane_n ? 4u : 0u;
     const unsigned choff = lane_c ? (unsigned)(K * C * 4) : 0u;
     const bool cnt_by_lane0 = C >= 32;   // no spare lane: lane 0 updates the counts itself
