@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list_kernel(EvalParams p) {
         const int v = task / nblk, blk = task - v * nblk;
         if (lane < nG) {
             const float post = S.post[v * nG + lane];
-            si->cpd[lane] = make_float4(S.cost[v * nG + lane], post, fsub(post, S.stale[v]), 0.0f);
+            stream_in_put(si, lane, S.cost[v * nG + lane], post, fsub(post, S.stale[v]));
         }
         if (lane < nL) {
             si->lf[lane] = S.lf[v * nL + lane];
@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list2_kernel(const __grid_con
                 const float po = post[v * nG + lane];
                 if (!(c >= 0.0f)) vok = false;
                 else if (!isinf(c)) vok &= in01(po);
-                si->cpd[lane] = make_float4(c, po, fsub(po, st), 0.0f);
+                stream_in_put(si, lane, c, po, fsub(po, st));
             }
             if (lane < nL) {
                 const float f = lf[v * nL + lane];
@@ -867,7 +867,7 @@ __global__ void __launch_bounds__(kListThreads, 1) list2_kernel(const __grid_con
             }
             __syncwarp();
             unsigned char* tv = smem + L.tabs + k * L.tabset + v * tb;
-            warp_build_tables<19, kL2G, kL2L, kListRow, 8>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
+            warp_build_tables<19, kL2G, kL2L, kListRow, 8, false, uint8_t, true>(si, U, nG, nL, d.unit_gpu_seconds, d.a_min, tv,
                                                           reinterpret_cast<unsigned long long*>(tv + 96), 0, U + 1,
                                                           true);
             mbar_arrive(&full[i & 7]);
