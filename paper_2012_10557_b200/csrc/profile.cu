@@ -849,8 +849,9 @@ __host__ __device__ inline C2Layout c2_layout(int H, int C, int G, int K) {
     size_t o = F.sums + al16(lloyd > gam ? lloyd : gam);
     L.cf_slot = al16((size_t)C * 4) + 16 + al16((size_t)G * 4) + 16;   // [cur][fallback] granule-staged
     L.cf = o;     o += 2 * L.cf_slot;
-    // + 128: lanes past column C read (and ignore) up to 31 floats beyond the last row
-    L.hist = o;   o += al16((size_t)H * C * 4) + 16 + 128;
+    // + 256: row H holds a copy of the query's histogram (cluster2_kernel, H < 512) and lanes past
+    // column C read (and ignore) up to 31 floats beyond the last row
+    L.hist = o;   o += al16((size_t)H * C * 4) + 16 + 256;
     L.total = o;
     return L;
 }
@@ -939,16 +940,20 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                                                         granules(P.fallback + q * G, 4).off);
         const float* hs = reinterpret_cast<const float*>(smem + L.hist +
                                                          granules(P.hist + (size_t)q * H * C, 4).off);
-        // the query's own histogram rides in the first unused window slot (H < 512): its
-        // distances to the centroids come out of every Lloyd pass with the same packed code and
-        // nearest rule (C19), so the query's cluster needs no separate computation; the slot is
-        // invalid (v false) for every sum, move, list and output
-        const float* x0 = h0 == qslot ? cur : hs + (size_t)(v0 ? h0 : 0) * C;
-        const float* x1 = h1 == qslot ? cur : hs + (size_t)(v1 ? h1 : (v0 ? h0 : 0)) * C;
+        // the query's own histogram rides in the first unused window slot (H < 512) as tile row
+        // H (copied there below): its distances to the centroids come out of every Lloyd pass
+        // with the same packed code and nearest rule (C19), so the query's cluster needs no
+        // separate computation; the slot is invalid (v false) for every sum, move, list and output
+        const int rw0 = (v0 || h0 == qslot) ? h0 : 0;
+        const int rw1 = (v1 || h1 == qslot) ? h1 : rw0;
+        const float* x0 = hs + (size_t)rw0 * C;
+        const float* x1 = hs + (size_t)rw1 * C;
         for (int t = tid; t < 2 * K * C; t += kC2Threads) slo[t] = 0u;
         for (int t = tid; t < K; t += kC2Threads) cnt[t] = 0;
         if (tid == 0) misc[0] = misc[1] = misc[3] = misc[4] = 0;
         mbar_wait(bar, (unsigned)(i & 1));
+        if (qslot >= 0)   // the query's histogram as tile row H (read after the barrier below)
+            for (int c = tid; c < C; c += kC2Threads) const_cast<float*>(hs)[(size_t)H * C + c] = cur[c];
         bool ok = true;
         for (int c = tid; c < C; c += kC2Threads) ok &= in01(cur[c]);
         if (KT != 5) {   // K = 5: checked during the first pass's distances
