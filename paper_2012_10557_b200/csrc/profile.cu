@@ -1014,7 +1014,26 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                 else c2_dists<KT, KS, false>(s, x0, x1, mu, C, CP, K, chg, one);
             }
             // nearest centroid, lowest index on ties (C19)
-            {
+            if constexpr (KT == 5) {
+                // min of the five by two 3-input min instructions, then the lowest index equal to
+                // it (same as the strict-'<' scan for non-NaN distances; a NaN distance -- invalid
+                // data, outputs zeroed -- is never the minimum)
+                float d0[5], d1[5];
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    d0[k] = lo2(s[k]);
+                    d1[k] = hi2(s[k]);
+                }
+                const float m0 = fminf(fminf(d0[0], d0[1]), fminf(d0[2], fminf(d0[3], d0[4])));
+                const float m1 = fminf(fminf(d1[0], d1[1]), fminf(d1[2], fminf(d1[3], d1[4])));
+                na0 = 4;
+                na1 = 4;
+#pragma unroll
+                for (int k = 3; k >= 0; --k) {
+                    na0 = d0[k] == m0 ? k : na0;
+                    na1 = d1[k] == m1 ? k : na1;
+                }
+            } else {
                 float b0 = lo2(s[0]), b1 = hi2(s[0]);
                 na0 = 0;
                 na1 = 0;
