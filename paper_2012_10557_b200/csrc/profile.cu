@@ -905,6 +905,7 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
     const unsigned cstride = lane_c ? (unsigned)(C * 4) : lane_n ? 4u : 0u;
     const unsigned choff = lane_c ? (unsigned)(K * C * 4) : 0u;
     const bool cnt_by_lane0 = C >= 32;   // no spare lane: lane 0 updates the counts itself
+    const int rstride = lane_c ? C * 4 : 0;   // member-row stride (lanes >= C: the constant word)
 
     // leader: TMA the history tile (+ cur, fallback into slot j & 1) of this CTA's j-th query and
     // bulk-prefetch its accuracy tile into L2
@@ -925,6 +926,7 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
     if (tid == 0) {
         mbar_init(bar, 1);
         fence_barrier_init();
+        misc[7] = (int)0x2F800000u;   // 2^-32 (read by lanes >= C in the member sums)
     }
     __syncthreads();
     if (tid == 0 && items > 0) issue(0);
@@ -1056,8 +1058,10 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                 // masks) are summed in registers -- low and high halves separately, so the
                 // shared counters keep each window's exact (v mod 2^16, v / 2^16) split that
                 // later moves subtract -- then one pair of shared adds per cluster and lane
-                const float* r0 = hs + (size_t)(warp * 32) * C + lane;
-                const float* r1 = r0 + (size_t)kC2Threads * C;
+                // lanes < C read column `lane` of the member rows; lanes >= C read misc[7] = 2^-32
+                // (q32 = 1) with stride 0, so lane C's sum is the member count with no select
+                const float* r0 = lane_c ? hs + (size_t)(warp * 32) * C + lane : reinterpret_cast<const float*>(misc + 7);
+                const float* r1 = lane_c ? r0 + (size_t)kC2Threads * C : r0;
                 for (int k = 0; k < K; ++k) {
                     const unsigned b0 = __ballot_sync(0xffffffffu, v0 && na0 == k);
                     const unsigned b1 = __ballot_sync(0xffffffffu, v1 && na1 == k);
@@ -1072,18 +1076,14 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                     for (unsigned m = b0; m;) {
                         const int j = msb(m);
                         m ^= 1u << j;
-                        acc += q32(*reinterpret_cast<const float*>(rb0 + j * (C * 4)));
+                        acc += q32(*reinterpret_cast<const float*>(rb0 + j * rstride));
                     }
                     for (unsigned m = b1; m;) {
                         const int j = msb(m);
                         m ^= 1u << j;
-                        acc += q32(*reinterpret_cast<const float*>(rb1 + j * (C * 4)));
+                        acc += q32(*reinterpret_cast<const float*>(rb1 + j * rstride));
                     }
                     unsigned alo = (unsigned)acc & 0xFFFFu, ahi = (unsigned)(acc >> 16);
-                    if (lane_n) {   // lane C: the members' count into cnt[k]
-                        alo = (unsigned)(__popc(b0) + __popc(b1));
-                        ahi = 0u;
-                    }
                     const unsigned a = cbase + (unsigned)k * cstride;
                     red_add_shared(a, alo);
                     red_add_shared(a + choff, ahi);
@@ -1091,17 +1091,17 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
             } else {
 #pragma unroll
                 for (int sl = 0; sl < 2; ++sl) {
-                    const float* rows = hs + (size_t)(warp * 32 + sl * kC2Threads) * C + lane;
+                    const float* rows = lane_c ? hs + (size_t)(warp * 32 + sl * kC2Threads) * C + lane
+                                               : reinterpret_cast<const float*>(misc + 7);
                     const int oav = sl ? oa1 : oa0, nav = sl ? na1 : na0;
                     for (unsigned m = sl ? bm1 : bm0; m;) {
                         const int j = msb(m);   // highest moved lane first (any order)
                         m ^= 1u << j;
                         const int o = __shfl_sync(0xffffffffu, oav, j);
                         const int n = __shfl_sync(0xffffffffu, nav, j);
-                        const u64 v = q32(rows[j * C]);
-                        // lane C: one window leaves cnt[o] and enters cnt[n]
-                        const unsigned lo = lane_n ? 1u : (unsigned)v & 0xFFFFu;
-                        const unsigned hi = lane_n ? 0u : (unsigned)(v >> 16);
+                        // lane C reads 2^-32 (q32 = 1): one window leaves cnt[o] and enters cnt[n]
+                        const u64 v = q32(*reinterpret_cast<const float*>(reinterpret_cast<const unsigned char*>(rows) + j * rstride));
+                        const unsigned lo = (unsigned)v & 0xFFFFu, hi = (unsigned)(v >> 16);
                         const unsigned ao = cbase + (unsigned)o * cstride, an = cbase + (unsigned)n * cstride;
                         red_add_shared(ao, 0u - lo);
                         red_add_shared(ao + choff, 0u - hi);
