@@ -972,19 +972,10 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
             mu[t] = c >= C ? 0.0f : ci < K ? hs[(size_t)(((long long)ci * H) / K) * C + c] : cur[c];
         }
         __syncthreads();
-        // fused RADIUS (rule 5, C17): both windows' distances to the query, similar iff
-        // sqrt(d2) <= tau -- the same sequential sum as radius_kernel (fl(x - c)^2 = fl(c - x)^2)
-        // (the similar flags are parked as per-warp ballot masks in misc[8..23] until the end)
-        if (rad) {
-            u64 sr[1];
-            c2_dists<1, 1, true>(sr, x0, x1, mu + K * CP, C, CP, 1, 1u, one);
-            const unsigned b0 = __ballot_sync(0xffffffffu, v0 && __fsqrt_rn(lo2(sr[0])) <= P.rad_tau);
-            const unsigned b1 = __ballot_sync(0xffffffffu, v1 && __fsqrt_rn(hi2(sr[0])) <= P.rad_tau);
-            if (lane == 0) {
-                misc[8 + warp] = (int)b0;
-                misc[16 + warp] = (int)b1;
-            }
-        }
+        // fused RADIUS (rule 5, C17): both windows' distances to the query are computed in pass 0
+        // as a sixth centroid row (mu row K = the query), similar iff sqrt(d2) <= tau -- the same
+        // sequential sum as radius_kernel (fl(x - c)^2 = fl(c - x)^2); the similar flags are
+        // parked as per-warp ballot masks in misc[8..23] until the end
 
         u64 s[KS];
 #pragma unroll
@@ -1001,7 +992,21 @@ __global__ void __launch_bounds__(kC2Threads, kC2Ctas) cluster2_kernel(const __g
                     // value on the way; a NaN value makes both windows' distances NaN.  Lanes
                     // without a second (or any) window read a duplicate row: still a real row.
                     float lo = 1.0f, hi = 0.0f;
-                    c2_dists<KT, KS, true, true>(s, x0, x1, mu, C, CP, K, chg, one, &lo, &hi);
+                    if (rad) {   // + the query row: one pass over the history loads for both
+                        u64 s6[KT + 1];
+                        c2_dists<KT + 1, KT + 1, true, true>(s6, x0, x1, mu, C, CP, KT + 1, (1u << (KT + 1)) - 1u,
+                                                             one, &lo, &hi);
+#pragma unroll
+                        for (int k = 0; k < KT; ++k) s[k] = s6[k];
+                        const unsigned b0 = __ballot_sync(0xffffffffu, v0 && __fsqrt_rn(lo2(s6[KT])) <= P.rad_tau);
+                        const unsigned b1 = __ballot_sync(0xffffffffu, v1 && __fsqrt_rn(hi2(s6[KT])) <= P.rad_tau);
+                        if (lane == 0) {
+                            misc[8 + warp] = (int)b0;
+                            misc[16 + warp] = (int)b1;
+                        }
+                    } else {
+                        c2_dists<KT, KS, true, true>(s, x0, x1, mu, C, CP, K, chg, one, &lo, &hi);
+                    }
                     ok &= lo >= 0.0f && hi <= 1.0f && lo2(s[0]) == lo2(s[0]) && hi2(s[0]) == hi2(s[0]);
                 } else switch (__popc(chg)) {
                     case 0: break;   // nothing moved: the cache is exact
