@@ -308,6 +308,8 @@ BOTH_CASES = PROF_CASES + [
     ("h513", synth.ProfileConfig("p", 12, 513, 27, 18)),          # not fused: two kernels
     ("h3", synth.ProfileConfig("p", 10, 3, 27, 18)),
     ("sparse-g1", synth.ProfileConfig("p", 40, 300, 27, 1, sparse=True)),
+    ("h511", synth.ProfileConfig("p", 24, 511, 27, 18)),          # fused: the query in slot 511
+    ("h255", synth.ProfileConfig("p", 24, 255, 27, 18)),          # fused: the query in slot 255
 ]
 
 
@@ -366,6 +368,12 @@ CLUSTER_EDGE = [
     ("c1-g40", synth.ProfileConfig("p", 20, 90, 1, 40), 3, 100),
     ("k9-fallback", synth.ProfileConfig("p", 10, 500, 27, 18), 9, 100),
     ("h3-k5", synth.ProfileConfig("p", 10, 3, 27, 18), 5, 100),
+    # the query's window slot (first unused slot, H < 512) at its extremes: slot 511 (last
+    # thread's second window) and slot 255 (last thread's first window); C = 26 puts the
+    # count-carrying lane C next to a real column lane
+    ("h511-k5", synth.ProfileConfig("p", 24, 511, 27, 18), 5, 100),
+    ("h255-k5", synth.ProfileConfig("p", 24, 255, 27, 18), 5, 100),
+    ("c26-h400", synth.ProfileConfig("p", 24, 400, 26, 18), 5, 100),
 ]
 
 
