@@ -160,13 +160,16 @@ __device__ __noinline__ float fdiv_cold(float a, float b) { return __fdiv_rn(a, 
 // t_l <= ri; so the thresholds are stored ascending (ties: lambda order) with
 // lambda*(t) and its factor, and F(ri) is the entry of the last threshold <= ri.
 // Slot rank(l) = #{l' : (t_l', l') < (t_l, l)}; slots nL..7 stay unused (0xFFFF).
+// NL: the loops' compile-time bound -- |Lambda| itself for the paper's shape (no guards, 5 x 5
+// comparisons), kMaxLambda with runtime guards otherwise.
+template <int NL>
 __device__ __forceinline__ void init_ladder_lane(const InstView& in, const WarpState& S, int v, const ekya_dims& d) {
-    const int nL = d.n_lambda;
-    unsigned t[kMaxLambda];
-    float acc[kMaxLambda], f[kMaxLambda];
+    const int nL = NL < kMaxLambda ? NL : d.n_lambda;
+    unsigned t[NL];
+    float acc[NL], f[NL];
     const float st = in.stale[v];
 #pragma unroll
-    for (int l = 0; l < kMaxLambda; ++l) {
+    for (int l = 0; l < NL; ++l) {
         t[l] = 0xFFFFu;
         acc[l] = 0.0f;
         f[l] = 0.0f;
@@ -181,13 +184,13 @@ __device__ __forceinline__ void init_ladder_lane(const InstView& in, const WarpS
 #pragma unroll
     for (int p = 0; p < 8; ++p) th[p] = 0xFFFFu;
 #pragma unroll
-    for (int l = 0; l < kMaxLambda; ++l) {
+    for (int l = 0; l < NL; ++l) {
         if (l < nL) {
             // lambda*(t_l) over {l' : t_l' <= t_l}: highest accuracy, lowest index on ties
             int best = 0, rank = 0;
             float bacc = -1.0f, fb = 0.0f;
 #pragma unroll
-            for (int l2 = 0; l2 < kMaxLambda; ++l2) {
+            for (int l2 = 0; l2 < NL; ++l2) {
                 if (l2 < nL) {
                     const bool take = t[l2] <= t[l] && acc[l2] > bacc;
                     best = take ? l2 : best;
@@ -473,8 +476,13 @@ __device__ __forceinline__ void thief_one(const ThiefParams& p, long long b, uns
         S.alloc[2 * v + 1] = rt;
         S.alloc[2 * v] = share - rt;
     }
+    if (nL == 5) {   // the paper's |Lambda|: compile-time loops (no guards)
 #pragma unroll 1
-    for (int v = lane; v < V; v += 32) init_ladder_lane(in, S, v, d);
+        for (int v = lane; v < V; v += 32) init_ladder_lane<5>(in, S, v, d);
+    } else {
+#pragma unroll 1
+        for (int v = lane; v < V; v += 32) init_ladder_lane<kMaxLambda>(in, S, v, d);
+    }
 #pragma unroll 1
     for (int i = lane; i < V * (nsm + 1); i += 32) S.gc[i] = make_uint2(0xFFFFFFFFu, 0u);
     __syncwarp();
