@@ -32,6 +32,7 @@
 #include <climits>
 
 #include "launch.h"
+#include <type_traits>
 #include "stream_tables.cuh"
 
 namespace ekya {
@@ -435,15 +436,22 @@ __device__ __forceinline__ void thief_one(const ThiefParams& p, long long b, uns
         ok &= in01(x);
         if (p.stage) st[i] = x;
     }
-    // flat over (stream, config): every lane's loads are independent (one latency round trip)
+    // flat over (stream, config): every lane's loads are independent (one latency round trip);
+    // the paper's |Gamma| = 18 divides by a constant
+    auto stage_pass = [&](auto ngc) {
+        constexpr int NGC = decltype(ngc)::value;
+        const int ng = NGC > 0 ? NGC : nG;
 #pragma unroll 2
-    for (int i = lane; i < V * nG; i += 32) {
-        const int v = i / nG;
-        const float c = __ldg(in.cost + i), po = __ldg(in.post + i);
-        ok &= c >= 0.0f && (isinf(c) || in01(po));
-        fast &= fast_dividend(c);
-        if (p.stage) cpd[i] = make_float4(c, po, fsub(po, __ldg(in.stale + v)), 0.0f);
-    }
+        for (int i = lane; i < V * ng; i += 32) {
+            const int v = i / ng;
+            const float c = __ldg(in.cost + i), po = __ldg(in.post + i);
+            ok &= c >= 0.0f && (isinf(c) || in01(po));
+            fast &= fast_dividend(c);
+            if (p.stage) cpd[i] = make_float4(c, po, fsub(po, __ldg(in.stale + v)), 0.0f);
+        }
+    };
+    if (nG == 18) stage_pass(std::integral_constant<int, 18>{});
+    else stage_pass(std::integral_constant<int, 0>{});
     for (int i = lane; i < V * nL; i += 32)
         if (__ldg(in.lmu + i) != kLmuPad) ok &= in01(__ldg(in.lf + i));
     __syncwarp();
